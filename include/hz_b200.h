@@ -1,0 +1,178 @@
+/*
+ * hz_b200.h -- C ABI of the B200-native multi-RHS Helmholtz solver.
+ *
+ * Drop-in boundary for the reference's Helmholtz solve path
+ * (seistomo, /root/reference/proj/core). Every entry point names the
+ * reference interface it replaces (file:line, paths relative to
+ * proj/core/). Plain pointers and sizes only: complex arrays are interleaved
+ * (re, im) doubles, node-major blocks a[i*k + j] exactly like
+ * seistomo::BlockVec<cplx> (include/seistomo/block.hpp:13-27), so reference
+ * buffers pass through without transposition.
+ *
+ * Errors: every function returns an hz_status; hz_last_error_message()
+ * returns the thread's last message. Status values map one-to-one to the
+ * reference's exception classes (include/seistomo/errors.hpp:10-46).
+ * There is no CPU fallback: without a CUDA device every compute entry point
+ * fails with HZ_CUDA.
+ */
+#ifndef HZ_B200_H
+#define HZ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HZ_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HZ_API __attribute__((visibility("default")))
+#else
+#define HZ_API
+#endif
+
+typedef enum hz_status {
+  HZ_OK = 0,
+  HZ_VALIDATION = 1,    /* seistomo::ValidationError */
+  HZ_CONVERGENCE = 2,   /* seistomo::ConvergenceError */
+  HZ_BREAKDOWN = 3,     /* seistomo::BreakdownError */
+  HZ_FACTORIZATION = 4, /* seistomo::FactorizationError */
+  HZ_STATE = 5,         /* seistomo::StateError */
+  HZ_IO = 6,            /* seistomo::IoError */
+  HZ_CUDA = 7,          /* CUDA runtime / device failure */
+  HZ_NCCL = 8           /* collective failure */
+} hz_status;
+
+/* include/seistomo/helmholtz_solver.hpp:12 (+ HZ_METHOD_MG_FGMRES: the
+ * build_hierarchy + MgHierarchy::cycle + block_fgmres composition with the
+ * cycle kind taken from hz_options.cycle_kind). */
+typedef enum hz_method {
+  HZ_METHOD_MG_BICGSTAB = 0,
+  HZ_METHOD_MG_FGMRES_W = 1,
+  HZ_METHOD_MG_FGMRES_K = 2,
+  HZ_METHOD_DENSE_LU_SMALL = 3,
+  HZ_METHOD_MG_FGMRES = 4,
+  HZ_METHOD_MG_BICGSTAB_CYCLE = 5 /* BiCGSTAB with hz_options.cycle_kind */
+} hz_method;
+
+typedef enum hz_cycle_kind { HZ_CYCLE_V = 0, HZ_CYCLE_W = 1, HZ_CYCLE_K = 2 } hz_cycle_kind;
+
+typedef enum hz_precision { HZ_C128 = 0, HZ_C64 = 1 } hz_precision;
+
+/* HelmholtzSolveOptions (include/seistomo/helmholtz_solver.hpp:14-24) +
+ * CycleSpec (include/seistomo/multigrid.hpp:17-23) + B200 fields. */
+typedef struct hz_options {
+  int method;              /* hz_method; default HZ_METHOD_MG_BICGSTAB */
+  double tol;              /* 1e-6 */
+  int max_cycles;          /* 200 */
+  int nlevels;             /* 3 */
+  double shift_factor;     /* 0.2 */
+  int cycle_kind;          /* hz_cycle_kind (derived from method unless MG_FGMRES) */
+  int pre;                 /* 2 */
+  int post;                /* 2 */
+  double jacobi_weight;    /* 0.8 */
+  int k_inner;             /* 2 */
+  int fgmres_restart;      /* 5 */
+  int64_t dense_threshold; /* 3000 */
+  int precond_precision;   /* hz_precision of the multigrid cycle; HZ_C128 */
+} hz_options;
+
+/* SolveReport (include/seistomo/krylov.hpp:19-40). Arrays are caller-owned
+ * (length k, history_cap); any may be NULL. */
+typedef struct hz_report {
+  int cycles;
+  int qr_factorizations;
+  int64_t block_gram_products;
+  double wall_s;
+  int history_len; /* full length; at most history_cap entries written */
+  int* col_cycles;
+  double* rel_residual;
+  int* converged;
+  double* history;
+  int history_cap;
+} hz_report;
+
+typedef struct hz_problem hz_problem;
+typedef struct hz_solver hz_solver;
+
+HZ_API int hz_abi_version(void);
+HZ_API const char* hz_last_error_message(void);
+/* number of CUDA devices visible (0 = none; compute calls then fail) */
+HZ_API int hz_device_count(void);
+
+/* Fill with the reference defaults (include/seistomo/helmholtz_solver.hpp:14-24). */
+HZ_API void hz_options_default(hz_options* opts);
+
+/* HelmholtzProblem(SlownessSquaredModel, omega, AttenuationField, allow_coarse)
+ * (include/seistomo/helmholtz.hpp:22-24, src/helmholtz.cpp:16-43) with
+ * RegularGrid(ndim, n, h) (include/seistomo/grid.hpp:26-35) and
+ * AttenuationField{base = gamma_base, ramp} (include/seistomo/attenuation.hpp:11-22):
+ * gamma(omega) = gamma_base + omega * ramp[i]. m and ramp are [n0*n1*n2]
+ * doubles, axis 0 fastest. */
+HZ_API int hz_problem_create(int ndim, const int64_t n[3], const double h[3], const double* m,
+                      double omega, double gamma_base, const double* ramp, int allow_coarse_ppw,
+                      int device, hz_problem** out);
+HZ_API int hz_problem_destroy(hz_problem* p);
+/* HelmholtzProblem::points_per_wavelength (src/helmholtz.cpp:40-43) */
+HZ_API int hz_problem_ppw(const hz_problem* p, double* ppw);
+HZ_API int64_t hz_problem_num_nodes(const hz_problem* p);
+
+/* HelmholtzProblem::apply_block (src/helmholtz.cpp:71-100): out = A u, host
+ * buffers [n][k] complex. */
+HZ_API int hz_apply_block(hz_problem* p, int64_t n, int k, const double* u, double* out);
+/* same on device buffers (double2*), enqueued on `stream` (cudaStream_t or NULL) */
+HZ_API int hz_apply_block_device(hz_problem* p, int64_t n, int k, const void* u_dev, void* out_dev,
+                          void* stream);
+
+/* HelmholtzSolver(problem, options) (src/helmholtz_solver.cpp:7-33):
+ * builds the shifted-Laplacian Galerkin hierarchy on the problem's device. */
+HZ_API int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** out);
+HZ_API int hz_solver_destroy(hz_solver* s);
+/* HelmholtzSolver::set_tolerance (include/seistomo/helmholtz_solver.hpp:46) */
+HZ_API int hz_solver_set_tolerance(hz_solver* s, double tol);
+
+/* HelmholtzSolver::solve_block (src/helmholtz_solver.cpp:35-72): host
+ * buffers B, X [n][k]; H2D / D2H copies included. Non-convergence is
+ * reported in the report (status stays HZ_OK), as in the reference. */
+HZ_API int hz_solve_block(hz_solver* s, int64_t n, int k, const double* B, double* X, hz_report* rep);
+/* device-resident variant (double2*) */
+HZ_API int hz_solve_block_device(hz_solver* s, int64_t n, int k, const void* B_dev, void* X_dev,
+                          hz_report* rep);
+
+/* solve_helmholtz contract (src/helmholtz_solver.cpp:81-93): like
+ * hz_solve_block but returns HZ_CONVERGENCE if any column misses tol. */
+HZ_API int hz_solve_helmholtz(hz_solver* s, int64_t n, int k, const double* B, double* X,
+                       hz_report* rep);
+
+/* One preconditioner application x := cycle(b) from x = 0
+ * (out := 0; MgHierarchy::cycle(opts.cycle), src/helmholtz_solver.cpp:65-68). */
+HZ_API int hz_cycle(hz_solver* s, int64_t n, int k, const double* b, double* x);
+HZ_API int hz_cycle_device(hz_solver* s, int64_t n, int k, const void* b_dev, void* x_dev);
+
+/* MgHierarchy::coarse_solve (src/multigrid.cpp:114-117) on the coarsest level */
+HZ_API int hz_coarse_solve(hz_solver* s, int64_t nc, int k, const double* b, double* x);
+
+/* Hierarchy inspection (MgHierarchy::level, include/seistomo/multigrid.hpp:48-49) */
+HZ_API int hz_hierarchy_num_levels(const hz_solver* s, int* nlevels);
+HZ_API int hz_hierarchy_level_dims(const hz_solver* s, int level, int64_t dims[3]);
+/* level 0: shifted centre [n] ; level >= 1: Galerkin planes [3^ndim][n]
+ * with plane s = (dz+1)*9 + (dy+1)*3 + (dx+1) holding A[i][i + offset]. */
+HZ_API int hz_hierarchy_level_coefficients(const hz_solver* s, int level, double* out, int64_t count);
+
+/* fwi_sensitivity_output summed over the k columns (src/helmholtz_solver.cpp:103-111):
+ * g[i] (+)= sum_s Re(-omega^2 (1 - i gamma_i/omega) U[i][s] L[i][s]). Host buffers. */
+HZ_API int hz_sensitivity_accumulate(hz_problem* p, int64_t n, int k, const double* U, const double* L,
+                              double* g, int accumulate);
+HZ_API int hz_sensitivity_accumulate_device(hz_problem* p, int64_t n, int k, const void* U_dev,
+                                     const void* L_dev, double* g_dev, int accumulate,
+                                     void* stream);
+
+/* number of this library's kernel launches so far (process-wide) */
+HZ_API int64_t hz_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HZ_B200_H */

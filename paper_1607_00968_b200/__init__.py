@@ -1,0 +1,457 @@
+"""B200-native multi-RHS Helmholtz solver (shifted-Laplacian MG + block Krylov).
+
+Python mirror of the reference's solver interface (seistomo,
+/root/reference/proj/core/include/seistomo/{helmholtz,helmholtz_solver,
+multigrid,krylov}.hpp) over the C ABI of include/hz_b200.h. Names, argument
+meaning and error classes follow the reference so callers (and the parity
+tests) read like the reference's own:
+
+    prob = HelmholtzProblem(ndim, n, h, m, omega, AttenuationField(base, ramp))
+    solver = HelmholtzSolver(prob, HelmholtzSolveOptions(method="MgFgmresW"))
+    X, report = solver.solve_block(B)          # B: [n][k] complex128
+
+Blocks are node-major [n][k] complex128 (BlockVec, inc/block.hpp:13-27), as
+numpy arrays (host; copies are part of the call) or torch CUDA tensors
+(device-resident; no copies). All compute runs in libhz_b200.so on the GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _native
+from ._native import hz_options, hz_report
+
+__all__ = [
+    "ValidationError", "ConvergenceError", "BreakdownError", "FactorizationError", "StateError",
+    "IoError", "CudaError", "NcclError", "AttenuationField", "HelmholtzProblem",
+    "HelmholtzSolveOptions", "CycleSpec", "HelmholtzSolver", "SolveReport", "solve_helmholtz",
+    "fwi_sensitivity_output", "kernel_launch_count", "device_count",
+]
+
+
+# ---------------------------------------------------------------- errors
+class HzError(RuntimeError):
+    code = -1
+
+
+class ValidationError(HzError, ValueError):  # seistomo::ValidationError
+    code = 1
+
+
+class ConvergenceError(HzError):  # seistomo::ConvergenceError{residual_history}
+    code = 2
+
+    def __init__(self, msg, residual_history=None):
+        super().__init__(msg)
+        self.residual_history = list(residual_history or [])
+
+
+class BreakdownError(HzError):
+    code = 3
+
+
+class FactorizationError(HzError):
+    code = 4
+
+
+class StateError(HzError):
+    code = 5
+
+
+class IoError(HzError):
+    code = 6
+
+
+class CudaError(HzError):
+    code = 7
+
+
+class NcclError(HzError):
+    code = 8
+
+
+_ERRORS = {c.code: c for c in (ValidationError, ConvergenceError, BreakdownError,
+                               FactorizationError, StateError, IoError, CudaError, NcclError)}
+
+
+def _check(status: int):
+    if status != 0:
+        msg = _native.lib().hz_last_error_message().decode(errors="replace")
+        raise _ERRORS.get(status, HzError)(msg)
+
+
+def kernel_launch_count() -> int:
+    return int(_native.lib().hz_kernel_launch_count())
+
+
+def device_count() -> int:
+    return int(_native.lib().hz_device_count())
+
+
+# ---------------------------------------------------------------- data
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+def _host_block(a, n: int) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    if a.ndim == 1:
+        a = a.reshape(n, 1)
+    if a.ndim != 2 or a.shape[0] != n:
+        raise ValidationError(f"block must be [n={n}][k] complex, got shape {a.shape}")
+    return a
+
+
+def _dev_block(t, n: int):
+    import torch
+    if t.dtype != torch.complex128 or not t.is_cuda:
+        raise ValidationError("device blocks must be complex128 CUDA tensors")
+    if t.dim() == 1:
+        t = t.reshape(n, 1)
+    if t.dim() != 2 or t.shape[0] != n:
+        raise ValidationError(f"block must be [n={n}][k], got {tuple(t.shape)}")
+    return t.contiguous()
+
+
+@dataclasses.dataclass
+class AttenuationField:
+    """AttenuationField (inc/attenuation.hpp:11-22): gamma(omega) = base + omega*ramp."""
+    base: float
+    ramp: np.ndarray
+
+
+@dataclasses.dataclass
+class SolveReport:
+    """seistomo::SolveReport (inc/krylov.hpp:19-40)."""
+    cycles: int
+    col_cycles: np.ndarray
+    rel_residual: np.ndarray
+    converged: np.ndarray
+    history: np.ndarray
+    wall_s: float
+    qr_factorizations: int
+    block_gram_products: int
+
+    def all_converged(self) -> bool:
+        return bool(len(self.converged) and np.all(self.converged))
+
+    def mean_col_cycles(self) -> float:
+        return float(np.mean(self.col_cycles)) if len(self.col_cycles) else 0.0
+
+
+class HelmholtzProblem:
+    """HelmholtzProblem (inc/helmholtz.hpp:19-57): A = Lap_h + w^2 (1 - i gamma/w) m,
+    5-point (2D) / 7-point (3D), truncated (Dirichlet) boundary rows."""
+
+    def __init__(self, ndim: int, n: Sequence[int], h: Sequence[float], m, omega: float,
+                 gamma: AttenuationField, allow_coarse_ppw: bool = False, device: int = 0):
+        n3 = list(n) + [1] * (3 - len(n))
+        h3 = list(h) + [1.0] * (3 - len(h))
+        self.ndim = int(ndim)
+        self.n = tuple(int(x) for x in n3)
+        if self.ndim == 2:
+            self.n = (self.n[0], self.n[1], 1)
+        self.h = tuple(float(x) for x in h3)
+        self.omega = float(omega)
+        self.num_nodes = self.n[0] * self.n[1] * self.n[2]
+        self.device = int(device)
+        m = np.ascontiguousarray(m, dtype=np.float64).reshape(-1)
+        ramp = np.ascontiguousarray(gamma.ramp, dtype=np.float64).reshape(-1)
+        if m.size != self.num_nodes or ramp.size != self.num_nodes:
+            raise ValidationError("model / attenuation size does not match grid")
+        self.m = m
+        self.gamma = AttenuationField(float(gamma.base), ramp)
+        nn = np.asarray(self.n, dtype=np.int64)
+        hh = np.asarray(self.h, dtype=np.float64)
+        out = C.c_void_p()
+        _check(_native.lib().hz_problem_create(self.ndim, nn.ctypes.data, hh.ctypes.data, m.ctypes.data,
+                                               self.omega, self.gamma.base, ramp.ctypes.data,
+                                               1 if allow_coarse_ppw else 0, self.device, C.byref(out)))
+        self._h = out
+
+    @classmethod
+    def from_config(cls, cfg, device: int = 0, allow_coarse_ppw: bool = False):
+        return cls(cfg.ndim, cfg.n, cfg.h, cfg.m, cfg.omega, AttenuationField(cfg.gamma_base, cfg.ramp),
+                   allow_coarse_ppw=allow_coarse_ppw, device=device)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _native.lib().hz_problem_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def points_per_wavelength(self) -> float:
+        v = C.c_double()
+        _check(_native.lib().hz_problem_ppw(self._h, C.byref(v)))
+        return float(v.value)
+
+    def gamma_factor(self) -> np.ndarray:
+        """(1 - i gamma/omega) per node (HelmholtzProblem::gamma_factor)."""
+        gam = self.gamma.base + self.omega * self.gamma.ramp
+        return 1.0 - 1j * (gam / self.omega)
+
+    def apply_block(self, u):
+        """v = A u (HelmholtzProblem::apply_block, src/helmholtz.cpp:71-100)."""
+        if _is_torch(u):
+            import torch
+            u = _dev_block(u, self.num_nodes)
+            out = torch.empty_like(u)
+            stream = torch.cuda.current_stream(u.device).cuda_stream
+            _check(_native.lib().hz_apply_block_device(self._h, self.num_nodes, u.shape[1], u.data_ptr(),
+                                                       out.data_ptr(), stream))
+            return out
+        u = _host_block(u, self.num_nodes)
+        out = np.empty_like(u)
+        _check(_native.lib().hz_apply_block(self._h, self.num_nodes, u.shape[1], u.ctypes.data,
+                                            out.ctypes.data))
+        return out
+
+    def point_source(self, x: Sequence[float], amplitude: complex = 1.0) -> np.ndarray:
+        """FV point source amp/prod(h) at the nearest node, ties to the lower
+        index (HelmholtzProblem::point_source, src/helmholtz.cpp:124-132;
+        RegularGrid::nearest_node, src/grid.cpp:46-55)."""
+        c = [0, 0, 0]
+        cell = 1.0
+        for a in range(self.ndim):
+            f = float(x[a]) / self.h[a]
+            lo, hi = -1e-9, (self.n[a] - 1) + 1e-9
+            if f < lo or f > hi:
+                raise ValidationError("point_source: position outside grid")
+            i = int(np.floor(f + 0.5))
+            if float(i) - f == 0.5:
+                i -= 1
+            c[a] = min(max(i, 0), self.n[a] - 1)
+            cell *= self.h[a]
+        q = np.zeros(self.num_nodes, dtype=np.complex128)
+        q[c[0] + self.n[0] * (c[1] + self.n[1] * c[2])] = amplitude / cell
+        return q
+
+
+_METHODS = {"MgBicgstab": 0, "MgFgmresW": 1, "MgFgmresK": 2, "DenseLuSmall": 3, "MgFgmres": 4,
+            "MgBicgstabCycle": 5}
+_KINDS = {"V": 0, "W": 1, "K": 2}
+
+
+@dataclasses.dataclass
+class CycleSpec:
+    """CycleSpec (inc/multigrid.hpp:17-23)."""
+    kind: str = "W"
+    pre: int = 2
+    post: int = 2
+    jacobi_weight: float = 0.8
+    k_inner: int = 2
+
+
+@dataclasses.dataclass
+class HelmholtzSolveOptions:
+    """HelmholtzSolveOptions (inc/helmholtz_solver.hpp:14-24). `method` adds
+    "MgFgmres" / "MgBicgstabCycle" (cycle kind taken from cycle.kind, the
+    SURVEY §3.3 composition) and `precond_precision` ("c128" | "c64")."""
+    method: str = "MgBicgstab"
+    tol: float = 1e-6
+    max_cycles: int = 200
+    nlevels: int = 3
+    shift_factor: float = 0.2
+    cycle: CycleSpec = dataclasses.field(default_factory=CycleSpec)
+    fgmres_restart: int = 5
+    dense_threshold: int = 3000
+    allow_coarse_ppw: bool = False
+    precond_precision: str = "c128"
+
+    def to_c(self) -> hz_options:
+        o = hz_options()
+        if self.method not in _METHODS:
+            raise ValidationError(f"unknown method {self.method}")
+        if self.cycle.kind not in _KINDS:
+            raise ValidationError(f"unknown cycle kind {self.cycle.kind}")
+        if self.precond_precision not in ("c128", "c64"):
+            raise ValidationError("precond_precision must be c128 or c64")
+        o.method = _METHODS[self.method]
+        o.tol = self.tol
+        o.max_cycles = self.max_cycles
+        o.nlevels = self.nlevels
+        o.shift_factor = self.shift_factor
+        o.cycle_kind = _KINDS[self.cycle.kind]
+        o.pre = self.cycle.pre
+        o.post = self.cycle.post
+        o.jacobi_weight = self.cycle.jacobi_weight
+        o.k_inner = self.cycle.k_inner
+        o.fgmres_restart = self.fgmres_restart
+        o.dense_threshold = self.dense_threshold
+        o.precond_precision = 0 if self.precond_precision == "c128" else 1
+        return o
+
+    @classmethod
+    def from_config(cls, cfg, **over):
+        kind = cfg.cycle
+        method = "MgFgmres" if cfg.method == "fgmres" else "MgBicgstabCycle"
+        o = cls(method=method, tol=cfg.tol, max_cycles=cfg.max_cycles, nlevels=cfg.nlevels,
+                shift_factor=cfg.shift, cycle=CycleSpec(kind, cfg.pre, cfg.post, cfg.jacobi_weight),
+                fgmres_restart=cfg.restart, precond_precision=cfg.precond_precision)
+        for k, v in over.items():
+            setattr(o, k, v)
+        return o
+
+
+class HelmholtzSolver:
+    """HelmholtzSolver (inc/helmholtz_solver.hpp:30-55): the multigrid
+    hierarchy is built once per (m, omega) on the GPU and reused for every
+    block of right-hand sides."""
+
+    def __init__(self, problem: HelmholtzProblem, options: Optional[HelmholtzSolveOptions] = None):
+        self.problem = problem
+        self.options = options or HelmholtzSolveOptions()
+        self._opts = self.options.to_c()
+        out = C.c_void_p()
+        _check(_native.lib().hz_solver_create(problem._h, C.byref(self._opts), C.byref(out)))
+        self._h = out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            try:
+                _native.lib().hz_solver_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def set_tolerance(self, tol: float):
+        self.options.tol = tol
+        _check(_native.lib().hz_solver_set_tolerance(self._h, tol))
+
+    def _report(self, k: int, cap: int):
+        cc = np.zeros(k, np.int32)
+        rr = np.zeros(k, np.float64)
+        cv = np.zeros(k, np.int32)
+        hist = np.zeros(cap, np.float64)
+        rep = hz_report()
+        rep.col_cycles = cc.ctypes.data_as(C.POINTER(C.c_int))
+        rep.rel_residual = rr.ctypes.data_as(C.POINTER(C.c_double))
+        rep.converged = cv.ctypes.data_as(C.POINTER(C.c_int))
+        rep.history = hist.ctypes.data_as(C.POINTER(C.c_double))
+        rep.history_cap = cap
+        return rep, (cc, rr, cv, hist)
+
+    @staticmethod
+    def _finish(rep, bufs) -> SolveReport:
+        cc, rr, cv, hist = bufs
+        return SolveReport(cycles=rep.cycles, col_cycles=cc.copy(), rel_residual=rr.copy(),
+                           converged=cv.astype(bool), history=hist[:min(rep.history_len, len(hist))].copy(),
+                           wall_s=rep.wall_s, qr_factorizations=rep.qr_factorizations,
+                           block_gram_products=rep.block_gram_products)
+
+    def solve_block(self, B, out=None) -> Tuple[object, SolveReport]:
+        """HelmholtzSolver::solve_block (src/helmholtz_solver.cpp:35-72)."""
+        n = self.problem.num_nodes
+        cap = self.options.max_cycles + 8
+        if _is_torch(B):
+            import torch
+            B = _dev_block(B, n)
+            X = out if out is not None else torch.empty_like(B)
+            rep, bufs = self._report(B.shape[1], cap)
+            torch.cuda.current_stream(B.device).synchronize()
+            _check(_native.lib().hz_solve_block_device(self._h, n, B.shape[1], B.data_ptr(), X.data_ptr(),
+                                                       C.byref(rep)))
+            return X, self._finish(rep, bufs)
+        B = _host_block(B, n)
+        X = out if out is not None else np.empty_like(B)
+        rep, bufs = self._report(B.shape[1], cap)
+        _check(_native.lib().hz_solve_block(self._h, n, B.shape[1], B.ctypes.data, X.ctypes.data,
+                                            C.byref(rep)))
+        return X, self._finish(rep, bufs)
+
+    def solve(self, rhs):
+        """HelmholtzSolver::solve (src/helmholtz_solver.cpp:74-79)."""
+        X, rep = self.solve_block(np.asarray(rhs).reshape(-1, 1))
+        return X[:, 0].copy(), rep
+
+    def cycle(self, b):
+        """One preconditioner application from x = 0 (out := 0;
+        MgHierarchy::cycle, src/helmholtz_solver.cpp:65-68)."""
+        n = self.problem.num_nodes
+        if _is_torch(b):
+            import torch
+            b = _dev_block(b, n)
+            x = torch.empty_like(b)
+            torch.cuda.current_stream(b.device).synchronize()
+            _check(_native.lib().hz_cycle_device(self._h, n, b.shape[1], b.data_ptr(), x.data_ptr()))
+            return x
+        b = _host_block(b, n)
+        x = np.empty_like(b)
+        _check(_native.lib().hz_cycle(self._h, n, b.shape[1], b.ctypes.data, x.ctypes.data))
+        return x
+
+    def num_levels(self) -> int:
+        v = C.c_int()
+        _check(_native.lib().hz_hierarchy_num_levels(self._h, C.byref(v)))
+        return int(v.value)
+
+    def level_dims(self, level: int):
+        d = np.zeros(3, np.int64)
+        _check(_native.lib().hz_hierarchy_level_dims(self._h, level, d.ctypes.data))
+        return tuple(int(x) for x in d)
+
+    def level_coefficients(self, level: int) -> np.ndarray:
+        """level 0: shifted centre [n]; level >= 1: Galerkin planes [3^ndim][n]."""
+        d = self.level_dims(level)
+        nn = d[0] * d[1] * d[2]
+        count = nn if level == 0 else nn * (27 if self.problem.ndim == 3 else 9)
+        out = np.empty(count, np.complex128)
+        _check(_native.lib().hz_hierarchy_level_coefficients(self._h, level, out.ctypes.data, count))
+        return out if level == 0 else out.reshape(-1, nn)
+
+    def coarse_solve(self, b) -> np.ndarray:
+        """MgHierarchy::coarse_solve (src/multigrid.cpp:114-117)."""
+        b = np.ascontiguousarray(b, dtype=np.complex128)
+        if b.ndim == 1:
+            b = b.reshape(-1, 1)
+        x = np.empty_like(b)
+        _check(_native.lib().hz_coarse_solve(self._h, b.shape[0], b.shape[1], b.ctypes.data, x.ctypes.data))
+        return x
+
+
+def solve_helmholtz(solver: HelmholtzSolver, rhs: List[np.ndarray], report: Optional[list] = None):
+    """solve_helmholtz (src/helmholtz_solver.cpp:81-93): one block solve,
+    ConvergenceError (with the residual history) if any column misses tol.
+    Returns the [n][k] solution block (Full storage)."""
+    B = np.stack([np.asarray(q, dtype=np.complex128).reshape(-1) for q in rhs], axis=1)
+    X, rep = solver.solve_block(B)
+    if not rep.all_converged():
+        raise ConvergenceError("helmholtz solve: tolerance not met within cycle cap", rep.history)
+    if report is not None:
+        report.append(rep)
+    return X
+
+
+def fwi_sensitivity_output(problem: HelmholtzProblem, U, L, g=None):
+    """sum_s fwi_sensitivity_output(problem, u_s, lambda_s)
+    (src/helmholtz_solver.cpp:103-111): g[i] = sum_s Re(-w^2 (1 - i gamma/w) u_s lambda_s).
+    Host numpy or device torch blocks; g accumulates when given."""
+    n = problem.num_nodes
+    if _is_torch(U):
+        import torch
+        U = _dev_block(U, n)
+        L = _dev_block(L, n)
+        acc = g is not None
+        if g is None:
+            g = torch.empty(n, dtype=torch.float64, device=U.device)
+        stream = torch.cuda.current_stream(U.device).cuda_stream
+        _check(_native.lib().hz_sensitivity_accumulate_device(problem._h, n, U.shape[1], U.data_ptr(),
+                                                              L.data_ptr(), g.data_ptr(), 1 if acc else 0,
+                                                              stream))
+        return g
+    U = _host_block(U, n)
+    L = _host_block(L, n)
+    acc = g is not None
+    if g is None:
+        g = np.empty(n, np.float64)
+    _check(_native.lib().hz_sensitivity_accumulate(problem._h, n, U.shape[1], U.ctypes.data, L.ctypes.data,
+                                                   g.ctypes.data, 1 if acc else 0))
+    return g

@@ -1,0 +1,85 @@
+"""ctypes binding of the C ABI in include/hz_b200.h (libhz_b200.so, in-tree).
+
+The library is the product: there is no Python or CPU fallback. Importing
+this module without the built library raises immediately; calling a compute
+entry point without a CUDA device raises CudaError (status HZ_CUDA).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhz_b200.so")
+
+# C-ABI symbols (include/hz_b200.h); tests check the library exports each one.
+EXPORTS = (
+    "hz_abi_version", "hz_last_error_message", "hz_device_count", "hz_options_default",
+    "hz_problem_create", "hz_problem_destroy", "hz_problem_ppw", "hz_problem_num_nodes",
+    "hz_apply_block", "hz_apply_block_device", "hz_solver_create", "hz_solver_destroy",
+    "hz_solver_set_tolerance", "hz_solve_block", "hz_solve_block_device", "hz_solve_helmholtz",
+    "hz_cycle", "hz_cycle_device", "hz_coarse_solve", "hz_hierarchy_num_levels",
+    "hz_hierarchy_level_dims", "hz_hierarchy_level_coefficients", "hz_sensitivity_accumulate",
+    "hz_sensitivity_accumulate_device", "hz_kernel_launch_count",
+)
+
+
+class hz_options(C.Structure):
+    _fields_ = [("method", C.c_int), ("tol", C.c_double), ("max_cycles", C.c_int),
+                ("nlevels", C.c_int), ("shift_factor", C.c_double), ("cycle_kind", C.c_int),
+                ("pre", C.c_int), ("post", C.c_int), ("jacobi_weight", C.c_double),
+                ("k_inner", C.c_int), ("fgmres_restart", C.c_int),
+                ("dense_threshold", C.c_int64), ("precond_precision", C.c_int)]
+
+
+class hz_report(C.Structure):
+    _fields_ = [("cycles", C.c_int), ("qr_factorizations", C.c_int),
+                ("block_gram_products", C.c_int64), ("wall_s", C.c_double),
+                ("history_len", C.c_int), ("col_cycles", C.POINTER(C.c_int)),
+                ("rel_residual", C.POINTER(C.c_double)), ("converged", C.POINTER(C.c_int)),
+                ("history", C.POINTER(C.c_double)), ("history_cap", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "or `python paper_1607_00968_b200/build_ext.py` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        L.hz_last_error_message.restype = C.c_char_p
+        L.hz_problem_num_nodes.restype = C.c_int64
+        L.hz_kernel_launch_count.restype = C.c_int64
+        vp, i64, dbl, i32 = C.c_void_p, C.c_int64, C.c_double, C.c_int
+        L.hz_problem_create.argtypes = [i32, vp, vp, vp, dbl, dbl, vp, i32, i32, C.POINTER(vp)]
+        L.hz_problem_destroy.argtypes = [vp]
+        L.hz_problem_ppw.argtypes = [vp, C.POINTER(dbl)]
+        L.hz_problem_num_nodes.argtypes = [vp]
+        L.hz_apply_block.argtypes = [vp, i64, i32, vp, vp]
+        L.hz_apply_block_device.argtypes = [vp, i64, i32, vp, vp, vp]
+        L.hz_solver_create.argtypes = [vp, C.POINTER(hz_options), C.POINTER(vp)]
+        L.hz_solver_destroy.argtypes = [vp]
+        L.hz_solver_set_tolerance.argtypes = [vp, dbl]
+        L.hz_solve_block.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report)]
+        L.hz_solve_block_device.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report)]
+        L.hz_solve_helmholtz.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report)]
+        L.hz_cycle.argtypes = [vp, i64, i32, vp, vp]
+        L.hz_cycle_device.argtypes = [vp, i64, i32, vp, vp]
+        L.hz_coarse_solve.argtypes = [vp, i64, i32, vp, vp]
+        L.hz_hierarchy_num_levels.argtypes = [vp, C.POINTER(i32)]
+        L.hz_hierarchy_level_dims.argtypes = [vp, i32, vp]
+        L.hz_hierarchy_level_coefficients.argtypes = [vp, i32, vp, i64]
+        L.hz_sensitivity_accumulate.argtypes = [vp, i64, i32, vp, vp, vp, i32]
+        L.hz_sensitivity_accumulate_device.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp]
+        L.hz_options_default.argtypes = [C.POINTER(hz_options)]
+        _lib = L
+    return _lib
+
+
+def loaded_path() -> str:
+    lib()
+    return LIB_PATH

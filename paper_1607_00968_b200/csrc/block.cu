@@ -1,0 +1,440 @@
+// Tall-skinny block kernels for the block Krylov methods (K6-K10) over
+// node-major [n][k] blocks: Gram products X^H Y, block updates Y -= X H,
+// column norms, Frobenius inner products and the block axpby
+// (inc/block.hpp:42-98, src/krylov.cpp:129-145).
+//
+// Reductions are deterministic two-stage: each CTA ("slot") writes a
+// private partial, and a second kernel sums the slots in fixed order -- no
+// floating-point atomics, so runs are bitwise reproducible.
+#include "kernels.hpp"
+
+namespace hz {
+
+namespace {
+
+constexpr int kBlk = 256;
+
+int slots_for(int64_t n) {
+  // ~4 CTAs per SM, at least 64 rows each
+  int64_t s = (n + 63) / 64;
+  if (s > 4 * kNumSMs) s = 4 * kNumSMs;
+  return int(s < 1 ? 1 : s);
+}
+
+// Register tile per thread over the k x k pair space.
+template <int TP, int TQ>
+struct PairTile {
+  static constexpr int P = TP, Q = TQ;
+};
+
+// CTA (i = blockIdx.x, slot = blockIdx.y) computes the slot's partial of
+// X_i^H Y over its row range. Thread t owns a TP x TQ tile of (p, q) pairs;
+// when k*k/(TP*TQ) < 256 the CTA splits into row groups reduced in smem.
+template <class T, int TP, int TQ>
+__global__ void __launch_bounds__(kBlk)
+multi_gram_kernel(int64_t n, int k, const BlockTab<T> X,
+                  const cplx_t<T>* __restrict__ Y, cplx_t<T>* __restrict__ partials, int nslots) {
+  using V = cplx_t<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* red = reinterpret_cast<V*>(smem_raw);
+  const int i = blockIdx.x, slot = blockIdx.y, nb = gridDim.x;
+  const V* __restrict__ Xi = X.p[i];
+  const int tp_count = (k + TP - 1) / TP, tq_count = (k + TQ - 1) / TQ;
+  const int tiles = tp_count * tq_count;
+  const int groups = max(1, kBlk / tiles);
+  const int tid = threadIdx.x;
+  const int g = tid / tiles, tile = tid - g * tiles;
+  const bool active = g < groups && tid < groups * tiles;
+  const int p0 = (tile / tq_count) * TP, q0 = (tile % tq_count) * TQ;
+  V acc[TP][TQ];
+#pragma unroll
+  for (int a = 0; a < TP; ++a)
+#pragma unroll
+    for (int b = 0; b < TQ; ++b) acc[a][b] = czero<V>();
+  const int64_t rows_per = (n + nslots - 1) / nslots;
+  const int64_t r0 = int64_t(slot) * rows_per, r1 = min(n, r0 + rows_per);
+  if (active) {
+    for (int64_t r = r0 + g; r < r1; r += groups) {
+      const V* xr = Xi + r * k;
+      const V* yr = Y + r * k;
+      V xv[TP], yv[TQ];
+#pragma unroll
+      for (int a = 0; a < TP; ++a) xv[a] = (p0 + a < k) ? __ldg(&xr[p0 + a]) : czero<V>();
+#pragma unroll
+      for (int b = 0; b < TQ; ++b) yv[b] = (q0 + b < k) ? __ldg(&yr[q0 + b]) : czero<V>();
+#pragma unroll
+      for (int a = 0; a < TP; ++a)
+#pragma unroll
+        for (int b = 0; b < TQ; ++b) acc[a][b] = cfmac(xv[a], yv[b], acc[a][b]);
+    }
+  }
+  // reduce row groups through smem in fixed group order
+  V* out = partials + (int64_t(slot) * nb + i) * k * k;
+  if (groups == 1) {
+    if (active) {
+#pragma unroll
+      for (int a = 0; a < TP; ++a)
+#pragma unroll
+        for (int b = 0; b < TQ; ++b)
+          if (p0 + a < k && q0 + b < k) out[(p0 + a) * k + q0 + b] = acc[a][b];
+    }
+    return;
+  }
+  // smem layout [groups][k*k]
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < TP; ++a)
+#pragma unroll
+      for (int b = 0; b < TQ; ++b)
+        if (p0 + a < k && q0 + b < k) red[g * k * k + (p0 + a) * k + q0 + b] = acc[a][b];
+  }
+  __syncthreads();
+  for (int e = tid; e < k * k; e += kBlk) {
+    V s = red[e];
+    for (int gg = 1; gg < groups; ++gg) s = cadd(s, red[gg * k * k + e]);
+    out[e] = s;
+  }
+}
+
+// out = (Yin ? Yin : 0) + sign * sum_i X_i H_i ; H_i row-major k x k.
+// Thread per (row, q) element; H_i staged in smem one block at a time.
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+multi_update_kernel(int64_t n, int k, int nb, const BlockTab<T> X,
+                    const cplx_t<T>* __restrict__ H, const cplx_t<T>* Yin, cplx_t<T>* Yout, T sign) {
+  using V = cplx_t<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* Hs = reinterpret_cast<V*>(smem_raw);  // [k][k]
+  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  const bool valid = e < n * k;
+  const int64_t r = valid ? e / k : 0;
+  const int q = valid ? int(e - r * k) : 0;
+  V acc = czero<V>();
+  for (int i = 0; i < nb; ++i) {
+    __syncthreads();
+    for (int t = threadIdx.x; t < k * k; t += kBlk) Hs[t] = H[int64_t(i) * k * k + t];
+    __syncthreads();
+    if (valid) {
+      const V* xr = X.p[i] + r * k;
+      for (int p = 0; p < k; ++p) acc = cfma(__ldg(&xr[p]), Hs[p * k + q], acc);
+    }
+  }
+  if (valid) {
+    V y = Yin ? Yin[e] : czero<V>();
+    y.x += sign * acc.x;
+    y.y += sign * acc.y;
+    Yout[e] = y;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+reduce_partials_kernel(int64_t count, int nslots, const cplx_t<T>* __restrict__ partials,
+                       cplx_t<T>* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  if (e >= count) return;
+  cplx_t<T> s = partials[e];
+  for (int t = 1; t < nslots; ++t) s = cadd(s, partials[int64_t(t) * count + e]);
+  out[e] = s;
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+reduce_real_kernel(int64_t count, int nslots, const T* __restrict__ partials, T* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  if (e >= count) return;
+  T s = partials[e];
+  for (int t = 1; t < nslots; ++t) s += partials[int64_t(t) * count + e];
+  out[e] = s;
+}
+
+// per-slot per-column sum |x|^2; thread handles column q = tid % k on rows
+// of its row group.
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+colnorm2_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ X, T* __restrict__ partials,
+                int nslots) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* red = reinterpret_cast<T*>(smem_raw);
+  const int slot = blockIdx.x;
+  const int groups = max(1, kBlk / k);
+  const int tid = threadIdx.x, g = tid / k, q = tid - g * k;
+  const bool active = g < groups;
+  const int64_t rows_per = (n + nslots - 1) / nslots;
+  const int64_t r0 = int64_t(slot) * rows_per, r1 = min(n, r0 + rows_per);
+  T acc[4] = {0, 0, 0, 0};  // k > 256 handled by striding q
+  const int qstride = kBlk;
+  if (k <= kBlk) {
+    if (active)
+      for (int64_t r = r0 + g; r < r1; r += groups) acc[0] += cabs2(__ldg(&X[r * k + q]));
+    red[tid] = active ? acc[0] : T(0);
+    __syncthreads();
+    if (tid < k) {
+      T s = red[tid];
+      for (int gg = 1; gg < groups; ++gg) s += red[gg * k + tid];
+      partials[int64_t(slot) * k + tid] = s;
+    }
+  } else {
+    for (int qq = tid; qq < k; qq += qstride) {
+      T s = 0;
+      for (int64_t r = r0; r < r1; ++r) s += cabs2(X[r * k + qq]);
+      partials[int64_t(slot) * k + qq] = s;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+axpby_kernel(int64_t count, cplx_t<T> a, cplx_t<T>* Y, cplx_t<T> b, const cplx_t<T>* X) {
+  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  if (e >= count) return;
+  Y[e] = cadd(cmul(a, Y[e]), cmul(b, X[e]));
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+bicgstab_update_kernel(int64_t count, cplx_t<T> omega, cplx_t<T>* __restrict__ X,
+                       const cplx_t<T>* __restrict__ ZS, cplx_t<T>* __restrict__ R,
+                       const cplx_t<T>* __restrict__ S, const cplx_t<T>* __restrict__ Tt) {
+  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  if (e >= count) return;
+  X[e] = cadd(X[e], cmul(omega, ZS[e]));
+  R[e] = csub(S[e], cmul(omega, Tt[e]));
+}
+
+// partial[slot] = (sum conj(T) S, sum conj(T) T)
+template <class T>
+__global__ void __launch_bounds__(kBlk)
+frob2_kernel(int64_t count, const cplx_t<T>* __restrict__ Tt, const cplx_t<T>* __restrict__ S,
+             cplx_t<T>* __restrict__ partials, int nslots) {
+  using V = cplx_t<T>;
+  __shared__ V red_a[kBlk], red_b[kBlk];
+  const int slot = blockIdx.x;
+  const int64_t per = (count + nslots - 1) / nslots;
+  const int64_t e0 = int64_t(slot) * per, e1 = min(count, e0 + per);
+  V a = czero<V>(), b = czero<V>();
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += kBlk) {
+    const V t = Tt[e];
+    a = cfmac(t, S[e], a);
+    b.x += cabs2(t);
+  }
+  red_a[threadIdx.x] = a;
+  red_b[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = kBlk / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      red_a[threadIdx.x] = cadd(red_a[threadIdx.x], red_a[threadIdx.x + o]);
+      red_b[threadIdx.x] = cadd(red_b[threadIdx.x], red_b[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    partials[2 * slot] = red_a[0];
+    partials[2 * slot + 1] = red_b[0];
+  }
+}
+
+// Single-CTA Cholesky G = R^H R (upper R, real positive diagonal) and R^{-1}.
+// flag = first column j whose pivot fails d_j > rel_tol^2 * G_jj (+1), else 0.
+template <class T>
+__global__ void __launch_bounds__(256)
+small_cholesky_kernel(int k, const cplx_t<T>* __restrict__ G, cplx_t<T>* __restrict__ R,
+                      cplx_t<T>* __restrict__ Rinv, int* flag, T rel_tol) {
+  using V = cplx_t<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* A = reinterpret_cast<V*>(smem_raw);  // [k][k]
+  __shared__ int fl;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < k * k; e += blockDim.x) A[e] = G[e];
+  if (tid == 0) fl = 0;
+  __syncthreads();
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) {
+      const T d = A[j * k + j].x;
+      const T g0 = G[j * k + j].x;
+      const bool dead = !(d > rel_tol * rel_tol * (g0 > T(0) ? g0 : T(1))) || !(d > T(0));
+      if (dead && fl == 0) fl = j + 1;
+      A[j * k + j] = dead ? czero<V>() : mk(sqrt(d), T(0));
+    }
+    __syncthreads();
+    const T piv = A[j * k + j].x;
+    const T inv = piv > T(0) ? T(1) / piv : T(0);  // collapsed column: zero row of R
+    for (int c = j + 1 + tid; c < k; c += blockDim.x) A[j * k + c] = cscale(inv, A[j * k + c]);
+    __syncthreads();
+    // trailing update A[a][c] -= conj(A[j][a]) A[j][c], j < a <= c
+    const int m = k - j - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int a = j + 1 + e / m, c = j + 1 + e % m;
+      if (c >= a) {
+        const V ra = A[j * k + a], rc = A[j * k + c];
+        A[a * k + c] = csub(A[a * k + c], cmulc(ra, rc));
+      }
+    }
+    __syncthreads();
+  }
+  // R = upper(A)
+  for (int e = tid; e < k * k; e += blockDim.x) {
+    const int a = e / k, c = e % k;
+    R[e] = c >= a ? A[e] : czero<V>();
+  }
+  __syncthreads();
+  // Rinv by back substitution, one column per thread
+  for (int c = tid; c < k; c += blockDim.x) {
+    for (int i = k - 1; i >= 0; --i) {
+      V s = (i == c) ? mk(T(1), T(0)) : czero<V>();
+      if (i <= c) {
+        for (int l = i + 1; l <= c; ++l) s = csub(s, cmul(A[i * k + l], Rinv[l * k + c]));
+        const T d = A[i * k + i].x;
+        Rinv[i * k + c] = (d > T(0) && A[c * k + c].x > T(0)) ? cscale(T(1) / d, s) : czero<V>();
+      } else {
+        Rinv[i * k + c] = czero<V>();
+      }
+    }
+  }
+  if (tid == 0) *flag = fl;
+}
+
+__global__ void __launch_bounds__(kBlk)
+sensitivity_kernel(int64_t n, int k, double w2, const double2* __restrict__ gf,
+                   const double2* __restrict__ U, const double2* __restrict__ L,
+                   double* __restrict__ g, int accumulate) {
+  const int64_t i = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  if (i >= n) return;
+  const double2 f = gf[i];
+  // reference per source: Re(-w2 * gf * u * lam), (-w2*gf) first
+  const double2 c = make_double2(-w2 * f.x, -w2 * f.y);
+  double s = accumulate ? g[i] : 0.0;
+  for (int q = 0; q < k; ++q) {
+    const double2 cu = cmul(c, U[i * k + q]);
+    s += cu.x * L[i * k + q].x - cu.y * L[i * k + q].y;
+  }
+  g[i] = s;
+}
+
+template <class T, int TP, int TQ>
+void gram_launch(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
+                 cplx_t<T>* partials, int nslots, cudaStream_t s) {
+  const int tiles = ((k + TP - 1) / TP) * ((k + TQ - 1) / TQ);
+  const int groups = std::max(1, kBlk / tiles);
+  const size_t smem = groups > 1 ? sizeof(cplx_t<T>) * size_t(groups) * k * k : 0;
+  auto kern = multi_gram_kernel<T, TP, TQ>;
+  if (smem > 48 * 1024)
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  dim3 grid(nb, nslots);
+  kern<<<grid, kBlk, smem, s>>>(n, k, X, Y, partials, nslots);
+}
+
+}  // namespace
+
+int gram_partial_slots(int64_t n, int k) {
+  (void)k;
+  return slots_for(n);
+}
+
+template <class T>
+void launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
+                       cplx_t<T>* partials, int nslots, cudaStream_t s) {
+  if (k > 64) throw HzError(kValidation, "block width k > 64 unsupported");
+  if (nb > kMaxBlocks) throw HzError(kValidation, "too many blocks in one Gram");
+  if (k <= 16)
+    gram_launch<T, 1, 1>(n, k, nb, X, Y, partials, nslots, s);
+  else if (k <= 32)
+    gram_launch<T, 2, 2>(n, k, nb, X, Y, partials, nslots, s);
+  else
+    gram_launch<T, 4, 4>(n, k, nb, X, Y, partials, nslots, s);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* H,
+                         const cplx_t<T>* Yin, cplx_t<T>* Yout, T sign, cudaStream_t s) {
+  const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
+  auto kern = multi_update_kernel<T>;
+  if (smem > 48 * 1024)
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<grid_for(n * k, kBlk), kBlk, smem, s>>>(n, k, nb, X, H, Yin, Yout, sign);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_reduce_partials(int64_t count, int nslots, const cplx_t<T>* partials, cplx_t<T>* out,
+                            cudaStream_t s) {
+  reduce_partials_kernel<T><<<grid_for(count, kBlk), kBlk, 0, s>>>(count, nslots, partials, out);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_colnorm2_partial(int64_t n, int k, const cplx_t<T>* X, T* partials, int nslots,
+                             cudaStream_t s) {
+  colnorm2_kernel<T><<<nslots, kBlk, sizeof(T) * kBlk, s>>>(n, k, X, partials, nslots);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_reduce_real(int64_t count, int nslots, const T* partials, T* out, cudaStream_t s) {
+  reduce_real_kernel<T><<<grid_for(count, kBlk), kBlk, 0, s>>>(count, nslots, partials, out);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_axpby(int64_t count, cplx_t<T> a, cplx_t<T>* Y, cplx_t<T> b, const cplx_t<T>* X,
+                  cudaStream_t s) {
+  axpby_kernel<T><<<grid_for(count, kBlk), kBlk, 0, s>>>(count, a, Y, b, X);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_bicgstab_update(int64_t count, cplx_t<T> omega, cplx_t<T>* X, const cplx_t<T>* ZS,
+                            cplx_t<T>* R, const cplx_t<T>* S, const cplx_t<T>* Tt, cudaStream_t s) {
+  bicgstab_update_kernel<T><<<grid_for(count, kBlk), kBlk, 0, s>>>(count, omega, X, ZS, R, S, Tt);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_frob2_partial(int64_t count, const cplx_t<T>* Tt, const cplx_t<T>* S,
+                          cplx_t<T>* partials, int nslots, cudaStream_t s) {
+  frob2_kernel<T><<<nslots, kBlk, 0, s>>>(count, Tt, S, partials, nslots);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* Rinv, int* flag,
+                           T rel_tol, cudaStream_t s) {
+  const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
+  auto kern = small_cholesky_kernel<T>;
+  if (smem > 48 * 1024)
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kern<<<1, 256, smem, s>>>(k, G, R, Rinv, flag, rel_tol);
+  HZ_LAUNCH_CHECK();
+}
+
+void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const double2* U,
+                        const double2* L, double* g, int accumulate, cudaStream_t s) {
+  sensitivity_kernel<<<grid_for(n, kBlk), kBlk, 0, s>>>(n, k, w2, gf, U, L, g, accumulate);
+  HZ_LAUNCH_CHECK();
+}
+
+#define HZ_INST(T)                                                                                 \
+  template void launch_multi_gram<T>(int64_t, int, int, const BlockTab<T>&, const cplx_t<T>*,     \
+                                     cplx_t<T>*, int, cudaStream_t);                              \
+  template void launch_multi_update<T>(int64_t, int, int, const BlockTab<T>&,                     \
+                                       const cplx_t<T>*, const cplx_t<T>*, cplx_t<T>*, T,         \
+                                       cudaStream_t);                                             \
+  template void launch_reduce_partials<T>(int64_t, int, const cplx_t<T>*, cplx_t<T>*,             \
+                                          cudaStream_t);                                          \
+  template void launch_colnorm2_partial<T>(int64_t, int, const cplx_t<T>*, T*, int, cudaStream_t); \
+  template void launch_reduce_real<T>(int64_t, int, const T*, T*, cudaStream_t);                  \
+  template void launch_axpby<T>(int64_t, cplx_t<T>, cplx_t<T>*, cplx_t<T>, const cplx_t<T>*,      \
+                                cudaStream_t);                                                    \
+  template void launch_bicgstab_update<T>(int64_t, cplx_t<T>, cplx_t<T>*, const cplx_t<T>*,       \
+                                          cplx_t<T>*, const cplx_t<T>*, const cplx_t<T>*,         \
+                                          cudaStream_t);                                          \
+  template void launch_frob2_partial<T>(int64_t, const cplx_t<T>*, const cplx_t<T>*, cplx_t<T>*,  \
+                                        int, cudaStream_t);                                       \
+  template void launch_small_cholesky<T>(int, const cplx_t<T>*, cplx_t<T>*, cplx_t<T>*, int*, T,  \
+                                         cudaStream_t);
+HZ_INST(double)
+HZ_INST(float)
+#undef HZ_INST
+
+}  // namespace hz

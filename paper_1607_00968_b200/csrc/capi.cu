@@ -1,0 +1,464 @@
+// extern "C" boundary (include/hz_b200.h). Maps the reference's exception
+// classes to status codes and owns the device-side state behind the opaque
+// hz_problem / hz_solver handles.
+#include <atomic>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "../../include/hz_b200.h"
+#include "solver.hpp"
+
+namespace hz {
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+}  // namespace hz
+
+using namespace hz;
+
+struct hz_problem {
+  std::shared_ptr<Problem> p;
+};
+
+struct hz_solver {
+  std::shared_ptr<Problem> prob;
+  hz_options opts{};
+  CycleSpec spec;
+  bool bicgstab = true;
+  bool dense = false;
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Hierarchy<double>> h64;
+  std::unique_ptr<Hierarchy<float>> h32;
+  std::unique_ptr<Fgmres<double>> fgm;
+  std::unique_ptr<Bicgstab> bicg;
+  DevBuf<double2> dB, dX;
+  DevBuf<float2> b32, x32;
+  // DenseLuSmall: explicit inverse of the unshifted operator
+  DevBuf<double2> dense_ainvT;
+  ~hz_solver() {
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return kOk;
+  } catch (const HzError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return kCuda;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return kState;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    throw HzError(kCuda, "no CUDA device visible (this library has no CPU fallback)");
+}
+
+void check_block(const Problem& p, int64_t n, int k) {
+  if (n != p.num_nodes()) throw HzError(kValidation, "helmholtz: block size does not match grid");
+  if (k < 1) throw HzError(kValidation, "helmholtz: block needs at least one column");
+  if (n * int64_t(k) >= (int64_t(1) << 32))
+    throw HzError(kValidation, "helmholtz: n*k too large for one device block");
+}
+
+void fill_report(const Report& r, int k, hz_report* out) {
+  if (!out) return;
+  out->cycles = r.cycles;
+  out->qr_factorizations = r.qr_factorizations;
+  out->block_gram_products = r.block_gram_products;
+  out->wall_s = r.wall_s;
+  out->history_len = int(r.history.size());
+  for (int j = 0; j < k; ++j) {
+    if (out->col_cycles) out->col_cycles[j] = r.col_cycles[j];
+    if (out->rel_residual) out->rel_residual[j] = r.rel_residual[j];
+    if (out->converged) out->converged[j] = r.converged[j];
+  }
+  if (out->history)
+    for (int i = 0; i < std::min<int>(out->history_cap, int(r.history.size())); ++i)
+      out->history[i] = r.history[i];
+}
+
+DevOp<double> make_op(hz_solver* s, int k) {
+  DevOp<double> op;
+  Problem* P = s->prob.get();
+  op.n = P->num_nodes();
+  op.apply = [P](const double2* in, double2* out, int kk, cudaStream_t st) {
+    launch_apply<double>(P->fine_op(kk), in, out, st);
+  };
+  if (s->opts.precond_precision == HZ_C64) {
+    const size_t e = size_t(op.n) * k;
+    s->b32.ensure(e);
+    s->x32.ensure(e);
+    op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
+      const int64_t cnt = s->prob->num_nodes() * kk;
+      launch_cast<float2, double2>(cnt, in, s->b32.get(), st);
+      s->h32->cycle(s->spec, kk, s->b32.get(), s->x32.get(), true, st);
+      launch_cast<double2, float2>(cnt, s->x32.get(), out, st);
+    };
+  } else {
+    op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
+      s->h64->cycle(s->spec, kk, in, out, true, st);
+    };
+  }
+  return op;
+}
+
+Report run_solve(hz_solver* s, int k, const double2* B, double2* X) {
+  Report rep;
+  if (s->dense) {
+    // DenseLuSmall (src/helmholtz_solver.cpp:38-59): direct solve, then the
+    // reported residuals
+    const int64_t n = s->prob->num_nodes();
+    launch_coarse_solve<double>(n, k, s->dense_ainvT.get(), B, X, s->stream);
+    BlockAlgebra<double> alg;
+    alg.ensure(n, k, 1);
+    DevBuf<double2> R(size_t(n) * k);
+    launch_apply<double>(s->prob->fine_op(k), X, R.get(), s->stream);
+    launch_axpby<double>(n * k, mk(-1.0, 0.0), R.get(), mk(1.0, 0.0), B, s->stream);
+    std::vector<double> rn, bn;
+    alg.col_norms(R.get(), rn, s->stream);
+    alg.col_norms(B, bn, s->stream);
+    rep.col_cycles.assign(k, 0);
+    for (int j = 0; j < k; ++j) {
+      const double b = bn[j] > 0 ? bn[j] : 1.0;
+      rep.rel_residual.push_back(rn[j] / b);
+      rep.converged.push_back(1);
+    }
+    return rep;
+  }
+  DevOp<double> op = make_op(s, k);
+  if (s->bicgstab) {
+    if (!s->bicg) s->bicg = std::make_unique<Bicgstab>();
+    return s->bicg->solve(op, k, B, X, s->opts.tol, s->opts.max_cycles, s->stream);
+  }
+  if (!s->fgm) s->fgm = std::make_unique<Fgmres<double>>();
+  return s->fgm->solve(op, k, B, X, s->opts.fgmres_restart, s->opts.tol, s->opts.max_cycles,
+                       s->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+int hz_abi_version(void) { return HZ_ABI_VERSION; }
+const char* hz_last_error_message(void) { return g_err.c_str(); }
+int hz_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+int64_t hz_kernel_launch_count(void) { return g_launches.load(); }
+
+void hz_options_default(hz_options* o) {
+  if (!o) return;
+  o->method = HZ_METHOD_MG_BICGSTAB;
+  o->tol = 1e-6;
+  o->max_cycles = 200;
+  o->nlevels = 3;
+  o->shift_factor = 0.2;
+  o->cycle_kind = HZ_CYCLE_W;
+  o->pre = 2;
+  o->post = 2;
+  o->jacobi_weight = 0.8;
+  o->k_inner = 2;
+  o->fgmres_restart = 5;
+  o->dense_threshold = 3000;
+  o->precond_precision = HZ_C128;
+}
+
+int hz_problem_create(int ndim, const int64_t n[3], const double h[3], const double* m,
+                      double omega, double gamma_base, const double* ramp, int allow_coarse_ppw,
+                      int device, hz_problem** out) {
+  return guarded([&] {
+    if (!out || !n || !h) throw HzError(kValidation, "hz_problem_create: null argument");
+    require_device();
+    DeviceGuard dg(device);
+    auto* hp = new hz_problem;
+    try {
+      hp->p = std::make_shared<Problem>(ndim, n, h, m, omega, gamma_base, ramp, allow_coarse_ppw != 0,
+                                        device);
+    } catch (...) {
+      delete hp;
+      throw;
+    }
+    *out = hp;
+  });
+}
+
+int hz_problem_destroy(hz_problem* p) {
+  return guarded([&] {
+    if (p) {
+      DeviceGuard dg(p->p->device);
+      delete p;
+    }
+  });
+}
+
+int hz_problem_ppw(const hz_problem* p, double* ppw) {
+  return guarded([&] {
+    if (!p || !ppw) throw HzError(kValidation, "null argument");
+    *ppw = p->p->points_per_wavelength();
+  });
+}
+
+int64_t hz_problem_num_nodes(const hz_problem* p) { return p ? p->p->num_nodes() : 0; }
+
+int hz_apply_block_device(hz_problem* p, int64_t n, int k, const void* u, void* out, void* stream) {
+  return guarded([&] {
+    if (!p) throw HzError(kValidation, "null problem");
+    check_block(*p->p, n, k);
+    DeviceGuard dg(p->p->device);
+    launch_apply<double>(p->p->fine_op(k), static_cast<const double2*>(u), static_cast<double2*>(out),
+                         static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hz_apply_block(hz_problem* p, int64_t n, int k, const double* u, double* out) {
+  return guarded([&] {
+    if (!p || !u || !out) throw HzError(kValidation, "null argument");
+    check_block(*p->p, n, k);
+    DeviceGuard dg(p->p->device);
+    const size_t e = size_t(n) * k;
+    DevBuf<double2> du(e), dv(e);
+    HZ_CUDA(cudaMemcpy(du.get(), u, e * sizeof(double2), cudaMemcpyHostToDevice));
+    launch_apply<double>(p->p->fine_op(k), du.get(), dv.get(), nullptr);
+    HZ_CUDA(cudaMemcpy(out, dv.get(), e * sizeof(double2), cudaMemcpyDeviceToHost));
+  });
+}
+
+int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** out) {
+  return guarded([&] {
+    if (!p || !out) throw HzError(kValidation, "hz_solver_create: null argument");
+    DeviceGuard dg(p->p->device);
+    auto s = std::make_unique<hz_solver>();
+    s->prob = p->p;
+    if (opts)
+      s->opts = *opts;
+    else
+      hz_options_default(&s->opts);
+    const hz_options& o = s->opts;
+    if (o.precond_precision != HZ_C128 && o.precond_precision != HZ_C64)
+      throw HzError(kValidation, "precond_precision must be HZ_C128 or HZ_C64");
+    HZ_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    s->spec.pre = o.pre;
+    s->spec.post = o.post;
+    s->spec.jacobi_weight = o.jacobi_weight;
+    s->spec.k_inner = o.k_inner;
+    if (o.pre < 0 || o.post < 0) throw HzError(kValidation, "relaxation counts must be >= 0");
+    switch (o.method) {  // src/helmholtz_solver.cpp:19-29
+      case HZ_METHOD_MG_BICGSTAB:
+        s->spec.kind = CycleKind::W;
+        s->bicgstab = true;
+        break;
+      case HZ_METHOD_MG_FGMRES_W:
+        s->spec.kind = CycleKind::W;
+        s->bicgstab = false;
+        break;
+      case HZ_METHOD_MG_FGMRES_K:
+        s->spec.kind = CycleKind::K;
+        s->bicgstab = false;
+        break;
+      case HZ_METHOD_MG_FGMRES:
+        s->spec.kind = static_cast<CycleKind>(o.cycle_kind);
+        s->bicgstab = false;
+        break;
+      case HZ_METHOD_MG_BICGSTAB_CYCLE:
+        s->spec.kind = static_cast<CycleKind>(o.cycle_kind);
+        s->bicgstab = true;
+        break;
+      case HZ_METHOD_DENSE_LU_SMALL:
+        s->dense = true;
+        break;
+      default:
+        throw HzError(kValidation, "unknown method");
+    }
+    if (o.cycle_kind < 0 || o.cycle_kind > 2) throw HzError(kValidation, "unknown cycle kind");
+    const Problem& P = *s->prob;
+    if (s->dense) {
+      const int64_t n = P.num_nodes();
+      if (n > o.dense_threshold)
+        throw HzError(kValidation, "dense_lu_small: grid has " + std::to_string(n) +
+                                       " nodes, above the threshold " + std::to_string(o.dense_threshold));
+      s->dense_ainvT = dense_inverse(P, s->stream);
+      *out = s.release();
+      return;
+    }
+    s->h64 = Hierarchy<double>::build(P, o.nlevels, o.shift_factor, s->stream);
+    if (o.precond_precision == HZ_C64) s->h32 = Hierarchy<float>::rounded(*s->h64, s->stream);
+    *out = s.release();
+  });
+}
+
+int hz_solver_destroy(hz_solver* s) {
+  return guarded([&] {
+    if (s) {
+      DeviceGuard dg(s->prob->device);
+      delete s;
+    }
+  });
+}
+
+int hz_solver_set_tolerance(hz_solver* s, double tol) {
+  return guarded([&] {
+    if (!s) throw HzError(kValidation, "null solver");
+    s->opts.tol = tol;
+  });
+}
+
+int hz_solve_block_device(hz_solver* s, int64_t n, int k, const void* B, void* X, hz_report* rep) {
+  return guarded([&] {
+    if (!s || !B || !X) throw HzError(kValidation, "null argument");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    Report r = run_solve(s, k, static_cast<const double2*>(B), static_cast<double2*>(X));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+  });
+}
+
+int hz_solve_block(hz_solver* s, int64_t n, int k, const double* B, double* X, hz_report* rep) {
+  return guarded([&] {
+    if (!s || !B || !X) throw HzError(kValidation, "null argument");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    const size_t e = size_t(n) * k;
+    s->dB.ensure(e);
+    s->dX.ensure(e);
+    HZ_CUDA(cudaMemcpyAsync(s->dB.get(), B, e * sizeof(double2), cudaMemcpyHostToDevice, s->stream));
+    Report r = run_solve(s, k, s->dB.get(), s->dX.get());
+    HZ_CUDA(cudaMemcpyAsync(X, s->dX.get(), e * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+  });
+}
+
+int hz_solve_helmholtz(hz_solver* s, int64_t n, int k, const double* B, double* X, hz_report* rep) {
+  int st = hz_solve_block(s, n, k, B, X, rep);
+  if (st != HZ_OK) return st;
+  if (rep && rep->converged)
+    for (int j = 0; j < k; ++j)
+      if (!rep->converged[j]) {
+        g_err = "helmholtz solve: tolerance not met within cycle cap";
+        return HZ_CONVERGENCE;
+      }
+  return HZ_OK;
+}
+
+int hz_cycle_device(hz_solver* s, int64_t n, int k, const void* b, void* x) {
+  return guarded([&] {
+    if (!s || !b || !x) throw HzError(kValidation, "null argument");
+    if (s->dense) throw HzError(kState, "dense solver has no multigrid cycle");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    DevOp<double> op = make_op(s, k);
+    op.prec(static_cast<const double2*>(b), static_cast<double2*>(x), k, s->stream);
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int hz_cycle(hz_solver* s, int64_t n, int k, const double* b, double* x) {
+  return guarded([&] {
+    if (!s || !b || !x) throw HzError(kValidation, "null argument");
+    if (s->dense) throw HzError(kState, "dense solver has no multigrid cycle");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    const size_t e = size_t(n) * k;
+    s->dB.ensure(e);
+    s->dX.ensure(e);
+    HZ_CUDA(cudaMemcpyAsync(s->dB.get(), b, e * sizeof(double2), cudaMemcpyHostToDevice, s->stream));
+    DevOp<double> op = make_op(s, k);
+    op.prec(s->dB.get(), s->dX.get(), k, s->stream);
+    HZ_CUDA(cudaMemcpyAsync(x, s->dX.get(), e * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int hz_coarse_solve(hz_solver* s, int64_t nc, int k, const double* b, double* x) {
+  return guarded([&] {
+    if (!s || !b || !x) throw HzError(kValidation, "null argument");
+    if (!s->h64) throw HzError(kState, "no hierarchy");
+    if (nc != s->h64->coarse_n()) throw HzError(kValidation, "coarse size mismatch");
+    DeviceGuard dg(s->prob->device);
+    const size_t e = size_t(nc) * k;
+    DevBuf<double2> db(e), dx(e);
+    HZ_CUDA(cudaMemcpyAsync(db.get(), b, e * sizeof(double2), cudaMemcpyHostToDevice, s->stream));
+    s->h64->coarse_solve(k, db.get(), dx.get(), s->stream);
+    HZ_CUDA(cudaMemcpyAsync(x, dx.get(), e * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+  });
+}
+
+int hz_hierarchy_num_levels(const hz_solver* s, int* nlevels) {
+  return guarded([&] {
+    if (!s || !nlevels) throw HzError(kValidation, "null argument");
+    *nlevels = s->h64 ? s->h64->num_levels() : 0;
+  });
+}
+
+int hz_hierarchy_level_dims(const hz_solver* s, int level, int64_t dims[3]) {
+  return guarded([&] {
+    if (!s || !dims || !s->h64) throw HzError(kValidation, "null argument");
+    if (level < 0 || level >= s->h64->num_levels()) throw HzError(kValidation, "level out of range");
+    for (int a = 0; a < 3; ++a) dims[a] = s->h64->level(level).dims[a];
+  });
+}
+
+int hz_hierarchy_level_coefficients(const hz_solver* s, int level, double* out, int64_t count) {
+  return guarded([&] {
+    if (!s || !out || !s->h64) throw HzError(kValidation, "null argument");
+    if (level < 0 || level >= s->h64->num_levels()) throw HzError(kValidation, "level out of range");
+    DeviceGuard dg(s->prob->device);
+    std::vector<cplx> c;
+    s->h64->download_level(level, c);
+    if (count != int64_t(c.size())) throw HzError(kValidation, "coefficient count mismatch");
+    std::memcpy(out, c.data(), c.size() * sizeof(cplx));
+  });
+}
+
+int hz_sensitivity_accumulate_device(hz_problem* p, int64_t n, int k, const void* U, const void* L,
+                                     double* g, int accumulate, void* stream) {
+  return guarded([&] {
+    if (!p || !U || !L || !g) throw HzError(kValidation, "null argument");
+    check_block(*p->p, n, k);
+    DeviceGuard dg(p->p->device);
+    launch_sensitivity(n, k, p->p->omega * p->p->omega, p->p->d_gf.get(),
+                       static_cast<const double2*>(U), static_cast<const double2*>(L), g, accumulate,
+                       static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hz_sensitivity_accumulate(hz_problem* p, int64_t n, int k, const double* U, const double* L,
+                              double* g, int accumulate) {
+  return guarded([&] {
+    if (!p || !U || !L || !g) throw HzError(kValidation, "null argument");
+    check_block(*p->p, n, k);
+    DeviceGuard dg(p->p->device);
+    const size_t e = size_t(n) * k;
+    DevBuf<double2> du(e), dl(e);
+    DevBuf<double> dg_(n);
+    HZ_CUDA(cudaMemcpy(du.get(), U, e * sizeof(double2), cudaMemcpyHostToDevice));
+    HZ_CUDA(cudaMemcpy(dl.get(), L, e * sizeof(double2), cudaMemcpyHostToDevice));
+    if (accumulate) HZ_CUDA(cudaMemcpy(dg_.get(), g, n * sizeof(double), cudaMemcpyHostToDevice));
+    launch_sensitivity(n, k, p->p->omega * p->p->omega, p->p->d_gf.get(), du.get(), dl.get(),
+                       dg_.get(), accumulate, nullptr);
+    HZ_CUDA(cudaMemcpy(g, dg_.get(), n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

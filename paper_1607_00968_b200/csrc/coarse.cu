@@ -1,0 +1,178 @@
+// Coarsest-level direct solve (K5; MgHierarchy::coarse_solve,
+// src/multigrid.cpp:114-117 -> BandedLU::solve, src/dense.cpp:39-61).
+//
+// The reference runs a sequential banded forward/back substitution per
+// column on every cycle. On the GPU that is a latency-bound chain of 2*n_c
+// dependent steps, so the hierarchy instead forms A_c^{-1} ONCE at setup from
+// the same pivoted banded LU factors (one warp per identity column), and every
+// cycle applies it as one bandwidth-bound dense pass: n_c^2 complex reads.
+#include "kernels.hpp"
+
+namespace hz {
+
+namespace {
+
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  // Smith's algorithm (robust against overflow), as libgcc's __divdc3
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, den = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+  }
+  const double r = b.x / b.y, den = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+
+// ab: gbtrf-style band storage, at(i, j) = ab[(kl + ku + i - j) + j * ld]
+// (inc/dense.hpp:207-208). One warp solves A x = e_c for column c.
+__global__ void __launch_bounds__(128)
+banded_inverse_kernel(int64_t n, int64_t kl, int64_t ku, int64_t ld, const double2* __restrict__ ab,
+                      const int64_t* __restrict__ piv, double2* __restrict__ ainvT) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (c >= n) return;
+  double2* x = ainvT + c * n;
+  for (int64_t i = lane; i < n; i += 32) x[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+  __syncwarp();
+  auto at = [&](int64_t i, int64_t j) { return ab[(kl + ku + i - j) + j * ld]; };
+  // forward: row interchanges + unit-lower elimination (src/dense.cpp:46-52)
+  for (int64_t k = 0; k < n; ++k) {
+    const int64_t p = piv[k];
+    if (p != k) {
+      if (lane == 0) {
+        const double2 t = x[k];
+        x[k] = x[p];
+        x[p] = t;
+      }
+      __syncwarp();
+    }
+    const double2 bk = x[k];
+    if (bk.x != 0.0 || bk.y != 0.0) {
+      const int64_t imax = min(n - 1, k + kl);
+      for (int64_t i = k + 1 + lane; i <= imax; i += 32) {
+        const double2 l = at(i, k);
+        double2 xi = x[i];
+        xi.x -= l.x * bk.x - l.y * bk.y;
+        xi.y -= l.x * bk.y + l.y * bk.x;
+        x[i] = xi;
+      }
+    }
+    __syncwarp();
+  }
+  // backward: upper solve (src/dense.cpp:53-58)
+  for (int64_t k = n - 1; k >= 0; --k) {
+    const int64_t jmax = min(n - 1, k + kl + ku);
+    double sx = 0.0, sy = 0.0;
+    for (int64_t j = k + 1 + lane; j <= jmax; j += 32) {
+      const double2 u = at(k, j);
+      const double2 xj = x[j];
+      sx += u.x * xj.x - u.y * xj.y;
+      sy += u.x * xj.y + u.y * xj.x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sx += __shfl_xor_sync(0xffffffffu, sx, o);
+      sy += __shfl_xor_sync(0xffffffffu, sy, o);
+    }
+    if (lane == 0) {
+      const double2 v = make_double2(x[k].x - sx, x[k].y - sy);
+      x[k] = cdiv(v, at(k, k));
+    }
+    __syncwarp();
+  }
+}
+
+// X[i][q] = sum_l ainvT[l][i] B[l][q]. CTA = TI output rows x all k columns;
+// ainvT is streamed once (coalesced TI-wide row segments), B chunks come
+// from L2.
+template <class T, int TI, int TL>
+__global__ void __launch_bounds__(256)
+coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT,
+                    const cplx_t<T>* __restrict__ b, cplx_t<T>* __restrict__ x) {
+  using V = cplx_t<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* As = reinterpret_cast<V*>(smem_raw);  // [TL][TI]
+  V* Bs = As + TL * TI;                    // [TL][k]
+  const int64_t i0 = int64_t(blockIdx.x) * TI;
+  const int nout = TI * k;
+  constexpr int kMaxPer = 16;  // TI*k <= 256*16
+  V acc[kMaxPer];
+#pragma unroll
+  for (int t = 0; t < kMaxPer; ++t) acc[t] = czero<V>();
+  for (int64_t l0 = 0; l0 < n; l0 += TL) {
+    const int tl = (n - l0) < TL ? int(n - l0) : TL;
+    for (int e = threadIdx.x; e < TL * TI; e += 256) {
+      const int l = e / TI, i = e % TI;
+      As[e] = (l < tl && i0 + i < n) ? ainvT[(l0 + l) * n + i0 + i] : czero<V>();
+    }
+    for (int e = threadIdx.x; e < TL * k; e += 256) {
+      const int l = e / k;
+      Bs[e] = l < tl ? b[(l0 + l) * k + (e - l * k)] : czero<V>();
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < kMaxPer; ++t) {
+      const int o = threadIdx.x + t * 256;
+      if (o < nout) {
+        const int i = o / k, q = o - i * k;
+        V a = acc[t];
+        for (int l = 0; l < TL; ++l) a = cfma(As[l * TI + i], Bs[l * k + q], a);
+        acc[t] = a;
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int t = 0; t < kMaxPer; ++t) {
+    const int o = threadIdx.x + t * 256;
+    if (o < nout) {
+      const int i = o / k, q = o - i * k;
+      if (i0 + i < n) x[(i0 + i) * k + q] = acc[t];
+    }
+  }
+}
+
+}  // namespace
+
+void launch_banded_inverse(int64_t n, int64_t kl, int64_t ku, int64_t ld, const double2* ab,
+                           const int64_t* piv, double2* ainvT, cudaStream_t s) {
+  banded_inverse_kernel<<<grid_for(n, 4), 128, 0, s>>>(n, kl, ku, ld, ab, piv, ainvT);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
+                         cplx_t<T>* x, cudaStream_t s) {
+  using V = cplx_t<T>;
+  constexpr int TL = 32;
+  if (k > 256) throw HzError(kValidation, "coarse solve: k > 256 unsupported");
+  // TI*k <= 4096 outputs per CTA (16 per thread)
+  int ti = 16;
+  if (k > 64) ti = 4096 / k >= 16 ? 16 : (4096 / k >= 8 ? 8 : (4096 / k >= 4 ? 4 : 1));
+  const size_t smem = sizeof(V) * (TL * 16 + TL * size_t(k));
+  const int grid = grid_for(n, ti);
+  if (ti == 16) {
+    auto kern = coarse_solve_kernel<T, 16, TL>;
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
+  } else if (ti == 8) {
+    auto kern = coarse_solve_kernel<T, 8, TL>;
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
+  } else if (ti == 4) {
+    auto kern = coarse_solve_kernel<T, 4, TL>;
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
+  } else {
+    auto kern = coarse_solve_kernel<T, 1, TL>;
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
+  }
+  HZ_LAUNCH_CHECK();
+}
+
+template void launch_coarse_solve<double>(int64_t, int, const double2*, const double2*, double2*,
+                                          cudaStream_t);
+template void launch_coarse_solve<float>(int64_t, int, const float2*, const float2*, float2*,
+                                         cudaStream_t);
+
+}  // namespace hz

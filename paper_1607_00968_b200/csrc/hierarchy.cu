@@ -1,0 +1,459 @@
+// Problem setup and the shifted-Laplacian Galerkin multigrid hierarchy.
+//
+// Setup arithmetic that the reference does on the host (mass, shifted
+// centre, Jacobi diagonal inverse, banded LU of the coarsest operator) is
+// restated here with std::complex<double> in the reference's evaluation
+// order, so these arrays are bitwise equal to the reference's; the Galerkin
+// planes are formed on the GPU in the reference's summation order (exact
+// power-of-two weights), so they are bitwise equal too (tests pin this).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "solver.hpp"
+
+namespace hz {
+
+// ------------------------------------------------------------------ Problem
+Problem::Problem(int ndim_, const int64_t* n_, const double* h_, const double* m_, double omega_,
+                 double gamma_base_, const double* ramp_, bool allow_coarse, int device_)
+    : ndim(ndim_), omega(omega_), gamma_base(gamma_base_), device(device_) {
+  // RegularGrid ctor (src/grid.cpp:10-27)
+  if (ndim != 2 && ndim != 3) throw HzError(kValidation, "grid: ndim must be 2 or 3");
+  for (int a = 0; a < 3; ++a) {
+    n[a] = n_[a];
+    h[a] = h_[a];
+  }
+  if (ndim == 2) {
+    n[2] = 1;
+    h[2] = 1.0;
+  }
+  for (int a = 0; a < ndim; ++a) {
+    if (n[a] < 3) throw HzError(kValidation, "grid: axis " + std::to_string(a) + " needs at least 3 nodes");
+    if (!(h[a] > 0.0))
+      throw HzError(kValidation, "grid: spacing on axis " + std::to_string(a) + " must be positive");
+  }
+  const int64_t nn = num_nodes();
+  if (nn * 64 >= (int64_t(1) << 32))
+    throw HzError(kValidation, "grid: node count too large for one device block (use slabs)");
+  if (!m_ || !ramp_) throw HzError(kValidation, "helmholtz: null model or attenuation");
+  m.assign(m_, m_ + nn);
+  ramp.assign(ramp_, ramp_ + nn);
+  for (double x : m)  // SlownessSquaredModel (src/model.cpp:13-19)
+    if (!(x > 0.0)) throw HzError(kValidation, "model: slowness-squared values must be positive");
+  // HelmholtzProblem ctor (src/helmholtz.cpp:16-38)
+  if (!(omega > 0.0)) throw HzError(kValidation, "helmholtz: omega must be positive");
+  const double ppw = points_per_wavelength();
+  if (ppw < 10.0 - 1e-12 && !allow_coarse)
+    throw HzError(kValidation, "helmholtz: " + std::to_string(ppw) +
+                                   " grid points per wavelength (need >= 10); pass allow_coarse to override");
+  center_lap = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    inv_h2[k] = (n[k] > 1) ? 1.0 / (h[k] * h[k]) : 0.0;
+    center_lap -= 2.0 * inv_h2[k];
+  }
+  mass.resize(nn);
+  gamma_factor.resize(nn);
+  std::vector<cplx> center(nn);
+  for (int64_t i = 0; i < nn; ++i) {
+    const double gam = gamma_base + omega * ramp[i];  // AttenuationField::gamma_at
+    gamma_factor[i] = cplx(1.0, -gam / omega);
+    mass[i] = omega * omega * gamma_factor[i] * m[i];
+    center[i] = center_lap + mass[i];  // apply_block centre (src/helmholtz.cpp:84)
+  }
+  DeviceGuard dg(device);
+  d_center.alloc(nn);
+  d_gf.alloc(nn);
+  HZ_CUDA(cudaMemcpy(d_center.get(), center.data(), nn * sizeof(double2), cudaMemcpyHostToDevice));
+  HZ_CUDA(cudaMemcpy(d_gf.get(), gamma_factor.data(), nn * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
+double Problem::min_h() const {
+  double mh = h[0];
+  for (int a = 1; a < ndim; ++a) mh = std::min(mh, h[a]);
+  return mh;
+}
+
+double Problem::points_per_wavelength() const {
+  const double smax = std::sqrt(*std::max_element(m.begin(), m.end()));
+  return 2.0 * M_PI / (omega * smax * min_h());
+}
+
+std::vector<cplx> Problem::shifted_center(double shift) const {
+  const int64_t nn = num_nodes();
+  std::vector<cplx> c(nn);
+  const cplx shift_term(0.0, -shift * omega * omega);
+  for (int64_t i = 0; i < nn; ++i) c[i] = center_lap + mass[i] + shift_term * m[i];
+  return c;
+}
+
+LevelOp<double> Problem::fine_op(int k) const {
+  LevelOp<double> op;
+  op.kind = kFine;
+  op.ndim = ndim;
+  op.g = LevelGeom(n[0], n[1], n[2], k);
+  op.center = d_center.get();
+  for (int a = 0; a < 3; ++a) op.w[a] = inv_h2[a];
+  return op;
+}
+
+// ------------------------------------------------------------------ helpers
+namespace {
+
+// coarsen_dims (src/multigrid.cpp:11-25)
+std::array<int64_t, 3> coarsen(const std::array<int64_t, 3>& d) {
+  std::array<int64_t, 3> out = d;
+  for (int k = 0; k < 3; ++k) {
+    if (d[k] <= 1) continue;
+    if (d[k] % 2 == 0)
+      throw HzError(kValidation, "multigrid: axis " + std::to_string(k) + " has even node count " +
+                                     std::to_string(d[k]) + "; not coarsenable");
+    const int64_t nc = (d[k] - 1) / 2 + 1;
+    if (nc < 3)
+      throw HzError(kValidation, "multigrid: axis " + std::to_string(k) +
+                                     " too small to coarsen (coarse count " + std::to_string(nc) + ")");
+    out[k] = nc;
+  }
+  return out;
+}
+
+std::vector<cplx> invert_diag(const std::vector<cplx>& d) {
+  std::vector<cplx> inv(d.size());
+  for (size_t i = 0; i < d.size(); ++i) {
+    if (d[i] == cplx{}) throw HzError(kFactorization, "multigrid: zero diagonal entry");
+    inv[i] = cplx{1} / d[i];
+  }
+  return inv;
+}
+
+// BandedLU::factor / factor_inplace restated (inc/dense.hpp:179-216,
+// src/dense.cpp:9-37): gbtrf-style row pivoting within kl subdiagonals.
+struct BandedFactor {
+  int64_t n = 0, kl = 0, ku = 0, ld = 0;
+  std::vector<cplx> ab;
+  std::vector<int64_t> piv;
+  cplx& at(int64_t i, int64_t j) { return ab[(kl + ku + i - j) + j * ld]; }
+  void factor() {
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t imax = std::min(n - 1, k + kl);
+      int64_t p = k;
+      double best = std::norm(at(k, k));
+      for (int64_t i = k + 1; i <= imax; ++i) {
+        const double v = std::norm(at(i, k));
+        if (v > best) {
+          best = v;
+          p = i;
+        }
+      }
+      if (!(best > 0.0)) throw HzError(kFactorization, "banded LU: singular pivot at " + std::to_string(k));
+      piv[k] = p;
+      const int64_t jmax = std::min(n - 1, k + kl + ku);
+      if (p != k)
+        for (int64_t j = k; j <= jmax; ++j) std::swap(at(k, j), at(p, j));
+      const cplx inv = cplx{1} / at(k, k);
+      for (int64_t i = k + 1; i <= imax; ++i) {
+        const cplx l = at(i, k) * inv;
+        at(i, k) = l;
+        if (l != cplx{})
+          for (int64_t j = k + 1; j <= jmax; ++j) at(i, j) -= l * at(k, j);
+      }
+    }
+  }
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ build
+template <>
+std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, int nlevels,
+                                                            double shift, cudaStream_t s) {
+  if (nlevels < 2) throw HzError(kValidation, "multigrid: need at least 2 levels");
+  auto H = std::make_unique<Hierarchy<double>>();
+  H->ndim_ = p.ndim;
+  std::vector<std::array<int64_t, 3>> dims(nlevels);
+  dims[0] = p.n;
+  for (int l = 0; l + 1 < nlevels; ++l) dims[l + 1] = coarsen(dims[l]);
+  H->levels_.resize(nlevels);
+  // level 0: shifted fine operator (to_csr(shift), src/helmholtz.cpp:102-122)
+  {
+    auto& L0 = H->levels_[0];
+    L0.dims = dims[0];
+    L0.kind = kFine;
+    for (int a = 0; a < 3; ++a) L0.w[a] = p.inv_h2[a];
+    const auto c = p.shifted_center(shift);
+    const auto inv = invert_diag(c);
+    L0.center.alloc(c.size());
+    L0.inv_diag.alloc(c.size());
+    L0.center.upload(c.data(), c.size(), s);
+    L0.inv_diag.upload(inv.data(), inv.size(), s);
+    HZ_CUDA(cudaStreamSynchronize(s));
+  }
+  const int S = p.ndim == 3 ? 27 : 9;
+  const int sc = p.ndim == 3 ? 13 : 4;  // centre plane
+  for (int l = 1; l < nlevels; ++l) {
+    auto& L = H->levels_[l];
+    L.dims = dims[l];
+    L.kind = kStencil;
+    const int64_t nc = L.nodes();
+    L.coef.alloc(size_t(S) * nc);
+    LevelGeom gc(dims[l][0], dims[l][1], dims[l][2], 1);
+    launch_galerkin(H->op(l - 1, 1), gc, L.coef.get(), s);
+    std::vector<cplx> diag(nc);
+    HZ_CUDA(cudaMemcpyAsync(diag.data(), L.coef.get() + size_t(sc) * nc, nc * sizeof(double2),
+                            cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+    const auto inv = invert_diag(diag);
+    L.inv_diag.alloc(nc);
+    L.inv_diag.upload(inv.data(), nc, s);
+  }
+  // coarsest: banded LU over the stencil profile, then explicit inverse
+  {
+    const auto& Lc = H->levels_.back();
+    const int64_t nc = Lc.nodes();
+    const int64_t n0 = Lc.dims[0], n1 = Lc.dims[1];
+    const int64_t band = p.ndim == 3 ? n0 * n1 + n0 + 1 : n0 + 1;
+    H->band_ = band;
+    std::vector<cplx> coef(size_t(S) * nc);
+    HZ_CUDA(cudaMemcpyAsync(coef.data(), Lc.coef.get(), coef.size() * sizeof(double2),
+                            cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+    BandedFactor f;
+    f.n = nc;
+    f.kl = f.ku = band;
+    f.ld = 2 * f.kl + f.ku + 1;
+    f.ab.assign(size_t(f.ld) * nc, cplx{});
+    f.piv.assign(nc, 0);
+    const int64_t n2 = Lc.dims[2];
+    for (int64_t kz = 0; kz < n2; ++kz)
+      for (int64_t j = 0; j < n1; ++j)
+        for (int64_t i = 0; i < n0; ++i) {
+          const int64_t r = i + n0 * (j + n1 * kz);
+          for (int dz = (p.ndim == 3 ? -1 : 0); dz <= (p.ndim == 3 ? 1 : 0); ++dz)
+            for (int dy = -1; dy <= 1; ++dy)
+              for (int dx = -1; dx <= 1; ++dx) {
+                const int64_t ii = i + dx, jj = j + dy, kk = kz + dz;
+                if (ii < 0 || ii >= n0 || jj < 0 || jj >= n1 || kk < 0 || kk >= n2) continue;
+                const int sidx = (p.ndim == 3 ? (dz + 1) * 9 : 0) + (dy + 1) * 3 + (dx + 1);
+                f.at(r, ii + n0 * (jj + n1 * kk)) += coef[size_t(sidx) * nc + r];
+              }
+        }
+    f.factor();
+    DevBuf<double2> dab(f.ab.size());
+    DevBuf<int64_t> dpiv(nc);
+    dab.upload(f.ab.data(), f.ab.size(), s);
+    dpiv.upload(f.piv.data(), nc, s);
+    H->ainvT_.alloc(size_t(nc) * nc);
+    launch_banded_inverse(nc, f.kl, f.ku, f.ld, dab.get(), dpiv.get(), H->ainvT_.get(), s);
+    HZ_CUDA(cudaStreamSynchronize(s));
+  }
+  return H;
+}
+
+// DenseLuSmall (src/helmholtz_solver.cpp:11-17): the reference factors the
+// dense unshifted operator with partial pivoting. Rows below the band are
+// zero in every pivot column, so the banded pivoted LU takes the same pivots
+// and produces the same factors; the solve is the explicit inverse.
+DevBuf<double2> dense_inverse(const Problem& p, cudaStream_t s) {
+  const int64_t nn = p.num_nodes();
+  const int64_t n0 = p.n[0], n1 = p.n[1], n2 = p.n[2];
+  const int64_t band = p.ndim == 3 ? n0 * n1 : n0;
+  BandedFactor f;
+  f.n = nn;
+  f.kl = f.ku = band;
+  f.ld = 2 * f.kl + f.ku + 1;
+  f.ab.assign(size_t(f.ld) * nn, cplx{});
+  f.piv.assign(nn, 0);
+  for (int64_t kz = 0; kz < n2; ++kz)
+    for (int64_t j = 0; j < n1; ++j)
+      for (int64_t i = 0; i < n0; ++i) {
+        const int64_t r = i + n0 * (j + n1 * kz);
+        f.at(r, r) += p.center_lap + p.mass[r];
+        if (i > 0) f.at(r, r - 1) += p.inv_h2[0];
+        if (i + 1 < n0) f.at(r, r + 1) += p.inv_h2[0];
+        if (j > 0) f.at(r, r - n0) += p.inv_h2[1];
+        if (j + 1 < n1) f.at(r, r + n0) += p.inv_h2[1];
+        if (kz > 0) f.at(r, r - n0 * n1) += p.inv_h2[2];
+        if (kz + 1 < n2) f.at(r, r + n0 * n1) += p.inv_h2[2];
+      }
+  f.factor();
+  DevBuf<double2> dab(f.ab.size());
+  DevBuf<int64_t> dpiv(nn);
+  dab.upload(f.ab.data(), f.ab.size(), s);
+  dpiv.upload(f.piv.data(), nn, s);
+  DevBuf<double2> out(size_t(nn) * nn);
+  launch_banded_inverse(nn, f.kl, f.ku, f.ld, dab.get(), dpiv.get(), out.get(), s);
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+
+template <>
+std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<double>& h64,
+                                                            cudaStream_t s) {
+  auto H = std::make_unique<Hierarchy<float>>();
+  H->ndim_ = h64.ndim_;
+  H->band_ = h64.band_;
+  H->levels_.resize(h64.levels_.size());
+  for (size_t l = 0; l < h64.levels_.size(); ++l) {
+    const auto& a = h64.levels_[l];
+    auto& b = H->levels_[l];
+    b.dims = a.dims;
+    b.kind = a.kind;
+    for (int q = 0; q < 3; ++q) b.w[q] = float(a.w[q]);
+    auto cast = [&](const DevBuf<double2>& src, DevBuf<float2>& dst) {
+      if (!src.size()) return;
+      dst.alloc(src.size());
+      launch_cast<float2, double2>(int64_t(src.size()), src.get(), dst.get(), s);
+    };
+    cast(a.center, b.center);
+    cast(a.coef, b.coef);
+    cast(a.inv_diag, b.inv_diag);
+  }
+  H->ainvT_.alloc(h64.ainvT_.size());
+  launch_cast<float2, double2>(int64_t(h64.ainvT_.size()), h64.ainvT_.get(), H->ainvT_.get(), s);
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return H;
+}
+
+template <class T>
+LevelOp<T> Hierarchy<T>::op(int l, int k) const {
+  const auto& L = levels_[l];
+  LevelOp<T> o;
+  o.kind = L.kind;
+  o.ndim = ndim_;
+  o.g = LevelGeom(L.dims[0], L.dims[1], L.dims[2], k);
+  o.center = L.center.get();
+  o.coef = L.coef.get();
+  o.inv_diag = L.inv_diag.get();
+  for (int a = 0; a < 3; ++a) o.w[a] = L.w[a];
+  return o;
+}
+
+template <class T>
+void Hierarchy<T>::download_level(int l, std::vector<cplx>& out) const {
+  const auto& L = levels_[l];
+  const DevBuf<V>& src = L.kind == kFine ? L.center : L.coef;
+  std::vector<V> tmp(src.size());
+  HZ_CUDA(cudaMemcpy(tmp.data(), src.get(), src.bytes(), cudaMemcpyDeviceToHost));
+  out.resize(tmp.size());
+  for (size_t i = 0; i < tmp.size(); ++i) out[i] = cplx(tmp[i].x, tmp[i].y);
+}
+
+// ------------------------------------------------------------------ cycle
+template <class T>
+void Hierarchy<T>::ensure_ws(int k) {
+  if (ws_k_ == k) return;
+  const int L = num_levels();
+  wx_.resize(L);
+  wt_.resize(L);
+  wb_.resize(L);
+  wr_.resize(L);
+  for (int l = 0; l < L; ++l) {
+    const size_t e = size_t(levels_[l].nodes()) * k;
+    if (l > 0) {
+      wx_[l].alloc(e);
+      wb_[l].alloc(e);
+    }
+    if (l + 1 < L) {
+      wt_[l].alloc(e);
+      wr_[l].alloc(e);
+    }
+  }
+  ws_k_ = k;
+}
+
+template <class T>
+void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
+  launch_coarse_solve<T>(coarse_n(), k, ainvT_.get(), b, x, s);
+}
+
+template <class T>
+void Hierarchy<T>::cycle(const CycleSpec& spec, int k, const V* b, V* x, bool x_zero,
+                         cudaStream_t s) {
+  ensure_ws(k);
+  cycle_rec(0, spec, k, b, x, x_zero, s);
+}
+
+// relax (src/multigrid.cpp:119-136): every sweep writes the other buffer and
+// swaps, so an even number of sweeps per visit ends in the caller's x.
+template <class T>
+void Hierarchy<T>::relax(int l, const CycleSpec& spec, int sweeps, int k, const V* b, V*& cur,
+                         V*& other, bool& cur_zero, cudaStream_t s) {
+  const LevelOp<T> o = op(l, k);
+  const T wj = T(spec.jacobi_weight);
+  for (int sw = 0; sw < sweeps; ++sw) {
+    if (cur_zero)
+      launch_jacobi_zero<T, V>(o, wj, b, other, s);
+    else
+      launch_jacobi<T>(o, wj, cur, b, other, s);
+    std::swap(cur, other);
+    cur_zero = false;
+  }
+}
+
+// cycle_rec (src/multigrid.cpp:162-199)
+template <class T>
+void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V* x, bool x_zero,
+                             cudaStream_t s) {
+  const int L = num_levels();
+  if (l == L - 1) {
+    coarse_solve(k, b, x, s);
+    return;
+  }
+  V* cur = x;
+  V* other = wt_[l].get();
+  bool cur_zero = x_zero;
+  relax(l, spec, spec.pre, k, b, cur, other, cur_zero, s);
+  const size_t bytes = size_t(levels_[l].nodes()) * k * sizeof(V);
+  if (cur_zero) HZ_CUDA(cudaMemsetAsync(cur, 0, bytes, s));
+  const LevelOp<T> o = op(l, k);
+  const LevelGeom gc(levels_[l + 1].dims[0], levels_[l + 1].dims[1], levels_[l + 1].dims[2], k);
+  launch_residual<T>(o, cur, b, wr_[l].get(), s);
+  launch_restrict<T>(o.g, gc, ndim_, wr_[l].get(), wb_[l + 1].get(), s);
+  V* ec = wx_[l + 1].get();
+  const V* rc = wb_[l + 1].get();
+  switch (spec.kind) {
+    case CycleKind::V:
+      cycle_rec(l + 1, spec, k, rc, ec, true, s);
+      break;
+    case CycleKind::W:
+      cycle_rec(l + 1, spec, k, rc, ec, true, s);
+      if (l + 1 < L - 1) cycle_rec(l + 1, spec, k, rc, ec, false, s);
+      break;
+    case CycleKind::K:
+      if (l + 1 == L - 1)
+        cycle_rec(l + 1, spec, k, rc, ec, true, s);
+      else
+        kcycle_coarse(l + 1, spec, k, rc, ec, s);
+      break;
+  }
+  launch_prolong_correct<T>(o.g, gc, ndim_, ec, cur, s);
+  cur_zero = false;
+  relax(l, spec, spec.post, k, b, cur, other, cur_zero, s);
+  if (cur != x) HZ_CUDA(cudaMemcpyAsync(x, cur, bytes, cudaMemcpyDeviceToDevice, s));
+}
+
+// kcycle_coarse (src/multigrid.cpp:138-160): k_inner block FGMRES iterations
+// on level l, tol 0, preconditioned by cycle_rec(l).
+template <class T>
+void Hierarchy<T>::kcycle_coarse(int l, const CycleSpec& spec, int k, const V* b, V* x,
+                                 cudaStream_t s) {
+  if (int(kfgm_.size()) < num_levels()) kfgm_.resize(num_levels());
+  if (!kfgm_[l]) kfgm_[l] = std::make_unique<Fgmres<T>>();
+  DevOp<T> dop;
+  dop.n = levels_[l].nodes();
+  dop.apply = [this, l](const V* in, V* out, int kk, cudaStream_t st) {
+    launch_apply<T>(op(l, kk), in, out, st);
+  };
+  const size_t bytes = size_t(levels_[l].nodes()) * k * sizeof(V);
+  dop.prec = [this, l, spec, bytes](const V* in, V* out, int kk, cudaStream_t st) {
+    cycle_rec(l, spec, kk, in, out, true, st);
+  };
+  (void)bytes;
+  kfgm_[l]->solve(dop, k, b, x, spec.k_inner, 0.0, spec.k_inner, s);
+}
+
+template class Hierarchy<double>;
+template class Hierarchy<float>;
+
+}  // namespace hz

@@ -1,0 +1,131 @@
+// Launch wrappers for the sm_100a kernels (declarations). Every wrapper
+// enqueues on the given stream and never synchronises.
+#pragma once
+
+#include "common.cuh"
+
+namespace hz {
+
+// One level operator as the kernels see it.
+//  * kind == kFine: the 5-point (2D) / 7-point (3D) fine operator with a
+//    per-node complex centre and constant off-diagonals w[a] = 1/h_a^2
+//    (HelmholtzProblem, src/helmholtz.cpp:45-122).
+//  * kind == kStencil: a Galerkin coarse operator stored as S = 3^ndim
+//    complex coefficient planes coef[s][node], s = (dz+1)*9 + (dy+1)*3 + (dx+1)
+//    -- ascending s is ascending CSR column, so sums run in the reference's
+//    Csr::mul_block order (inc/csr.hpp:40-54).
+enum OpKind : int { kFine = 0, kStencil = 1 };
+
+template <class T>
+struct LevelOp {
+  using V = cplx_t<T>;
+  int kind = kFine;
+  int ndim = 2;
+  LevelGeom g;                 // k is set per launch
+  const V* center = nullptr;   // kFine: diagonal (centre) per node
+  const V* coef = nullptr;     // kStencil: [S][nodes]
+  const V* inv_diag = nullptr; // Jacobi D^{-1} per node
+  T w[3] = {0, 0, 0};          // kFine off-diagonal weights (0 on flat axes)
+};
+
+// out = A u                                    (K1: apply_block)
+template <class T>
+void launch_apply(const LevelOp<T>& op, const cplx_t<T>* u, cplx_t<T>* out, cudaStream_t s);
+// r = b - A x                                  (residual, src/multigrid.cpp:173-175)
+template <class T>
+void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
+                     cudaStream_t s);
+// xout = x + (wj D^{-1}) (b - A x)             (K2: relax, src/multigrid.cpp:119-136)
+template <class T>
+void launch_jacobi(const LevelOp<T>& op, T wj, const cplx_t<T>* x, const cplx_t<T>* b,
+                   cplx_t<T>* xout, cudaStream_t s);
+// xout = (wj D^{-1}) b  -- the first sweep from x = 0, bitwise the same as
+// b - A*0 = b. In may be a wider type (c128 -> c64 cast).
+template <class T, class In>
+void launch_jacobi_zero(const LevelOp<T>& op, T wj, const In* b, cplx_t<T>* xout, cudaStream_t s);
+// bc = P^T r   (R unscaled, src/multigrid.cpp:87-88,176-178)
+template <class T>
+void launch_restrict(const LevelGeom& gf, const LevelGeom& gc, int ndim, const cplx_t<T>* r,
+                     cplx_t<T>* bc, cudaStream_t s);
+// x += P ec    (bi/trilinear, src/multigrid.cpp:27-69,195-197)
+template <class T>
+void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
+                            const cplx_t<T>* ec, cplx_t<T>* x, cudaStream_t s);
+// Galerkin A_c = P^T A_f P as 3^ndim stencil planes, in the reference's
+// sparse triple-product summation order (src/multigrid.cpp:85-93,
+// inc/csr.hpp:130-160). Always f64.
+void launch_galerkin(const LevelOp<double>& fine, const LevelGeom& gc, double2* coef_c,
+                     cudaStream_t s);
+
+// elementwise casts / copies
+template <class Dst, class Src>
+void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);
+
+// ---- coarsest level (K5)
+// Columns of A^{-1} from banded LU factors (gbtrf storage as in
+// BandedLU, inc/dense.hpp:179-216): one warp per column, written as
+// ainvT[c][i] = (A^{-1})[i][c].
+void launch_banded_inverse(int64_t n, int64_t kl, int64_t ku, int64_t ld, const double2* ab,
+                           const int64_t* piv, double2* ainvT, cudaStream_t s);
+// X[i][:] = sum_l ainvT[l][i] * B[l][:]   (dense coarse solve, all k columns)
+template <class T>
+void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
+                         cplx_t<T>* x, cudaStream_t s);
+
+// ---- block (tall-skinny) kernels, node-major [n][k] blocks (inc/block.hpp)
+// Tables of block pointers travel by value in the kernel parameters (no
+// device-side pointer arrays, no host round trip to build them).
+constexpr int kMaxBlocks = 48;
+template <class T>
+struct BlockTab {
+  const cplx_t<T>* p[kMaxBlocks];
+};
+// Stage 1 of a deterministic two-stage reduction: per-CTA partial Grams
+// G_i = X_i^H Y for nb blocks X_i against one Y (k x k each).
+// Returns the number of partial slices written to `partials`
+// (partials must hold gram_partial_slots(n) * nb * k * k entries).
+int gram_partial_slots(int64_t n, int k);
+template <class T>
+void launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
+                       cplx_t<T>* partials, int nslots, cudaStream_t s);
+// Yout = (Yin ? Yin : 0) + sign * sum_i X_i H_i  (H_i k x k row-major, on
+// device). Yout may alias Yin but not any X_i.
+template <class T>
+void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* H,
+                         const cplx_t<T>* Yin, cplx_t<T>* Yout, T sign, cudaStream_t s);
+// sum over slots: out[e] = sum_s partials[s][e], fixed slot order
+template <class T>
+void launch_reduce_partials(int64_t count, int nslots, const cplx_t<T>* partials, cplx_t<T>* out,
+                            cudaStream_t s);
+// per-column sums of |x|^2 (partials per slot, then reduce)
+template <class T>
+void launch_colnorm2_partial(int64_t n, int k, const cplx_t<T>* X, T* partials, int nslots,
+                             cudaStream_t s);
+template <class T>
+void launch_reduce_real(int64_t count, int nslots, const T* partials, T* out, cudaStream_t s);
+// Y = a*Y + b*X (complex scalars, host values)
+template <class T>
+void launch_axpby(int64_t count, cplx_t<T> a, cplx_t<T>* Y, cplx_t<T> b, const cplx_t<T>* X,
+                  cudaStream_t s);
+// X += omega ZS ; R = S - omega T   (block BiCGSTAB update, src/krylov.cpp:140-145)
+template <class T>
+void launch_bicgstab_update(int64_t count, cplx_t<T> omega, cplx_t<T>* X, const cplx_t<T>* ZS,
+                            cplx_t<T>* R, const cplx_t<T>* S, const cplx_t<T>* Tt, cudaStream_t s);
+// partial sums of conj(T).S and conj(T).T over all entries (Frobenius)
+template <class T>
+void launch_frob2_partial(int64_t count, const cplx_t<T>* Tt, const cplx_t<T>* S,
+                          cplx_t<T>* partials, int nslots, cudaStream_t s);
+
+// upper-triangular Cholesky factor of a k x k Hermitian Gram on device:
+// R (k x k), Rinv, and flag[0] = first failing column + 1 (0 = ok). A failing
+// pivot marks the column collapsed exactly as thin_qr does
+// (inc/block.hpp:126-131): zero row in R, zero column in Q = W Rinv.
+template <class T>
+void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* Rinv, int* flag,
+                           T rel_tol, cudaStream_t s);
+
+// sensitivity: g[i] (+)= sum_s Re(-omega^2 gf[i] u[i][s] lam[i][s])  (K13)
+void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const double2* U,
+                        const double2* L, double* g, int accumulate, cudaStream_t s);
+
+}  // namespace hz

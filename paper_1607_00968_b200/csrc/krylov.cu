@@ -1,0 +1,614 @@
+// Block Krylov methods on device blocks: flexible block FGMRES(m) and block
+// BiCGSTAB, right-preconditioned, following src/krylov.cpp:60-280.
+//
+// B200 design vs the reference:
+//  * Arnoldi orthogonalisation is block classical Gram-Schmidt with one full
+//    re-orthogonalisation (CGS2): every pass is ONE multi-block Gram kernel
+//    (reads W once for all V_0..V_j) and ONE multi-block update, instead of
+//    the reference's 2(j+1) separate Gram + update sweeps (block MGS2,
+//    src/krylov.cpp:218-226). Same Krylov space and H to rounding.
+//  * thin_qr is CholQR2 (Gram -> k x k Cholesky on device -> triangular
+//    solve, twice) instead of column-serial MGS (inc/block.hpp:104-137); R has
+//    the same real positive diagonal and the same collapsed-column rule.
+//  * The block-Hessenberg least-squares problem is the reference's
+//    Householder LS (inc/dense.hpp:118-175) applied incrementally: reflectors
+//    of earlier columns are kept, so each iteration only processes its new
+//    k columns -- the same arithmetic, O(j k^3) instead of O(j^3 k^3).
+//  * One host synchronisation per Arnoldi step (to read the k x k tiles).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "solver.hpp"
+
+namespace hz {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+template <class V>
+cplx to_c(V v) {
+  return cplx(double(v.x), double(v.y));
+}
+template <class V>
+V from_c(cplx c) {
+  V v;
+  v.x = static_cast<decltype(v.x)>(c.real());
+  v.y = static_cast<decltype(v.y)>(c.imag());
+  return v;
+}
+
+// record_convergence (src/krylov.cpp:22-31)
+void record_convergence(Report& rep, const std::vector<double>& res,
+                        const std::vector<double>& bnorm, double tol, int cycle) {
+  double worst = 0.0;
+  for (size_t j = 0; j < res.size(); ++j) {
+    const double rel = res[j] / bnorm[j];
+    worst = std::max(worst, rel);
+    if (rep.col_cycles[j] < 0 && rel <= tol) rep.col_cycles[j] = cycle;
+  }
+  rep.history.push_back(worst);
+}
+
+// ---------------------------------------------------------------- LS
+// Householder least squares of the block Hessenberg system, restated from
+// least_squares (inc/dense.hpp:118-175) and kept incrementally.
+class BlockLsq {
+ public:
+  void reset(int k, int m, const std::vector<cplx>& S0) {
+    k_ = k;
+    m_ = m;
+    rows_ = (m + 1) * k;
+    cols_ = m * k;
+    A_.assign(size_t(rows_) * cols_, cplx{});
+    B_.assign(size_t(rows_) * k, cplx{});
+    for (int p = 0; p < k; ++p)
+      for (int q = 0; q < k; ++q) B(p, q) = S0[size_t(p) * k + q];
+    v_.assign(cols_, {});
+    beta_.assign(cols_, 0.0);
+    live_.assign(cols_, 0);
+    blocks_ = 0;
+  }
+  int blocks() const { return blocks_; }
+  // tiles: H[i][j] for i = 0..j+1, each k x k row-major
+  void add_block(int j, const std::vector<std::vector<cplx>>& tiles) {
+    const int k = k_;
+    const int m = (j + 2) * k;  // rows of the system at this iteration
+    for (int bi = 0; bi <= j + 1; ++bi)
+      for (int p = 0; p < k; ++p)
+        for (int q = 0; q < k; ++q) A(bi * k + p, j * k + q) = tiles[bi][size_t(p) * k + q];
+    // apply earlier reflectors to the new columns, in column order
+    for (int c = 0; c < j * k; ++c)
+      if (live_[c]) apply_reflector(c, j * k, (j + 1) * k, false);
+    // new reflectors (src: inc/dense.hpp:121-148)
+    for (int c = j * k; c < (j + 1) * k; ++c) {
+      double norm2 = 0.0;
+      for (int i = c; i < m; ++i) norm2 += std::norm(A(i, c));
+      const double norm = std::sqrt(norm2);
+      if (norm == 0.0) {
+        A(c, c) = cplx{};
+        live_[c] = 0;
+        continue;
+      }
+      const cplx x0 = A(c, c);
+      const double ax0 = std::sqrt(std::norm(x0));
+      const cplx phase = ax0 > 0 ? x0 / cplx{ax0} : cplx{1};
+      const cplx alpha = phase * cplx{norm};
+      A(c, c) = x0 + alpha;
+      double v2 = 0.0;
+      for (int i = c; i < m; ++i) v2 += std::norm(A(i, c));
+      if (v2 == 0.0) throw HzError(kFactorization, "least_squares: degenerate reflector");
+      beta_[c] = 2.0 / v2;
+      v_[c].assign(m - c, cplx{});
+      for (int i = c; i < m; ++i) v_[c][i - c] = A(i, c);
+      live_[c] = 1;
+      apply_reflector(c, c + 1, (j + 1) * k, true);
+      A(c, c) = -alpha;
+    }
+    blocks_ = j + 1;
+  }
+  // per-column residual norms of the current system (rows n..m-1)
+  void residuals(std::vector<double>& res) const {
+    const int n = blocks_ * k_, m = (blocks_ + 1) * k_;
+    res.assign(k_, 0.0);
+    for (int c = 0; c < k_; ++c) {
+      double s = 0.0;
+      for (int i = n; i < m; ++i) s += std::norm(B(i, c));
+      res[c] = std::sqrt(s);
+    }
+  }
+  // back substitution (inc/dense.hpp:150-160) over nb blocks
+  std::vector<cplx> solve(int nb) const {
+    const int n = nb * k_;
+    std::vector<cplx> Y(size_t(n) * k_, cplx{});
+    for (int c = 0; c < k_; ++c)
+      for (int r = n - 1; r >= 0; --r) {
+        if (A(r, r) == cplx{}) {
+          Y[size_t(r) * k_ + c] = cplx{};
+          continue;
+        }
+        cplx x = B(r, c);
+        for (int j2 = r + 1; j2 < n; ++j2) x -= A(r, j2) * Y[size_t(j2) * k_ + c];
+        Y[size_t(r) * k_ + c] = x / A(r, r);
+      }
+    return Y;
+  }
+
+ private:
+  cplx& A(int i, int j) { return A_[size_t(i) * cols_ + j]; }
+  const cplx& A(int i, int j) const { return A_[size_t(i) * cols_ + j]; }
+  cplx& B(int i, int j) { return B_[size_t(i) * k_ + j]; }
+  const cplx& B(int i, int j) const { return B_[size_t(i) * k_ + j]; }
+  // apply reflector of column c to A columns [c0, c1) and, if rhs, to B
+  void apply_reflector(int c, int c0, int c1, bool rhs) {
+    const std::vector<cplx>& v = v_[c];
+    const int len = int(v.size());
+    const cplx beta{beta_[c]};
+    for (int col = c0; col < c1; ++col) {
+      cplx dot{};
+      for (int i = 0; i < len; ++i) dot += std::conj(v[i]) * A(c + i, col);
+      dot *= beta;
+      for (int i = 0; i < len; ++i) A(c + i, col) -= dot * v[i];
+    }
+    if (rhs)
+      for (int col = 0; col < k_; ++col) {
+        cplx dot{};
+        for (int i = 0; i < len; ++i) dot += std::conj(v[i]) * B(c + i, col);
+        dot *= beta;
+        for (int i = 0; i < len; ++i) B(c + i, col) -= dot * v[i];
+      }
+  }
+  int k_ = 0, m_ = 0, rows_ = 0, cols_ = 0, blocks_ = 0;
+  std::vector<cplx> A_, B_;
+  std::vector<std::vector<cplx>> v_;
+  std::vector<double> beta_;
+  std::vector<char> live_;
+};
+
+// lu_factor / lu_solve / solve_small restated (inc/dense.hpp:50-113)
+std::vector<cplx> solve_small(std::vector<cplx> A, std::vector<cplx> B, int n, int nrhs) {
+  std::vector<int64_t> piv(n);
+  double scale = 0.0;
+  for (const cplx& x : A) scale = std::max(scale, std::sqrt(std::norm(x)));
+  if (scale == 0.0) throw HzError(kFactorization, "lu_factor: zero matrix");
+  auto a = [&](int i, int j) -> cplx& { return A[size_t(i) * n + j]; };
+  auto b = [&](int i, int j) -> cplx& { return B[size_t(i) * nrhs + j]; };
+  for (int k = 0; k < n; ++k) {
+    int p = k;
+    double best = std::norm(a(k, k));
+    for (int i = k + 1; i < n; ++i) {
+      const double v = std::norm(a(i, k));
+      if (v > best) {
+        best = v;
+        p = i;
+      }
+    }
+    if (std::sqrt(best) < 1e-14 * scale)
+      throw HzError(kFactorization, "lu_factor: singular pivot at column " + std::to_string(k));
+    piv[k] = p;
+    if (p != k)
+      for (int c = 0; c < n; ++c) std::swap(a(k, c), a(p, c));
+    const cplx inv = cplx{1} / a(k, k);
+    for (int i = k + 1; i < n; ++i) {
+      const cplx l = a(i, k) * inv;
+      a(i, k) = l;
+      for (int c = k + 1; c < n; ++c) a(i, c) -= l * a(k, c);
+    }
+  }
+  for (int k = 0; k < n; ++k)
+    if (piv[k] != k)
+      for (int c = 0; c < nrhs; ++c) std::swap(b(k, c), b(int(piv[k]), c));
+  for (int k = 0; k < n; ++k)
+    for (int i = k + 1; i < n; ++i) {
+      const cplx l = a(i, k);
+      if (l != cplx{})
+        for (int c = 0; c < nrhs; ++c) b(i, c) -= l * b(k, c);
+    }
+  for (int k = n - 1; k >= 0; --k) {
+    const cplx inv = cplx{1} / a(k, k);
+    for (int c = 0; c < nrhs; ++c) {
+      cplx x = b(k, c);
+      for (int j = k + 1; j < n; ++j) x -= a(k, j) * b(j, c);
+      b(k, c) = x * inv;
+    }
+  }
+  return B;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- algebra
+template <class T>
+void BlockAlgebra<T>::ensure(int64_t n_, int k_, int max_blocks) {
+  if (n_ * int64_t(k_) >= (int64_t(1) << 32)) throw HzError(kValidation, "block too large");
+  if (k_ < 1 || k_ > 64) throw HzError(kValidation, "block width must be in [1, 64]");
+  n = n_;
+  k = k_;
+  nslots = gram_partial_slots(n, k);
+  partials.ensure(size_t(nslots) * std::max(max_blocks, 2) * k * k);
+  tmp_blk.ensure(size_t(n) * k);
+  G.ensure(size_t(k) * k);
+  R1.ensure(size_t(k) * k);
+  R1i.ensure(size_t(k) * k);
+  R2.ensure(size_t(k) * k);
+  R2i.ensure(size_t(k) * k);
+  rpart.ensure(size_t(nslots) * k);
+  rnorm.ensure(k);
+  flags.ensure(2);
+  h_norm.ensure(k);
+  h_R.ensure(2 * size_t(k) * k);
+  h_flags.ensure(2);
+}
+
+template <class T>
+void BlockAlgebra<T>::gram(const BlockTab<T>& tab, int nb, const V* Y, V* out, cudaStream_t s) {
+  launch_multi_gram<T>(n, k, nb, tab, Y, partials.get(), nslots, s);
+  launch_reduce_partials<T>(int64_t(nb) * k * k, nslots, partials.get(), out, s);
+}
+
+template <class T>
+void BlockAlgebra<T>::col_norms(const V* X, std::vector<double>& out, cudaStream_t s) {
+  launch_colnorm2_partial<T>(n, k, X, rpart.get(), nslots, s);
+  launch_reduce_real<T>(k, nslots, rpart.get(), rnorm.get(), s);
+  HZ_CUDA(cudaMemcpyAsync(h_norm.get(), rnorm.get(), sizeof(T) * k, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  out.resize(k);
+  for (int j = 0; j < k; ++j) out[j] = std::sqrt(double(h_norm[j]));
+}
+
+template <class T>
+void BlockAlgebra<T>::thin_qr_enqueue(V* W, cudaStream_t s) {
+  // collapse threshold of thin_qr (inc/block.hpp:105,126): 1e-12 relative
+  const T tol = std::is_same<T, double>::value ? T(1e-12) : T(1e-6);
+  BlockTab<T> t{};
+  t.p[0] = W;
+  gram(t, 1, W, G.get(), s);
+  launch_small_cholesky<T>(k, G.get(), R1.get(), R1i.get(), flags.get(), tol, s);
+  launch_multi_update<T>(n, k, 1, t, R1i.get(), nullptr, tmp_blk.get(), T(1), s);
+  t.p[0] = tmp_blk.get();
+  gram(t, 1, tmp_blk.get(), G.get(), s);
+  launch_small_cholesky<T>(k, G.get(), R2.get(), R2i.get(), flags.get() + 1, tol, s);
+  launch_multi_update<T>(n, k, 1, t, R2i.get(), nullptr, W, T(1), s);
+  const size_t kk = size_t(k) * k;
+  HZ_CUDA(cudaMemcpyAsync(h_R.get(), R1.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaMemcpyAsync(h_R.get() + kk, R2.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaMemcpyAsync(h_flags.get(), flags.get(), sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+}
+
+template <class T>
+void BlockAlgebra<T>::thin_qr_finish(std::vector<cplx>& R, bool& deficient) {
+  const size_t kk = size_t(k) * k;
+  R.assign(kk, cplx{});
+  // R = R2 R1 (both upper triangular)
+  for (int p = 0; p < k; ++p)
+    for (int q = p; q < k; ++q) {
+      cplx s{};
+      for (int l = p; l <= q; ++l) s += to_c(h_R[kk + size_t(p) * k + l]) * to_c(h_R[size_t(l) * k + q]);
+      R[size_t(p) * k + q] = s;
+    }
+  deficient = h_flags[0] != 0 || h_flags[1] != 0;
+}
+
+// ---------------------------------------------------------------- FGMRES
+template <class T>
+void Fgmres<T>::ensure(int64_t n, int k, int restart) {
+  if (restart < 1) throw HzError(kValidation, "fgmres: restart must be >= 1");
+  if (restart + 1 > kMaxBlocks) throw HzError(kValidation, "fgmres: restart too large");
+  if (n == n_ && k == k_ && restart == m_) return;
+  Vb_.clear();
+  Zb_.clear();
+  Vb_.resize(restart + 1);
+  Zb_.resize(restart);
+  for (auto& b : Vb_) b.alloc(size_t(n) * k);
+  for (auto& b : Zb_) b.alloc(size_t(n) * k);
+  R_.alloc(size_t(n) * k);
+  hcol1_.alloc(size_t(restart + 1) * k * k);
+  hcol2_.alloc(size_t(restart + 1) * k * k);
+  ydev_.alloc(size_t(restart) * k * k);
+  h_hcol_.ensure(2 * size_t(restart + 1) * k * k);
+  h_y_.ensure(size_t(restart) * k * k);
+  vtab_ = BlockTab<T>{};
+  ztab_ = BlockTab<T>{};
+  for (int i = 0; i <= restart; ++i) vtab_.p[i] = Vb_[i].get();
+  for (int i = 0; i < restart; ++i) ztab_.p[i] = Zb_[i].get();
+  alg_.ensure(n, k, restart + 1);
+  n_ = n;
+  k_ = k;
+  m_ = restart;
+}
+
+template <class T>
+Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart, double tol,
+                        int max_cycles, cudaStream_t s) {
+  const auto t0 = Clock::now();
+  const int64_t n = op.n;
+  ensure(n, k, restart);
+  const size_t blk = size_t(n) * k * sizeof(V);
+  const size_t kk = size_t(k) * k;
+  Report rep;
+  rep.col_cycles.assign(k, -1);
+  std::vector<double> bnorm;
+  alg_.col_norms(B, bnorm, s);
+  std::vector<double> r0 = bnorm;
+  for (double& x : bnorm)
+    if (x == 0.0) x = 1.0;  // rhs_norms (src/krylov.cpp:15-20)
+  HZ_CUDA(cudaMemsetAsync(X, 0, blk, s));
+  HZ_CUDA(cudaMemcpyAsync(R_.get(), B, blk, cudaMemcpyDeviceToDevice, s));
+  bool done = true;
+  for (int j = 0; j < k; ++j) done = done && r0[j] / bnorm[j] <= tol;
+  const int m = restart;
+  BlockLsq lsq;
+  std::vector<std::vector<std::vector<cplx>>> H(m);  // H[j] = tiles i = 0..j+1
+  std::vector<double> res;
+  std::vector<cplx> Rk;
+  while (!done && rep.cycles < max_cycles) {
+    // Arnoldi from the current residual: V_0 = thin_qr(R)
+    HZ_CUDA(cudaMemcpyAsync(Vb_[0].get(), R_.get(), blk, cudaMemcpyDeviceToDevice, s));
+    alg_.thin_qr_enqueue(Vb_[0].get(), s);
+    HZ_CUDA(cudaStreamSynchronize(s));
+    bool rd = false;
+    alg_.thin_qr_finish(Rk, rd);
+    ++rep.qr_factorizations;
+    lsq.reset(k, m, Rk);
+    int j = 0;
+    for (; j < m && rep.cycles < max_cycles; ++j) {
+      V* Zj = Zb_[j].get();
+      if (op.prec) {
+        op.prec(Vb_[j].get(), Zj, k, s);
+        ++rep.cycles;
+      } else {
+        HZ_CUDA(cudaMemcpyAsync(Zj, Vb_[j].get(), blk, cudaMemcpyDeviceToDevice, s));
+        ++rep.cycles;
+      }
+      V* W = Vb_[j + 1].get();
+      op.apply(Zj, W, k, s);
+      // block CGS2 against V_0..V_j
+      alg_.gram(vtab_, j + 1, W, hcol1_.get(), s);
+      launch_multi_update<T>(n, k, j + 1, vtab_, hcol1_.get(), W, W, T(-1), s);
+      alg_.gram(vtab_, j + 1, W, hcol2_.get(), s);
+      launch_multi_update<T>(n, k, j + 1, vtab_, hcol2_.get(), W, W, T(-1), s);
+      rep.block_gram_products += 2 * (j + 1);
+      const size_t hc = size_t(j + 1) * kk;
+      HZ_CUDA(cudaMemcpyAsync(h_hcol_.get(), hcol1_.get(), sizeof(V) * hc, cudaMemcpyDeviceToHost, s));
+      HZ_CUDA(cudaMemcpyAsync(h_hcol_.get() + hc, hcol2_.get(), sizeof(V) * hc,
+                              cudaMemcpyDeviceToHost, s));
+      alg_.thin_qr_enqueue(W, s);
+      HZ_CUDA(cudaStreamSynchronize(s));
+      bool deficient = false;
+      alg_.thin_qr_finish(Rk, deficient);
+      ++rep.qr_factorizations;
+      H[j].assign(j + 2, std::vector<cplx>(kk));
+      for (int i = 0; i <= j; ++i)
+        for (size_t e = 0; e < kk; ++e)
+          H[j][i][e] = (cplx{} + to_c(h_hcol_[i * kk + e])) + to_c(h_hcol_[hc + i * kk + e]);
+      H[j][j + 1] = Rk;
+      if (deficient) {
+        ++j;
+        break;  // happy breakdown
+      }
+      lsq.add_block(j, H[j]);
+      lsq.residuals(res);
+      record_convergence(rep, res, bnorm, tol, rep.cycles);
+      if (rep.history.back() <= tol) {
+        ++j;
+        break;
+      }
+    }
+    if (j == 0) break;
+    while (lsq.blocks() < j) lsq.add_block(lsq.blocks(), H[lsq.blocks()]);
+    const std::vector<cplx> Y = lsq.solve(j);
+    for (size_t e = 0; e < size_t(j) * kk; ++e) h_y_[e] = from_c<V>(Y[e]);
+    HZ_CUDA(cudaMemcpyAsync(ydev_.get(), h_y_.get(), sizeof(V) * size_t(j) * kk,
+                            cudaMemcpyHostToDevice, s));
+    launch_multi_update<T>(n, k, j, ztab_, ydev_.get(), X, X, T(1), s);
+    // true residual for the restart / convergence decision
+    op.apply(X, R_.get(), k, s);
+    launch_axpby<T>(int64_t(n) * k, mk(T(-1), T(0)), R_.get(), mk(T(1), T(0)), B, s);
+    std::vector<double> rn;
+    alg_.col_norms(R_.get(), rn, s);
+    double worst = 0.0;
+    for (int c = 0; c < k; ++c) worst = std::max(worst, rn[c] / bnorm[c]);
+    if (worst <= tol) done = true;
+  }
+  // finalize (src/krylov.cpp:33-46)
+  op.apply(X, R_.get(), k, s);
+  launch_axpby<T>(int64_t(n) * k, mk(T(-1), T(0)), R_.get(), mk(T(1), T(0)), B, s);
+  std::vector<double> rn;
+  alg_.col_norms(R_.get(), rn, s);
+  rep.rel_residual.resize(k);
+  rep.converged.resize(k);
+  for (int c = 0; c < k; ++c) {
+    rep.rel_residual[c] = rn[c] / bnorm[c];
+    rep.converged[c] = rep.rel_residual[c] <= tol ? 1 : 0;
+    if (rep.col_cycles[c] < 0) rep.col_cycles[c] = rep.cycles;
+  }
+  rep.wall_s = std::chrono::duration<double>(Clock::now() - t0).count();
+  return rep;
+}
+
+template class BlockAlgebra<double>;
+template class BlockAlgebra<float>;
+template class Fgmres<double>;
+template class Fgmres<float>;
+
+// ---------------------------------------------------------------- BiCGSTAB
+void Bicgstab::ensure(int64_t n, int k) {
+  if (n == n_ && k == k_) return;
+  for (DevBuf<V>* b : {&R_, &Rt_, &P_, &ZP_, &V_, &S_, &ZS_, &T_, &PmV_}) b->alloc(size_t(n) * k);
+  cdev_.alloc(4 * size_t(k) * k);
+  alg_.ensure(n, k, 2);
+  fpart_.alloc(2 * size_t(alg_.nslots));
+  fsum_.alloc(2);
+  h_small_.ensure(2 * size_t(k) * k + 2);
+  n_ = n;
+  k_ = k;
+}
+
+Report Bicgstab::solve(const DevOp<double>& op, int k, const V* B, V* X, double tol,
+                       int max_cycles, cudaStream_t s) {
+  const auto t0 = Clock::now();
+  const int64_t n = op.n;
+  ensure(n, k);
+  const size_t blk = size_t(n) * k * sizeof(V);
+  const size_t kk = size_t(k) * k;
+  const int64_t cnt = n * k;
+  Report rep;
+  rep.col_cycles.assign(k, -1);
+  std::vector<double> bnorm, tmp;
+  alg_.col_norms(B, bnorm, s);
+  std::vector<double> r0 = bnorm;
+  for (double& x : bnorm)
+    if (x == 0.0) x = 1.0;
+  HZ_CUDA(cudaMemsetAsync(X, 0, blk, s));
+  HZ_CUDA(cudaMemcpyAsync(R_.get(), B, blk, cudaMemcpyDeviceToDevice, s));
+  auto copy = [&](V* dst, const V* src) {
+    HZ_CUDA(cudaMemcpyAsync(dst, src, blk, cudaMemcpyDeviceToDevice, s));
+  };
+  auto true_residual = [&]() {
+    op.apply(X, R_.get(), k, s);
+    launch_axpby<double>(cnt, mk(-1.0, 0.0), R_.get(), mk(1.0, 0.0), B, s);
+  };
+  auto finalize = [&]() {
+    op.apply(X, T_.get(), k, s);  // T_ as scratch
+    launch_axpby<double>(cnt, mk(-1.0, 0.0), T_.get(), mk(1.0, 0.0), B, s);
+    std::vector<double> rn;
+    alg_.col_norms(T_.get(), rn, s);
+    rep.rel_residual.resize(k);
+    rep.converged.resize(k);
+    for (int c = 0; c < k; ++c) {
+      rep.rel_residual[c] = rn[c] / bnorm[c];
+      rep.converged[c] = rep.rel_residual[c] <= tol ? 1 : 0;
+      if (rep.col_cycles[c] < 0) rep.col_cycles[c] = rep.cycles;
+    }
+  };
+  {
+    bool trivial = true;
+    for (int j = 0; j < k; ++j) trivial = trivial && r0[j] / bnorm[j] <= tol;
+    if (trivial) {
+      finalize();
+      rep.wall_s = std::chrono::duration<double>(Clock::now() - t0).count();
+      return rep;
+    }
+  }
+  copy(Rt_.get(), R_.get());
+  copy(P_.get(), R_.get());
+  int restarts = 0;
+  auto try_restart = [&](int iter) {
+    if (++restarts > 2) throw HzError(kBreakdown, "block BiCGSTAB: singular block recurrence (iteration " +
+                                                      std::to_string(iter) + ")");
+    true_residual();
+    copy(Rt_.get(), R_.get());
+    copy(P_.get(), R_.get());
+  };
+  V* RtV_d = cdev_.get();
+  V* RtR_d = cdev_.get() + kk;
+  V* alpha_d = cdev_.get() + 2 * kk;
+  V* beta_d = cdev_.get() + 3 * kk;
+  auto download_kk = [&](const V* src, std::vector<cplx>& dst) {
+    HZ_CUDA(cudaMemcpyAsync(h_small_.get(), src, sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+    dst.resize(kk);
+    for (size_t e = 0; e < kk; ++e) dst[e] = to_c(h_small_[e]);
+  };
+  auto upload_kk = [&](const std::vector<cplx>& src, V* dst) {
+    for (size_t e = 0; e < kk; ++e) h_small_[e] = from_c<V>(src[e]);
+    HZ_CUDA(cudaMemcpyAsync(dst, h_small_.get(), sizeof(V) * kk, cudaMemcpyHostToDevice, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+  };
+  BlockTab<double> tRt{}, tV{}, tZP{}, tPmV{};
+  tRt.p[0] = Rt_.get();
+  tV.p[0] = V_.get();
+  tZP.p[0] = ZP_.get();
+  tPmV.p[0] = PmV_.get();
+  std::vector<cplx> RtV, RtR, RtT;
+  while (rep.cycles < max_cycles) {
+    if (op.prec) {
+      op.prec(P_.get(), ZP_.get(), k, s);
+      ++rep.cycles;
+    } else {
+      copy(ZP_.get(), P_.get());
+    }
+    op.apply(ZP_.get(), V_.get(), k, s);
+    alg_.gram(tRt, 1, V_.get(), RtV_d, s);
+    alg_.gram(tRt, 1, R_.get(), RtR_d, s);
+    rep.block_gram_products += 2;
+    download_kk(RtV_d, RtV);
+    download_kk(RtR_d, RtR);
+    std::vector<cplx> alpha;
+    try {
+      alpha = solve_small(RtV, RtR, k, k);
+    } catch (const HzError& e) {
+      if (e.code != kFactorization) throw;
+      try_restart(rep.cycles);
+      continue;
+    }
+    upload_kk(alpha, alpha_d);
+    // S = R - V alpha
+    launch_multi_update<double>(n, k, 1, tV, alpha_d, R_.get(), S_.get(), -1.0, s);
+    alg_.col_norms(S_.get(), tmp, s);
+    record_convergence(rep, tmp, bnorm, tol, rep.cycles);
+    if (rep.history.back() <= tol) {
+      launch_multi_update<double>(n, k, 1, tZP, alpha_d, X, X, 1.0, s);
+      finalize();
+      if (rep.all_converged()) break;
+      true_residual();
+      copy(P_.get(), R_.get());
+      copy(Rt_.get(), R_.get());
+      continue;
+    }
+    if (op.prec) {
+      op.prec(S_.get(), ZS_.get(), k, s);
+      ++rep.cycles;
+    } else {
+      copy(ZS_.get(), S_.get());
+    }
+    op.apply(ZS_.get(), T_.get(), k, s);
+    launch_frob2_partial<double>(cnt, T_.get(), S_.get(), fpart_.get(), alg_.nslots, s);
+    launch_reduce_partials<double>(2, alg_.nslots, fpart_.get(), fsum_.get(), s);
+    HZ_CUDA(cudaMemcpyAsync(h_small_.get(), fsum_.get(), sizeof(V) * 2, cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+    const cplx num = to_c(h_small_[0]), den = to_c(h_small_[1]);
+    if (std::abs(den) == 0.0) {
+      try_restart(rep.cycles);
+      continue;
+    }
+    const cplx omega = num / den;
+    launch_multi_update<double>(n, k, 1, tZP, alpha_d, X, X, 1.0, s);
+    launch_bicgstab_update<double>(cnt, from_c<V>(omega), X, ZS_.get(), R_.get(), S_.get(), T_.get(),
+                                   s);
+    alg_.col_norms(R_.get(), tmp, s);
+    record_convergence(rep, tmp, bnorm, tol, rep.cycles);
+    if (rep.history.back() <= tol) {
+      finalize();
+      if (rep.all_converged()) break;
+      true_residual();
+      copy(P_.get(), R_.get());
+      copy(Rt_.get(), R_.get());
+      continue;
+    }
+    alg_.gram(tRt, 1, T_.get(), RtR_d, s);
+    ++rep.block_gram_products;
+    download_kk(RtR_d, RtT);
+    for (auto& x : RtT) x = -x;
+    std::vector<cplx> beta;
+    try {
+      beta = solve_small(RtV, RtT, k, k);
+    } catch (const HzError& e) {
+      if (e.code != kFactorization) throw;
+      try_restart(rep.cycles);
+      continue;
+    }
+    upload_kk(beta, beta_d);
+    // P = R + (P - omega V) beta
+    copy(PmV_.get(), P_.get());
+    launch_axpby<double>(cnt, mk(1.0, 0.0), PmV_.get(), from_c<V>(-omega), V_.get(), s);
+    launch_multi_update<double>(n, k, 1, tPmV, beta_d, R_.get(), P_.get(), 1.0, s);
+    if (!op.prec) ++rep.cycles;
+  }
+  if (rep.rel_residual.empty()) finalize();
+  rep.wall_s = std::chrono::duration<double>(Clock::now() - t0).count();
+  return rep;
+}
+
+}  // namespace hz

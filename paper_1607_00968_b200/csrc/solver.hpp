@@ -1,0 +1,211 @@
+// Host-side C++ driver of the B200 solver: the Helmholtz problem, the
+// shifted-Laplacian multigrid hierarchy and the block Krylov methods. The
+// control flow (cycle recursion, Krylov iterations, k x k algebra) runs on the
+// host; every grid- or block-sized operation is an sm_100a kernel enqueued on
+// the solver's stream.
+#pragma once
+
+#include <array>
+#include <complex>
+#include <functional>
+#include <memory>
+#include <vector>
+
+#include "devbuf.hpp"
+#include "kernels.hpp"
+
+namespace hz {
+
+using cplx = std::complex<double>;
+
+// ------------------------------------------------------------------ problem
+// Mirrors seistomo::HelmholtzProblem (inc/helmholtz.hpp:19-57,
+// src/helmholtz.cpp:16-43): A = Lap_h + omega^2 (1 - i gamma/omega) m with
+// gamma = base + omega * ramp (AttenuationField, inc/attenuation.hpp:11-22).
+struct Problem {
+  int ndim = 2;
+  std::array<int64_t, 3> n{1, 1, 1};
+  std::array<double, 3> h{1, 1, 1};
+  double omega = 0, gamma_base = 0;
+  std::vector<double> m, ramp;
+  std::vector<cplx> mass, gamma_factor;  // host copies (reference arithmetic)
+  double inv_h2[3] = {0, 0, 0};
+  double center_lap = 0;
+  int device = 0;
+  // device: centre of the unshifted operator (center_lap + mass) and (1 - i gamma/omega)
+  DevBuf<double2> d_center, d_gf;
+
+  Problem(int ndim, const int64_t* n, const double* h, const double* m, double omega,
+          double gamma_base, const double* ramp, bool allow_coarse, int device);
+  int64_t num_nodes() const { return n[0] * n[1] * n[2]; }
+  double points_per_wavelength() const;
+  double min_h() const;
+  // shifted centre (HelmholtzProblem::to_csr diagonal, src/helmholtz.cpp:108)
+  std::vector<cplx> shifted_center(double shift) const;
+  LevelOp<double> fine_op(int k) const;  // unshifted, for apply / residual
+};
+
+// ------------------------------------------------------------------ cycles
+enum class CycleKind : int { V = 0, W = 1, K = 2 };
+
+struct CycleSpec {  // inc/multigrid.hpp:17-23
+  CycleKind kind = CycleKind::W;
+  int pre = 2;
+  int post = 2;
+  double jacobi_weight = 0.8;
+  int k_inner = 2;
+};
+
+template <class T> class Fgmres;
+
+// Per-level device storage of one precision.
+template <class T>
+struct MgLevelDev {
+  using V = cplx_t<T>;
+  std::array<int64_t, 3> dims{1, 1, 1};
+  int kind = kFine;
+  DevBuf<V> center;    // level 0: shifted centre
+  DevBuf<V> coef;      // levels >= 1: [S][n] Galerkin planes
+  DevBuf<V> inv_diag;  // D^{-1}
+  T w[3] = {0, 0, 0};
+  int64_t nodes() const { return dims[0] * dims[1] * dims[2]; }
+};
+
+// Shifted-Laplacian Galerkin hierarchy (MgHierarchy, inc/multigrid.hpp:44-80)
+// held on the device in precision T, with the coarsest operator applied as
+// an explicit inverse formed from the reference's banded LU factors.
+template <class T>
+class Hierarchy {
+ public:
+  using V = cplx_t<T>;
+  // Build from f64 setup data (the f64 hierarchy is always built first; the
+  // c64 one is a rounded copy so both apply the same operators).
+  static std::unique_ptr<Hierarchy<double>> build(const Problem& p, int nlevels, double shift,
+                                                  cudaStream_t s);
+  static std::unique_ptr<Hierarchy<float>> rounded(const Hierarchy<double>& h64, cudaStream_t s);
+
+  int num_levels() const { return int(levels_.size()); }
+  const MgLevelDev<T>& level(int l) const { return levels_[l]; }
+  int ndim() const { return ndim_; }
+  int64_t coarse_n() const { return levels_.back().nodes(); }
+  int64_t coarse_band() const { return band_; }
+
+  LevelOp<T> op(int l, int k) const;
+  // One cycle on the level-0 system A X = B (x updated in place; x_zero
+  // means the caller guarantees x == 0 on entry, as the preconditioner
+  // application does, src/helmholtz_solver.cpp:65-68).
+  void cycle(const CycleSpec& spec, int k, const V* b, V* x, bool x_zero, cudaStream_t s);
+  void coarse_solve(int k, const V* b, V* x, cudaStream_t s);
+  // Galerkin planes / diagonal of level l (host copy, f64) for parity checks
+  void download_level(int l, std::vector<cplx>& coef_or_center) const;
+
+  std::vector<MgLevelDev<T>> levels_;
+  DevBuf<V> ainvT_;  // coarsest inverse, transposed [n_c][n_c]
+  int ndim_ = 2;
+  int64_t band_ = 0;
+
+ private:
+  void ensure_ws(int k);
+  void cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V* x, bool x_zero,
+                 cudaStream_t s);
+  void relax(int l, const CycleSpec& spec, int sweeps, int k, const V* b, V*& cur, V*& other,
+             bool& cur_zero, cudaStream_t s);
+  void kcycle_coarse(int l, const CycleSpec& spec, int k, const V* b, V* x, cudaStream_t s);
+  int ws_k_ = 0;
+  std::vector<DevBuf<V>> wx_, wt_, wb_, wr_;  // per level: solution, ping-pong, rhs, residual
+  std::vector<std::unique_ptr<Fgmres<T>>> kfgm_;
+};
+
+// explicit inverse of the unshifted operator (HelmholtzMethod::DenseLuSmall)
+DevBuf<double2> dense_inverse(const Problem& p, cudaStream_t s);
+
+// ------------------------------------------------------------------ Krylov
+struct Report {  // seistomo::SolveReport (inc/krylov.hpp:19-40)
+  int cycles = 0;
+  std::vector<int> col_cycles;
+  std::vector<double> rel_residual;
+  std::vector<char> converged;
+  std::vector<double> history;
+  double wall_s = 0;
+  int qr_factorizations = 0;
+  int64_t block_gram_products = 0;
+  bool all_converged() const {
+    for (char c : converged)
+      if (!c) return false;
+    return !converged.empty();
+  }
+};
+
+// Matrix-free block operator on device blocks (BlockOperator, inc/krylov.hpp:13-17).
+template <class T>
+struct DevOp {
+  using V = cplx_t<T>;
+  int64_t n = 0;
+  std::function<void(const V* in, V* out, int k, cudaStream_t)> apply;
+  std::function<void(const V* in, V* out, int k, cudaStream_t)> prec;  // optional
+};
+
+// Device block algebra shared by the Krylov methods.
+template <class T>
+class BlockAlgebra {
+ public:
+  using V = cplx_t<T>;
+  void ensure(int64_t n, int k, int max_blocks);
+  // G_i = X_i^H Y for nb blocks, result on device (nb k^2, row-major tiles)
+  void gram(const BlockTab<T>& tab, int nb, const V* Y, V* out, cudaStream_t s);
+  // per-column 2-norms to host
+  void col_norms(const V* X, std::vector<double>& out, cudaStream_t s);
+  // CholQR2 thin QR of W in place (inc/block.hpp:104-137 semantics):
+  // enqueues the work; R (k x k, row-major) and the rank-deficient flag are
+  // available after sync in host_R()/host_deficient().
+  void thin_qr_enqueue(V* W, cudaStream_t s);
+  void thin_qr_finish(std::vector<cplx>& R, bool& deficient);  // after stream sync
+
+  int64_t n = 0;
+  int k = 0;
+  int nslots = 0;
+  DevBuf<V> partials, tmp_blk, G, R1, R1i, R2, R2i;
+  DevBuf<T> rpart, rnorm;
+  DevBuf<int> flags;
+  PinnedBuf<T> h_norm;
+  PinnedBuf<V> h_R;     // [R1 | R2]
+  PinnedBuf<int> h_flags;
+};
+
+template <class T>
+class Fgmres {
+ public:
+  using V = cplx_t<T>;
+  // block_fgmres (src/krylov.cpp:178-280): X = 0 start, flexible, restart m.
+  Report solve(const DevOp<T>& op, int k, const V* B, V* X, int restart, double tol,
+               int max_cycles, cudaStream_t s);
+
+ private:
+  void ensure(int64_t n, int k, int restart);
+  int64_t n_ = 0;
+  int k_ = 0, m_ = 0;
+  std::vector<DevBuf<V>> Vb_, Zb_;
+  DevBuf<V> R_;
+  BlockTab<T> vtab_{}, ztab_{};
+  DevBuf<V> hcol1_, hcol2_, ydev_;
+  PinnedBuf<V> h_hcol_, h_y_;
+  BlockAlgebra<T> alg_;
+};
+
+// block_bicgstab (src/krylov.cpp:60-176), f64.
+class Bicgstab {
+ public:
+  using V = double2;
+  Report solve(const DevOp<double>& op, int k, const V* B, V* X, double tol, int max_cycles,
+               cudaStream_t s);
+
+ private:
+  void ensure(int64_t n, int k);
+  int64_t n_ = 0;
+  int k_ = 0;
+  DevBuf<V> R_, Rt_, P_, ZP_, V_, S_, ZS_, T_, PmV_, cdev_, fpart_, fsum_;
+  PinnedBuf<V> h_small_;
+  BlockAlgebra<double> alg_;
+};
+
+}  // namespace hz

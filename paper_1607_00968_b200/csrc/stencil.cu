@@ -1,0 +1,449 @@
+// Grid kernels of the shifted-Laplacian multigrid and the Helmholtz operator
+// over node-major RHS-interleaved blocks x[node][k] (inc/block.hpp:13-27).
+//
+// Thread mapping: one thread per (node, column) element, consecutive threads
+// on consecutive elements, so every warp-wide load of a neighbour plane is a
+// contiguous, fully coalesced 512 B (c128) / 256 B (c64) transaction and each
+// per-node coefficient is fetched once per warp and broadcast across the k
+// columns that share it. x-neighbours hit L1; y/z neighbour planes were
+// fetched moments earlier by neighbouring CTAs and hit the 126 MB L2, so HBM
+// sees (close to) one read per input and one write per output: these kernels
+// are HBM-bandwidth bound.
+#include "kernels.hpp"
+
+namespace hz {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+template <class T>
+struct Elem {
+  uint32_t node, col, i, j, kz;
+};
+
+template <class T>
+__device__ __forceinline__ bool decode(const LevelGeom& g, uint32_t e, Elem<T>& el) {
+  if (e >= g.nodes * g.k) return false;
+  g.div_k.divmod(e, el.node, el.col);
+  g.unpack(el.node, el.i, el.j, el.kz);
+  return true;
+}
+
+// (A x)[e] for the fine 5/7-point operator.
+// CSR=false: HelmholtzProblem::apply_block order -- centre first, then
+//            x-, x+, y-, y+, z-, z+ (src/helmholtz.cpp:85-98).
+// CSR=true : Csr::mul_block order over the sorted row -- z-, y-, x-, centre,
+//            x+, y+, z+ (inc/csr.hpp:43-53), used by the multigrid levels.
+template <class T, int NDIM, bool CSR>
+__device__ __forceinline__ cplx_t<T> fine_ax(const LevelOp<T>& op, const cplx_t<T>* __restrict__ x,
+                                             uint32_t e, const Elem<T>& el) {
+  using V = cplx_t<T>;
+  const LevelGeom& g = op.g;
+  const uint32_t sx = g.k, sy = g.n0 * g.k, sz = g.n0 * g.n1 * g.k;
+  const V c = __ldg(&op.center[el.node]);
+  V acc;
+  if (!CSR) {
+    acc = cmul(c, __ldg(&x[e]));
+    if (el.i > 0) acc = crfma(op.w[0], __ldg(&x[e - sx]), acc);
+    if (el.i + 1 < g.n0) acc = crfma(op.w[0], __ldg(&x[e + sx]), acc);
+    if (el.j > 0) acc = crfma(op.w[1], __ldg(&x[e - sy]), acc);
+    if (el.j + 1 < g.n1) acc = crfma(op.w[1], __ldg(&x[e + sy]), acc);
+    if (NDIM == 3) {
+      if (el.kz > 0) acc = crfma(op.w[2], __ldg(&x[e - sz]), acc);
+      if (el.kz + 1 < g.n2) acc = crfma(op.w[2], __ldg(&x[e + sz]), acc);
+    }
+  } else {
+    acc = czero<V>();
+    if (NDIM == 3 && el.kz > 0) acc = crfma(op.w[2], __ldg(&x[e - sz]), acc);
+    if (el.j > 0) acc = crfma(op.w[1], __ldg(&x[e - sy]), acc);
+    if (el.i > 0) acc = crfma(op.w[0], __ldg(&x[e - sx]), acc);
+    acc = cfma(c, __ldg(&x[e]), acc);
+    if (el.i + 1 < g.n0) acc = crfma(op.w[0], __ldg(&x[e + sx]), acc);
+    if (el.j + 1 < g.n1) acc = crfma(op.w[1], __ldg(&x[e + sy]), acc);
+    if (NDIM == 3 && el.kz + 1 < g.n2) acc = crfma(op.w[2], __ldg(&x[e + sz]), acc);
+  }
+  return acc;
+}
+
+// (A x)[e] for a Galerkin 9/27-point stencil, ascending CSR column order.
+template <class T, int NDIM>
+__device__ __forceinline__ cplx_t<T> stencil_ax(const LevelOp<T>& op,
+                                                const cplx_t<T>* __restrict__ x, uint32_t e,
+                                                const Elem<T>& el) {
+  using V = cplx_t<T>;
+  const LevelGeom& g = op.g;
+  const int64_t sx = g.k, sy = int64_t(g.n0) * g.k, sz = int64_t(g.n0) * g.n1 * g.k;
+  const V* __restrict__ cf = op.coef + el.node;
+  V acc = czero<V>();
+  const int zlo = NDIM == 3 ? -1 : 0, zhi = NDIM == 3 ? 1 : 0;
+#pragma unroll
+  for (int dz = zlo; dz <= zhi; ++dz) {
+    const bool okz = NDIM == 2 || (dz < 0 ? el.kz > 0 : (dz > 0 ? el.kz + 1 < g.n2 : true));
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const bool oky = dy < 0 ? el.j > 0 : (dy > 0 ? el.j + 1 < g.n1 : true);
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const bool okx = dx < 0 ? el.i > 0 : (dx > 0 ? el.i + 1 < g.n0 : true);
+        const int s = (NDIM == 3 ? (dz + 1) * 9 : 0) + (dy + 1) * 3 + (dx + 1);
+        if (okz && oky && okx) {
+          const V a = __ldg(&cf[int64_t(s) * g.nodes]);
+          acc = cfma(a, __ldg(&x[int64_t(e) + dz * sz + dy * sy + dx * sx]), acc);
+        }
+      }
+    }
+  }
+  return acc;
+}
+
+template <class T, int NDIM, int KIND, bool CSR>
+__device__ __forceinline__ cplx_t<T> level_ax(const LevelOp<T>& op, const cplx_t<T>* x, uint32_t e,
+                                              const Elem<T>& el) {
+  if constexpr (KIND == kFine)
+    return fine_ax<T, NDIM, CSR>(op, x, e, el);
+  else
+    return stencil_ax<T, NDIM>(op, x, e, el);
+}
+
+// MODE 0: out = A x ; 1: out = b - A x ; 2: out = x + (wj dinv)(b - A x)
+template <class T, int NDIM, int KIND, int MODE>
+__global__ void __launch_bounds__(kBlock)
+level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
+             cplx_t<T>* __restrict__ out, T wj) {
+  using V = cplx_t<T>;
+  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  Elem<T> el;
+  if (!decode(op.g, e, el)) return;
+  const V ax = level_ax<T, NDIM, KIND, MODE != 0>(op, x, e, el);
+  if (MODE == 0) {
+    out[e] = ax;
+  } else if (MODE == 1) {
+    out[e] = csub(__ldg(&b[e]), ax);
+  } else {
+    const V d = __ldg(&op.inv_diag[el.node]);
+    const V wd = mk(wj * d.x, wj * d.y);
+    out[e] = cadd(__ldg(&x[e]), cmul(wd, csub(__ldg(&b[e]), ax)));
+  }
+}
+
+template <class T, class In>
+__global__ void __launch_bounds__(kBlock)
+jacobi_zero_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj,
+                   const In* __restrict__ b, cplx_t<T>* __restrict__ out) {
+  using V = cplx_t<T>;
+  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  if (e >= g.nodes * g.k) return;
+  const uint32_t node = g.div_k.div(e);
+  const V d = __ldg(&inv_diag[node]);
+  const V wd = mk(wj * d.x, wj * d.y);
+  out[e] = cmul(wd, ccast<V>(__ldg(&b[e])));
+}
+
+// rc[C] = sum_{f in 3^d box around 2C} w_f r[f], f ascending (the CSR of
+// R = P^T visits fine rows in order, inc/csr.hpp:110-127).
+template <class T, int NDIM>
+__global__ void __launch_bounds__(kBlock)
+restrict_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r,
+                cplx_t<T>* __restrict__ bc) {
+  using V = cplx_t<T>;
+  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  Elem<T> el;
+  if (!decode(gc, e, el)) return;
+  const int64_t k = gf.k;
+  V acc = czero<V>();
+  const int zlo = NDIM == 3 ? -1 : 0, zhi = NDIM == 3 ? 1 : 0;
+#pragma unroll
+  for (int ez = zlo; ez <= zhi; ++ez) {
+    const int64_t fz = 2 * int64_t(el.kz) + ez;
+    if (fz < 0 || fz >= gf.n2) continue;
+    const T wz = ez == 0 ? T(1) : T(0.5);
+#pragma unroll
+    for (int ey = -1; ey <= 1; ++ey) {
+      const int64_t fy = 2 * int64_t(el.j) + ey;
+      if (fy < 0 || fy >= gf.n1) continue;
+      const T wy = ey == 0 ? T(1) : T(0.5);
+#pragma unroll
+      for (int ex = -1; ex <= 1; ++ex) {
+        const int64_t fx = 2 * int64_t(el.i) + ex;
+        if (fx < 0 || fx >= gf.n0) continue;
+        const T wx = ex == 0 ? T(1) : T(0.5);
+        const int64_t f = fx + int64_t(gf.n0) * (fy + int64_t(gf.n1) * fz);
+        acc = crfma(wx * wy * wz, __ldg(&r[f * k + el.col]), acc);
+      }
+    }
+  }
+  bc[e] = acc;
+}
+
+// x[f] += sum_{C parents of f} w ec[C]  (corr summed first, then added:
+// axpby(x, 1, corr, 1), src/multigrid.cpp:195-197)
+template <class T, int NDIM>
+__global__ void __launch_bounds__(kBlock)
+prolong_correct_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec,
+                       cplx_t<T>* __restrict__ x) {
+  using V = cplx_t<T>;
+  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  Elem<T> el;
+  if (!decode(gf, e, el)) return;
+  const int64_t k = gf.k;
+  uint32_t cx[2], cy[2], cz[2];
+  T wxv[2], wyv[2], wzv[2];
+  int nx, ny, nz;
+  auto axis = [](uint32_t f, uint32_t* c, T* w) -> int {
+    if ((f & 1u) == 0) {
+      c[0] = f >> 1;
+      w[0] = T(1);
+      return 1;
+    }
+    c[0] = (f - 1) >> 1;
+    c[1] = (f + 1) >> 1;
+    w[0] = w[1] = T(0.5);
+    return 2;
+  };
+  nx = axis(el.i, cx, wxv);
+  ny = axis(el.j, cy, wyv);
+  if (NDIM == 3) {
+    nz = axis(el.kz, cz, wzv);
+  } else {
+    nz = 1;
+    cz[0] = 0;
+    wzv[0] = T(1);
+  }
+  V corr = czero<V>();
+  for (int c = 0; c < nz; ++c)
+    for (int b = 0; b < ny; ++b)
+      for (int a = 0; a < nx; ++a) {
+        const int64_t C = cx[a] + int64_t(gc.n0) * (cy[b] + int64_t(gc.n1) * cz[c]);
+        corr = crfma(wxv[a] * wyv[b] * wzv[c], __ldg(&ec[C * k + el.col]), corr);
+      }
+  x[e] = cadd(x[e], corr);
+}
+
+// ---------------------------------------------------------------- Galerkin
+// Fine-operator entry A[f][f+o], o in {-1,0,1}^3 (0 if absent).
+template <int NDIM, int KIND>
+__device__ __forceinline__ double2 fine_entry(const LevelOp<double>& op, int64_t f, int ox, int oy,
+                                              int oz) {
+  if constexpr (KIND == kFine) {
+    const int nz = (ox != 0) + (oy != 0) + (oz != 0);
+    if (nz == 0) return op.center[f];
+    if (nz > 1) return make_double2(0.0, 0.0);
+    const int a = ox != 0 ? 0 : (oy != 0 ? 1 : 2);
+    return make_double2(op.w[a], 0.0);
+  } else {
+    const int s = (NDIM == 3 ? (oz + 1) * 9 : 0) + (oy + 1) * 3 + (ox + 1);
+    return op.coef[int64_t(s) * op.g.nodes + f];
+  }
+}
+
+// One thread per coarse node C. Follows the reference's two Gustavson
+// products: AP = A P (row f, g ascending, then P-row targets ascending),
+// then (R AP)[C] over f ascending (inc/csr.hpp:130-160). All weights are
+// powers of two, so each product is exact and the sums run in the reference
+// order.
+template <int NDIM, int KIND>
+__global__ void __launch_bounds__(128)
+galerkin_kernel(LevelOp<double> fine, LevelGeom gc, double2* __restrict__ coef_c) {
+  const uint32_t C = blockIdx.x * 128 + threadIdx.x;
+  if (C >= gc.nodes) return;
+  const LevelGeom& gf = fine.g;
+  uint32_t I, J, K;
+  gc.unpack(C, I, J, K);
+  constexpr int S = NDIM == 3 ? 27 : 9;
+  double2 acc[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) acc[s] = make_double2(0.0, 0.0);
+  const int zlo = NDIM == 3 ? -1 : 0, zhi = NDIM == 3 ? 1 : 0;
+  for (int ez = zlo; ez <= zhi; ++ez) {
+    const int64_t fz = 2 * int64_t(K) + ez;
+    if (fz < 0 || fz >= gf.n2) continue;
+    for (int ey = -1; ey <= 1; ++ey) {
+      const int64_t fy = 2 * int64_t(J) + ey;
+      if (fy < 0 || fy >= gf.n1) continue;
+      for (int ex = -1; ex <= 1; ++ex) {
+        const int64_t fx = 2 * int64_t(I) + ex;
+        if (fx < 0 || fx >= gf.n0) continue;
+        const double wf = (ex ? 0.5 : 1.0) * (ey ? 0.5 : 1.0) * (ez ? 0.5 : 1.0);
+        const int64_t f = fx + int64_t(gf.n0) * (fy + int64_t(gf.n1) * fz);
+        double2 ap[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) ap[s] = make_double2(0.0, 0.0);
+        // A row f, ascending column: oz, oy, ox
+        for (int oz = zlo; oz <= zhi; ++oz) {
+          const int64_t gz = fz + oz;
+          if (gz < 0 || gz >= gf.n2) continue;
+          for (int oy = -1; oy <= 1; ++oy) {
+            const int64_t gy = fy + oy;
+            if (gy < 0 || gy >= gf.n1) continue;
+            for (int ox = -1; ox <= 1; ++ox) {
+              const int64_t gx = fx + ox;
+              if (gx < 0 || gx >= gf.n0) continue;
+              if (KIND == kFine && ((ox != 0) + (oy != 0) + (oz != 0)) > 1) continue;
+              const double2 a = fine_entry<NDIM, KIND>(fine, f, ox, oy, oz);
+              if (KIND == kStencil && a.x == 0.0 && a.y == 0.0) continue;
+              // P row g: parents ascending (z, y, x)
+              int64_t pz[2], py[2], px[2];
+              double wz[2], wy[2], wx[2];
+              int nzp, nyp, nxp;
+              auto par = [](int64_t gcoord, int64_t* p, double* w) -> int {
+                if ((gcoord & 1) == 0) {
+                  p[0] = gcoord / 2;
+                  w[0] = 1.0;
+                  return 1;
+                }
+                p[0] = (gcoord - 1) / 2;
+                p[1] = (gcoord + 1) / 2;
+                w[0] = w[1] = 0.5;
+                return 2;
+              };
+              nxp = par(gx, px, wx);
+              nyp = par(gy, py, wy);
+              if (NDIM == 3) {
+                nzp = par(gz, pz, wz);
+              } else {
+                nzp = 1;
+                pz[0] = 0;
+                wz[0] = 1.0;
+              }
+              for (int c = 0; c < nzp; ++c)
+                for (int b = 0; b < nyp; ++b)
+                  for (int q = 0; q < nxp; ++q) {
+                    const int dx = int(px[q] - I), dy = int(py[b] - J),
+                              dz = NDIM == 3 ? int(pz[c] - K) : 0;
+                    const int s = (NDIM == 3 ? (dz + 1) * 9 : 0) + (dy + 1) * 3 + (dx + 1);
+                    const double p = wx[q] * wy[b] * wz[c];
+                    ap[s].x += a.x * p;
+                    ap[s].y += a.y * p;
+                  }
+            }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          acc[s].x += wf * ap[s].x;
+          acc[s].y += wf * ap[s].y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) coef_c[int64_t(s) * gc.nodes + C] = acc[s];
+}
+
+template <class Dst, class Src>
+__global__ void __launch_bounds__(kBlock) cast_kernel(int64_t count, const Src* __restrict__ in,
+                                                      Dst* __restrict__ out) {
+  const int64_t e = int64_t(blockIdx.x) * kBlock + threadIdx.x;
+  if (e < count) out[e] = ccast<Dst>(in[e]);
+}
+
+template <class T, int MODE>
+void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out,
+                    T wj, cudaStream_t s) {
+  const int64_t total = int64_t(op.g.nodes) * op.g.k;
+  const int grid = grid_for(total, kBlock);
+  if (op.kind == kFine) {
+    if (op.ndim == 3)
+      level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+    else
+      level_kernel<T, 2, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+  } else {
+    if (op.ndim == 3)
+      level_kernel<T, 3, kStencil, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+    else
+      level_kernel<T, 2, kStencil, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+  }
+  HZ_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+template <class T>
+void launch_apply(const LevelOp<T>& op, const cplx_t<T>* u, cplx_t<T>* out, cudaStream_t s) {
+  dispatch_level<T, 0>(op, u, nullptr, out, T(0), s);
+}
+template <class T>
+void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
+                     cudaStream_t s) {
+  dispatch_level<T, 1>(op, x, b, r, T(0), s);
+}
+template <class T>
+void launch_jacobi(const LevelOp<T>& op, T wj, const cplx_t<T>* x, const cplx_t<T>* b,
+                   cplx_t<T>* xout, cudaStream_t s) {
+  dispatch_level<T, 2>(op, x, b, xout, wj, s);
+}
+template <class T, class In>
+void launch_jacobi_zero(const LevelOp<T>& op, T wj, const In* b, cplx_t<T>* xout, cudaStream_t s) {
+  const int64_t total = int64_t(op.g.nodes) * op.g.k;
+  jacobi_zero_kernel<T, In><<<grid_for(total, kBlock), kBlock, 0, s>>>(op.g, op.inv_diag, wj, b, xout);
+  HZ_LAUNCH_CHECK();
+}
+template <class T>
+void launch_restrict(const LevelGeom& gf, const LevelGeom& gc, int ndim, const cplx_t<T>* r,
+                     cplx_t<T>* bc, cudaStream_t s) {
+  const int grid = grid_for(int64_t(gc.nodes) * gc.k, kBlock);
+  if (ndim == 3)
+    restrict_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, r, bc);
+  else
+    restrict_kernel<T, 2><<<grid, kBlock, 0, s>>>(gf, gc, r, bc);
+  HZ_LAUNCH_CHECK();
+}
+template <class T>
+void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
+                            const cplx_t<T>* ec, cplx_t<T>* x, cudaStream_t s) {
+  const int grid = grid_for(int64_t(gf.nodes) * gf.k, kBlock);
+  if (ndim == 3)
+    prolong_correct_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
+  else
+    prolong_correct_kernel<T, 2><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
+  HZ_LAUNCH_CHECK();
+}
+
+void launch_galerkin(const LevelOp<double>& fine, const LevelGeom& gc, double2* coef_c,
+                     cudaStream_t s) {
+  const int grid = grid_for(gc.nodes, 128);
+  if (fine.kind == kFine) {
+    if (fine.ndim == 3)
+      galerkin_kernel<3, kFine><<<grid, 128, 0, s>>>(fine, gc, coef_c);
+    else
+      galerkin_kernel<2, kFine><<<grid, 128, 0, s>>>(fine, gc, coef_c);
+  } else {
+    if (fine.ndim == 3)
+      galerkin_kernel<3, kStencil><<<grid, 128, 0, s>>>(fine, gc, coef_c);
+    else
+      galerkin_kernel<2, kStencil><<<grid, 128, 0, s>>>(fine, gc, coef_c);
+  }
+  HZ_LAUNCH_CHECK();
+}
+
+template <class Dst, class Src>
+void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s) {
+  cast_kernel<Dst, Src><<<grid_for(count, kBlock), kBlock, 0, s>>>(count, in, out);
+  HZ_LAUNCH_CHECK();
+}
+
+#define HZ_INST(T)                                                                                 \
+  template void launch_apply<T>(const LevelOp<T>&, const cplx_t<T>*, cplx_t<T>*, cudaStream_t);   \
+  template void launch_residual<T>(const LevelOp<T>&, const cplx_t<T>*, const cplx_t<T>*,         \
+                                   cplx_t<T>*, cudaStream_t);                                     \
+  template void launch_jacobi<T>(const LevelOp<T>&, T, const cplx_t<T>*, const cplx_t<T>*,        \
+                                 cplx_t<T>*, cudaStream_t);                                       \
+  template void launch_restrict<T>(const LevelGeom&, const LevelGeom&, int, const cplx_t<T>*,     \
+                                   cplx_t<T>*, cudaStream_t);                                     \
+  template void launch_prolong_correct<T>(const LevelGeom&, const LevelGeom&, int,                \
+                                          const cplx_t<T>*, cplx_t<T>*, cudaStream_t);
+HZ_INST(double)
+HZ_INST(float)
+#undef HZ_INST
+template void launch_jacobi_zero<double, double2>(const LevelOp<double>&, double, const double2*,
+                                                  double2*, cudaStream_t);
+template void launch_jacobi_zero<float, float2>(const LevelOp<float>&, float, const float2*,
+                                                float2*, cudaStream_t);
+template void launch_jacobi_zero<float, double2>(const LevelOp<float>&, float, const double2*,
+                                                 float2*, cudaStream_t);
+template void launch_cast<float2, double2>(int64_t, const double2*, float2*, cudaStream_t);
+template void launch_cast<double2, float2>(int64_t, const float2*, double2*, cudaStream_t);
+template void launch_cast<double2, double2>(int64_t, const double2*, double2*, cudaStream_t);
+
+}  // namespace hz
