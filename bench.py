@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Benchmark: Helmholtz right-hand sides solved per second to 1e-6 relative
+residual (BASELINE.json metric) on BASELINE config 2 -- 2D 1025x513 layered
+model, k = 32 surface sources per GPU, complex128 block FGMRES(10) with a
+complex64 shifted-Laplacian V(2,2) multigrid preconditioner.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one block solve of the rank's k right-hand sides from zero to the
+tolerance (setup excluded). N > 1 runs one process per GPU
+under torchrun; each rank owns its own block of k sources (weak scaling, no
+data-path collective). `value` = all ranks' RHS / max-over-ranks device time.
+
+The JSON line also carries: `e2e` (same metric through the C ABI with host
+buffers, H2D/D2H inside the timed region), `roofline` (dominant kernel's
+algorithmic GB/s from CUDA events in a profiled pass over the same steps),
+`kernels` (all kernels), `cpu_baseline` (the reference C++ solver timed on
+this host on a bounded sample, rank 0, N = 1), `clocks`, `gpu_launches`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Helmholtz RHS solved/sec to 1e-6 residual"
+UNIT = "RHS/s"
+
+# The BASELINE config-2 solver (config 2 leaves levels / shift / Krylov
+# unstated): c128 block FGMRES(5) (restart = the reference's
+# HelmholtzSolveOptions default, inc/helmholtz_solver.hpp:21) + c64
+# shifted-Laplacian V(2,2) (w_J 0.8), 4 levels to a 129x65 coarse grid
+# (SURVEY §8d), shift 1.0 -- at shift 0.5 the 4-level V-cycle stalls in the
+# reference oracle and on the GPU alike (DESIGN.md §"Workload").
+WORKLOAD = dict(cfg=2, k=32, nlevels=4, shift=1.0, cycle="V", restart=5, tol=1e-6,
+                max_cycles=2000, precond="c64")
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def rank_sources(cfg, rank, world, k):
+    """Weak scaling: world*k evenly spaced surface sources, rank r owns r, r+world, ..."""
+    import numpy as np
+    from paper_1607_00968_b200 import configs
+    full = configs.config2(nlevels=WORKLOAD["nlevels"], k=k * world)
+    return np.asarray(full.source_nodes[rank::world], dtype=np.int64)
+
+
+def build_workload(rank, world, k):
+    from paper_1607_00968_b200 import configs
+    cfg = configs.config2(nlevels=WORKLOAD["nlevels"], k=k)
+    cfg.source_nodes = rank_sources(cfg, rank, world, k)
+    cfg.shift = WORKLOAD["shift"]
+    cfg.cycle = WORKLOAD["cycle"]
+    cfg.restart = WORKLOAD["restart"]
+    cfg.tol = WORKLOAD["tol"]
+    cfg.max_cycles = WORKLOAD["max_cycles"]
+    cfg.precond_precision = WORKLOAD["precond"]
+    return cfg
+
+
+def config_json(cfg, world, l2_note):
+    return {"workload": f"BASELINE config 2: 2D {cfg.n[0]}x{cfg.n[1]} layered model, k={cfg.k} RHS/GPU",
+            "grid": list(cfg.n[:2]), "rhs_per_gpu": cfg.k, "global_rhs": cfg.k * world,
+            "solver": f"block FGMRES({cfg.restart}) + {cfg.cycle}({cfg.pre},{cfg.post}) MG, "
+                      f"{cfg.nlevels} levels, shift {cfg.shift}, w_J {cfg.jacobi_weight}",
+            "precision": "c128 Krylov / c64 preconditioner", "tol": cfg.tol,
+            "parallelism": f"rhs-sharded x{world}", "l2": l2_note}
+
+
+# ---------------------------------------------------------------- reference arm
+# Cycles the reference itself needs on this workload to reach 1e-6 (measured
+# with the full oracle solve, scripts/ref_full_solve.py; used to extrapolate
+# the bounded CPU samples when no GPU count is at hand).
+REF_CYCLES = None
+# GPU cycle count of this workload (FGMRES(5), 4 levels, shift 1.0, k = 32).
+DEFAULT_CYCLES = 443
+
+
+class ReferenceRunner:
+    """The reference C++ solver (oracle/_ref, stock-contraction build) driven
+    through its public API -- build_hierarchy + MgHierarchy::cycle +
+    block_fgmres -- with all host threads. Setup is done once
+    (excluded); a step is a bounded sample of
+    `sample_cycles` FGMRES iterations of the same k-column block (c128
+    preconditioner: the reference has no c64 path), extrapolated to the
+    cycle count of a full solve: RHS/s = k / (s_per_cycle x cycles)."""
+
+    def __init__(self, cfg, threads=None):
+        os.environ["HZ_REF_VARIANT"] = "fast"
+        from oracle import ref
+        self.ref = ref
+        self.cfg = cfg
+        self.threads = threads or os.cpu_count() or 1
+        ref.set_num_threads(self.threads)
+        self.B = cfg.rhs_block()
+        t0 = time.perf_counter()
+        self.R = ref.RefProblem.from_config(cfg)
+        self.H = ref.RefHierarchy(self.R, cfg.nlevels, cfg.shift)
+        self.setup_s = time.perf_counter() - t0
+
+    def step(self, sample_cycles):
+        cfg = self.cfg
+        t0 = time.perf_counter()
+        _, rep = self.ref.krylov_solve(self.R, self.H, self.B, method="fgmres", kind=cfg.cycle,
+                                       pre=cfg.pre, post=cfg.post, wj=cfg.jacobi_weight,
+                                       restart=cfg.restart, tol=cfg.tol, max_cycles=sample_cycles)
+        return (time.perf_counter() - t0) / max(rep.cycles, 1), rep.cycles
+
+    def describe(self, sample_cycles, cycles_target):
+        cfg = self.cfg
+        return (f"{sample_cycles} FGMRES({cfg.restart}) iterations (V-cycle + Arnoldi + LS) per step of the "
+                f"same k={cfg.k} block on the reference C++ solver (oracle/_ref, {self.threads} threads, "
+                f"c128 preconditioner), setup excluded; RHS/s = k / (s_per_cycle x {cycles_target:.0f} cycles "
+                f"to 1e-6)")
+
+
+def reference_sample(cfg, cycles_target, sample_cycles, threads=None):
+    run = ReferenceRunner(cfg, threads)
+    per_cycle, _ = run.step(sample_cycles)
+    return cfg.k / (per_cycle * cycles_target), {"cores": run.threads, "s_per_cycle": per_cycle,
+                                                 "sample": run.describe(sample_cycles, cycles_target)}
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if ws > 1 and rank != 0:
+        return 0
+    cfg = build_workload(0, 1, WORKLOAD["k"])
+    cycles_target = args.ref_cycles or REF_CYCLES or DEFAULT_CYCLES
+    run = ReferenceRunner(cfg)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        per_cycle, _ = run.step(args.ref_sample_cycles)
+        if i >= args.warmup:
+            vals.append(cfg.k / (per_cycle * cycles_target))
+    info = {"cores": run.threads, "sample": run.describe(args.ref_sample_cycles, cycles_target)}
+    value = statistics.mean(vals)
+    ms = 1e3 * cfg.k / value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY §8d)",
+            "config": config_json(cfg, 1, "n/a (CPU)"), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
+                             "sample": info["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_1607_00968_b200 as hz
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = build_workload(rank, ws, WORKLOAD["k"])
+    n, k = cfg.num_nodes, cfg.k
+    t0 = time.perf_counter()
+    P = hz.HelmholtzProblem.from_config(cfg, device=local)
+    S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions.from_config(cfg))
+    setup_s = time.perf_counter() - t0
+    B_host = cfg.rhs_block()
+    Bd = torch.from_numpy(B_host).to(f"cuda:{local}")
+    Xd = torch.empty_like(Bd)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if ws == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # warm-up (also fixes the cycle count of the workload)
+    rep = None
+    for _ in range(args.warmup):
+        _, rep = S.solve_block(Bd, out=Xd)
+    assert rep is not None and rep.all_converged(), f"warm-up solve did not converge: {rep}"
+    # ---- timed region: device-resident inputs (inputs > L2: 269 MB block)
+    cycles = []
+    launches0 = hz.kernel_launch_count()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            _, rep = S.solve_block(Bd, out=Xd)  # library stream; synchronised on return
+            cycles.append(rep.cycles)
+            if not rep.all_converged():
+                raise RuntimeError(f"solve did not converge: {rep.rel_residual}")
+        ev1.record(stream)
+        barrier()
+    launches = hz.kernel_launch_count() - launches0
+    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
+    value = ws * k * args.steps / (t_ms / 1e3)
+    # ---- e2e: the public C ABI with pinned host buffers (H2D + D2H per step)
+    Bp = torch.from_numpy(B_host).pin_memory()
+    Xp = torch.empty_like(Bp).pin_memory()
+    Bn, Xn = Bp.numpy(), Xp.numpy()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, rep_e = S.solve_block(Bn, out=Xn)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = ws * k * args.steps / e2e_s
+    # ---- profiled pass (same steps) for the per-kernel roofline
+    with hz.kernel_profile() as prof:
+        for _ in range(max(1, min(args.steps, 3))):
+            S.solve_block(Bd, out=Xd)
+    kern = prof.result
+    peak, peak_kind = peaks()
+    table = {}
+    for name, r in kern.items():
+        avg_ms = r["ms"] / max(r["count"], 1)
+        gbs = r["bytes"] / (r["ms"] / 1e3) / 1e9 if r["ms"] > 0 else 0.0
+        table[name] = {"launches": r["count"], "avg_us": round(1e3 * avg_ms, 3),
+                       "share": 0.0, "gbs": round(gbs, 1), "frac": round(gbs / peak, 3)}
+    total_ms = sum(r["ms"] for r in kern.values()) or 1.0
+    for name, r in kern.items():
+        table[name]["share"] = round(r["ms"] / total_ms, 4)
+    # dominant HBM-roofline kernel: the grid stencil / smoother with the largest share
+    stencil = {n_: r for n_, r in kern.items() if n_.startswith(("jacobi", "residual", "apply", "restrict",
+                                                                  "prolong"))}
+    dom = max(stencil or kern, key=lambda n_: kern[n_]["ms"])
+    r = kern[dom]
+    achieved = r["bytes"] / (r["ms"] / 1e3) / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                "algorithmic_bytes_per_launch": r["bytes"] / r["count"], "peak_source": peak_kind}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded, SURVEY §8d; random-free point sources)",
+            "config": config_json(cfg, ws, "inputs larger than L2 (269 MB block, 5.6 GB Krylov basis)"),
+            "cycles_per_solve": statistics.mean(cycles), "setup_s": round(setup_s, 3),
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B_host.nbytes),
+                    "d2h_bytes_per_step": int(B_host.nbytes)},
+            "roofline": roofline, "kernels": table, "gpu_launches": int(launches),
+            "clocks": clk.summary()}
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, info = reference_sample(cfg, statistics.mean(cycles), sample_cycles=args.cpu_sample_cycles)
+            line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": "reference",
+                                    "sample": info["sample"]}
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample-cycles", type=int, default=2,
+                    help="FGMRES iterations per reference step (bounded CPU sample)")
+    ap.add_argument("--cpu-sample-cycles", type=int, default=5,
+                    help="FGMRES iterations of the cpu_baseline sample in our arm (one restart)")
+    ap.add_argument("--ref-cycles", type=float, default=None,
+                    help="cycle count to extrapolate the reference sample to (default: the sample's own)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

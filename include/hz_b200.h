@@ -171,6 +171,15 @@ HZ_API int hz_sensitivity_accumulate_device(hz_problem* p, int64_t n, int k, con
 /* number of this library's kernel launches so far (process-wide) */
 HZ_API int64_t hz_kernel_launch_count(void);
 
+/* Per-kernel CUDA-event profiling of this library's launches (measurement
+ * support for bench.py): begin clears and enables, end disables, report
+ * writes a JSON object {kernel: {count, ms, bytes, flops}} with the summed
+ * event durations and ALGORITHMIC bytes / flops; returns the length needed
+ * (incl. NUL) or -1. */
+HZ_API int hz_profile_begin(void);
+HZ_API int hz_profile_end(void);
+HZ_API int64_t hz_profile_report(char* buf, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

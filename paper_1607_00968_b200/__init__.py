@@ -47,7 +47,7 @@ class ConvergenceError(HzError):  # seistomo::ConvergenceError{residual_history}
 
     def __init__(self, msg, residual_history=None):
         super().__init__(msg)
-        self.residual_history = list(residual_history or [])
+        self.residual_history = [] if residual_history is None else [float(x) for x in residual_history]
 
 
 class BreakdownError(HzError):
@@ -90,6 +90,29 @@ def kernel_launch_count() -> int:
 
 def device_count() -> int:
     return int(_native.lib().hz_device_count())
+
+
+class kernel_profile:
+    """Context manager: CUDA-event timing of every library kernel launched
+    inside the block. `.result` maps kernel name -> {count, ms, bytes, flops}
+    (summed event durations and algorithmic bytes / flops)."""
+
+    def __enter__(self):
+        _check(_native.lib().hz_profile_begin())
+        self.result = {}
+        return self
+
+    def __exit__(self, *exc):
+        import json
+        L = _native.lib()
+        _check(L.hz_profile_end())
+        need = L.hz_profile_report(None, 0)
+        if need < 0:
+            raise CudaError(L.hz_last_error_message().decode())
+        buf = C.create_string_buffer(int(need))
+        L.hz_profile_report(buf, need)
+        self.result = json.loads(buf.value.decode())
+        return False
 
 
 # ---------------------------------------------------------------- data

@@ -20,7 +20,8 @@ EXPORTS = (
     "hz_solver_set_tolerance", "hz_solve_block", "hz_solve_block_device", "hz_solve_helmholtz",
     "hz_cycle", "hz_cycle_device", "hz_coarse_solve", "hz_hierarchy_num_levels",
     "hz_hierarchy_level_dims", "hz_hierarchy_level_coefficients", "hz_sensitivity_accumulate",
-    "hz_sensitivity_accumulate_device", "hz_kernel_launch_count",
+    "hz_sensitivity_accumulate_device", "hz_kernel_launch_count", "hz_profile_begin",
+    "hz_profile_end", "hz_profile_report",
 )
 
 
@@ -54,6 +55,8 @@ def lib():
         L.hz_last_error_message.restype = C.c_char_p
         L.hz_problem_num_nodes.restype = C.c_int64
         L.hz_kernel_launch_count.restype = C.c_int64
+        L.hz_profile_report.restype = C.c_int64
+        L.hz_profile_report.argtypes = [C.c_char_p, C.c_int64]
         vp, i64, dbl, i32 = C.c_void_p, C.c_int64, C.c_double, C.c_int
         L.hz_problem_create.argtypes = [i32, vp, vp, vp, dbl, dbl, vp, i32, i32, C.POINTER(vp)]
         L.hz_problem_destroy.argtypes = [vp]

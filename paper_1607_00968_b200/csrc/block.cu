@@ -7,6 +7,8 @@
 // private partial, and a second kernel sums the slots in fixed order -- no
 // floating-point atomics, so runs are bitwise reproducible.
 #include "kernels.hpp"
+#include "profile.hpp"
+#include "block_tiled.cuh"
 
 namespace hz {
 
@@ -21,11 +23,6 @@ int slots_for(int64_t n) {
   return int(s < 1 ? 1 : s);
 }
 
-// Register tile per thread over the k x k pair space.
-template <int TP, int TQ>
-struct PairTile {
-  static constexpr int P = TP, Q = TQ;
-};
 
 // CTA (i = blockIdx.x, slot = blockIdx.y) computes the slot's partial of
 // X_i^H Y over its row range. Thread t owns a TP x TQ tile of (p, q) pairs;
@@ -131,11 +128,23 @@ template <class T>
 __global__ void __launch_bounds__(kBlk)
 reduce_partials_kernel(int64_t count, int nslots, const cplx_t<T>* __restrict__ partials,
                        cplx_t<T>* __restrict__ out) {
-  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
-  if (e >= count) return;
-  cplx_t<T> s = partials[e];
-  for (int t = 1; t < nslots; ++t) s = cadd(s, partials[int64_t(t) * count + e]);
-  out[e] = s;
+  // CTA = 32 consecutive outputs x 8 slot groups; each group sums a strided
+  // subset of the slots, then the 8 group sums are added in fixed order.
+  using V = cplx_t<T>;
+  __shared__ V red[8][32];
+  const int o = threadIdx.x & 31, sg = threadIdx.x >> 5;
+  const int64_t e = int64_t(blockIdx.x) * 32 + o;
+  V s = czero<V>();
+  if (e < count)
+    for (int t = sg; t < nslots; t += 8) s = cadd(s, partials[int64_t(t) * count + e]);
+  red[sg][o] = s;
+  __syncthreads();
+  if (sg == 0 && e < count) {
+    V r = red[0][o];
+#pragma unroll
+    for (int gg = 1; gg < 8; ++gg) r = cadd(r, red[gg][o]);
+    out[e] = r;
+  }
 }
 
 template <class T>
@@ -331,41 +340,93 @@ int gram_partial_slots(int64_t n, int k) {
   return slots_for(n);
 }
 
-template <class T>
-void launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
+template <class T, int K>
+void gram_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
                        cplx_t<T>* partials, int nslots, cudaStream_t s) {
+  const size_t smem = tiled::gram_smem<T, K>();
+  auto kern = tiled::gram_kernel<T, K>;
+  static bool attr = false;
+  if (!attr) {
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  kern<<<dim3(nb, nslots), 256, smem, s>>>(n, X, Y, partials, nslots);
+}
+
+template <class T, int K>
+void update_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T>* H,
+                         const cplx_t<T>* Yin, cplx_t<T>* Yout, T sign, cudaStream_t s) {
+  constexpr int RC = tiled::update_rows<K>();
+  const size_t smem = tiled::update_smem<T, K>();
+  auto kern = tiled::update_kernel<T, K>;
+  static bool attr = false;
+  if (!attr) {
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  kern<<<grid_for(n, RC), 256, smem, s>>>(n, nb, X, H, Yin, Yout, sign);
+}
+
+template <class T>
+int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
+                      cplx_t<T>* partials, int max_slots, cudaStream_t s) {
   if (k > 64) throw HzError(kValidation, "block width k > 64 unsupported");
   if (nb > kMaxBlocks) throw HzError(kValidation, "too many blocks in one Gram");
-  if (k <= 16)
+  ProfScope prof(sizeof(T) == 8 ? "multi_gram_c128" : "multi_gram_c64",
+                 double(nb + 1) * n * k * sizeof(cplx_t<T>), s, 8.0 * double(n) * k * k * nb);
+  // ~4 CTAs per SM in total over the nb blocks; at least 32 rows per slot
+  int64_t want = (4 * kNumSMs + nb - 1) / nb;
+  want = std::min<int64_t>(want, (n + 31) / 32);
+  const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(want, max_slots)));
+  if (k == 32)
+    gram_tiled_launch<T, 32>(n, nb, X, Y, partials, nslots, s);
+  else if (k == 16)
+    gram_tiled_launch<T, 16>(n, nb, X, Y, partials, nslots, s);
+  else if (k == 64)
+    gram_tiled_launch<T, 64>(n, nb, X, Y, partials, nslots, s);
+  else if (k < 16)
     gram_launch<T, 1, 1>(n, k, nb, X, Y, partials, nslots, s);
   else if (k <= 32)
     gram_launch<T, 2, 2>(n, k, nb, X, Y, partials, nslots, s);
   else
     gram_launch<T, 4, 4>(n, k, nb, X, Y, partials, nslots, s);
   HZ_LAUNCH_CHECK();
+  return nslots;
 }
 
 template <class T>
 void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* H,
                          const cplx_t<T>* Yin, cplx_t<T>* Yout, T sign, cudaStream_t s) {
-  const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
-  auto kern = multi_update_kernel<T>;
-  if (smem > 48 * 1024)
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  kern<<<grid_for(n * k, kBlk), kBlk, smem, s>>>(n, k, nb, X, H, Yin, Yout, sign);
+  ProfScope prof(sizeof(T) == 8 ? "multi_update_c128" : "multi_update_c64",
+                 double(nb + (Yin ? 2 : 1)) * n * k * sizeof(cplx_t<T>), s, 8.0 * double(n) * k * k * nb);
+  if (k == 32) {
+    update_tiled_launch<T, 32>(n, nb, X, H, Yin, Yout, sign, s);
+  } else if (k == 16) {
+    update_tiled_launch<T, 16>(n, nb, X, H, Yin, Yout, sign, s);
+  } else if (k == 64) {
+    update_tiled_launch<T, 64>(n, nb, X, H, Yin, Yout, sign, s);
+  } else {
+    const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
+    auto kern = multi_update_kernel<T>;
+    if (smem > 48 * 1024)
+      HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<grid_for(n * k, kBlk), kBlk, smem, s>>>(n, k, nb, X, H, Yin, Yout, sign);
+  }
   HZ_LAUNCH_CHECK();
 }
 
 template <class T>
 void launch_reduce_partials(int64_t count, int nslots, const cplx_t<T>* partials, cplx_t<T>* out,
                             cudaStream_t s) {
-  reduce_partials_kernel<T><<<grid_for(count, kBlk), kBlk, 0, s>>>(count, nslots, partials, out);
+  ProfScope prof("reduce_partials", double(count) * (nslots + 1) * sizeof(cplx_t<T>), s);
+  reduce_partials_kernel<T><<<grid_for(count, 32), kBlk, 0, s>>>(count, nslots, partials, out);
   HZ_LAUNCH_CHECK();
 }
 
 template <class T>
 void launch_colnorm2_partial(int64_t n, int k, const cplx_t<T>* X, T* partials, int nslots,
                              cudaStream_t s) {
+  ProfScope prof("colnorm2", double(n) * k * sizeof(cplx_t<T>), s);
   colnorm2_kernel<T><<<nslots, kBlk, sizeof(T) * kBlk, s>>>(n, k, X, partials, nslots);
   HZ_LAUNCH_CHECK();
 }
@@ -379,6 +440,7 @@ void launch_reduce_real(int64_t count, int nslots, const T* partials, T* out, cu
 template <class T>
 void launch_axpby(int64_t count, cplx_t<T> a, cplx_t<T>* Y, cplx_t<T> b, const cplx_t<T>* X,
                   cudaStream_t s) {
+  ProfScope prof("axpby", 3.0 * count * sizeof(cplx_t<T>), s);
   axpby_kernel<T><<<grid_for(count, kBlk), kBlk, 0, s>>>(count, a, Y, b, X);
   HZ_LAUNCH_CHECK();
 }
@@ -404,6 +466,7 @@ void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* R
   auto kern = small_cholesky_kernel<T>;
   if (smem > 48 * 1024)
     HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ProfScope prof("small_cholesky", 4.0 * k * k * sizeof(cplx_t<T>), s);
   kern<<<1, 256, smem, s>>>(k, G, R, Rinv, flag, rel_tol);
   HZ_LAUNCH_CHECK();
 }
@@ -415,7 +478,7 @@ void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const do
 }
 
 #define HZ_INST(T)                                                                                 \
-  template void launch_multi_gram<T>(int64_t, int, int, const BlockTab<T>&, const cplx_t<T>*,     \
+  template int launch_multi_gram<T>(int64_t, int, int, const BlockTab<T>&, const cplx_t<T>*,      \
                                      cplx_t<T>*, int, cudaStream_t);                              \
   template void launch_multi_update<T>(int64_t, int, int, const BlockTab<T>&,                     \
                                        const cplx_t<T>*, const cplx_t<T>*, cplx_t<T>*, T,         \

@@ -10,10 +10,47 @@
 #include "../../include/hz_b200.h"
 #include "solver.hpp"
 
+#include <map>
+#include <mutex>
+#include <sstream>
+
+#include "profile.hpp"
+
 namespace hz {
 
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+// ---- per-kernel event profiler (profile.hpp)
+namespace {
+struct ProfRec {
+  const char* name;
+  double bytes, flops;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::vector<cudaEvent_t> g_prof_pool;
+size_t g_prof_next = 0;
+std::vector<ProfRec> g_prof_recs;
+}  // namespace
+
+bool profiling_enabled() { return g_prof_on; }
+
+cudaEvent_t profile_event() {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (g_prof_next == g_prof_pool.size()) {
+    cudaEvent_t e;
+    HZ_CUDA(cudaEventCreate(&e));
+    g_prof_pool.push_back(e);
+  }
+  return g_prof_pool[g_prof_next++];
+}
+
+void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_recs.push_back({name, bytes, flops, a, b});
+}
 
 }  // namespace hz
 
@@ -125,7 +162,8 @@ Report run_solve(hz_solver* s, int k, const double2* B, double2* X) {
     // DenseLuSmall (src/helmholtz_solver.cpp:38-59): direct solve, then the
     // reported residuals
     const int64_t n = s->prob->num_nodes();
-    launch_coarse_solve<double>(n, k, s->dense_ainvT.get(), B, X, s->stream);
+    DevBuf<double2> part(size_t(std::max(coarse_split(n, k), 1)) * n * k);
+    launch_coarse_solve<double>(n, k, s->dense_ainvT.get(), B, X, part.get(), s->stream);
     BlockAlgebra<double> alg;
     alg.ensure(n, k, 1);
     DevBuf<double2> R(size_t(n) * k);
@@ -164,6 +202,60 @@ int hz_device_count(void) {
   return n;
 }
 int64_t hz_kernel_launch_count(void) { return g_launches.load(); }
+
+int hz_profile_begin(void) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof_recs.clear();
+    g_prof_next = 0;
+    g_prof_on = true;
+  });
+}
+
+int hz_profile_end(void) {
+  return guarded([&] { g_prof_on = false; });
+}
+
+int64_t hz_profile_report(char* buf, int64_t cap) {
+  std::string js;
+  const int st = guarded([&] {
+    HZ_CUDA(cudaDeviceSynchronize());
+    struct Agg {
+      int64_t count = 0;
+      double ms = 0, bytes = 0, flops = 0;
+    };
+    std::map<std::string, Agg> agg;
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    for (const auto& r : g_prof_recs) {
+      float ms = 0;
+      HZ_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      Agg& a = agg[r.name];
+      a.count += 1;
+      a.ms += ms;
+      a.bytes += r.bytes;
+      a.flops += r.flops;
+    }
+    std::ostringstream os;
+    os.precision(17);
+    os << "{";
+    bool first = true;
+    for (const auto& kv : agg) {
+      if (!first) os << ",";
+      first = false;
+      os << "\"" << kv.first << "\":{\"count\":" << kv.second.count << ",\"ms\":" << kv.second.ms
+         << ",\"bytes\":" << kv.second.bytes << ",\"flops\":" << kv.second.flops << "}";
+    }
+    os << "}";
+    js = os.str();
+  });
+  if (st != kOk) return -1;
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>(size_t(cap) - 1, js.size());
+    std::memcpy(buf, js.data(), n);
+    buf[n] = 0;
+  }
+  return int64_t(js.size()) + 1;
+}
 
 void hz_options_default(hz_options* o) {
   if (!o) return;

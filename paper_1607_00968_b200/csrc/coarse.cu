@@ -6,7 +6,9 @@
 // dependent steps, so the hierarchy instead forms A_c^{-1} ONCE at setup from
 // the same pivoted banded LU factors (one warp per identity column), and every
 // cycle applies it as one bandwidth-bound dense pass: n_c^2 complex reads.
+#include "block_tiled.cuh"
 #include "kernels.hpp"
+#include "profile.hpp"
 
 namespace hz {
 
@@ -30,8 +32,9 @@ banded_inverse_kernel(int64_t n, int64_t kl, int64_t ku, int64_t ld, const doubl
   const int lane = threadIdx.x & 31;
   const int64_t c = int64_t(blockIdx.x) * 4 + (threadIdx.x >> 5);
   if (c >= n) return;
-  double2* x = ainvT + c * n;
-  for (int64_t i = lane; i < n; i += 32) x[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+  const int64_t ldx = inv_ld(n);
+  double2* x = ainvT + c * ldx;
+  for (int64_t i = lane; i < ldx; i += 32) x[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
   __syncwarp();
   auto at = [&](int64_t i, int64_t j) { return ab[(kl + ku + i - j) + j * ld]; };
   // forward: row interchanges + unit-lower elimination (src/dense.cpp:46-52)
@@ -102,7 +105,7 @@ coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT,
     const int tl = (n - l0) < TL ? int(n - l0) : TL;
     for (int e = threadIdx.x; e < TL * TI; e += 256) {
       const int l = e / TI, i = e % TI;
-      As[e] = (l < tl && i0 + i < n) ? ainvT[(l0 + l) * n + i0 + i] : czero<V>();
+      As[e] = (l < tl && i0 + i < n) ? ainvT[(l0 + l) * inv_ld(n) + i0 + i] : czero<V>();
     }
     for (int e = threadIdx.x; e < TL * k; e += 256) {
       const int l = e / k;
@@ -131,7 +134,140 @@ coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT,
   }
 }
 
+// Tiled dense coarse solve for K in {16, 32, 64}: CTA = 64 output rows x K
+// columns over one split-K slice of l; A^{-1} rows and B rows are streamed
+// through double-buffered cp.async stages; thread tile 4 (i) x K/16 (q),
+// both strided so a warp's shared loads are broadcast / contiguous; 3-mult
+// complex products. Slices write partials summed in fixed order afterwards.
+template <class T, int K>
+__global__ void __launch_bounds__(256)
+coarse_gemm_kernel(int64_t n, const cplx_t<T>* __restrict__ ainvT, const cplx_t<T>* __restrict__ b,
+                   cplx_t<T>* __restrict__ part, int nsplit) {
+  using V = cplx_t<T>;
+  constexpr int TI = 64, TL = 16, NQT = 16, TQ = K / NQT, NIT = 16, TA = TI / NIT;
+  constexpr int AT = TL * TI, BT = TL * K, STAGE = AT + BT;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* buf = reinterpret_cast<V*>(smem_raw);
+  const int tid = threadIdx.x, qt = tid % NQT, it = tid / NQT;
+  const int64_t i0 = int64_t(blockIdx.x) * TI;
+  const int split = blockIdx.y;
+  const int64_t per = (n + nsplit - 1) / nsplit;
+  const int64_t l0 = int64_t(split) * per, l1 = (l0 + per) < n ? (l0 + per) : n;
+  const int nch = l1 > l0 ? int((l1 - l0 + TL - 1) / TL) : 0;
+  const int icount = (n - i0) < TI ? int(n - i0) : TI;
+  T t1[TA][TQ], t2[TA][TQ], t3[TA][TQ];
+#pragma unroll
+  for (int a = 0; a < TA; ++a)
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) t1[a][q] = t2[a][q] = t3[a][q] = T(0);
+  constexpr int PER16 = 16 / sizeof(V);
+  auto stage = [&](int c, V* dst) {
+    const int64_t lc = l0 + int64_t(c) * TL;
+    const int lrows = (l1 - lc) < TL ? int(l1 - lc) : TL;
+    for (int e = tid; e < TL * (TI / PER16); e += 256) {
+      const int l = e / (TI / PER16), ii = (e - l * (TI / PER16)) * PER16;
+      V* d = dst + l * TI + ii;
+      if (l < lrows && ii < icount)  // icount is a multiple of PER16 unless at the end
+        tiled::cp_async16(d, ainvT + (lc + l) * inv_ld(n) + i0 + ii);
+      else
+        for (int u = 0; u < PER16; ++u) d[u] = czero<V>();
+    }
+    for (int e = tid; e < TL * (K / PER16); e += 256) {
+      const int l = e / (K / PER16), qq = (e - l * (K / PER16)) * PER16;
+      V* d = dst + AT + l * K + qq;
+      if (l < lrows)
+        tiled::cp_async16(d, b + (lc + l) * K + qq);
+      else
+        for (int u = 0; u < PER16; ++u) d[u] = czero<V>();
+    }
+  };
+  if (nch > 0) stage(0, buf);
+  tiled::cp_async_commit();
+  for (int c = 0; c < nch; ++c) {
+    const int st = c & 1;
+    if (c + 1 < nch) stage(c + 1, buf + (st ^ 1) * STAGE);
+    tiled::cp_async_commit();
+    tiled::cp_async_wait<1>();
+    __syncthreads();
+    const V* as = buf + st * STAGE;
+    const V* bs = as + AT;
+#pragma unroll 4
+    for (int l = 0; l < TL; ++l) {
+      V bv[TQ];
+      T bsum[TQ];
+#pragma unroll
+      for (int q = 0; q < TQ; ++q) {
+        bv[q] = bs[l * K + qt + NQT * q];
+        bsum[q] = bv[q].x + bv[q].y;
+      }
+#pragma unroll
+      for (int a = 0; a < TA; ++a) {
+        const V av = as[l * TI + it + NIT * a];
+        const T asum = av.x + av.y;
+#pragma unroll
+        for (int q = 0; q < TQ; ++q) {
+          t1[a][q] = fma(av.x, bv[q].x, t1[a][q]);
+          t2[a][q] = fma(av.y, bv[q].y, t2[a][q]);
+          t3[a][q] = fma(asum, bsum[q], t3[a][q]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  tiled::cp_async_wait<0>();
+  V* out = part + int64_t(split) * n * K;
+#pragma unroll
+  for (int a = 0; a < TA; ++a) {
+    const int64_t i = i0 + it + NIT * a;
+    if (i >= n) continue;
+#pragma unroll
+    for (int q = 0; q < TQ; ++q) {
+      V v;
+      v.x = t1[a][q] - t2[a][q];
+      v.y = t3[a][q] - t1[a][q] - t2[a][q];
+      out[i * K + qt + NQT * q] = v;
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+split_reduce_kernel(int64_t count, int nsplit, const cplx_t<T>* __restrict__ part,
+                    cplx_t<T>* __restrict__ x) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= count) return;
+  cplx_t<T> s = part[e];
+  for (int t = 1; t < nsplit; ++t) s = cadd(s, part[int64_t(t) * count + e]);
+  x[e] = s;
+}
+
+template <class T, int K>
+void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, const cplx_t<T>* b, cplx_t<T>* x,
+                        cplx_t<T>* part, int nsplit, cudaStream_t s) {
+  using V = cplx_t<T>;
+  constexpr int TI = 64, TL = 16;
+  const size_t smem = sizeof(V) * 2 * (TL * TI + TL * K);
+  auto kern = coarse_gemm_kernel<T, K>;
+  static bool attr = false;
+  if (!attr) {
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  const int tiles = grid_for(n, TI);
+  kern<<<dim3(tiles, nsplit), 256, smem, s>>>(n, ainvT, b, nsplit == 1 ? x : part, nsplit);
+  if (nsplit > 1)
+    split_reduce_kernel<T><<<grid_for(n * K, 256), 256, 0, s>>>(n * K, nsplit, part, x);
+}
+
 }  // namespace
+
+int coarse_split(int64_t n, int k) {
+  if (k != 16 && k != 32 && k != 64) return 0;
+  const int tiles = grid_for(n, 64);
+  int sk = (4 * kNumSMs) / tiles;
+  return sk < 1 ? 1 : (sk > 32 ? 32 : sk);
+}
+
 
 void launch_banded_inverse(int64_t n, int64_t kl, int64_t ku, int64_t ld, const double2* ab,
                            const int64_t* piv, double2* ainvT, cudaStream_t s) {
@@ -141,8 +277,21 @@ void launch_banded_inverse(int64_t n, int64_t kl, int64_t ku, int64_t ld, const 
 
 template <class T>
 void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
-                         cplx_t<T>* x, cudaStream_t s) {
+                         cplx_t<T>* x, cplx_t<T>* part, cudaStream_t s) {
   using V = cplx_t<T>;
+  const int sk = coarse_split(n, k);
+  if (sk > 0 && (part != nullptr || sk == 1)) {
+    ProfScope prof(sizeof(T) == 8 ? "coarse_solve_c128" : "coarse_solve_c64",
+                   (double(n) * n + 2.0 * n * k) * sizeof(V), s, 8.0 * double(n) * n * k);
+    if (k == 32)
+      coarse_gemm_launch<T, 32>(n, ainvT, b, x, part, sk, s);
+    else if (k == 16)
+      coarse_gemm_launch<T, 16>(n, ainvT, b, x, part, sk, s);
+    else
+      coarse_gemm_launch<T, 64>(n, ainvT, b, x, part, sk, s);
+    HZ_LAUNCH_CHECK();
+    return;
+  }
   constexpr int TL = 32;
   if (k > 256) throw HzError(kValidation, "coarse solve: k > 256 unsupported");
   // TI*k <= 4096 outputs per CTA (16 per thread)
@@ -150,6 +299,8 @@ void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<
   if (k > 64) ti = 4096 / k >= 16 ? 16 : (4096 / k >= 8 ? 8 : (4096 / k >= 4 ? 4 : 1));
   const size_t smem = sizeof(V) * (TL * 16 + TL * size_t(k));
   const int grid = grid_for(n, ti);
+  ProfScope prof(sizeof(T) == 8 ? "coarse_solve_c128" : "coarse_solve_c64",
+                 (double(n) * n + 2.0 * n * k) * sizeof(V), s, 8.0 * double(n) * n * k);
   if (ti == 16) {
     auto kern = coarse_solve_kernel<T, 16, TL>;
     HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -171,8 +322,8 @@ void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<
 }
 
 template void launch_coarse_solve<double>(int64_t, int, const double2*, const double2*, double2*,
-                                          cudaStream_t);
+                                          double2*, cudaStream_t);
 template void launch_coarse_solve<float>(int64_t, int, const float2*, const float2*, float2*,
-                                         cudaStream_t);
+                                         float2*, cudaStream_t);
 
 }  // namespace hz

@@ -243,7 +243,7 @@ std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, in
     DevBuf<int64_t> dpiv(nc);
     dab.upload(f.ab.data(), f.ab.size(), s);
     dpiv.upload(f.piv.data(), nc, s);
-    H->ainvT_.alloc(size_t(nc) * nc);
+    H->ainvT_.alloc(size_t(nc) * inv_ld(nc));
     launch_banded_inverse(nc, f.kl, f.ku, f.ld, dab.get(), dpiv.get(), H->ainvT_.get(), s);
     HZ_CUDA(cudaStreamSynchronize(s));
   }
@@ -281,7 +281,7 @@ DevBuf<double2> dense_inverse(const Problem& p, cudaStream_t s) {
   DevBuf<int64_t> dpiv(nn);
   dab.upload(f.ab.data(), f.ab.size(), s);
   dpiv.upload(f.piv.data(), nn, s);
-  DevBuf<double2> out(size_t(nn) * nn);
+  DevBuf<double2> out(size_t(nn) * inv_ld(nn));
   launch_banded_inverse(nn, f.kl, f.ku, f.ld, dab.get(), dpiv.get(), out.get(), s);
   HZ_CUDA(cudaStreamSynchronize(s));
   return out;
@@ -359,12 +359,15 @@ void Hierarchy<T>::ensure_ws(int k) {
       wr_[l].alloc(e);
     }
   }
+  const int64_t nc = coarse_n();
+  cpart_.alloc(size_t(std::max(coarse_split(nc, k), 1)) * nc * k);
   ws_k_ = k;
 }
 
 template <class T>
 void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
-  launch_coarse_solve<T>(coarse_n(), k, ainvT_.get(), b, x, s);
+  ensure_ws(k);
+  launch_coarse_solve<T>(coarse_n(), k, ainvT_.get(), b, x, cpart_.get(), s);
 }
 
 template <class T>

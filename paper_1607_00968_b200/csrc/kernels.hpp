@@ -67,10 +67,15 @@ void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);
 // ainvT[c][i] = (A^{-1})[i][c].
 void launch_banded_inverse(int64_t n, int64_t kl, int64_t ku, int64_t ld, const double2* ab,
                            const int64_t* piv, double2* ainvT, cudaStream_t s);
+// Row stride of ainvT (even, so complex64 rows stay 16-byte aligned).
+__host__ __device__ inline int64_t inv_ld(int64_t n) { return n + (n & 1); }
+// Split-K factor of the tiled coarse solve (0: k not tiled). The tiled path
+// needs `part` with coarse_split(n, k) * n * k entries when the split is > 1.
+int coarse_split(int64_t n, int k);
 // X[i][:] = sum_l ainvT[l][i] * B[l][:]   (dense coarse solve, all k columns)
 template <class T>
 void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
-                         cplx_t<T>* x, cudaStream_t s);
+                         cplx_t<T>* x, cplx_t<T>* part, cudaStream_t s);
 
 // ---- block (tall-skinny) kernels, node-major [n][k] blocks (inc/block.hpp)
 // Tables of block pointers travel by value in the kernel parameters (no
@@ -86,7 +91,7 @@ struct BlockTab {
 // (partials must hold gram_partial_slots(n) * nb * k * k entries).
 int gram_partial_slots(int64_t n, int k);
 template <class T>
-void launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
+int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
                        cplx_t<T>* partials, int nslots, cudaStream_t s);
 // Yout = (Yin ? Yin : 0) + sign * sum_i X_i H_i  (H_i k x k row-major, on
 // device). Yout may alias Yin but not any X_i.

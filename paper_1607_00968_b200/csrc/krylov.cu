@@ -243,8 +243,8 @@ void BlockAlgebra<T>::ensure(int64_t n_, int k_, int max_blocks) {
 
 template <class T>
 void BlockAlgebra<T>::gram(const BlockTab<T>& tab, int nb, const V* Y, V* out, cudaStream_t s) {
-  launch_multi_gram<T>(n, k, nb, tab, Y, partials.get(), nslots, s);
-  launch_reduce_partials<T>(int64_t(nb) * k * k, nslots, partials.get(), out, s);
+  const int used = launch_multi_gram<T>(n, k, nb, tab, Y, partials.get(), nslots, s);
+  launch_reduce_partials<T>(int64_t(nb) * k * k, used, partials.get(), out, s);
 }
 
 template <class T>

@@ -1,0 +1,42 @@
+// Optional per-kernel CUDA-event profiling of the library's own launches.
+// When enabled (hz_profile_begin), every launch wrapper brackets its kernel
+// with events on the stream it launches on and records the kernel's
+// ALGORITHMIC bytes (the SURVEY §8d formulas), so bench.py can report
+// achieved GB/s per kernel class against the HBM roofline.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace hz {
+
+bool profiling_enabled();
+void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b);
+cudaEvent_t profile_event();
+
+class ProfScope {
+ public:
+  ProfScope(const char* name, double bytes, cudaStream_t s, double flops = 0.0)
+      : name_(name), bytes_(bytes), flops_(flops), s_(s) {
+    if (profiling_enabled()) {
+      a_ = profile_event();
+      b_ = profile_event();
+      cudaEventRecord(a_, s_);
+    }
+  }
+  ~ProfScope() {
+    if (a_) {
+      cudaEventRecord(b_, s_);
+      profile_record(name_, bytes_, flops_, a_, b_);
+    }
+  }
+
+ private:
+  const char* name_;
+  double bytes_, flops_;
+  cudaStream_t s_;
+  cudaEvent_t a_ = nullptr, b_ = nullptr;
+};
+
+}  // namespace hz

@@ -100,7 +100,8 @@ class Hierarchy {
   void download_level(int l, std::vector<cplx>& coef_or_center) const;
 
   std::vector<MgLevelDev<T>> levels_;
-  DevBuf<V> ainvT_;  // coarsest inverse, transposed [n_c][n_c]
+  DevBuf<V> ainvT_;  // coarsest inverse, transposed [n_c][inv_ld(n_c)]
+  DevBuf<V> cpart_;  // split-K partials of the coarse solve
   int ndim_ = 2;
   int64_t band_ = 0;
 

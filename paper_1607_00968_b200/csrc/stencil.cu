@@ -10,6 +10,7 @@
 // sees (close to) one read per input and one write per output: these kernels
 // are HBM-bandwidth bound.
 #include "kernels.hpp"
+#include "profile.hpp"
 
 namespace hz {
 
@@ -338,11 +339,38 @@ __global__ void __launch_bounds__(kBlock) cast_kernel(int64_t count, const Src* 
   if (e < count) out[e] = ccast<Dst>(in[e]);
 }
 
+template <class T>
+constexpr const char* prec_tag() {
+  return sizeof(T) == 8 ? "c128" : "c64";
+}
+
+// algorithmic bytes of one level_kernel launch: vectors read /
+// written once per element, coefficients once per node
+template <class T>
+double level_bytes(const LevelOp<T>& op, int mode) {
+  const double s = sizeof(cplx_t<T>), n = op.g.nodes, k = op.g.k;
+  const double coef = op.kind == kFine ? 1.0 : (op.ndim == 3 ? 27.0 : 9.0);
+  const double vec = mode == 0 ? 2.0 : 3.0;
+  const double diag = mode == 2 ? 1.0 : 0.0;
+  return n * (vec * k * s + (coef + diag) * s);
+}
+
+template <class T, int MODE>
+const char* level_name(int kind) {
+  static const char* names[2][3][2] = {
+      {{"apply_fine_c128", "apply_fine_c64"}, {"residual_fine_c128", "residual_fine_c64"},
+       {"jacobi_fine_c128", "jacobi_fine_c64"}},
+      {{"apply_stencil_c128", "apply_stencil_c64"}, {"residual_stencil_c128", "residual_stencil_c64"},
+       {"jacobi_stencil_c128", "jacobi_stencil_c64"}}};
+  return names[kind][MODE][sizeof(T) == 8 ? 0 : 1];
+}
+
 template <class T, int MODE>
 void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out,
                     T wj, cudaStream_t s) {
   const int64_t total = int64_t(op.g.nodes) * op.g.k;
   const int grid = grid_for(total, kBlock);
+  ProfScope prof(level_name<T, MODE>(op.kind), level_bytes(op, MODE), s);
   if (op.kind == kFine) {
     if (op.ndim == 3)
       level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
@@ -376,6 +404,8 @@ void launch_jacobi(const LevelOp<T>& op, T wj, const cplx_t<T>* x, const cplx_t<
 template <class T, class In>
 void launch_jacobi_zero(const LevelOp<T>& op, T wj, const In* b, cplx_t<T>* xout, cudaStream_t s) {
   const int64_t total = int64_t(op.g.nodes) * op.g.k;
+  ProfScope prof(sizeof(T) == 8 ? "jacobi_zero_c128" : "jacobi_zero_c64",
+                 double(op.g.nodes) * ((double(sizeof(In)) + sizeof(cplx_t<T>)) * op.g.k + sizeof(cplx_t<T>)), s);
   jacobi_zero_kernel<T, In><<<grid_for(total, kBlock), kBlock, 0, s>>>(op.g, op.inv_diag, wj, b, xout);
   HZ_LAUNCH_CHECK();
 }
@@ -383,6 +413,8 @@ template <class T>
 void launch_restrict(const LevelGeom& gf, const LevelGeom& gc, int ndim, const cplx_t<T>* r,
                      cplx_t<T>* bc, cudaStream_t s) {
   const int grid = grid_for(int64_t(gc.nodes) * gc.k, kBlock);
+  ProfScope prof(sizeof(T) == 8 ? "restrict_c128" : "restrict_c64",
+                 (double(gf.nodes) + gc.nodes) * gf.k * sizeof(cplx_t<T>), s);
   if (ndim == 3)
     restrict_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, r, bc);
   else
@@ -393,6 +425,8 @@ template <class T>
 void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
                             const cplx_t<T>* ec, cplx_t<T>* x, cudaStream_t s) {
   const int grid = grid_for(int64_t(gf.nodes) * gf.k, kBlock);
+  ProfScope prof(sizeof(T) == 8 ? "prolong_correct_c128" : "prolong_correct_c64",
+                 (2.0 * gf.nodes + gc.nodes) * gf.k * sizeof(cplx_t<T>), s);
   if (ndim == 3)
     prolong_correct_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
   else
@@ -419,6 +453,7 @@ void launch_galerkin(const LevelOp<double>& fine, const LevelGeom& gc, double2* 
 
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s) {
+  ProfScope prof("cast", double(count) * (sizeof(Src) + sizeof(Dst)), s);
   cast_kernel<Dst, Src><<<grid_for(count, kBlock), kBlock, 0, s>>>(count, in, out);
   HZ_LAUNCH_CHECK();
 }
