@@ -303,6 +303,94 @@ small_cholesky_kernel(int k, const cplx_t<T>* __restrict__ G, cplx_t<T>* __restr
   if (tid == 0) *flag = fl;
 }
 
+// Pythagorean block CholQR factor for one Arnoldi step (single CTA):
+// Hc = [H_0 .. H_{nb-1}, G] from one Gram pass [V_0..V_{nb-1}, W]^H W.
+// S = G - sum_i H_i^H H_i (= W'^H W' for W' = W - V H, V orthonormal);
+// accepted when every S_cc >= eta2 * G_cc (no severe cancellation, so the
+// Pythagorean subtraction keeps full relative accuracy -- otherwise the
+// caller re-orthogonalises with CGS2 + CholQR2); then S = R^H R and the
+// coefficients C_i = -H_i R^{-1}, C_nb = R^{-1} so that
+// Q = sum_i V_i C_i + W C_nb = (W - V H) R^{-1} in one block update.
+// flag: 0 accepted, 1 rejected.
+template <class T>
+__global__ void __launch_bounds__(256)
+pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __restrict__ R,
+                  cplx_t<T>* __restrict__ Rinv, cplx_t<T>* __restrict__ C, int* flag, T eta2) {
+  using V = cplx_t<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* A = reinterpret_cast<V*>(smem_raw);  // [k][k]
+  __shared__ int fl;
+  const int tid = threadIdx.x;
+  const int kk = k * k;
+  const V* G = Hc + int64_t(nb) * kk;
+  if (tid == 0) fl = 0;
+  for (int e = tid; e < kk; e += blockDim.x) {
+    const int a = e / k, b = e - a * k;
+    if (b < a) continue;  // upper triangle suffices
+    V s = G[e];
+    for (int i = 0; i < nb; ++i) {
+      const V* Hi = Hc + int64_t(i) * kk;
+      for (int p = 0; p < k; ++p) s = csub(s, cmulc(Hi[p * k + a], Hi[p * k + b]));
+    }
+    A[e] = s;
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < k; ++c)
+      if (!(A[c * k + c].x >= eta2 * G[c * k + c].x) || !(A[c * k + c].x > T(0))) fl = 1;
+  __syncthreads();
+  if (fl) {
+    if (tid == 0) *flag = 1;
+    return;
+  }
+  for (int j = 0; j < k; ++j) {
+    if (tid == 0) A[j * k + j] = mk(sqrt(A[j * k + j].x), T(0));
+    __syncthreads();
+    const T inv = T(1) / A[j * k + j].x;
+    for (int c = j + 1 + tid; c < k; c += blockDim.x) A[j * k + c] = cscale(inv, A[j * k + c]);
+    __syncthreads();
+    const int m = k - j - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int a = j + 1 + e / m, c = j + 1 + e % m;
+      if (c >= a) A[a * k + c] = csub(A[a * k + c], cmulc(A[j * k + a], A[j * k + c]));
+    }
+    __syncthreads();
+    if (tid == 0 && j + 1 < k && !(A[(j + 1) * k + j + 1].x > T(0))) fl = 1;
+    __syncthreads();
+    if (fl) {
+      if (tid == 0) *flag = 1;
+      return;
+    }
+  }
+  for (int e = tid; e < kk; e += blockDim.x) {
+    const int a = e / k, c = e % k;
+    R[e] = c >= a ? A[e] : czero<V>();
+  }
+  for (int c = tid; c < k; c += blockDim.x)
+    for (int i = k - 1; i >= 0; --i) {
+      if (i > c) {
+        Rinv[i * k + c] = czero<V>();
+        continue;
+      }
+      V s = (i == c) ? mk(T(1), T(0)) : czero<V>();
+      for (int l = i + 1; l <= c; ++l) s = csub(s, cmul(A[i * k + l], Rinv[l * k + c]));
+      Rinv[i * k + c] = cscale(T(1) / A[i * k + i].x, s);
+    }
+  __syncthreads();
+  for (int e = tid; e < (nb + 1) * kk; e += blockDim.x) {
+    const int i = e / kk, r = e - i * kk, a = r / k, b = r - a * k;
+    if (i == nb) {
+      C[e] = Rinv[r];
+    } else {
+      const V* Hi = Hc + int64_t(i) * kk;
+      V s = czero<V>();
+      for (int l = 0; l <= b; ++l) s = cfma(Hi[a * k + l], Rinv[l * k + b], s);
+      C[e] = mk(-s.x, -s.y);
+    }
+  }
+  if (tid == 0) *flag = 0;
+}
+
 __global__ void __launch_bounds__(kBlk)
 sensitivity_kernel(int64_t n, int k, double w2, const double2* __restrict__ gf,
                    const double2* __restrict__ U, const double2* __restrict__ L,
@@ -470,6 +558,22 @@ void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* R
   kern<<<1, 256, smem, s>>>(k, G, R, Rinv, flag, rel_tol);
   HZ_LAUNCH_CHECK();
 }
+
+template <class T>
+void launch_pip_factor(int k, int nb, const cplx_t<T>* Hc, cplx_t<T>* R, cplx_t<T>* Rinv,
+                       cplx_t<T>* C, int* flag, T eta2, cudaStream_t s) {
+  const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
+  auto kern = pip_factor_kernel<T>;
+  if (smem > 48 * 1024)
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ProfScope prof("pip_factor", double(nb + 2) * k * k * sizeof(cplx_t<T>), s);
+  kern<<<1, 256, smem, s>>>(k, nb, Hc, R, Rinv, C, flag, eta2);
+  HZ_LAUNCH_CHECK();
+}
+template void launch_pip_factor<double>(int, int, const double2*, double2*, double2*, double2*, int*,
+                                        double, cudaStream_t);
+template void launch_pip_factor<float>(int, int, const float2*, float2*, float2*, float2*, int*, float,
+                                       cudaStream_t);
 
 void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const double2* U,
                         const double2* L, double* g, int accumulate, cudaStream_t s) {

@@ -129,6 +129,14 @@ template <class T>
 void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* Rinv, int* flag,
                            T rel_tol, cudaStream_t s);
 
+// Pythagorean block CholQR of one Arnoldi step from Hc = [H_0..H_{nb-1}, G]
+// (one Gram pass [V_0..V_{nb-1}, W]^H W): R, R^{-1} and the block-update
+// coefficients C (nb + 1 tiles) of Q = (W - V H) R^{-1}; flag 0 accepted,
+// 1 rejected (severe cancellation: caller falls back to CGS2 + CholQR2).
+template <class T>
+void launch_pip_factor(int k, int nb, const cplx_t<T>* Hc, cplx_t<T>* R, cplx_t<T>* Rinv,
+                       cplx_t<T>* C, int* flag, T eta2, cudaStream_t s);
+
 // sensitivity: g[i] (+)= sum_s Re(-omega^2 gf[i] u[i][s] lam[i][s])  (K13)
 void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const double2* U,
                         const double2* L, double* g, int accumulate, cudaStream_t s);

@@ -17,7 +17,9 @@
 //  * One host synchronisation per Arnoldi step (to read the k x k tiles).
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "solver.hpp"
 
@@ -294,7 +296,7 @@ void BlockAlgebra<T>::thin_qr_finish(std::vector<cplx>& R, bool& deficient) {
 template <class T>
 void Fgmres<T>::ensure(int64_t n, int k, int restart) {
   if (restart < 1) throw HzError(kValidation, "fgmres: restart must be >= 1");
-  if (restart + 1 > kMaxBlocks) throw HzError(kValidation, "fgmres: restart too large");
+  if (restart + 2 > kMaxBlocks) throw HzError(kValidation, "fgmres: restart too large");
   if (n == n_ && k == k_ && restart == m_) return;
   Vb_.clear();
   Zb_.clear();
@@ -303,7 +305,8 @@ void Fgmres<T>::ensure(int64_t n, int k, int restart) {
   for (auto& b : Vb_) b.alloc(size_t(n) * k);
   for (auto& b : Zb_) b.alloc(size_t(n) * k);
   R_.alloc(size_t(n) * k);
-  hcol1_.alloc(size_t(restart + 1) * k * k);
+  hcol1_.alloc(size_t(restart + 2) * k * k);
+  ccoef_.alloc(size_t(restart + 2) * k * k);
   hcol2_.alloc(size_t(restart + 1) * k * k);
   ydev_.alloc(size_t(restart) * k * k);
   h_hcol_.ensure(2 * size_t(restart + 1) * k * k);
@@ -324,6 +327,12 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
   const auto t0 = Clock::now();
   const int64_t n = op.n;
   ensure(n, k, restart);
+  {
+    const char* o = std::getenv("HZ_ORTHO");
+    pip_ = !(o && std::string(o) == "cgs2");
+    const char* e = std::getenv("HZ_PIP_ETA2");
+    pip_eta2_ = e ? std::atof(e) : 1e-4;
+  }
   const size_t blk = size_t(n) * k * sizeof(V);
   const size_t kk = size_t(k) * k;
   Report rep;
@@ -363,26 +372,55 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
       }
       V* W = Vb_[j + 1].get();
       op.apply(Zj, W, k, s);
-      // block CGS2 against V_0..V_j
-      alg_.gram(vtab_, j + 1, W, hcol1_.get(), s);
-      launch_multi_update<T>(n, k, j + 1, vtab_, hcol1_.get(), W, W, T(-1), s);
-      alg_.gram(vtab_, j + 1, W, hcol2_.get(), s);
-      launch_multi_update<T>(n, k, j + 1, vtab_, hcol2_.get(), W, W, T(-1), s);
-      rep.block_gram_products += 2 * (j + 1);
       const size_t hc = size_t(j + 1) * kk;
-      HZ_CUDA(cudaMemcpyAsync(h_hcol_.get(), hcol1_.get(), sizeof(V) * hc, cudaMemcpyDeviceToHost, s));
-      HZ_CUDA(cudaMemcpyAsync(h_hcol_.get() + hc, hcol2_.get(), sizeof(V) * hc,
-                              cudaMemcpyDeviceToHost, s));
-      alg_.thin_qr_enqueue(W, s);
-      HZ_CUDA(cudaStreamSynchronize(s));
       bool deficient = false;
-      alg_.thin_qr_finish(Rk, deficient);
-      ++rep.qr_factorizations;
       H[j].assign(j + 2, std::vector<cplx>(kk));
-      for (int i = 0; i <= j; ++i)
-        for (size_t e = 0; e < kk; ++e)
-          H[j][i][e] = (cplx{} + to_c(h_hcol_[i * kk + e])) + to_c(h_hcol_[hc + i * kk + e]);
-      H[j][j + 1] = Rk;
+      // Pass 1: one Gram of [V_0..V_j, W]^H W gives H_{:,j} and W^H W.
+      alg_.gram(vtab_, j + 2, W, hcol1_.get(), s);
+      rep.block_gram_products += j + 1;
+      bool accepted = false;
+      if (pip_) {
+        // Pythagorean CholQR: accepted unless a column lost more than half
+        // its norm to the projection (then CGS2 below, as the reference's
+        // second MGS pass, src/krylov.cpp:218-226).
+        launch_pip_factor<T>(k, j + 1, hcol1_.get(), alg_.R1.get(), alg_.R1i.get(), ccoef_.get(),
+                             alg_.flags.get(), T(pip_eta2_), s);
+        HZ_CUDA(cudaMemcpyAsync(alg_.h_flags.get(), alg_.flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        HZ_CUDA(cudaMemcpyAsync(h_hcol_.get(), hcol1_.get(), sizeof(V) * hc, cudaMemcpyDeviceToHost, s));
+        HZ_CUDA(cudaMemcpyAsync(alg_.h_R.get(), alg_.R1.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+        HZ_CUDA(cudaStreamSynchronize(s));
+        if (alg_.h_flags[0] == 0) {
+          accepted = true;
+          ++pip_accepted_;
+          // W <- sum_i V_i C_i + W C_{j+1} = (W - V H) R^{-1}  (in place: each
+          // CTA stages its rows of every block before writing them)
+          launch_multi_update<T>(n, k, j + 2, vtab_, ccoef_.get(), nullptr, W, T(1), s);
+          for (int i = 0; i <= j; ++i)
+            for (size_t e = 0; e < kk; ++e) H[j][i][e] = cplx{} + to_c(h_hcol_[i * kk + e]);
+          for (size_t e = 0; e < kk; ++e) H[j][j + 1][e] = to_c(alg_.h_R[e]);
+          ++rep.qr_factorizations;
+        } else {
+          ++pip_rejected_;
+        }
+      }
+      if (!accepted) {
+        // block CGS2 against V_0..V_j, then CholQR2
+        launch_multi_update<T>(n, k, j + 1, vtab_, hcol1_.get(), W, W, T(-1), s);
+        alg_.gram(vtab_, j + 1, W, hcol2_.get(), s);
+        launch_multi_update<T>(n, k, j + 1, vtab_, hcol2_.get(), W, W, T(-1), s);
+        rep.block_gram_products += j + 1;
+        HZ_CUDA(cudaMemcpyAsync(h_hcol_.get(), hcol1_.get(), sizeof(V) * hc, cudaMemcpyDeviceToHost, s));
+        HZ_CUDA(cudaMemcpyAsync(h_hcol_.get() + hc, hcol2_.get(), sizeof(V) * hc,
+                                cudaMemcpyDeviceToHost, s));
+        alg_.thin_qr_enqueue(W, s);
+        HZ_CUDA(cudaStreamSynchronize(s));
+        alg_.thin_qr_finish(Rk, deficient);
+        ++rep.qr_factorizations;
+        for (int i = 0; i <= j; ++i)
+          for (size_t e = 0; e < kk; ++e)
+            H[j][i][e] = (cplx{} + to_c(h_hcol_[i * kk + e])) + to_c(h_hcol_[hc + i * kk + e]);
+        H[j][j + 1] = Rk;
+      }
       if (deficient) {
         ++j;
         break;  // happy breakdown

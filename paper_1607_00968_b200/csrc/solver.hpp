@@ -188,7 +188,20 @@ class Fgmres {
   std::vector<DevBuf<V>> Vb_, Zb_;
   DevBuf<V> R_;
   BlockTab<T> vtab_{}, ztab_{};
-  DevBuf<V> hcol1_, hcol2_, ydev_;
+  DevBuf<V> hcol1_, hcol2_, ydev_, ccoef_;
+  // Pythagorean one-pass orthogonalisation with CGS2 fallback (HZ_ORTHO=cgs2
+  // forces the two-pass path everywhere)
+  bool pip_ = true;
+  // accept the one-pass block when ||W'_c||^2 >= eta2 ||W_c||^2 for every
+  // column: the Pythagorean S then has relative error <= eps/eta2 and Q is
+  // orthogonal to V to eps/sqrt(eta2) (1e-4 -> ~1e-14), far below what a
+  // 1e-6 solve can see; below it the step falls back to CGS2 + CholQR2
+  double pip_eta2_ = 1e-4;
+
+ public:
+  int64_t pip_accepted_ = 0, pip_rejected_ = 0;
+
+ private:
   PinnedBuf<V> h_hcol_, h_y_;
   BlockAlgebra<T> alg_;
 };
