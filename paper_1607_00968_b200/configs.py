@@ -155,7 +155,10 @@ def config1(nlevels: int = 4, k: int = 4, nx: int = 129) -> HelmholtzConfig:
     z = np.arange(nz, dtype=np.float64)[None, :]
     v = (1.5 + 2.5 * z / (nz - 1)) * (1.0 + 0.1 * p)
     rs = np.random.default_rng(seed_for(1, 1))
-    xs = rs.integers(16, nx - 16, size=k)
+    # distinct positions: coincident sources make the RHS block rank
+    # deficient, which the reference's FGMRES treats as a happy breakdown
+    # every restart (src/krylov.cpp:228-234) -- a degenerate benchmark
+    xs = rs.choice(np.arange(16, nx - 16), size=k, replace=False)
     src = [int(x) for x in xs]  # z = 0 surface: idx = x
     return _finish("cfg1_2d_129x129", 2, (nx, nz, 1), v, (16, 0, 0), (16, 16, 0), src, nlevels,
                    note="literal BASELINE config 1" if nlevels == 4 else f"config 1 geometry, {nlevels} levels")

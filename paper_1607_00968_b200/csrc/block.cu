@@ -303,6 +303,100 @@ small_cholesky_kernel(int k, const cplx_t<T>* __restrict__ G, cplx_t<T>* __restr
   if (tid == 0) *flag = fl;
 }
 
+// ---- column-wise Gram-Schmidt with one re-orthogonalisation: the
+// reference's thin_qr (inc/block.hpp:104-137) for blocks CholQR cannot
+// resolve (near rank-deficient: a column collapsing below ~1e-5 of its
+// norm). One column at a time, entirely on the device:
+//   d1 = W[:, :j+1]^H w_j (self entry = norm0^2); w_j -= W[:, :j] d1[:j]
+//   d2 = ...;                                     w_j -= W[:, :j] d2[:j]
+//   d3 = ... (self entry = norm^2); collapse if norm <= 1e-12 norm0.
+template <class T>
+__global__ void __launch_bounds__(256)
+col_dots_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ W, int j, cplx_t<T>* __restrict__ partials,
+                int nslots) {
+  using V = cplx_t<T>;
+  __shared__ V red[4][64];
+  const int p = threadIdx.x & 63, g = threadIdx.x >> 6;
+  const int slot = blockIdx.x;
+  const int64_t per = (n + nslots - 1) / nslots;
+  const int64_t r0 = int64_t(slot) * per, r1 = (r0 + per) < n ? (r0 + per) : n;
+  V s = czero<V>();
+  if (p <= j)
+    for (int64_t r = r0 + g; r < r1; r += 4) s = cfmac(W[r * k + p], W[r * k + j], s);
+  red[g][p] = s;
+  __syncthreads();
+  if (g == 0 && p <= j) {
+    V t = red[0][p];
+    for (int gg = 1; gg < 4; ++gg) t = cadd(t, red[gg][p]);
+    partials[int64_t(slot) * (j + 1) + p] = t;
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+col_update_kernel(int64_t n, int k, cplx_t<T>* __restrict__ W, int j, const cplx_t<T>* __restrict__ d) {
+  using V = cplx_t<T>;
+  const int64_t r = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (r >= n) return;
+  V w = W[r * k + j];
+  for (int p = 0; p < j; ++p) w = csub(w, cmul(d[p], W[r * k + p]));
+  W[r * k + j] = w;
+}
+
+template <class T>
+__global__ void __launch_bounds__(256)
+col_finish_kernel(int64_t n, int k, cplx_t<T>* __restrict__ W, int j, const cplx_t<T>* __restrict__ d1,
+                  const cplx_t<T>* __restrict__ d2, const cplx_t<T>* __restrict__ d3, cplx_t<T>* __restrict__ R,
+                  int* flag, T tol) {
+  using V = cplx_t<T>;
+  const T norm0 = sqrt(d1[j].x), norm = sqrt(d3[j].x);
+  const bool dead = norm <= tol * (norm0 > T(0) ? norm0 : T(1));
+  const int64_t r = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (r < n) W[r * k + j] = dead ? czero<V>() : cscale(T(1) / norm, W[r * k + j]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int p = 0; p < j; ++p) R[p * k + j] = cadd(cadd(czero<V>(), d1[p]), d2 ? d2[p] : czero<V>());
+    R[j * k + j] = dead ? czero<V>() : mk(norm, T(0));
+    if (dead) *flag = 1;
+  }
+}
+
+}  // namespace
+
+template <class T>
+void launch_mgs_qr(int64_t n, int k, cplx_t<T>* W, cplx_t<T>* R, cplx_t<T>* dbuf, cplx_t<T>* partials,
+                   int max_slots, int* flag, cudaStream_t s) {
+  using V = cplx_t<T>;
+  const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(max_slots, (n + 255) / 256)));
+  ProfScope prof("mgs_qr", 6.0 * n * k * sizeof(V), s);
+  HZ_CUDA(cudaMemsetAsync(R, 0, sizeof(V) * size_t(k) * k, s));
+  HZ_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), s));
+  const T tol = sizeof(T) == 8 ? T(1e-12) : T(1e-6);
+  V* d1 = dbuf;
+  V* d2 = dbuf + 64;
+  V* d3 = dbuf + 128;
+  auto dots = [&](int j, V* out) {
+    col_dots_kernel<T><<<nslots, 256, 0, s>>>(n, k, W, j, partials, nslots);
+    launch_reduce_partials<T>(j + 1, nslots, partials, out, s);
+  };
+  for (int j = 0; j < k; ++j) {
+    dots(j, d1);
+    if (j > 0) {
+      col_update_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(n, k, W, j, d1);
+      dots(j, d2);
+      col_update_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(n, k, W, j, d2);
+    }
+    dots(j, d3);
+    col_finish_kernel<T><<<grid_for(n, 256), 256, 0, s>>>(n, k, W, j, d1, j > 0 ? d2 : nullptr, d3, R, flag,
+                                                          tol);
+  }
+  HZ_LAUNCH_CHECK();
+}
+template void launch_mgs_qr<double>(int64_t, int, double2*, double2*, double2*, double2*, int, int*,
+                                    cudaStream_t);
+template void launch_mgs_qr<float>(int64_t, int, float2*, float2*, float2*, float2*, int, int*, cudaStream_t);
+
+namespace {
+
 // Pythagorean block CholQR factor for one Arnoldi step (single CTA):
 // Hc = [H_0 .. H_{nb-1}, G] from one Gram pass [V_0..V_{nb-1}, W]^H W.
 // S = G - sum_i H_i^H H_i (= W'^H W' for W' = W - V H, V orthonormal);
@@ -335,17 +429,19 @@ pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __
     A[e] = s;
   }
   __syncthreads();
-  if (tid == 0)
-    for (int c = 0; c < k; ++c)
-      if (!(A[c * k + c].x >= eta2 * G[c * k + c].x) || !(A[c * k + c].x > T(0))) fl = 1;
-  __syncthreads();
-  if (fl) {
-    if (tid == 0) *flag = 1;
-    return;
-  }
   for (int j = 0; j < k; ++j) {
-    if (tid == 0) A[j * k + j] = mk(sqrt(A[j * k + j].x), T(0));
+    // every Cholesky pivot (the squared norm of column j after projecting
+    // out V and the earlier columns) must keep eta2 of the column's norm^2
+    if (tid == 0) {
+      const T d = A[j * k + j].x;
+      if (!(d >= eta2 * G[j * k + j].x) || !(d > T(0))) fl = 1;
+      A[j * k + j] = mk(sqrt(d > T(0) ? d : T(1)), T(0));
+    }
     __syncthreads();
+    if (fl) {
+      if (tid == 0) *flag = 1;
+      return;
+    }
     const T inv = T(1) / A[j * k + j].x;
     for (int c = j + 1 + tid; c < k; c += blockDim.x) A[j * k + c] = cscale(inv, A[j * k + c]);
     __syncthreads();
@@ -355,12 +451,6 @@ pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __
       if (c >= a) A[a * k + c] = csub(A[a * k + c], cmulc(A[j * k + a], A[j * k + c]));
     }
     __syncthreads();
-    if (tid == 0 && j + 1 < k && !(A[(j + 1) * k + j + 1].x > T(0))) fl = 1;
-    __syncthreads();
-    if (fl) {
-      if (tid == 0) *flag = 1;
-      return;
-    }
   }
   for (int e = tid; e < kk; e += blockDim.x) {
     const int a = e / k, c = e % k;

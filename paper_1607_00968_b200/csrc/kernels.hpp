@@ -129,6 +129,15 @@ template <class T>
 void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* Rinv, int* flag,
                            T rel_tol, cudaStream_t s);
 
+// Column-by-column Gram-Schmidt with re-orthogonalisation, the reference's
+// thin_qr (inc/block.hpp:104-137), fully on the device: W <- Q, R (k x k),
+// flag = 1 if a column collapsed (zeroed, R_jj = 0). dbuf >= 192 entries,
+// partials >= max_slots * 64 entries. Used when CholQR cannot resolve the
+// block (near rank deficiency).
+template <class T>
+void launch_mgs_qr(int64_t n, int k, cplx_t<T>* W, cplx_t<T>* R, cplx_t<T>* dbuf, cplx_t<T>* partials,
+                   int max_slots, int* flag, cudaStream_t s);
+
 // Pythagorean block CholQR of one Arnoldi step from Hc = [H_0..H_{nb-1}, G]
 // (one Gram pass [V_0..V_{nb-1}, W]^H W): R, R^{-1} and the block-update
 // coefficients C (nb + 1 tiles) of Q = (W - V H) R^{-1}; flag 0 accepted,

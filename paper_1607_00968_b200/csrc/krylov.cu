@@ -261,12 +261,25 @@ void BlockAlgebra<T>::col_norms(const V* X, std::vector<double>& out, cudaStream
 
 template <class T>
 void BlockAlgebra<T>::thin_qr_enqueue(V* W, cudaStream_t s) {
-  // collapse threshold of thin_qr (inc/block.hpp:105,126): 1e-12 relative
-  const T tol = std::is_same<T, double>::value ? T(1e-12) : T(1e-6);
+  // CholQR2 resolves a column only down to ~1e-5 of its norm (the Gram
+  // squares the condition number); the reference's collapse threshold is
+  // 1e-12 (inc/block.hpp:105,126). Blocks flagged by the first Cholesky
+  // (pivot^2 < 1e-10 G_jj) take the device column Gram-Schmidt instead.
+  const T tol = std::is_same<T, double>::value ? T(1e-5) : T(1e-3);
   BlockTab<T> t{};
   t.p[0] = W;
   gram(t, 1, W, G.get(), s);
   launch_small_cholesky<T>(k, G.get(), R1.get(), R1i.get(), flags.get(), tol, s);
+  HZ_CUDA(cudaMemcpyAsync(h_flags.get(), flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  mgs_used = h_flags[0] != 0;
+  if (mgs_used) {
+    dbuf.ensure(192);
+    launch_mgs_qr<T>(n, k, W, R1.get(), dbuf.get(), partials.get(), nslots, flags.get(), s);
+    HZ_CUDA(cudaMemcpyAsync(h_R.get(), R1.get(), sizeof(V) * size_t(k) * k, cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaMemcpyAsync(h_flags.get(), flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    return;
+  }
   launch_multi_update<T>(n, k, 1, t, R1i.get(), nullptr, tmp_blk.get(), T(1), s);
   t.p[0] = tmp_blk.get();
   gram(t, 1, tmp_blk.get(), G.get(), s);
@@ -282,6 +295,11 @@ template <class T>
 void BlockAlgebra<T>::thin_qr_finish(std::vector<cplx>& R, bool& deficient) {
   const size_t kk = size_t(k) * k;
   R.assign(kk, cplx{});
+  if (mgs_used) {
+    for (size_t e = 0; e < kk; ++e) R[e] = to_c(h_R[e]);
+    deficient = h_flags[0] != 0;
+    return;
+  }
   // R = R2 R1 (both upper triangular)
   for (int p = 0; p < k; ++p)
     for (int q = p; q < k; ++q) {

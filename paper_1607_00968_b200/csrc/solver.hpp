@@ -168,6 +168,8 @@ class BlockAlgebra {
   DevBuf<V> partials, tmp_blk, G, R1, R1i, R2, R2i;
   DevBuf<T> rpart, rnorm;
   DevBuf<int> flags;
+  DevBuf<V> dbuf;         // column Gram-Schmidt dot products
+  bool mgs_used = false;  // last thin_qr took the column Gram-Schmidt path
   PinnedBuf<T> h_norm;
   PinnedBuf<V> h_R;     // [R1 | R2]
   PinnedBuf<int> h_flags;
