@@ -9,6 +9,10 @@
 #include "kernels.hpp"
 #include "profile.hpp"
 #include "block_tiled.cuh"
+#include "block_dmma.cuh"
+
+#include <cstdlib>
+#include <type_traits>
 
 namespace hz {
 
@@ -518,9 +522,49 @@ int gram_partial_slots(int64_t n, int k) {
   return slots_for(n);
 }
 
+// FP64 tensor-core (DMMA) path for complex128; HZ_DMMA=0 selects the FFMA
+// tiles instead (for comparison).
+bool use_dmma() {
+  static const bool on = [] {
+    const char* e = std::getenv("HZ_DMMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int K>
+void gram_dmma_launch(int64_t n, int nb, const BlockTab<double>& X, const double2* Y, double2* partials,
+                      int nslots, cudaStream_t s) {
+  const size_t smem = dmma::gram_smem<K>();
+  auto kern = dmma::gram_kernel<K>;
+  static bool attr = false;
+  if (!attr) {
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  kern<<<dim3(nb, nslots), 256, smem, s>>>(n, X, Y, partials, nslots);
+}
+
+template <int K>
+void update_dmma_launch(int64_t n, int nb, const BlockTab<double>& X, const double2* H, const double2* Yin,
+                        double2* Yout, double sign, cudaStream_t s) {
+  const size_t smem = dmma::update_smem<K>();
+  auto kern = dmma::update_kernel<K>;
+  static bool attr = false;
+  if (!attr) {
+    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  kern<<<grid_for(n, dmma::UpdateCfg<K>::RC), dmma::UpdateCfg<K>::THREADS, smem, s>>>(n, nb, X, H, Yin, Yout,
+                                                                                    sign);
+}
+
 template <class T, int K>
 void gram_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
                        cplx_t<T>* partials, int nslots, cudaStream_t s) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (use_dmma()) return gram_dmma_launch<K>(n, nb, X, Y, partials, nslots, s);
+  }
   const size_t smem = tiled::gram_smem<T, K>();
   auto kern = tiled::gram_kernel<T, K>;
   static bool attr = false;
@@ -534,6 +578,9 @@ void gram_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T>*
 template <class T, int K>
 void update_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T>* H,
                          const cplx_t<T>* Yin, cplx_t<T>* Yout, T sign, cudaStream_t s) {
+  if constexpr (std::is_same<T, double>::value) {
+    if (use_dmma()) return update_dmma_launch<K>(n, nb, X, H, Yin, Yout, sign, s);
+  }
   constexpr int RC = tiled::update_rows<K>();
   const size_t smem = tiled::update_smem<T, K>();
   auto kern = tiled::update_kernel<T, K>;

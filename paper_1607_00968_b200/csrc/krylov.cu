@@ -379,17 +379,25 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     ++rep.qr_factorizations;
     lsq.reset(k, m, Rk);
     int j = 0;
+    // Z_j = M^{-1} V_j ; V_{j+1} <- A Z_j  (enqueue only)
+    auto enqueue_step = [&](int jj) {
+      V* Zj = Zb_[jj].get();
+      if (op.prec)
+        op.prec(Vb_[jj].get(), Zj, k, s);
+      else
+        HZ_CUDA(cudaMemcpyAsync(Zj, Vb_[jj].get(), blk, cudaMemcpyDeviceToDevice, s));
+      op.apply(Zj, Vb_[jj + 1].get(), k, s);
+    };
+    // The next step's preconditioner + matvec depend only on V_{j+1}, not on
+    // the host least-squares update of step j, so they are enqueued before
+    // the host LS and overlap it; if step j converges, the speculative work
+    // is simply discarded (its buffers are rewritten by the next restart).
+    bool prefetched = false;
     for (; j < m && rep.cycles < max_cycles; ++j) {
-      V* Zj = Zb_[j].get();
-      if (op.prec) {
-        op.prec(Vb_[j].get(), Zj, k, s);
-        ++rep.cycles;
-      } else {
-        HZ_CUDA(cudaMemcpyAsync(Zj, Vb_[j].get(), blk, cudaMemcpyDeviceToDevice, s));
-        ++rep.cycles;
-      }
+      if (!prefetched) enqueue_step(j);
+      prefetched = false;
+      ++rep.cycles;
       V* W = Vb_[j + 1].get();
-      op.apply(Zj, W, k, s);
       const size_t hc = size_t(j + 1) * kk;
       bool deficient = false;
       H[j].assign(j + 2, std::vector<cplx>(kk));
@@ -442,6 +450,10 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
       if (deficient) {
         ++j;
         break;  // happy breakdown
+      }
+      if (j + 1 < m && rep.cycles < max_cycles) {
+        enqueue_step(j + 1);
+        prefetched = true;
       }
       lsq.add_block(j, H[j]);
       lsq.residuals(res);
