@@ -401,41 +401,51 @@ template void launch_mgs_qr<float>(int64_t, int, float2*, float2*, float2*, floa
 
 namespace {
 
-// Pythagorean block CholQR factor for one Arnoldi step (single CTA):
+// Pythagorean block CholQR factor for one Arnoldi step (single CTA of
+// 1024 threads, operands staged in shared memory when they fit):
 // Hc = [H_0 .. H_{nb-1}, G] from one Gram pass [V_0..V_{nb-1}, W]^H W.
 // S = G - sum_i H_i^H H_i (= W'^H W' for W' = W - V H, V orthonormal);
-// accepted when every S_cc >= eta2 * G_cc (no severe cancellation, so the
-// Pythagorean subtraction keeps full relative accuracy -- otherwise the
-// caller re-orthogonalises with CGS2 + CholQR2); then S = R^H R and the
-// coefficients C_i = -H_i R^{-1}, C_nb = R^{-1} so that
+// accepted when every Cholesky pivot keeps eta2 of its column's norm^2 (no
+// severe cancellation, so the Pythagorean subtraction keeps full relative
+// accuracy -- otherwise the caller re-orthogonalises with CGS2 + CholQR2);
+// then S = R^H R and C_i = -H_i R^{-1}, C_nb = R^{-1}, so that
 // Q = sum_i V_i C_i + W C_nb = (W - V H) R^{-1} in one block update.
 // flag: 0 accepted, 1 rejected.
 template <class T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __restrict__ R,
-                  cplx_t<T>* __restrict__ Rinv, cplx_t<T>* __restrict__ C, int* flag, T eta2) {
+                  cplx_t<T>* __restrict__ Rinv, cplx_t<T>* __restrict__ C, int* flag, T eta2, int staged) {
   using V = cplx_t<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* A = reinterpret_cast<V*>(smem_raw);  // [k][k]
-  __shared__ int fl;
-  const int tid = threadIdx.x;
   const int kk = k * k;
-  const V* G = Hc + int64_t(nb) * kk;
+  V* A = reinterpret_cast<V*>(smem_raw);  // [k][k] S, then R
+  V* Ri = A + kk;                         // [k][k] R^{-1}
+  V* Hs = Ri + kk;                        // [nb+1][k][k] when staged
+  __shared__ int fl;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const V* H = Hc;
+  if (staged) {
+    for (int e = tid; e < (nb + 1) * kk; e += nt) Hs[e] = Hc[e];
+    H = Hs;
+  }
   if (tid == 0) fl = 0;
-  for (int e = tid; e < kk; e += blockDim.x) {
+  __syncthreads();
+  const V* G = H + int64_t(nb) * kk;
+  for (int e = tid; e < kk; e += nt) {
     const int a = e / k, b = e - a * k;
     if (b < a) continue;  // upper triangle suffices
     V s = G[e];
     for (int i = 0; i < nb; ++i) {
-      const V* Hi = Hc + int64_t(i) * kk;
+      const V* Hi = H + int64_t(i) * kk;
+#pragma unroll 4
       for (int p = 0; p < k; ++p) s = csub(s, cmulc(Hi[p * k + a], Hi[p * k + b]));
     }
     A[e] = s;
   }
   __syncthreads();
   for (int j = 0; j < k; ++j) {
-    // every Cholesky pivot (the squared norm of column j after projecting
-    // out V and the earlier columns) must keep eta2 of the column's norm^2
+    // every pivot (squared norm of column j after projecting out V and the
+    // earlier columns) must keep eta2 of the column's norm^2
     if (tid == 0) {
       const T d = A[j * k + j].x;
       if (!(d >= eta2 * G[j * k + j].x) || !(d > T(0))) fl = 1;
@@ -447,38 +457,40 @@ pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __
       return;
     }
     const T inv = T(1) / A[j * k + j].x;
-    for (int c = j + 1 + tid; c < k; c += blockDim.x) A[j * k + c] = cscale(inv, A[j * k + c]);
+    for (int c = j + 1 + tid; c < k; c += nt) A[j * k + c] = cscale(inv, A[j * k + c]);
     __syncthreads();
     const int m = k - j - 1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
+    for (int e = tid; e < m * m; e += nt) {
       const int a = j + 1 + e / m, c = j + 1 + e % m;
       if (c >= a) A[a * k + c] = csub(A[a * k + c], cmulc(A[j * k + a], A[j * k + c]));
     }
     __syncthreads();
   }
-  for (int e = tid; e < kk; e += blockDim.x) {
-    const int a = e / k, c = e % k;
-    R[e] = c >= a ? A[e] : czero<V>();
-  }
-  for (int c = tid; c < k; c += blockDim.x)
+  // R^{-1}: column c solved by one warp-strided thread group (back substitution)
+  for (int c = tid; c < k; c += nt)
     for (int i = k - 1; i >= 0; --i) {
       if (i > c) {
-        Rinv[i * k + c] = czero<V>();
+        Ri[i * k + c] = czero<V>();
         continue;
       }
       V s = (i == c) ? mk(T(1), T(0)) : czero<V>();
-      for (int l = i + 1; l <= c; ++l) s = csub(s, cmul(A[i * k + l], Rinv[l * k + c]));
-      Rinv[i * k + c] = cscale(T(1) / A[i * k + i].x, s);
+      for (int l = i + 1; l <= c; ++l) s = csub(s, cmul(A[i * k + l], Ri[l * k + c]));
+      Ri[i * k + c] = cscale(T(1) / A[i * k + i].x, s);
     }
   __syncthreads();
-  for (int e = tid; e < (nb + 1) * kk; e += blockDim.x) {
+  for (int e = tid; e < kk; e += nt) {
+    const int a = e / k, c = e % k;
+    R[e] = c >= a ? A[e] : czero<V>();
+    Rinv[e] = Ri[e];
+  }
+  for (int e = tid; e < (nb + 1) * kk; e += nt) {
     const int i = e / kk, r = e - i * kk, a = r / k, b = r - a * k;
     if (i == nb) {
-      C[e] = Rinv[r];
+      C[e] = Ri[r];
     } else {
-      const V* Hi = Hc + int64_t(i) * kk;
+      const V* Hi = H + int64_t(i) * kk;
       V s = czero<V>();
-      for (int l = 0; l <= b; ++l) s = cfma(Hi[a * k + l], Rinv[l * k + b], s);
+      for (int l = 0; l <= b; ++l) s = cfma(Hi[a * k + l], Ri[l * k + b], s);
       C[e] = mk(-s.x, -s.y);
     }
   }
@@ -600,7 +612,9 @@ int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx
   ProfScope prof(sizeof(T) == 8 ? "multi_gram_c128" : "multi_gram_c64",
                  double(nb + 1) * n * k * sizeof(cplx_t<T>), s, 8.0 * double(n) * k * k * nb);
   // ~4 CTAs per SM in total over the nb blocks; at least 32 rows per slot
-  int64_t want = (4 * kNumSMs + nb - 1) / nb;
+  // exactly one wave of resident CTAs (3 per SM for the tiled / DMMA Grams)
+  // over the nb blocks: a partial last wave would idle up to 2/3 of the GPU
+  int64_t want = std::max<int64_t>(1, (3 * kNumSMs) / nb);
   want = std::min<int64_t>(want, (n + 31) / 32);
   const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(want, max_slots)));
   if (k == 32)
@@ -699,12 +713,14 @@ void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* R
 template <class T>
 void launch_pip_factor(int k, int nb, const cplx_t<T>* Hc, cplx_t<T>* R, cplx_t<T>* Rinv,
                        cplx_t<T>* C, int* flag, T eta2, cudaStream_t s) {
-  const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
+  const size_t base = sizeof(cplx_t<T>) * 2 * size_t(k) * k;
+  const size_t full = base + sizeof(cplx_t<T>) * size_t(nb + 1) * k * k;
+  const int staged = full <= 200 * 1024 ? 1 : 0;
+  const size_t smem = staged ? full : base;
   auto kern = pip_factor_kernel<T>;
-  if (smem > 48 * 1024)
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   ProfScope prof("pip_factor", double(nb + 2) * k * k * sizeof(cplx_t<T>), s);
-  kern<<<1, 256, smem, s>>>(k, nb, Hc, R, Rinv, C, flag, eta2);
+  kern<<<1, 1024, smem, s>>>(k, nb, Hc, R, Rinv, C, flag, eta2, staged);
   HZ_LAUNCH_CHECK();
 }
 template void launch_pip_factor<double>(int, int, const double2*, double2*, double2*, double2*, int*,

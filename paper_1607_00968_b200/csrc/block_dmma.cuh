@@ -38,6 +38,9 @@ struct GramCfg {
   static constexpr int QT = K / (8 * WQ);            // 8-wide q tiles per warp
   static constexpr int NG = 8 / (WP * WQ);           // row groups
   static constexpr int RC = 32;                      // staged rows per chunk
+  // Row stride == 2 (mod 8) complex: a quarter-warp's fragment loads
+  // (rows t = 0..3, columns g, g+1) then hit 8 distinct 16-byte bank groups.
+  static constexpr int LD = K + 2;
 };
 
 template <int K>
@@ -45,7 +48,8 @@ __global__ void __launch_bounds__(256)
 gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
             double2* __restrict__ partials, int nslots) {
   using C = GramCfg<K>;
-  constexpr int WP = C::WP, WQ = C::WQ, NG = C::NG, QT = C::QT, RC = C::RC, TILE = RC * K;
+  constexpr int WP = C::WP, WQ = C::WQ, NG = C::NG, QT = C::QT, RC = C::RC, LD = C::LD;
+  constexpr int TILE = RC * LD;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);  // [2][x|y][RC][K]
   const int i = blockIdx.x, slot = blockIdx.y, nb = gridDim.x;
@@ -70,8 +74,8 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
     return (r1 - c0) < RC ? int(r1 - c0) : RC;
   };
   if (nchunks > 0) {
-    tiled::stage_rows<double2, K, RC, K>(buf, Xi + r0 * K, rows_of(0), tid);
-    tiled::stage_rows<double2, K, RC, K>(buf + TILE, Y + r0 * K, rows_of(0), tid);
+    tiled::stage_rows<double2, K, RC, LD>(buf, Xi + r0 * K, rows_of(0), tid);
+    tiled::stage_rows<double2, K, RC, LD>(buf + TILE, Y + r0 * K, rows_of(0), tid);
   }
   tiled::cp_async_commit();
   for (int c = 0; c < nchunks; ++c) {
@@ -79,8 +83,8 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
     if (c + 1 < nchunks) {
       const int64_t c1 = r0 + int64_t(c + 1) * RC;
       double2* nx = buf + (st ^ 1) * 2 * TILE;
-      tiled::stage_rows<double2, K, RC, K>(nx, Xi + c1 * K, rows_of(c + 1), tid);
-      tiled::stage_rows<double2, K, RC, K>(nx + TILE, Y + c1 * K, rows_of(c + 1), tid);
+      tiled::stage_rows<double2, K, RC, LD>(nx, Xi + c1 * K, rows_of(c + 1), tid);
+      tiled::stage_rows<double2, K, RC, LD>(nx + TILE, Y + c1 * K, rows_of(c + 1), tid);
     }
     tiled::cp_async_commit();
     tiled::cp_async_wait<1>();
@@ -94,14 +98,14 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
       double xa[2][3], yb[QT][3];
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
-        const double2 x = xs[r * K + wp * 16 + a * 8 + g];
+        const double2 x = xs[r * LD + wp * 16 + a * 8 + g];
         xa[a][0] = x.x;
         xa[a][1] = x.y;
         xa[a][2] = x.x + x.y;
       }
 #pragma unroll
       for (int b = 0; b < QT; ++b) {
-        const double2 y = ys[r * K + (wq * QT + b) * 8 + g];
+        const double2 y = ys[r * LD + (wq * QT + b) * 8 + g];
         yb[b][0] = y.x;
         yb[b][1] = y.y;
         yb[b][2] = y.x - y.y;
@@ -144,7 +148,7 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
 template <int K>
 size_t gram_smem() {
   using C = GramCfg<K>;
-  const size_t a = 4 * size_t(C::RC) * K, b = size_t(K) * K;
+  const size_t a = 4 * size_t(C::RC) * C::LD, b = size_t(K) * K;
   return sizeof(double2) * (a > b ? a : b);
 }
 
@@ -158,7 +162,11 @@ struct UpdateCfg {
   static constexpr int WR = 8 / WQ;                  // 16-row warp tiles
   static constexpr int RC = WR * 16, QT = K / (8 * WQ);
   static constexpr int THREADS = 256;
-  static constexpr int LDX = K + 2;  // padded X rows
+  // padded strides: A loads (rows g, columns t) want LDX == 4 (mod 8) and
+  // B loads (rows t, columns g) want LDH == 2 (mod 8) for conflict-free
+  // quarter-warps of 16-byte accesses
+  static constexpr int LDX = K + 4;
+  static constexpr int LDH = K + 2;
 };
 
 template <int K>
@@ -167,7 +175,8 @@ update_kernel(int64_t n, int nb, const BlockTab<double> X, const double2* __rest
               const double2* Yin, double2* Yout, double sign) {
   using C = UpdateCfg<K>;
   constexpr int RC = C::RC, QT = C::QT, LDX = C::LDX, WQ = C::WQ, NT = C::THREADS;
-  constexpr int XT = RC * LDX, HT = K * K, STAGE = XT + HT;
+  constexpr int LDH = C::LDH;
+  constexpr int XT = RC * LDX, HT = K * LDH, STAGE = XT + HT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -194,7 +203,10 @@ update_kernel(int64_t n, int nb, const BlockTab<double> X, const double2* __rest
         *d = czero<double2>();
     }
     const double2* hsrc = H + int64_t(i) * K * K;
-    for (int e = tid; e < K * K; e += NT) tiled::cp_async16(dst + XT + e, hsrc + e);
+    for (int e = tid; e < K * K; e += NT) {
+      const int p = e / K, q = e - p * K;
+      tiled::cp_async16(dst + XT + p * LDH + q, hsrc + e);
+    }
   };
   if (nb > 0) stage(0, buf);
   tiled::cp_async_commit();
@@ -218,7 +230,7 @@ update_kernel(int64_t n, int nb, const BlockTab<double> X, const double2* __rest
       }
 #pragma unroll
       for (int b = 0; b < QT; ++b) {  // B[t][g] = C[p0+t][b*8+g]
-        const double2 h = hs[(p0 + t) * K + (wq * QT + b) * 8 + g];
+        const double2 h = hs[(p0 + t) * LDH + (wq * QT + b) * 8 + g];
         hb[b][0] = h.x;
         hb[b][1] = h.y;
         hb[b][2] = h.x + h.y;
@@ -254,7 +266,7 @@ update_kernel(int64_t n, int nb, const BlockTab<double> X, const double2* __rest
 template <int K>
 size_t update_smem() {
   using C = UpdateCfg<K>;
-  return sizeof(double2) * 2 * (size_t(C::RC) * C::LDX + size_t(K) * K);
+  return sizeof(double2) * 2 * (size_t(C::RC) * C::LDX + size_t(K) * C::LDH);
 }
 
 }  // namespace dmma

@@ -12,6 +12,8 @@
 
 namespace hz {
 
+int split_for_tiles(int tiles);
+
 namespace {
 
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
@@ -270,6 +272,8 @@ void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, const cplx_t<T>* b, c
     attr = true;
   }
   const int tiles = grid_for(n, TI);
+  nsplit = std::min(nsplit, split_for_tiles(tiles));
+  if (nsplit > 1 && part == nullptr) nsplit = 1;
   kern<<<dim3(tiles, nsplit), 256, smem, s>>>(n, ainvT, b, nsplit == 1 ? x : part, nsplit);
   if (nsplit > 1)
     split_reduce_kernel<T><<<grid_for(n * K, 256), 256, 0, s>>>(n * K, nsplit, part, x);
@@ -277,12 +281,18 @@ void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, const cplx_t<T>* b, c
 
 }  // namespace
 
+// Split-K factor: fill a whole number of waves (2 resident CTAs per SM x 148
+// SMs) instead of leaving a partial last wave.
+int split_for_tiles(int tiles) {
+  int sk = (2 * kNumSMs) / tiles;
+  return sk < 1 ? 1 : (sk > 32 ? 32 : sk);
+}
+
 int coarse_split(int64_t n, int k) {
   if (k != 16 && k != 32 && k != 64) return 0;
-  // the c64 tile (256 rows) is the larger one; c128 uses 64-row tiles
-  const int tiles = grid_for(n, 128);
-  int sk = (4 * kNumSMs) / tiles;
-  return sk < 1 ? 1 : (sk > 32 ? 32 : sk);
+  // upper bound over both precisions: the fewest row tiles (256-row c64
+  // tiles) give the largest split
+  return split_for_tiles(grid_for(n, 256));
 }
 
 

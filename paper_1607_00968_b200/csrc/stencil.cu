@@ -42,27 +42,40 @@ __device__ __forceinline__ cplx_t<T> fine_ax(const LevelOp<T>& op, const cplx_t<
   using V = cplx_t<T>;
   const LevelGeom& g = op.g;
   const uint32_t sx = g.k, sy = g.n0 * g.k, sz = g.n0 * g.n1 * g.k;
+  // All loads are issued before any arithmetic (out-of-range neighbours read
+  // the centre element and are dropped by a select, not a branch), so each
+  // thread has its 5-7 independent loads in flight at once instead of a
+  // chain of dependent round trips.
+  const bool xm = el.i > 0, xp = el.i + 1 < g.n0, ym = el.j > 0, yp = el.j + 1 < g.n1;
+  const bool zm = NDIM == 3 && el.kz > 0, zp = NDIM == 3 && el.kz + 1 < g.n2;
   const V c = __ldg(&op.center[el.node]);
+  const V u0 = __ldg(&x[e]);
+  const V uxm = __ldg(&x[xm ? e - sx : e]), uxp = __ldg(&x[xp ? e + sx : e]);
+  const V uym = __ldg(&x[ym ? e - sy : e]), uyp = __ldg(&x[yp ? e + sy : e]);
+  V uzm = u0, uzp = u0;
+  if (NDIM == 3) {
+    uzm = __ldg(&x[zm ? e - sz : e]);
+    uzp = __ldg(&x[zp ? e + sz : e]);
+  }
+  const T wx = op.w[0], wy = op.w[1], wz = op.w[2];
   V acc;
   if (!CSR) {
-    acc = cmul(c, __ldg(&x[e]));
-    if (el.i > 0) acc = crfma(op.w[0], __ldg(&x[e - sx]), acc);
-    if (el.i + 1 < g.n0) acc = crfma(op.w[0], __ldg(&x[e + sx]), acc);
-    if (el.j > 0) acc = crfma(op.w[1], __ldg(&x[e - sy]), acc);
-    if (el.j + 1 < g.n1) acc = crfma(op.w[1], __ldg(&x[e + sy]), acc);
-    if (NDIM == 3) {
-      if (el.kz > 0) acc = crfma(op.w[2], __ldg(&x[e - sz]), acc);
-      if (el.kz + 1 < g.n2) acc = crfma(op.w[2], __ldg(&x[e + sz]), acc);
-    }
+    acc = cmul(c, u0);
+    if (xm) acc = crfma(wx, uxm, acc);
+    if (xp) acc = crfma(wx, uxp, acc);
+    if (ym) acc = crfma(wy, uym, acc);
+    if (yp) acc = crfma(wy, uyp, acc);
+    if (zm) acc = crfma(wz, uzm, acc);
+    if (zp) acc = crfma(wz, uzp, acc);
   } else {
     acc = czero<V>();
-    if (NDIM == 3 && el.kz > 0) acc = crfma(op.w[2], __ldg(&x[e - sz]), acc);
-    if (el.j > 0) acc = crfma(op.w[1], __ldg(&x[e - sy]), acc);
-    if (el.i > 0) acc = crfma(op.w[0], __ldg(&x[e - sx]), acc);
-    acc = cfma(c, __ldg(&x[e]), acc);
-    if (el.i + 1 < g.n0) acc = crfma(op.w[0], __ldg(&x[e + sx]), acc);
-    if (el.j + 1 < g.n1) acc = crfma(op.w[1], __ldg(&x[e + sy]), acc);
-    if (NDIM == 3 && el.kz + 1 < g.n2) acc = crfma(op.w[2], __ldg(&x[e + sz]), acc);
+    if (zm) acc = crfma(wz, uzm, acc);
+    if (ym) acc = crfma(wy, uym, acc);
+    if (xm) acc = crfma(wx, uxm, acc);
+    acc = cfma(c, u0, acc);
+    if (xp) acc = crfma(wx, uxp, acc);
+    if (yp) acc = crfma(wy, uyp, acc);
+    if (zp) acc = crfma(wz, uzp, acc);
   }
   return acc;
 }
@@ -76,7 +89,12 @@ __device__ __forceinline__ cplx_t<T> stencil_ax(const LevelOp<T>& op,
   const LevelGeom& g = op.g;
   const int64_t sx = g.k, sy = int64_t(g.n0) * g.k, sz = int64_t(g.n0) * g.n1 * g.k;
   const V* __restrict__ cf = op.coef + el.node;
-  V acc = czero<V>();
+  constexpr int S = NDIM == 3 ? 27 : 9;
+  // Issue every coefficient and neighbour load first (out-of-range
+  // neighbours read the centre and are masked), then accumulate in the
+  // ascending-column order of the reference's CSR row.
+  V av[S], xv[S];
+  bool ok[S];
   const int zlo = NDIM == 3 ? -1 : 0, zhi = NDIM == 3 ? 1 : 0;
 #pragma unroll
   for (int dz = zlo; dz <= zhi; ++dz) {
@@ -88,13 +106,16 @@ __device__ __forceinline__ cplx_t<T> stencil_ax(const LevelOp<T>& op,
       for (int dx = -1; dx <= 1; ++dx) {
         const bool okx = dx < 0 ? el.i > 0 : (dx > 0 ? el.i + 1 < g.n0 : true);
         const int s = (NDIM == 3 ? (dz + 1) * 9 : 0) + (dy + 1) * 3 + (dx + 1);
-        if (okz && oky && okx) {
-          const V a = __ldg(&cf[int64_t(s) * g.nodes]);
-          acc = cfma(a, __ldg(&x[int64_t(e) + dz * sz + dy * sy + dx * sx]), acc);
-        }
+        ok[s] = okz && oky && okx;
+        av[s] = __ldg(&cf[int64_t(s) * g.nodes]);
+        xv[s] = __ldg(&x[ok[s] ? int64_t(e) + dz * sz + dy * sy + dx * sx : int64_t(e)]);
       }
     }
   }
+  V acc = czero<V>();
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (ok[s]) acc = cfma(av[s], xv[s], acc);
   return acc;
 }
 
@@ -152,28 +173,36 @@ restrict_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r,
   Elem<T> el;
   if (!decode(gc, e, el)) return;
   const int64_t k = gf.k;
-  V acc = czero<V>();
+  constexpr int S = NDIM == 3 ? 27 : 9;
+  // loads first (masked, see fine_ax), then the ascending-f accumulation
+  V rv[S];
+  T wv[S];
+  const int64_t fc = (2 * int64_t(el.i) + int64_t(gf.n0) * (2 * int64_t(el.j) + int64_t(gf.n1) * 2 * el.kz)) * k +
+                     el.col;
   const int zlo = NDIM == 3 ? -1 : 0, zhi = NDIM == 3 ? 1 : 0;
 #pragma unroll
   for (int ez = zlo; ez <= zhi; ++ez) {
     const int64_t fz = 2 * int64_t(el.kz) + ez;
-    if (fz < 0 || fz >= gf.n2) continue;
-    const T wz = ez == 0 ? T(1) : T(0.5);
+    const bool okz = fz >= 0 && fz < gf.n2;
 #pragma unroll
     for (int ey = -1; ey <= 1; ++ey) {
       const int64_t fy = 2 * int64_t(el.j) + ey;
-      if (fy < 0 || fy >= gf.n1) continue;
-      const T wy = ey == 0 ? T(1) : T(0.5);
+      const bool oky = fy >= 0 && fy < gf.n1;
 #pragma unroll
       for (int ex = -1; ex <= 1; ++ex) {
         const int64_t fx = 2 * int64_t(el.i) + ex;
-        if (fx < 0 || fx >= gf.n0) continue;
-        const T wx = ex == 0 ? T(1) : T(0.5);
-        const int64_t f = fx + int64_t(gf.n0) * (fy + int64_t(gf.n1) * fz);
-        acc = crfma(wx * wy * wz, __ldg(&r[f * k + el.col]), acc);
+        const bool ok = okz && oky && fx >= 0 && fx < gf.n0;
+        const int s = (NDIM == 3 ? (ez + 1) * 9 : 0) + (ey + 1) * 3 + (ex + 1);
+        wv[s] = ok ? (ex == 0 ? T(1) : T(0.5)) * (ey == 0 ? T(1) : T(0.5)) * (ez == 0 ? T(1) : T(0.5)) : T(0);
+        const int64_t off = (int64_t(ex) + int64_t(gf.n0) * (ey + int64_t(gf.n1) * ez)) * k;
+        rv[s] = __ldg(&r[ok ? fc + off : fc]);
       }
     }
   }
+  V acc = czero<V>();
+#pragma unroll
+  for (int s = 0; s < S; ++s)
+    if (wv[s] != T(0)) acc = crfma(wv[s], rv[s], acc);
   bc[e] = acc;
 }
 
@@ -188,37 +217,38 @@ prolong_correct_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__
   Elem<T> el;
   if (!decode(gf, e, el)) return;
   const int64_t k = gf.k;
-  uint32_t cx[2], cy[2], cz[2];
-  T wxv[2], wyv[2], wzv[2];
-  int nx, ny, nz;
-  auto axis = [](uint32_t f, uint32_t* c, T* w) -> int {
-    if ((f & 1u) == 0) {
-      c[0] = f >> 1;
-      w[0] = T(1);
-      return 1;
-    }
-    c[0] = (f - 1) >> 1;
-    c[1] = (f + 1) >> 1;
-    w[0] = w[1] = T(0.5);
-    return 2;
-  };
-  nx = axis(el.i, cx, wxv);
-  ny = axis(el.j, cy, wyv);
-  if (NDIM == 3) {
-    nz = axis(el.kz, cz, wzv);
-  } else {
-    nz = 1;
-    cz[0] = 0;
-    wzv[0] = T(1);
-  }
-  V corr = czero<V>();
-  for (int c = 0; c < nz; ++c)
-    for (int b = 0; b < ny; ++b)
-      for (int a = 0; a < nx; ++a) {
-        const int64_t C = cx[a] + int64_t(gc.n0) * (cy[b] + int64_t(gc.n1) * cz[c]);
-        corr = crfma(wxv[a] * wyv[b] * wzv[c], __ldg(&ec[C * k + el.col]), corr);
+  // parents per axis: even f -> (f/2, weight 1); odd f -> (f-1)/2, (f+1)/2
+  // with 1/2 each. Always gather 2 per axis (the second of an even f has
+  // weight 0 and is skipped in the sum), all loads issued up front.
+  const uint32_t cx0 = el.i >> 1, cx1 = (el.i + 1) >> 1;
+  const uint32_t cy0 = el.j >> 1, cy1 = (el.j + 1) >> 1;
+  const uint32_t cz0 = NDIM == 3 ? (el.kz >> 1) : 0, cz1 = NDIM == 3 ? ((el.kz + 1) >> 1) : 0;
+  const T wx0 = (el.i & 1u) ? T(0.5) : T(1), wx1 = (el.i & 1u) ? T(0.5) : T(0);
+  const T wy0 = (el.j & 1u) ? T(0.5) : T(1), wy1 = (el.j & 1u) ? T(0.5) : T(0);
+  const T wz0 = NDIM == 3 && (el.kz & 1u) ? T(0.5) : T(1), wz1 = NDIM == 3 && (el.kz & 1u) ? T(0.5) : T(0);
+  constexpr int NZ = NDIM == 3 ? 2 : 1;
+  V ev[NZ][2][2];
+  T wv[NZ][2][2];
+#pragma unroll
+  for (int c = 0; c < NZ; ++c)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int64_t C = (a ? cx1 : cx0) + int64_t(gc.n0) * ((b ? cy1 : cy0) + int64_t(gc.n1) * (c ? cz1 : cz0));
+        ev[c][b][a] = __ldg(&ec[C * k + el.col]);
+        wv[c][b][a] = (a ? wx1 : wx0) * (b ? wy1 : wy0) * (c ? wz1 : wz0);
       }
-  x[e] = cadd(x[e], corr);
+  const V xe = x[e];
+  V corr = czero<V>();
+#pragma unroll
+  for (int c = 0; c < NZ; ++c)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+        if (wv[c][b][a] != T(0)) corr = crfma(wv[c][b][a], ev[c][b][a], corr);
+  x[e] = cadd(xe, corr);
 }
 
 // ---------------------------------------------------------------- Galerkin
