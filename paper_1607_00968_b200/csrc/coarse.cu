@@ -91,8 +91,8 @@ banded_inverse_kernel(int64_t n, int64_t kl, int64_t ku, int64_t ld, const doubl
 // from L2.
 template <class T, int TI, int TL>
 __global__ void __launch_bounds__(256)
-coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT,
-                    const cplx_t<T>* __restrict__ b, cplx_t<T>* __restrict__ x) {
+coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT, int64_t ld,
+                    const cplx_t<T>* __restrict__ b, cplx_t<T>* x, const cplx_t<T>* c_in, T sign) {
   using V = cplx_t<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* As = reinterpret_cast<V*>(smem_raw);  // [TL][TI]
@@ -107,7 +107,7 @@ coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT,
     const int tl = (n - l0) < TL ? int(n - l0) : TL;
     for (int e = threadIdx.x; e < TL * TI; e += 256) {
       const int l = e / TI, i = e % TI;
-      As[e] = (l < tl && i0 + i < n) ? ainvT[(l0 + l) * inv_ld(n) + i0 + i] : czero<V>();
+      As[e] = (l < tl && i0 + i < n) ? ainvT[(l0 + l) * ld + i0 + i] : czero<V>();
     }
     for (int e = threadIdx.x; e < TL * k; e += 256) {
       const int l = e / k;
@@ -131,7 +131,14 @@ coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT,
     const int o = threadIdx.x + t * 256;
     if (o < nout) {
       const int i = o / k, q = o - i * k;
-      if (i0 + i < n) x[(i0 + i) * k + q] = acc[t];
+      if (i0 + i < n) {
+        V v = acc[t];
+        if (c_in) {
+          const V c = c_in[(i0 + i) * k + q];
+          v = mk(c.x + sign * v.x, c.y + sign * v.y);
+        }
+        x[(i0 + i) * k + q] = v;
+      }
     }
   }
 }
@@ -157,8 +164,8 @@ struct CoarseTile {
 // complex products. Slices write partials summed in fixed order afterwards.
 template <class T, int K>
 __global__ void __launch_bounds__(256)
-coarse_gemm_kernel(int64_t n, const cplx_t<T>* __restrict__ ainvT, const cplx_t<T>* __restrict__ b,
-                   cplx_t<T>* __restrict__ part, int nsplit) {
+coarse_gemm_kernel(int64_t n, const cplx_t<T>* __restrict__ ainvT, int64_t ld, const cplx_t<T>* __restrict__ b,
+                   cplx_t<T>* part, int nsplit, const cplx_t<T>* c_in, T sign) {
   using V = cplx_t<T>;
   using Tile = CoarseTile<T, K>;
   constexpr int TI = Tile::TI, TL = Tile::TL, NQT = Tile::NQT, TQ = Tile::TQ, NIT = Tile::NIT,
@@ -186,7 +193,7 @@ coarse_gemm_kernel(int64_t n, const cplx_t<T>* __restrict__ ainvT, const cplx_t<
       const int l = e / (TI / PER16), ii = (e - l * (TI / PER16)) * PER16;
       V* d = dst + l * TI + ii;
       if (l < lrows && ii < icount)  // icount is a multiple of PER16 unless at the end
-        tiled::cp_async16(d, ainvT + (lc + l) * inv_ld(n) + i0 + ii);
+        tiled::cp_async16(d, ainvT + (lc + l) * ld + i0 + ii);
       else
         for (int u = 0; u < PER16; ++u) d[u] = czero<V>();
     }
@@ -243,6 +250,10 @@ coarse_gemm_kernel(int64_t n, const cplx_t<T>* __restrict__ ainvT, const cplx_t<
       V v;
       v.x = t1[a][q] - t2[a][q];
       v.y = t3[a][q] - t1[a][q] - t2[a][q];
+      if (nsplit == 1 && c_in) {  // unsplit: fuse the x = c_in + sign * (A b) epilogue
+        const V c = c_in[i * K + qt + NQT * q];
+        v = mk(c.x + sign * v.x, c.y + sign * v.y);
+      }
       out[i * K + qt + NQT * q] = v;
     }
   }
@@ -250,18 +261,22 @@ coarse_gemm_kernel(int64_t n, const cplx_t<T>* __restrict__ ainvT, const cplx_t<
 
 template <class T>
 __global__ void __launch_bounds__(256)
-split_reduce_kernel(int64_t count, int nsplit, const cplx_t<T>* __restrict__ part,
-                    cplx_t<T>* __restrict__ x) {
+split_reduce_kernel(int64_t count, int nsplit, const cplx_t<T>* __restrict__ part, cplx_t<T>* x,
+                    const cplx_t<T>* c_in, T sign) {
   const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
   if (e >= count) return;
   cplx_t<T> s = part[e];
   for (int t = 1; t < nsplit; ++t) s = cadd(s, part[int64_t(t) * count + e]);
+  if (c_in) {
+    const cplx_t<T> c = c_in[e];
+    s = mk(c.x + sign * s.x, c.y + sign * s.y);
+  }
   x[e] = s;
 }
 
 template <class T, int K>
-void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, const cplx_t<T>* b, cplx_t<T>* x,
-                        cplx_t<T>* part, int nsplit, cudaStream_t s) {
+void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, int64_t ld, const cplx_t<T>* b, cplx_t<T>* x,
+                        const cplx_t<T>* c_in, T sign, cplx_t<T>* part, int nsplit, cudaStream_t s) {
   using V = cplx_t<T>;
   constexpr int TI = CoarseTile<T, K>::TI, TL = CoarseTile<T, K>::TL;
   const size_t smem = sizeof(V) * 2 * (TL * TI + TL * K);
@@ -274,9 +289,9 @@ void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, const cplx_t<T>* b, c
   const int tiles = grid_for(n, TI);
   nsplit = std::min(nsplit, split_for_tiles(tiles));
   if (nsplit > 1 && part == nullptr) nsplit = 1;
-  kern<<<dim3(tiles, nsplit), 256, smem, s>>>(n, ainvT, b, nsplit == 1 ? x : part, nsplit);
+  kern<<<dim3(tiles, nsplit), 256, smem, s>>>(n, ainvT, ld, b, nsplit == 1 ? x : part, nsplit, c_in, sign);
   if (nsplit > 1)
-    split_reduce_kernel<T><<<grid_for(n * K, 256), 256, 0, s>>>(n * K, nsplit, part, x);
+    split_reduce_kernel<T><<<grid_for(n * K, 256), 256, 0, s>>>(n * K, nsplit, part, x, c_in, sign);
 }
 
 }  // namespace
@@ -303,19 +318,17 @@ void launch_banded_inverse(int64_t n, int64_t kl, int64_t ku, int64_t ld, const 
 }
 
 template <class T>
-void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
-                         cplx_t<T>* x, cplx_t<T>* part, cudaStream_t s) {
+void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, const cplx_t<T>* b, cplx_t<T>* x,
+                        const cplx_t<T>* c_in, T sign, cplx_t<T>* part, cudaStream_t s) {
   using V = cplx_t<T>;
   const int sk = coarse_split(n, k);
   if (sk > 0 && (part != nullptr || sk == 1)) {
-    ProfScope prof(sizeof(T) == 8 ? "coarse_solve_c128" : "coarse_solve_c64",
-                   (double(n) * n + 2.0 * n * k) * sizeof(V), s, 8.0 * double(n) * n * k);
     if (k == 32)
-      coarse_gemm_launch<T, 32>(n, ainvT, b, x, part, sk, s);
+      coarse_gemm_launch<T, 32>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
     else if (k == 16)
-      coarse_gemm_launch<T, 16>(n, ainvT, b, x, part, sk, s);
+      coarse_gemm_launch<T, 16>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
     else
-      coarse_gemm_launch<T, 64>(n, ainvT, b, x, part, sk, s);
+      coarse_gemm_launch<T, 64>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
     HZ_LAUNCH_CHECK();
     return;
   }
@@ -326,28 +339,33 @@ void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<
   if (k > 64) ti = 4096 / k >= 16 ? 16 : (4096 / k >= 8 ? 8 : (4096 / k >= 4 ? 4 : 1));
   const size_t smem = sizeof(V) * (TL * 16 + TL * size_t(k));
   const int grid = grid_for(n, ti);
-  ProfScope prof(sizeof(T) == 8 ? "coarse_solve_c128" : "coarse_solve_c64",
-                 (double(n) * n + 2.0 * n * k) * sizeof(V), s, 8.0 * double(n) * n * k);
-  if (ti == 16) {
-    auto kern = coarse_solve_kernel<T, 16, TL>;
+  auto go = [&](auto kern) {
     HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
-  } else if (ti == 8) {
-    auto kern = coarse_solve_kernel<T, 8, TL>;
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
-  } else if (ti == 4) {
-    auto kern = coarse_solve_kernel<T, 4, TL>;
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
-  } else {
-    auto kern = coarse_solve_kernel<T, 1, TL>;
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<grid, 256, smem, s>>>(n, k, ainvT, b, x);
-  }
+    kern<<<grid, 256, smem, s>>>(n, k, ainvT, ld, b, x, c_in, sign);
+  };
+  if (ti == 16)
+    go(coarse_solve_kernel<T, 16, TL>);
+  else if (ti == 8)
+    go(coarse_solve_kernel<T, 8, TL>);
+  else if (ti == 4)
+    go(coarse_solve_kernel<T, 4, TL>);
+  else
+    go(coarse_solve_kernel<T, 1, TL>);
   HZ_LAUNCH_CHECK();
 }
 
+template <class T>
+void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
+                         cplx_t<T>* x, cplx_t<T>* part, cudaStream_t s) {
+  ProfScope prof(sizeof(T) == 8 ? "coarse_solve_c128" : "coarse_solve_c64",
+                 (double(n) * n + 2.0 * n * k) * sizeof(cplx_t<T>), s, 8.0 * double(n) * n * k);
+  launch_coarse_gemm<T>(n, k, ainvT, inv_ld(n), b, x, nullptr, T(1), part, s);
+}
+
+template void launch_coarse_gemm<double>(int64_t, int, const double2*, int64_t, const double2*, double2*,
+                                         const double2*, double, double2*, cudaStream_t);
+template void launch_coarse_gemm<float>(int64_t, int, const float2*, int64_t, const float2*, float2*,
+                                        const float2*, float, float2*, cudaStream_t);
 template void launch_coarse_solve<double>(int64_t, int, const double2*, const double2*, double2*,
                                           double2*, cudaStream_t);
 template void launch_coarse_solve<float>(int64_t, int, const float2*, const float2*, float2*,

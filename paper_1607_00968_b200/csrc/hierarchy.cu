@@ -35,8 +35,8 @@ Problem::Problem(int ndim_, const int64_t* n_, const double* h_, const double* m
       throw HzError(kValidation, "grid: spacing on axis " + std::to_string(a) + " must be positive");
   }
   const int64_t nn = num_nodes();
-  if (nn * 64 >= (int64_t(1) << 32))
-    throw HzError(kValidation, "grid: node count too large for one device block (use slabs)");
+  // element indices of a block are 32-bit (n*k checked per solve)
+  if (nn >= (int64_t(1) << 31)) throw HzError(kValidation, "grid: node count overflows the index type");
   if (!m_ || !ramp_) throw HzError(kValidation, "helmholtz: null model or attenuation");
   m.assign(m_, m_ + nn);
   ramp.assign(ramp_, ramp_ + nn);
@@ -207,6 +207,26 @@ std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, in
     L.inv_diag.alloc(nc);
     L.inv_diag.upload(inv.data(), nc, s);
   }
+  // coarsest, large 3D: block-tridiagonal plane factorisation on the device
+  // (HZ_COARSE=dense|bt overrides the size rule)
+  {
+    const auto& Lc = H->levels_.back();
+    const int64_t nc = Lc.nodes();
+    const char* mode = std::getenv("HZ_COARSE");
+    bool bt = p.ndim == 3 && nc > 6000;
+    if (mode && std::string(mode) == "bt") bt = p.ndim == 3;
+    if (mode && std::string(mode) == "dense") bt = false;
+    if (bt) {
+      const LevelGeom gc(Lc.dims[0], Lc.dims[1], Lc.dims[2], 1);
+      const int64_t m = Lc.dims[0] * Lc.dims[1];
+      const size_t sz = size_t(Lc.dims[2]) * m * inv_ld(m);
+      H->bt_ = true;
+      H->bt_ET_.alloc(sz);
+      H->bt_FT_.alloc(sz);
+      bt_factor(gc, Lc.coef.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
+      return H;
+    }
+  }
   // coarsest: banded LU over the stencil profile, then explicit inverse
   {
     const auto& Lc = H->levels_.back();
@@ -309,8 +329,15 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
     cast(a.coef, b.coef);
     cast(a.inv_diag, b.inv_diag);
   }
-  H->ainvT_.alloc(h64.ainvT_.size());
-  launch_cast<float2, double2>(int64_t(h64.ainvT_.size()), h64.ainvT_.get(), H->ainvT_.get(), s);
+  auto cast_all = [&](const DevBuf<double2>& src, DevBuf<float2>& dst) {
+    if (!src.size()) return;
+    dst.alloc(src.size());
+    launch_cast<float2, double2>(int64_t(src.size()), src.get(), dst.get(), s);
+  };
+  cast_all(h64.ainvT_, H->ainvT_);
+  H->bt_ = h64.bt_;
+  cast_all(h64.bt_ET_, H->bt_ET_);
+  cast_all(h64.bt_FT_, H->bt_FT_);
   HZ_CUDA(cudaStreamSynchronize(s));
   return H;
 }
@@ -360,13 +387,26 @@ void Hierarchy<T>::ensure_ws(int k) {
     }
   }
   const int64_t nc = coarse_n();
-  cpart_.alloc(size_t(std::max(coarse_split(nc, k), 1)) * nc * k);
+  if (bt_) {
+    const auto& Lc = levels_.back();
+    const int64_t m = Lc.dims[0] * Lc.dims[1];
+    cpart_.alloc(size_t(std::max(coarse_split(m, k), 1)) * m * k);
+    bt_r_.alloc(size_t(m) * k);
+  } else {
+    cpart_.alloc(size_t(std::max(coarse_split(nc, k), 1)) * nc * k);
+  }
   ws_k_ = k;
 }
 
 template <class T>
 void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
   ensure_ws(k);
+  if (bt_) {
+    const auto& Lc = levels_.back();
+    const LevelGeom gc(Lc.dims[0], Lc.dims[1], Lc.dims[2], k);
+    bt_solve<T>(gc, Lc.coef.get(), bt_ET_.get(), bt_FT_.get(), k, b, x, bt_r_.get(), cpart_.get(), s);
+    return;
+  }
   launch_coarse_solve<T>(coarse_n(), k, ainvT_.get(), b, x, cpart_.get(), s);
 }
 

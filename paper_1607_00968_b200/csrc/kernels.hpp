@@ -76,6 +76,19 @@ int coarse_split(int64_t n, int k);
 template <class T>
 void launch_coarse_solve(int64_t n, int k, const cplx_t<T>* ainvT, const cplx_t<T>* b,
                          cplx_t<T>* x, cplx_t<T>* part, cudaStream_t s);
+// general form: x = (c_in ? c_in : 0) + sign * (A b), A given transposed with
+// row stride ld (x may alias c_in)
+template <class T>
+void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, const cplx_t<T>* b, cplx_t<T>* x,
+                        const cplx_t<T>* c_in, T sign, cplx_t<T>* part, cudaStream_t s);
+
+// Block-tridiagonal (plane) direct solver of a 3D coarsest Galerkin operator
+// (coarse_bt.cu): ET/FT = [n2][m][inv_ld(m)] transposed plane blocks,
+// m = n0*n1; g.k unused. Solve scratch: r (m*k), part (split partials).
+void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s);
+template <class T>
+void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, const cplx_t<T>* FT, int k,
+              const cplx_t<T>* b, cplx_t<T>* x, cplx_t<T>* r, cplx_t<T>* part, cudaStream_t s);
 
 // ---- block (tall-skinny) kernels, node-major [n][k] blocks (inc/block.hpp)
 // Tables of block pointers travel by value in the kernel parameters (no

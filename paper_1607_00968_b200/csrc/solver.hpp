@@ -102,6 +102,9 @@ class Hierarchy {
   std::vector<MgLevelDev<T>> levels_;
   DevBuf<V> ainvT_;  // coarsest inverse, transposed [n_c][inv_ld(n_c)]
   DevBuf<V> cpart_;  // split-K partials of the coarse solve
+  // block-tridiagonal plane solver of a large 3D coarsest level
+  bool bt_ = false;
+  DevBuf<V> bt_ET_, bt_FT_, bt_r_;
   int ndim_ = 2;
   int64_t band_ = 0;
 

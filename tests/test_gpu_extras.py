@@ -177,3 +177,45 @@ def test_rank_deficient_block_matches_reference(ref):
     for j in range(4):
         assert rel_err(X[:, j], Xr[:, j]) <= 1e-4
     assert rel_err(X[:, 2], X[:, 0]) <= 1e-12  # coincident sources, identical columns
+
+
+@pytest.mark.parametrize("n,nl", [((17, 17, 9), 2), ((33, 33, 17), 3), ((33, 17, 17), 2)])
+def test_block_tridiagonal_coarse_solve_matches_reference(ref, n, nl, monkeypatch):
+    """The plane block-tridiagonal coarsest solver (coarse_bt.cu) against the
+    reference's banded LU (MgHierarchy::coarse_solve, src/multigrid.cpp:114-117)."""
+    monkeypatch.setenv("HZ_COARSE", "bt")
+    cfg = configs.small_problem(3, n, seed=3)
+    P = hz.HelmholtzProblem.from_config(cfg)
+    S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
+                                                       cycle=hz.CycleSpec("V")))
+    R = ref.RefProblem.from_config(cfg)
+    H = ref.RefHierarchy(R, nl, 0.5)
+    dims, _ = H.level_dims(nl - 1)
+    nc = dims[0] * dims[1] * dims[2]
+    for k in (1, 16):
+        b = configs.random_block(nc, k, seed=21 + k)
+        assert rel_err(S.coarse_solve(b), H.coarse_solve(b)) <= 1e-11
+    b = configs.random_block(cfg.num_nodes, 4, seed=5)
+    assert rel_err(S.cycle(b), H.cycle(b, kind="V")) <= 1e-11
+
+
+def test_config3_three_levels_block_tridiagonal(ref):
+    """Config-3 recipe at 65x65x33 with the converging 3-level hierarchy: the
+    coarsest level (17x17x9) is solved by the plane block-tridiagonal solver."""
+    import os
+    os.environ["HZ_COARSE"] = "bt"
+    try:
+        cfg = configs.config3(nlevels=3, n=(65, 65, 33), sgrid=2, layer=8)
+        P = hz.HelmholtzProblem.from_config(cfg)
+        S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions.from_config(cfg))
+    finally:
+        del os.environ["HZ_COARSE"]
+    B = cfg.rhs_block()
+    X, rep = S.solve_block(B)
+    R = ref.RefProblem.from_config(cfg)
+    H = ref.RefHierarchy(R, 3, cfg.shift)
+    Xr, rr = ref.krylov_solve(R, H, B, method="fgmres", kind="V", restart=10, tol=1e-6, max_cycles=cfg.max_cycles)
+    assert rep.all_converged() and rr.all_converged()
+    assert abs(rep.cycles - rr.cycles) <= 0.05 * rr.cycles + 2
+    for j in range(B.shape[1]):
+        assert rel_err(X[:, j], Xr[:, j]) <= 1e-5
