@@ -623,6 +623,8 @@ int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx
     gram_tiled_launch<T, 16>(n, nb, X, Y, partials, nslots, s);
   else if (k == 64)
     gram_tiled_launch<T, 64>(n, nb, X, Y, partials, nslots, s);
+  else if (k == 8)
+    gram_tiled_launch<T, 8>(n, nb, X, Y, partials, nslots, s);
   else if (k < 16)
     gram_launch<T, 1, 1>(n, k, nb, X, Y, partials, nslots, s);
   else if (k <= 32)
@@ -644,6 +646,8 @@ void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const c
     update_tiled_launch<T, 16>(n, nb, X, H, Yin, Yout, sign, s);
   } else if (k == 64) {
     update_tiled_launch<T, 64>(n, nb, X, H, Yin, Yout, sign, s);
+  } else if (k == 8) {
+    update_tiled_launch<T, 8>(n, nb, X, H, Yin, Yout, sign, s);
   } else {
     const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
     auto kern = multi_update_kernel<T>;

@@ -33,8 +33,9 @@ __device__ __forceinline__ void mma884(double& c0, double& c1, double a, double 
 // takes (k-steps of 4 rows, round robin over the staged chunk).
 template <int K>
 struct GramCfg {
-  static constexpr int WP = K / 16;                  // warps across p (16 p each)
-  static constexpr int WQ = K >= 64 ? 2 : K / 16;    // warps across q
+  static constexpr int PT = K >= 16 ? 2 : 1;         // 8-wide p tiles per warp
+  static constexpr int WP = K / (8 * PT);            // warps across p
+  static constexpr int WQ = K >= 64 ? 2 : (K >= 16 ? K / 16 : 1);  // warps across q
   static constexpr int QT = K / (8 * WQ);            // 8-wide q tiles per warp
   static constexpr int NG = 8 / (WP * WQ);           // row groups
   static constexpr int RC = 32;                      // staged rows per chunk
@@ -58,9 +59,10 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
   const int grp = warp / (WP * WQ), wpq = warp - grp * WP * WQ;
   const int wp = wpq / WQ, wq = wpq - wp * WQ;
   const int g = lane >> 2, t = lane & 3;
-  double acc[2][QT][3][2];
+  constexpr int PT = C::PT;
+  double acc[PT][QT][3][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < PT; ++a)
 #pragma unroll
     for (int b = 0; b < QT; ++b)
 #pragma unroll
@@ -95,10 +97,10 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
 #pragma unroll 2
     for (int ks = grp; ks < RC / 4; ks += NG) {
       const int r = ks * 4 + t;  // A[g][t] / B[t][g]: row index = t
-      double xa[2][3], yb[QT][3];
+      double xa[PT][3], yb[QT][3];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const double2 x = xs[r * LD + wp * 16 + a * 8 + g];
+      for (int a = 0; a < PT; ++a) {
+        const double2 x = xs[r * LD + (wp * PT + a) * 8 + g];
         xa[a][0] = x.x;
         xa[a][1] = x.y;
         xa[a][2] = x.x + x.y;
@@ -111,7 +113,7 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
         yb[b][2] = y.x - y.y;
       }
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < PT; ++a)
 #pragma unroll
         for (int b = 0; b < QT; ++b)
 #pragma unroll
@@ -126,12 +128,12 @@ gram_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y,
   for (int gg = 0; gg < NG; ++gg) {
     if (grp == gg) {
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < PT; ++a)
 #pragma unroll
         for (int b = 0; b < QT; ++b)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int p = wp * 16 + a * 8 + g, q = (wq * QT + b) * 8 + 2 * t + h;
+            const int p = (wp * PT + a) * 8 + g, q = (wq * QT + b) * 8 + 2 * t + h;
             double2 v;
             v.x = acc[a][b][0][h] + acc[a][b][1][h];
             v.y = acc[a][b][0][h] - acc[a][b][1][h] - acc[a][b][2][h];

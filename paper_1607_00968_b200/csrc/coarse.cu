@@ -149,7 +149,7 @@ coarse_solve_kernel(int64_t n, int k, const cplx_t<T>* __restrict__ ainvT, int64
 template <class T, int K>
 struct CoarseTile {
   static constexpr bool F32 = sizeof(T) == 4;
-  static constexpr int NQT = (F32 && K <= 32) ? 8 : 16;  // column threads
+  static constexpr int NQT = K < 16 ? K : ((F32 && K <= 32) ? 8 : 16);  // column threads
   static constexpr int TQ = K / NQT;                        // columns per thread (strided)
   static constexpr int NIT = 256 / NQT;                     // row threads
   static constexpr int TA = F32 ? (K <= 32 ? 8 : 4) : 4;    // rows per thread (strided)
@@ -304,7 +304,7 @@ int split_for_tiles(int tiles) {
 }
 
 int coarse_split(int64_t n, int k) {
-  if (k != 16 && k != 32 && k != 64) return 0;
+  if (k != 8 && k != 16 && k != 32 && k != 64) return 0;
   // upper bound over both precisions: the fewest row tiles (256-row c64
   // tiles) give the largest split
   return split_for_tiles(grid_for(n, 256));
@@ -327,6 +327,8 @@ void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, co
       coarse_gemm_launch<T, 32>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
     else if (k == 16)
       coarse_gemm_launch<T, 16>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
+    else if (k == 8)
+      coarse_gemm_launch<T, 8>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
     else
       coarse_gemm_launch<T, 64>(n, ainvT, ld, b, x, c_in, sign, part, sk, s);
     HZ_LAUNCH_CHECK();

@@ -149,6 +149,62 @@ level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __
   }
 }
 
+// Galerkin 9/27-point level kernel, CPT consecutive columns per thread: the
+// neighbour index math and the coefficient loads (shared by all k columns of
+// a node) are amortised over CPT outputs -- the one-column-per-thread form
+// is instruction-issue bound at 27 neighbours. Branch-free: out-of-range
+// neighbours have exactly zero Galerkin coefficients and read the centre.
+template <class T, int NDIM, int MODE, int CPT>
+__global__ void __launch_bounds__(kBlock)
+stencil_mc_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
+                  cplx_t<T>* __restrict__ out, T wj) {
+  using V = cplx_t<T>;
+  const LevelGeom& g = op.g;
+  const uint32_t t = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t e0 = t * CPT;
+  if (e0 >= g.nodes * g.k) return;
+  uint32_t node, col, i, j, kz;
+  g.div_k.divmod(e0, node, col);
+  g.unpack(node, i, j, kz);
+  const int64_t sx = g.k, sy = int64_t(g.n0) * g.k, sz = int64_t(g.n0) * g.n1 * g.k;
+  const V* __restrict__ cf = op.coef + node;
+  V acc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) acc[c] = czero<V>();
+  const int zlo = NDIM == 3 ? -1 : 0, zhi = NDIM == 3 ? 1 : 0;
+#pragma unroll
+  for (int dz = zlo; dz <= zhi; ++dz) {
+    const bool okz = NDIM == 2 || (dz < 0 ? kz > 0 : (dz > 0 ? kz + 1 < g.n2 : true));
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+      const bool oky = dy < 0 ? j > 0 : (dy > 0 ? j + 1 < g.n1 : true);
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        const bool okx = dx < 0 ? i > 0 : (dx > 0 ? i + 1 < g.n0 : true);
+        const int s = (NDIM == 3 ? (dz + 1) * 9 : 0) + (dy + 1) * 3 + (dx + 1);
+        const int64_t off = (okz && oky && okx) ? dz * sz + dy * sy + dx * sx : 0;
+        const V a = __ldg(&cf[int64_t(s) * g.nodes]);
+        const V* xp = x + int64_t(e0) + off;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[c] = cfma(a, __ldg(&xp[c]), acc[c]);
+      }
+    }
+  }
+  if (MODE == 0) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) out[e0 + c] = acc[c];
+  } else if (MODE == 1) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) out[e0 + c] = csub(__ldg(&b[e0 + c]), acc[c]);
+  } else {
+    const V d = __ldg(&op.inv_diag[node]);
+    const V wd = mk(wj * d.x, wj * d.y);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+      out[e0 + c] = cadd(__ldg(&x[e0 + c]), cmul(wd, csub(__ldg(&b[e0 + c]), acc[c])));
+  }
+}
+
 template <class T, class In>
 __global__ void __launch_bounds__(kBlock)
 jacobi_zero_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj,
@@ -406,6 +462,12 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
       level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
     else
       level_kernel<T, 2, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+  } else if (op.g.k % 4 == 0) {
+    const int g4 = grid_for(total / 4, kBlock);
+    if (op.ndim == 3)
+      stencil_mc_kernel<T, 3, MODE, 4><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+    else
+      stencil_mc_kernel<T, 2, MODE, 4><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
   } else {
     if (op.ndim == 3)
       level_kernel<T, 3, kStencil, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
