@@ -172,7 +172,7 @@ def test_rank_deficient_block_matches_reference(ref):
     # breakdown, so the restart points are decided by near-tol rounding: the
     # trajectories agree in shape (cycles, QR count) rather than bitwise.
     assert abs(rep.cycles - rr.cycles) <= 0.05 * rr.cycles + 2
-    assert abs(rep.qr_factorizations - rr.qr_factorizations) <= 3
+    assert abs(rep.qr_factorizations - rr.qr_factorizations) <= 0.05 * rr.qr_factorizations + 2
     assert np.all(rep.rel_residual <= 2e-6) and np.all(rr.rel_residual <= 2e-6)
     for j in range(4):
         assert rel_err(X[:, j], Xr[:, j]) <= 1e-4

@@ -166,7 +166,9 @@ def test_block_cycle_equals_column_cycles():
     xb = S.cycle(b)
     for j in range(4):
         xj = S.cycle(b[:, j:j + 1].copy())
-        assert np.array_equal(xj[:, 0], xb[:, j])
+        # k = 4 runs the multi-column stencil kernel, k = 1 the per-column one:
+        # same summation order, FMA contraction may differ in the epilogue
+        assert rel_err(xj[:, 0], xb[:, j]) <= 1e-13
 
 
 def test_zero_is_fixed_point():
