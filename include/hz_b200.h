@@ -131,6 +131,18 @@ HZ_API int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** o
 HZ_API int hz_solver_destroy(hz_solver* s);
 /* HelmholtzSolver::set_tolerance (include/seistomo/helmholtz_solver.hpp:46) */
 HZ_API int hz_solver_set_tolerance(hz_solver* s, double tol);
+/* Slab decomposition of the slow grid axis (config 5; no reference
+ * counterpart -- the reference is single-node). Splits every
+ * following solve / cycle of `s` over `nparts` parts; part p runs on GPU
+ * devices[p] (NULL: all parts on the problem's GPU, as separate streams);
+ * devices[0] must be the problem's GPU. Level-0 planes are cut on multiples
+ * of 2^(nlevels-1); levels on which a part would own < 2 planes, and the
+ * coarsest solve, run on part 0. Block FGMRES methods with V/W cycles only.
+ * nparts <= 1 with devices == NULL returns to the single-stream solver. */
+HZ_API int hz_solver_set_slabs(hz_solver* s, int nparts, const int* devices);
+/* parts, first agglomerated level and planes[l*(nparts+1)+p] = first plane of
+ * part p on level l (p = nparts: plane count), up to `cap` entries */
+HZ_API int hz_solver_slab_info(const hz_solver* s, int* nparts, int* agg_level, int64_t* planes, int cap);
 
 /* HelmholtzSolver::solve_block (src/helmholtz_solver.cpp:35-72): host
  * buffers B, X [n][k]; H2D / D2H copies included. Non-convergence is

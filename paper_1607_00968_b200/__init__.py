@@ -349,6 +349,35 @@ class HelmholtzSolver:
         self.options.tol = tol
         _check(_native.lib().hz_solver_set_tolerance(self._h, tol))
 
+    def set_slabs(self, nparts: int, devices=None):
+        """Slab-decompose every following solve / cycle along the slow grid
+        axis over `nparts` parts (config 5): part p runs on GPU
+        devices[p] (default: all on the problem's GPU as separate streams).
+        nparts=1 with devices=None returns to the single-stream solver."""
+        if devices is None:
+            arr = None
+        else:
+            devs = np.ascontiguousarray(devices, dtype=np.int32)
+            if devs.size != nparts:
+                raise ValidationError("set_slabs: one device per part")
+            arr = devs
+        _check(_native.lib().hz_solver_set_slabs(
+            self._h, int(nparts), None if arr is None else arr.ctypes.data_as(C.c_void_p)))
+        self._slab_devices = arr
+
+    def slab_info(self):
+        """(nparts, agg_level, planes) with planes[l][p] the first plane of
+        part p on level l and planes[l][nparts] the level's plane count."""
+        P = C.c_int(0)
+        agg = C.c_int(0)
+        _check(_native.lib().hz_solver_slab_info(self._h, C.byref(P), C.byref(agg), None, 0))
+        nl = C.c_int(0)
+        _check(_native.lib().hz_hierarchy_num_levels(self._h, C.byref(nl)))
+        planes = np.zeros((max(nl.value, 1), P.value + 1), np.int64)
+        _check(_native.lib().hz_solver_slab_info(self._h, C.byref(P), C.byref(agg),
+                                                 planes.ctypes.data_as(C.c_void_p), planes.size))
+        return P.value, agg.value, planes
+
     def _report(self, k: int, cap: int):
         cc = np.zeros(k, np.int32)
         rr = np.zeros(k, np.float64)

@@ -21,7 +21,7 @@ EXPORTS = (
     "hz_cycle", "hz_cycle_device", "hz_coarse_solve", "hz_hierarchy_num_levels",
     "hz_hierarchy_level_dims", "hz_hierarchy_level_coefficients", "hz_sensitivity_accumulate",
     "hz_sensitivity_accumulate_device", "hz_kernel_launch_count", "hz_profile_begin",
-    "hz_profile_end", "hz_profile_report",
+    "hz_profile_end", "hz_profile_report", "hz_solver_set_slabs", "hz_solver_slab_info",
 )
 
 
@@ -79,6 +79,8 @@ def lib():
         L.hz_sensitivity_accumulate.argtypes = [vp, i64, i32, vp, vp, vp, i32]
         L.hz_sensitivity_accumulate_device.argtypes = [vp, i64, i32, vp, vp, vp, i32, vp]
         L.hz_options_default.argtypes = [C.POINTER(hz_options)]
+        L.hz_solver_set_slabs.argtypes = [vp, i32, vp]
+        L.hz_solver_slab_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), vp, i32]
         _lib = L
     return _lib
 

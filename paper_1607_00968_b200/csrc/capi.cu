@@ -75,7 +75,45 @@ struct hz_solver {
   DevBuf<float2> b32, x32;
   // DenseLuSmall: explicit inverse of the unshifted operator
   DevBuf<double2> dense_ainvT;
+  // slab decomposition (slabs.hpp): per-GPU copies of the fine centre and of
+  // the cycle's hierarchy for parts not on the problem's GPU
+  std::unique_ptr<Slabs> slabs;
+  std::map<int, std::unique_ptr<Hierarchy<double>>> rep64;
+  std::map<int, std::unique_ptr<Hierarchy<float>>> rep32;
+  std::map<int, DevBuf<double2>> center_rep;
+  int span_k = 0;  // k the spanning dB/dX/b32/x32 are laid out for
+  const double2* center_on(int device) const {
+    if (device == prob->device) return prob->d_center.get();
+    return center_rep.at(device).get();
+  }
+  // (re)lay out the solver-owned level-0 blocks for k columns
+  void ensure_blocks(int k) {
+    const size_t e = size_t(prob->num_nodes()) * k;
+    if (!slabs) {
+      dB.ensure(e);
+      dX.ensure(e);
+      if (opts.precond_precision == HZ_C64) {
+        b32.ensure(e);
+        x32.ensure(e);
+      }
+      return;
+    }
+    if (span_k == k) return;
+    alloc_span(dB, *slabs, 0, k);
+    alloc_span(dX, *slabs, 0, k);
+    if (opts.precond_precision == HZ_C64) {
+      alloc_span(b32, *slabs, 0, k);
+      alloc_span(x32, *slabs, 0, k);
+    }
+    span_k = k;
+  }
   ~hz_solver() {
+    fgm.reset();
+    h32.reset();
+    h64.reset();
+    rep32.clear();
+    rep64.clear();
+    slabs.reset();
     if (stream) cudaStreamDestroy(stream);
   }
 };
@@ -131,7 +169,43 @@ void fill_report(const Report& r, int k, hz_report* out) {
       out->history[i] = r.history[i];
 }
 
+// Slab mode (hz_solver_set_slabs): the fine operator and the casts run per
+// part on the part's planes / rows; the cycle is the hierarchy's slab cycle.
+DevOp<double> make_slab_op(hz_solver* s, int k) {
+  DevOp<double> op;
+  Problem* P = s->prob.get();
+  const Slabs* sl = s->slabs.get();
+  op.n = P->num_nodes();
+  op.apply = [s, P, sl](const double2* in, double2* out, int kk, cudaStream_t) {
+    sl->neighbours();
+    sl->each(0, [&](int p, int64_t, int64_t, cudaStream_t st) {
+      LevelOp<double> o = P->fine_op(kk);
+      o.center = s->center_on(sl->part(p).device);
+      o.g = o.g.slab(sl->z0(0, p), sl->z1(0, p));
+      launch_apply<double>(o, in, out, st);
+    });
+  };
+  if (s->opts.precond_precision == HZ_C64) {
+    s->ensure_blocks(k);
+    op.prec = [s, sl](const double2* in, double2* out, int kk, cudaStream_t st) {
+      sl->each(0, [&](int, int64_t r0, int64_t nr, cudaStream_t pst) {
+        launch_cast<float2, double2>(nr * kk, in + r0 * kk, s->b32.get() + r0 * kk, pst);
+      });
+      s->h32->cycle(s->spec, kk, s->b32.get(), s->x32.get(), true, st);
+      sl->each(0, [&](int, int64_t r0, int64_t nr, cudaStream_t pst) {
+        launch_cast<double2, float2>(nr * kk, s->x32.get() + r0 * kk, out + r0 * kk, pst);
+      });
+    };
+  } else {
+    op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
+      s->h64->cycle(s->spec, kk, in, out, true, st);
+    };
+  }
+  return op;
+}
+
 DevOp<double> make_op(hz_solver* s, int k) {
+  if (s->slabs) return make_slab_op(s, k);
   DevOp<double> op;
   Problem* P = s->prob.get();
   op.n = P->num_nodes();
@@ -154,6 +228,33 @@ DevOp<double> make_op(hz_solver* s, int k) {
     };
   }
   return op;
+}
+
+// host <-> solver block copies, one per part (each part's rows live on its GPU)
+void upload_rows(hz_solver* s, int k, const double* host, double2* dev) {
+  const auto* h = reinterpret_cast<const double2*>(host);
+  if (!s->slabs) {
+    HZ_CUDA(cudaMemcpyAsync(dev, h, size_t(s->prob->num_nodes()) * k * sizeof(double2), cudaMemcpyHostToDevice,
+                            s->stream));
+    return;
+  }
+  s->slabs->each(0, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+    HZ_CUDA(cudaMemcpyAsync(dev + r0 * k, h + r0 * k, size_t(nr) * k * sizeof(double2), cudaMemcpyHostToDevice, st));
+  });
+}
+void download_rows(hz_solver* s, int k, const double2* dev, double* host) {
+  auto* h = reinterpret_cast<double2*>(host);
+  if (!s->slabs) {
+    HZ_CUDA(cudaMemcpyAsync(h, dev, size_t(s->prob->num_nodes()) * k * sizeof(double2), cudaMemcpyDeviceToHost,
+                            s->stream));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    return;
+  }
+  s->slabs->each(0, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+    HZ_CUDA(cudaMemcpyAsync(h + r0 * k, dev + r0 * k, size_t(nr) * k * sizeof(double2), cudaMemcpyDeviceToHost, st));
+  });
+  s->slabs->join();
+  HZ_CUDA(cudaStreamSynchronize(s->stream));
 }
 
 Report run_solve(hz_solver* s, int k, const double2* B, double2* X) {
@@ -397,6 +498,92 @@ int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** out) {
   });
 }
 
+int hz_solver_set_slabs(hz_solver* s, int nparts, const int* devices) {
+  return guarded([&] {
+    if (!s) throw HzError(kValidation, "null solver");
+    DeviceGuard dg(s->prob->device);
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    auto detach = [&] {
+      if (s->h64) s->h64->attach_slabs(nullptr, {});
+      if (s->h32) s->h32->attach_slabs(nullptr, {});
+      if (s->fgm) s->fgm->set_slabs(nullptr);
+      s->dB.release();
+      s->dX.release();
+      s->b32.release();
+      s->x32.release();
+      s->span_k = 0;
+      s->slabs.reset();
+      s->rep32.clear();
+      s->rep64.clear();
+      s->center_rep.clear();
+    };
+    if (nparts <= 1 && !devices) {
+      detach();
+      return;
+    }
+    if (nparts < 1) throw HzError(kValidation, "slabs: nparts must be >= 1");
+    if (s->dense || s->bicgstab)
+      throw HzError(kValidation, "slab decomposition supports the block FGMRES methods");
+    if (s->spec.kind == CycleKind::K) throw HzError(kValidation, "slab decomposition supports V and W cycles");
+    std::vector<int> devs(nparts, s->prob->device);
+    if (devices) devs.assign(devices, devices + nparts);
+    if (devs[0] != s->prob->device) throw HzError(kValidation, "slabs: part 0 must be on the problem's GPU");
+    int ndev = 0;
+    HZ_CUDA(cudaGetDeviceCount(&ndev));
+    for (int d : devs)
+      if (d < 0 || d >= ndev) throw HzError(kValidation, "slabs: device index out of range");
+    detach();
+    std::vector<std::array<int64_t, 3>> dims;
+    for (int l = 0; l < s->h64->num_levels(); ++l) dims.push_back(s->h64->level(l).dims);
+    s->slabs = std::make_unique<Slabs>(devs, dims, s->prob->ndim, s->stream);
+    const bool c64 = s->opts.precond_precision == HZ_C64;
+    std::vector<const Hierarchy<double>*> r64;
+    std::vector<const Hierarchy<float>*> r32;
+    const size_t nn = size_t(s->prob->num_nodes());
+    for (int d : devs) {
+      if (d != s->prob->device && !s->center_rep.count(d)) {
+        DeviceGuard g(d);
+        DevBuf<double2>& c = s->center_rep[d];
+        c.alloc(nn);
+        HZ_CUDA(cudaMemcpyPeer(c.get(), d, s->prob->d_center.get(), s->prob->device, nn * sizeof(double2)));
+        if (c64)
+          s->rep32[d] = s->h32->replica(d, nullptr);
+        else
+          s->rep64[d] = s->h64->replica(d, nullptr);
+      }
+      r64.push_back(d == s->prob->device || c64 ? nullptr : s->rep64[d].get());
+      r32.push_back(d == s->prob->device || !c64 ? nullptr : s->rep32[d].get());
+    }
+    if (c64)
+      s->h32->attach_slabs(s->slabs.get(), r32);
+    else
+      s->h64->attach_slabs(s->slabs.get(), r64);
+    if (!s->fgm) s->fgm = std::make_unique<Fgmres<double>>();
+    s->fgm->set_slabs(s->slabs.get());
+  });
+}
+
+int hz_solver_slab_info(const hz_solver* s, int* nparts, int* agg_level, int64_t* planes, int cap) {
+  return guarded([&] {
+    if (!s || !nparts) throw HzError(kValidation, "null argument");
+    if (!s->slabs) {
+      *nparts = 1;
+      if (agg_level) *agg_level = 0;
+      return;
+    }
+    const Slabs& sl = *s->slabs;
+    *nparts = sl.parts();
+    if (agg_level) *agg_level = sl.agg_level();
+    // planes[l * (P + 1) + p] = first plane of part p on level l
+    if (planes)
+      for (int l = 0; l < sl.levels(); ++l)
+        for (int p = 0; p <= sl.parts(); ++p) {
+          const int i = l * (sl.parts() + 1) + p;
+          if (i < cap) planes[i] = p < sl.parts() ? sl.z0(l, p) : sl.z1(l, sl.parts() - 1);
+        }
+  });
+}
+
 int hz_solver_destroy(hz_solver* s) {
   return guarded([&] {
     if (s) {
@@ -429,13 +616,10 @@ int hz_solve_block(hz_solver* s, int64_t n, int k, const double* B, double* X, h
     if (!s || !B || !X) throw HzError(kValidation, "null argument");
     check_block(*s->prob, n, k);
     DeviceGuard dg(s->prob->device);
-    const size_t e = size_t(n) * k;
-    s->dB.ensure(e);
-    s->dX.ensure(e);
-    HZ_CUDA(cudaMemcpyAsync(s->dB.get(), B, e * sizeof(double2), cudaMemcpyHostToDevice, s->stream));
+    s->ensure_blocks(k);
+    upload_rows(s, k, B, s->dB.get());
     Report r = run_solve(s, k, s->dB.get(), s->dX.get());
-    HZ_CUDA(cudaMemcpyAsync(X, s->dX.get(), e * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
-    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    download_rows(s, k, s->dX.get(), X);
     fill_report(r, k, rep);
   });
 }
@@ -460,6 +644,7 @@ int hz_cycle_device(hz_solver* s, int64_t n, int k, const void* b, void* x) {
     DeviceGuard dg(s->prob->device);
     DevOp<double> op = make_op(s, k);
     op.prec(static_cast<const double2*>(b), static_cast<double2*>(x), k, s->stream);
+    if (s->slabs) s->slabs->join();
     HZ_CUDA(cudaStreamSynchronize(s->stream));
   });
 }
@@ -470,14 +655,11 @@ int hz_cycle(hz_solver* s, int64_t n, int k, const double* b, double* x) {
     if (s->dense) throw HzError(kState, "dense solver has no multigrid cycle");
     check_block(*s->prob, n, k);
     DeviceGuard dg(s->prob->device);
-    const size_t e = size_t(n) * k;
-    s->dB.ensure(e);
-    s->dX.ensure(e);
-    HZ_CUDA(cudaMemcpyAsync(s->dB.get(), b, e * sizeof(double2), cudaMemcpyHostToDevice, s->stream));
+    s->ensure_blocks(k);
+    upload_rows(s, k, b, s->dB.get());
     DevOp<double> op = make_op(s, k);
     op.prec(s->dB.get(), s->dX.get(), k, s->stream);
-    HZ_CUDA(cudaMemcpyAsync(x, s->dX.get(), e * sizeof(double2), cudaMemcpyDeviceToHost, s->stream));
-    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    download_rows(s, k, s->dX.get(), x);
   });
 }
 

@@ -170,11 +170,26 @@ struct LevelGeom {
   uint32_t n0 = 1, n1 = 1, n2 = 1;
   uint32_t nodes = 1;
   uint32_t k = 1;
+  // planes [z0, z1) of the slow axis (axis 2, or axis 1 of a 2D grid) this
+  // launch computes: a slab of the grid; neighbours outside it are still
+  // read, through the global layout
+  uint32_t z0 = 0, z1 = 1;
   FastDiv div_k, div_n0, div_n1;
   LevelGeom() = default;
   LevelGeom(int64_t a, int64_t b, int64_t c, int kk)
       : n0(uint32_t(a)), n1(uint32_t(b)), n2(uint32_t(c)), nodes(uint32_t(a * b * c)), k(uint32_t(kk)),
-        div_k(uint32_t(kk)), div_n0(uint32_t(a)), div_n1(uint32_t(b)) {}
+        z1(uint32_t(c > 1 ? c : b)), div_k(uint32_t(kk)), div_n0(uint32_t(a)), div_n1(uint32_t(b)) {}
+  LevelGeom slab(int64_t za, int64_t zb) const {
+    LevelGeom g = *this;
+    g.z0 = uint32_t(za);
+    g.z1 = uint32_t(zb);
+    return g;
+  }
+  __host__ __device__ __forceinline__ uint32_t plane_elems() const { return (n2 > 1 ? n0 * n1 : n0) * k; }
+  __host__ __device__ __forceinline__ uint32_t e_begin() const { return z0 * plane_elems(); }
+  __host__ __device__ __forceinline__ uint32_t e_end() const { return z1 * plane_elems(); }
+  int64_t owned_elems() const { return int64_t(z1 - z0) * plane_elems(); }
+  int64_t owned_nodes() const { return int64_t(z1 - z0) * (n2 > 1 ? n0 * n1 : n0); }
   __host__ __device__ __forceinline__ void unpack(uint32_t node, uint32_t& i, uint32_t& j,
                                                   uint32_t& kz) const {
     uint32_t r;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstddef>
+#include <memory>
 #include <utility>
 
 #include "common.cuh"
@@ -19,7 +20,7 @@ class DevBuf {
   ~DevBuf() { release(); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_) {
+  DevBuf(DevBuf&& o) noexcept : p_(o.p_), n_(o.n_), owner_(std::move(o.owner_)) {
     o.p_ = nullptr;
     o.n_ = 0;
   }
@@ -28,6 +29,7 @@ class DevBuf {
       release();
       p_ = o.p_;
       n_ = o.n_;
+      owner_ = std::move(o.owner_);
       o.p_ = nullptr;
       o.n_ = 0;
     }
@@ -43,8 +45,18 @@ class DevBuf {
   void ensure(size_t count) {
     if (count > n_) alloc(count);
   }
+  // take an allocation owned elsewhere (e.g. a slab-spanning mapping)
+  void adopt(std::shared_ptr<void> owner, size_t count) {
+    release();
+    p_ = static_cast<E*>(owner.get());
+    n_ = count;
+    owner_ = std::move(owner);
+  }
   void release() {
-    if (p_) cudaFree(p_);
+    if (owner_)
+      owner_.reset();
+    else if (p_)
+      cudaFree(p_);
     p_ = nullptr;
     n_ = 0;
   }
@@ -64,6 +76,7 @@ class DevBuf {
  private:
   E* p_ = nullptr;
   size_t n_ = 0;
+  std::shared_ptr<void> owner_;
 };
 
 // Pinned host staging for the small k x k / k-vector results the host driver

@@ -366,6 +366,61 @@ void Hierarchy<T>::download_level(int l, std::vector<cplx>& out) const {
   for (size_t i = 0; i < tmp.size(); ++i) out[i] = cplx(tmp[i].x, tmp[i].y);
 }
 
+template <class T>
+std::unique_ptr<Hierarchy<T>> Hierarchy<T>::replica(int device, cudaStream_t s) const {
+  DeviceGuard g(device);
+  auto H = std::make_unique<Hierarchy<T>>();
+  H->ndim_ = ndim_;
+  H->band_ = band_;
+  H->levels_.resize(levels_.size());
+  auto copy = [&](const DevBuf<V>& src, DevBuf<V>& dst) {
+    if (!src.size()) return;
+    dst.alloc(src.size());
+    int sdev = 0;
+    cudaPointerAttributes a{};
+    HZ_CUDA(cudaPointerGetAttributes(&a, src.get()));
+    sdev = a.device;
+    HZ_CUDA(cudaMemcpyPeerAsync(dst.get(), device, src.get(), sdev, src.bytes(), s));
+  };
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    const auto& A = levels_[l];
+    auto& B = H->levels_[l];
+    B.dims = A.dims;
+    B.kind = A.kind;
+    for (int a = 0; a < 3; ++a) B.w[a] = A.w[a];
+    copy(A.center, B.center);
+    copy(A.coef, B.coef);
+    copy(A.inv_diag, B.inv_diag);
+  }
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return H;
+}
+
+template <class T>
+void Hierarchy<T>::attach_slabs(const Slabs* sl, std::vector<const Hierarchy<T>*> reps) {
+  if (sl && sl->levels() != num_levels()) throw HzError(kValidation, "slabs: level count mismatch");
+  if (sl && int(reps.size()) != sl->parts()) throw HzError(kValidation, "slabs: one hierarchy per part");
+  sl_ = sl;
+  reps_ = std::move(reps);
+  for (auto& r : reps_)
+    if (!r) r = this;
+  ws_k_ = 0;  // workspaces are re-laid out over the slabs
+}
+
+template <class T>
+template <class F>
+void Hierarchy<T>::on_level(int l, int k, cudaStream_t s, F&& f) {
+  if (!slab_level(l)) {
+    f(op(l, k), s, int64_t(0), levels_[l].nodes());
+    return;
+  }
+  sl_->each(l, [&](int p, int64_t r0, int64_t nr, cudaStream_t st) {
+    LevelOp<T> o = reps_[p]->op(l, k);
+    o.g = o.g.slab(sl_->z0(l, p), sl_->z1(l, p));
+    f(o, st, r0, nr);
+  });
+}
+
 // ------------------------------------------------------------------ cycle
 template <class T>
 void Hierarchy<T>::ensure_ws(int k) {
@@ -377,13 +432,22 @@ void Hierarchy<T>::ensure_ws(int k) {
   wr_.resize(L);
   for (int l = 0; l < L; ++l) {
     const size_t e = size_t(levels_[l].nodes()) * k;
+    // slab levels (and the first agglomerated level, written by every
+    // part's restriction) follow the slab layout
+    const bool span = sl_ && l <= sl_->agg_level();
+    auto get = [&](DevBuf<V>& b) {
+      if (span)
+        alloc_span(b, *sl_, l, k);
+      else
+        b.alloc(e);
+    };
     if (l > 0) {
-      wx_[l].alloc(e);
-      wb_[l].alloc(e);
+      get(wx_[l]);
+      get(wb_[l]);
     }
     if (l + 1 < L) {
-      wt_[l].alloc(e);
-      wr_[l].alloc(e);
+      get(wt_[l]);
+      get(wr_[l]);
     }
   }
   const int64_t nc = coarse_n();
@@ -422,13 +486,21 @@ void Hierarchy<T>::cycle(const CycleSpec& spec, int k, const V* b, V* x, bool x_
 template <class T>
 void Hierarchy<T>::relax(int l, const CycleSpec& spec, int sweeps, int k, const V* b, V*& cur,
                          V*& other, bool& cur_zero, cudaStream_t s) {
-  const LevelOp<T> o = op(l, k);
   const T wj = T(spec.jacobi_weight);
+  const bool sl = slab_level(l);
   for (int sw = 0; sw < sweeps; ++sw) {
-    if (cur_zero)
-      launch_jacobi_zero<T, V>(o, wj, b, other, s);
-    else
-      launch_jacobi<T>(o, wj, cur, b, other, s);
+    // one exchange step per sweep: a part's sweep reads its neighbours'
+    // faces of cur (and must not overwrite `other` while they still read it)
+    if (sl) sl_->neighbours();
+    const V* c = cur;
+    V* o = other;
+    const bool z = cur_zero;
+    on_level(l, k, s, [&](const LevelOp<T>& op_, cudaStream_t st, int64_t, int64_t) {
+      if (z)
+        launch_jacobi_zero<T, V>(op_, wj, b, o, st);
+      else
+        launch_jacobi<T>(op_, wj, c, b, o, st);
+    });
     std::swap(cur, other);
     cur_zero = false;
   }
@@ -447,14 +519,34 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
   V* other = wt_[l].get();
   bool cur_zero = x_zero;
   relax(l, spec, spec.pre, k, b, cur, other, cur_zero, s);
-  const size_t bytes = size_t(levels_[l].nodes()) * k * sizeof(V);
-  if (cur_zero) HZ_CUDA(cudaMemsetAsync(cur, 0, bytes, s));
-  const LevelOp<T> o = op(l, k);
+  const bool sl = slab_level(l);
+  const size_t rowb = size_t(k) * sizeof(V);
+  if (cur_zero)
+    on_level(l, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
+      HZ_CUDA(cudaMemsetAsync(cur + r0 * k, 0, size_t(nr) * rowb, st));
+    });
   const LevelGeom gc(levels_[l + 1].dims[0], levels_[l + 1].dims[1], levels_[l + 1].dims[2], k);
-  launch_residual<T>(o, cur, b, wr_[l].get(), s);
-  launch_restrict<T>(o.g, gc, ndim_, wr_[l].get(), wb_[l + 1].get(), s);
+  if (sl) sl_->neighbours();
+  on_level(l, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
+    launch_residual<T>(o, cur, b, wr_[l].get(), st);
+  });
+  if (sl) {
+    // every part restricts onto its planes of level l+1 (also when l+1 is
+    // agglomerated: the restriction reads level-l faces of the neighbours)
+    sl_->neighbours();
+    sl_->each(l, [&](int p, int64_t, int64_t, cudaStream_t st) {
+      const LevelGeom gf = reps_[p]->op(l, k).g;
+      launch_restrict<T>(gf, gc.slab(sl_->z0(l + 1, p), sl_->z1(l + 1, p)), ndim_, wr_[l].get(),
+                         wb_[l + 1].get(), st);
+    });
+  } else {
+    launch_restrict<T>(op(l, k).g, gc, ndim_, wr_[l].get(), wb_[l + 1].get(), s);
+  }
   V* ec = wx_[l + 1].get();
   const V* rc = wb_[l + 1].get();
+  // the first agglomerated level runs on part 0 alone
+  const bool agg = sl && !slab_level(l + 1);
+  if (agg) sl_->join();
   switch (spec.kind) {
     case CycleKind::V:
       cycle_rec(l + 1, spec, k, rc, ec, true, s);
@@ -466,14 +558,23 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
     case CycleKind::K:
       if (l + 1 == L - 1)
         cycle_rec(l + 1, spec, k, rc, ec, true, s);
+      else if (sl && slab_level(l + 1))
+        throw HzError(kValidation, "slabs: K-cycle inner Krylov levels must be agglomerated");
       else
         kcycle_coarse(l + 1, spec, k, rc, ec, s);
       break;
   }
-  launch_prolong_correct<T>(o.g, gc, ndim_, ec, cur, s);
+  if (agg) sl_->fork();
+  if (sl) sl_->neighbours();
+  on_level(l, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
+    launch_prolong_correct<T>(o.g, gc, ndim_, ec, cur, st);
+  });
   cur_zero = false;
   relax(l, spec, spec.post, k, b, cur, other, cur_zero, s);
-  if (cur != x) HZ_CUDA(cudaMemcpyAsync(x, cur, bytes, cudaMemcpyDeviceToDevice, s));
+  if (cur != x)
+    on_level(l, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
+      HZ_CUDA(cudaMemcpyAsync(x + r0 * k, cur + r0 * k, size_t(nr) * rowb, cudaMemcpyDeviceToDevice, st));
+    });
 }
 
 // kcycle_coarse (src/multigrid.cpp:138-160): k_inner block FGMRES iterations

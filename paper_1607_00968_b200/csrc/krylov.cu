@@ -222,14 +222,31 @@ std::vector<cplx> solve_small(std::vector<cplx> A, std::vector<cplx> B, int n, i
 
 // ---------------------------------------------------------------- algebra
 template <class T>
-void BlockAlgebra<T>::ensure(int64_t n_, int k_, int max_blocks) {
+void BlockAlgebra<T>::ensure(int64_t n_, int k_, int max_blocks, const Slabs* sl_) {
   if (n_ * int64_t(k_) >= (int64_t(1) << 32)) throw HzError(kValidation, "block too large");
   if (k_ < 1 || k_ > 64) throw HzError(kValidation, "block width must be in [1, 64]");
+  const bool relayout = sl_ != sl_alloc_ || (sl_ && (n_ != n || k_ != k));
   n = n_;
   k = k_;
-  nslots = gram_partial_slots(n, k);
+  sl = sl_;
+  pslots.clear();
+  if (sl) {
+    if (sl->rows(0) != n) throw HzError(kValidation, "slabs: row count mismatch");
+    for (int p = 0; p < sl->parts(); ++p) pslots.push_back(gram_partial_slots(sl->row1(0, p) - sl->row0(0, p), k));
+  } else {
+    pslots.push_back(gram_partial_slots(n, k));
+  }
+  nslots = 0;
+  for (int q : pslots) nslots += q;
   partials.ensure(size_t(nslots) * std::max(max_blocks, 2) * k * k);
-  tmp_blk.ensure(size_t(n) * k);
+  if (relayout) {
+    tmp_blk.release();
+    sl_alloc_ = sl;
+  }
+  if (sl && !tmp_blk.size())
+    alloc_span(tmp_blk, *sl, 0, k);
+  else
+    tmp_blk.ensure(size_t(n) * k);
   G.ensure(size_t(k) * k);
   R1.ensure(size_t(k) * k);
   R1i.ensure(size_t(k) * k);
@@ -245,14 +262,34 @@ void BlockAlgebra<T>::ensure(int64_t n_, int k_, int max_blocks) {
 
 template <class T>
 void BlockAlgebra<T>::gram(const BlockTab<T>& tab, int nb, const V* Y, V* out, cudaStream_t s) {
-  const int used = launch_multi_gram<T>(n, k, nb, tab, Y, partials.get(), nslots, s);
-  launch_reduce_partials<T>(int64_t(nb) * k * k, used, partials.get(), out, s);
+  const size_t cnt = size_t(nb) * k * k;
+  int used = 0;
+  each(s, [&](int p, int64_t r0, int64_t nr, cudaStream_t st) {
+    used += launch_multi_gram<T>(nr, k, nb, shift(tab, nb, r0 * k), Y + r0 * k, partials.get() + used * cnt,
+                                 pslots[p], st);
+  });
+  join();
+  launch_reduce_partials<T>(int64_t(cnt), used, partials.get(), out, s);
+}
+
+template <class T>
+void BlockAlgebra<T>::update(int nb, const BlockTab<T>& X, const V* H, const V* Yin, V* Yout, T sign,
+                             cudaStream_t s) {
+  each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+    launch_multi_update<T>(nr, k, nb, shift(X, nb, r0 * k), H, Yin ? Yin + r0 * k : nullptr, Yout + r0 * k, sign,
+                           st);
+  });
 }
 
 template <class T>
 void BlockAlgebra<T>::col_norms(const V* X, std::vector<double>& out, cudaStream_t s) {
-  launch_colnorm2_partial<T>(n, k, X, rpart.get(), nslots, s);
-  launch_reduce_real<T>(k, nslots, rpart.get(), rnorm.get(), s);
+  int used = 0;
+  each(s, [&](int p, int64_t r0, int64_t nr, cudaStream_t st) {
+    launch_colnorm2_partial<T>(nr, k, X + r0 * k, rpart.get() + size_t(used) * k, pslots[p], st);
+    used += pslots[p];
+  });
+  join();
+  launch_reduce_real<T>(k, used, rpart.get(), rnorm.get(), s);
   HZ_CUDA(cudaMemcpyAsync(h_norm.get(), rnorm.get(), sizeof(T) * k, cudaMemcpyDeviceToHost, s));
   HZ_CUDA(cudaStreamSynchronize(s));
   out.resize(k);
@@ -274,17 +311,22 @@ void BlockAlgebra<T>::thin_qr_enqueue(V* W, cudaStream_t s) {
   HZ_CUDA(cudaStreamSynchronize(s));
   mgs_used = h_flags[0] != 0;
   if (mgs_used) {
+    // rare path; in slab mode part 0 runs it over the whole spanning block
+    // (every part is idle after the join above)
     dbuf.ensure(192);
     launch_mgs_qr<T>(n, k, W, R1.get(), dbuf.get(), partials.get(), nslots, flags.get(), s);
     HZ_CUDA(cudaMemcpyAsync(h_R.get(), R1.get(), sizeof(V) * size_t(k) * k, cudaMemcpyDeviceToHost, s));
     HZ_CUDA(cudaMemcpyAsync(h_flags.get(), flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    fork();
     return;
   }
-  launch_multi_update<T>(n, k, 1, t, R1i.get(), nullptr, tmp_blk.get(), T(1), s);
+  fork();
+  update(1, t, R1i.get(), nullptr, tmp_blk.get(), T(1), s);
   t.p[0] = tmp_blk.get();
   gram(t, 1, tmp_blk.get(), G.get(), s);
   launch_small_cholesky<T>(k, G.get(), R2.get(), R2i.get(), flags.get() + 1, tol, s);
-  launch_multi_update<T>(n, k, 1, t, R2i.get(), nullptr, W, T(1), s);
+  fork();
+  update(1, t, R2i.get(), nullptr, W, T(1), s);
   const size_t kk = size_t(k) * k;
   HZ_CUDA(cudaMemcpyAsync(h_R.get(), R1.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
   HZ_CUDA(cudaMemcpyAsync(h_R.get() + kk, R2.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
@@ -320,9 +362,15 @@ void Fgmres<T>::ensure(int64_t n, int k, int restart) {
   Zb_.clear();
   Vb_.resize(restart + 1);
   Zb_.resize(restart);
-  for (auto& b : Vb_) b.alloc(size_t(n) * k);
-  for (auto& b : Zb_) b.alloc(size_t(n) * k);
-  R_.alloc(size_t(n) * k);
+  auto get = [&](DevBuf<V>& b) {
+    if (sl_)
+      alloc_span(b, *sl_, 0, k);
+    else
+      b.alloc(size_t(n) * k);
+  };
+  for (auto& b : Vb_) get(b);
+  for (auto& b : Zb_) get(b);
+  get(R_);
   hcol1_.alloc(size_t(restart + 2) * k * k);
   ccoef_.alloc(size_t(restart + 2) * k * k);
   hcol2_.alloc(size_t(restart + 1) * k * k);
@@ -333,7 +381,7 @@ void Fgmres<T>::ensure(int64_t n, int k, int restart) {
   ztab_ = BlockTab<T>{};
   for (int i = 0; i <= restart; ++i) vtab_.p[i] = Vb_[i].get();
   for (int i = 0; i < restart; ++i) ztab_.p[i] = Zb_[i].get();
-  alg_.ensure(n, k, restart + 1);
+  alg_.ensure(n, k, restart + 1, sl_);
   n_ = n;
   k_ = k;
   m_ = restart;
@@ -351,7 +399,6 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     const char* e = std::getenv("HZ_PIP_ETA2");
     pip_eta2_ = e ? std::atof(e) : 1e-4;
   }
-  const size_t blk = size_t(n) * k * sizeof(V);
   const size_t kk = size_t(k) * k;
   Report rep;
   rep.col_cycles.assign(k, -1);
@@ -360,8 +407,17 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
   std::vector<double> r0 = bnorm;
   for (double& x : bnorm)
     if (x == 0.0) x = 1.0;  // rhs_norms (src/krylov.cpp:15-20)
-  HZ_CUDA(cudaMemsetAsync(X, 0, blk, s));
-  HZ_CUDA(cudaMemcpyAsync(R_.get(), B, blk, cudaMemcpyDeviceToDevice, s));
+  const size_t rowb = size_t(k) * sizeof(V);
+  // row-split copies (one call per part in slab mode)
+  auto copy_blk = [&](V* dst, const V* src) {
+    alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+      HZ_CUDA(cudaMemcpyAsync(dst + r0 * k, src + r0 * k, size_t(nr) * rowb, cudaMemcpyDeviceToDevice, st));
+    });
+  };
+  alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+    HZ_CUDA(cudaMemsetAsync(X + r0 * k, 0, size_t(nr) * rowb, st));
+  });
+  copy_blk(R_.get(), B);
   bool done = true;
   for (int j = 0; j < k; ++j) done = done && r0[j] / bnorm[j] <= tol;
   const int m = restart;
@@ -371,7 +427,7 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
   std::vector<cplx> Rk;
   while (!done && rep.cycles < max_cycles) {
     // Arnoldi from the current residual: V_0 = thin_qr(R)
-    HZ_CUDA(cudaMemcpyAsync(Vb_[0].get(), R_.get(), blk, cudaMemcpyDeviceToDevice, s));
+    copy_blk(Vb_[0].get(), R_.get());
     alg_.thin_qr_enqueue(Vb_[0].get(), s);
     HZ_CUDA(cudaStreamSynchronize(s));
     bool rd = false;
@@ -385,7 +441,7 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
       if (op.prec)
         op.prec(Vb_[jj].get(), Zj, k, s);
       else
-        HZ_CUDA(cudaMemcpyAsync(Zj, Vb_[jj].get(), blk, cudaMemcpyDeviceToDevice, s));
+        copy_blk(Zj, Vb_[jj].get());
       op.apply(Zj, Vb_[jj + 1].get(), k, s);
     };
     // The next step's preconditioner + matvec depend only on V_{j+1}, not on
@@ -420,7 +476,8 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
           ++pip_accepted_;
           // W <- sum_i V_i C_i + W C_{j+1} = (W - V H) R^{-1}  (in place: each
           // CTA stages its rows of every block before writing them)
-          launch_multi_update<T>(n, k, j + 2, vtab_, ccoef_.get(), nullptr, W, T(1), s);
+          alg_.fork();
+          alg_.update(j + 2, vtab_, ccoef_.get(), nullptr, W, T(1), s);
           for (int i = 0; i <= j; ++i)
             for (size_t e = 0; e < kk; ++e) H[j][i][e] = cplx{} + to_c(h_hcol_[i * kk + e]);
           for (size_t e = 0; e < kk; ++e) H[j][j + 1][e] = to_c(alg_.h_R[e]);
@@ -431,9 +488,11 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
       }
       if (!accepted) {
         // block CGS2 against V_0..V_j, then CholQR2
-        launch_multi_update<T>(n, k, j + 1, vtab_, hcol1_.get(), W, W, T(-1), s);
+        alg_.fork();
+        alg_.update(j + 1, vtab_, hcol1_.get(), W, W, T(-1), s);
         alg_.gram(vtab_, j + 1, W, hcol2_.get(), s);
-        launch_multi_update<T>(n, k, j + 1, vtab_, hcol2_.get(), W, W, T(-1), s);
+        alg_.fork();
+        alg_.update(j + 1, vtab_, hcol2_.get(), W, W, T(-1), s);
         rep.block_gram_products += j + 1;
         HZ_CUDA(cudaMemcpyAsync(h_hcol_.get(), hcol1_.get(), sizeof(V) * hc, cudaMemcpyDeviceToHost, s));
         HZ_CUDA(cudaMemcpyAsync(h_hcol_.get() + hc, hcol2_.get(), sizeof(V) * hc,
@@ -469,10 +528,13 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     for (size_t e = 0; e < size_t(j) * kk; ++e) h_y_[e] = from_c<V>(Y[e]);
     HZ_CUDA(cudaMemcpyAsync(ydev_.get(), h_y_.get(), sizeof(V) * size_t(j) * kk,
                             cudaMemcpyHostToDevice, s));
-    launch_multi_update<T>(n, k, j, ztab_, ydev_.get(), X, X, T(1), s);
+    alg_.fork();
+    alg_.update(j, ztab_, ydev_.get(), X, X, T(1), s);
     // true residual for the restart / convergence decision
     op.apply(X, R_.get(), k, s);
-    launch_axpby<T>(int64_t(n) * k, mk(T(-1), T(0)), R_.get(), mk(T(1), T(0)), B, s);
+    alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+      launch_axpby<T>(nr * k, mk(T(-1), T(0)), R_.get() + r0 * k, mk(T(1), T(0)), B + r0 * k, st);
+    });
     std::vector<double> rn;
     alg_.col_norms(R_.get(), rn, s);
     double worst = 0.0;
@@ -481,7 +543,9 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
   }
   // finalize (src/krylov.cpp:33-46)
   op.apply(X, R_.get(), k, s);
-  launch_axpby<T>(int64_t(n) * k, mk(T(-1), T(0)), R_.get(), mk(T(1), T(0)), B, s);
+  alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+    launch_axpby<T>(nr * k, mk(T(-1), T(0)), R_.get() + r0 * k, mk(T(1), T(0)), B + r0 * k, st);
+  });
   std::vector<double> rn;
   alg_.col_norms(R_.get(), rn, s);
   rep.rel_residual.resize(k);

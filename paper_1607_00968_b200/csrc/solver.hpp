@@ -13,6 +13,7 @@
 
 #include "devbuf.hpp"
 #include "kernels.hpp"
+#include "slabs.hpp"
 
 namespace hz {
 
@@ -98,6 +99,15 @@ class Hierarchy {
   void coarse_solve(int k, const V* b, V* x, cudaStream_t s);
   // Galerkin planes / diagonal of level l (host copy, f64) for parity checks
   void download_level(int l, std::vector<cplx>& coef_or_center) const;
+  // copy of the level operators (not the coarsest solver) on another GPU
+  std::unique_ptr<Hierarchy<T>> replica(int device, cudaStream_t s) const;
+  // Slab mode (slabs.hpp): levels below sl->agg_level() run on every part,
+  // each part computing its own planes with the operators of reps[p] (a
+  // hierarchy resident on part p's GPU); coarser levels and the coarsest
+  // solve run on part 0. cycle() must then be called on part 0's stream
+  // with b, x spanning level-0 vectors.
+  void attach_slabs(const Slabs* sl, std::vector<const Hierarchy<T>*> reps);
+  const Slabs* slabs() const { return sl_; }
 
   std::vector<MgLevelDev<T>> levels_;
   DevBuf<V> ainvT_;  // coarsest inverse, transposed [n_c][inv_ld(n_c)]
@@ -115,6 +125,13 @@ class Hierarchy {
   void relax(int l, const CycleSpec& spec, int sweeps, int k, const V* b, V*& cur, V*& other,
              bool& cur_zero, cudaStream_t s);
   void kcycle_coarse(int l, const CycleSpec& spec, int k, const V* b, V* x, cudaStream_t s);
+  bool slab_level(int l) const { return sl_ && l < sl_->agg_level(); }
+  // f(op, stream, row0, rows) once per part owning level l (slab levels), or
+  // once on stream s over the whole grid
+  template <class F>
+  void on_level(int l, int k, cudaStream_t s, F&& f);
+  const Slabs* sl_ = nullptr;
+  std::vector<const Hierarchy<T>*> reps_;
   int ws_k_ = 0;
   std::vector<DevBuf<V>> wx_, wt_, wb_, wr_;  // per level: solution, ping-pong, rhs, residual
   std::vector<std::unique_ptr<Fgmres<T>>> kfgm_;
@@ -154,7 +171,8 @@ template <class T>
 class BlockAlgebra {
  public:
   using V = cplx_t<T>;
-  void ensure(int64_t n, int k, int max_blocks);
+  // sl: rows of level 0 split over slab parts (nullptr: one stream)
+  void ensure(int64_t n, int k, int max_blocks, const Slabs* sl = nullptr);
   // G_i = X_i^H Y for nb blocks, result on device (nb k^2, row-major tiles)
   void gram(const BlockTab<T>& tab, int nb, const V* Y, V* out, cudaStream_t s);
   // per-column 2-norms to host
@@ -176,6 +194,36 @@ class BlockAlgebra {
   PinnedBuf<T> h_norm;
   PinnedBuf<V> h_R;     // [R1 | R2]
   PinnedBuf<int> h_flags;
+
+  // ---- slab mode: row-local work runs per part on the part's rows; the
+  // k x k partials of all parts are summed on part 0 (stream s) in a fixed
+  // slot order
+  const Slabs* sl = nullptr;
+  std::vector<int> pslots;  // partial slots per part
+  template <class F>
+  void each(cudaStream_t s, F&& f) const {
+    if (!sl) {
+      f(0, int64_t(0), n, s);
+      return;
+    }
+    sl->each(0, [&](int p, int64_t r0, int64_t nr, cudaStream_t st) { f(p, r0, nr, st); });
+  }
+  void join() const {
+    if (sl) sl->join();
+  }
+  void fork() const {
+    if (sl) sl->fork();
+  }
+  static BlockTab<T> shift(const BlockTab<T>& t, int nb, int64_t off) {
+    BlockTab<T> r{};
+    for (int i = 0; i < nb; ++i) r.p[i] = t.p[i] ? t.p[i] + off : nullptr;
+    return r;
+  }
+  // row-split block update: Yout = (Yin ? Yin : 0) + sign * sum_i X_i H_i
+  void update(int nb, const BlockTab<T>& X, const V* H, const V* Yin, V* Yout, T sign, cudaStream_t s);
+
+ private:
+  const Slabs* sl_alloc_ = nullptr;
 };
 
 template <class T>
@@ -185,9 +233,15 @@ class Fgmres {
   // block_fgmres (src/krylov.cpp:178-280): X = 0 start, flexible, restart m.
   Report solve(const DevOp<T>& op, int k, const V* B, V* X, int restart, double tol,
                int max_cycles, cudaStream_t s);
+  // slab mode: B, X and the basis span the parts; s must be part 0's stream
+  void set_slabs(const Slabs* sl) {
+    if (sl != sl_) n_ = 0;
+    sl_ = sl;
+  }
 
  private:
   void ensure(int64_t n, int k, int restart);
+  const Slabs* sl_ = nullptr;
   int64_t n_ = 0;
   int k_ = 0, m_ = 0;
   std::vector<DevBuf<V>> Vb_, Zb_;

@@ -25,7 +25,7 @@ struct Elem {
 
 template <class T>
 __device__ __forceinline__ bool decode(const LevelGeom& g, uint32_t e, Elem<T>& el) {
-  if (e >= g.nodes * g.k) return false;
+  if (e >= g.e_end()) return false;
   g.div_k.divmod(e, el.node, el.col);
   g.unpack(el.node, el.i, el.j, el.kz);
   return true;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kBlock)
 level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
              cplx_t<T>* __restrict__ out, T wj) {
   using V = cplx_t<T>;
-  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t e = op.g.e_begin() + blockIdx.x * kBlock + threadIdx.x;
   Elem<T> el;
   if (!decode(op.g, e, el)) return;
   const V ax = level_ax<T, NDIM, KIND, MODE != 0>(op, x, e, el);
@@ -161,8 +161,8 @@ stencil_mc_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
   using V = cplx_t<T>;
   const LevelGeom& g = op.g;
   const uint32_t t = blockIdx.x * kBlock + threadIdx.x;
-  const uint32_t e0 = t * CPT;
-  if (e0 >= g.nodes * g.k) return;
+  const uint32_t e0 = g.e_begin() + t * CPT;
+  if (e0 >= g.e_end()) return;
   uint32_t node, col, i, j, kz;
   g.div_k.divmod(e0, node, col);
   g.unpack(node, i, j, kz);
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(kBlock)
 jacobi_zero_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj,
                    const In* __restrict__ b, cplx_t<T>* __restrict__ out) {
   using V = cplx_t<T>;
-  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
-  if (e >= g.nodes * g.k) return;
+  const uint32_t e = g.e_begin() + blockIdx.x * kBlock + threadIdx.x;
+  if (e >= g.e_end()) return;
   const uint32_t node = g.div_k.div(e);
   const V d = __ldg(&inv_diag[node]);
   const V wd = mk(wj * d.x, wj * d.y);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kBlock)
 restrict_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r,
                 cplx_t<T>* __restrict__ bc) {
   using V = cplx_t<T>;
-  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t e = gc.e_begin() + blockIdx.x * kBlock + threadIdx.x;
   Elem<T> el;
   if (!decode(gc, e, el)) return;
   const int64_t k = gf.k;
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kBlock)
 prolong_correct_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec,
                        cplx_t<T>* __restrict__ x) {
   using V = cplx_t<T>;
-  const uint32_t e = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t e = gf.e_begin() + blockIdx.x * kBlock + threadIdx.x;
   Elem<T> el;
   if (!decode(gf, e, el)) return;
   const int64_t k = gf.k;
@@ -434,7 +434,7 @@ constexpr const char* prec_tag() {
 // written once per element, coefficients once per node
 template <class T>
 double level_bytes(const LevelOp<T>& op, int mode) {
-  const double s = sizeof(cplx_t<T>), n = op.g.nodes, k = op.g.k;
+  const double s = sizeof(cplx_t<T>), n = double(op.g.owned_nodes()), k = op.g.k;
   const double coef = op.kind == kFine ? 1.0 : (op.ndim == 3 ? 27.0 : 9.0);
   const double vec = mode == 0 ? 2.0 : 3.0;
   const double diag = mode == 2 ? 1.0 : 0.0;
@@ -454,7 +454,7 @@ const char* level_name(int kind) {
 template <class T, int MODE>
 void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out,
                     T wj, cudaStream_t s) {
-  const int64_t total = int64_t(op.g.nodes) * op.g.k;
+  const int64_t total = op.g.owned_elems();
   const int grid = grid_for(total, kBlock);
   ProfScope prof(level_name<T, MODE>(op.kind), level_bytes(op, MODE), s);
   if (op.kind == kFine) {
@@ -495,18 +495,18 @@ void launch_jacobi(const LevelOp<T>& op, T wj, const cplx_t<T>* x, const cplx_t<
 }
 template <class T, class In>
 void launch_jacobi_zero(const LevelOp<T>& op, T wj, const In* b, cplx_t<T>* xout, cudaStream_t s) {
-  const int64_t total = int64_t(op.g.nodes) * op.g.k;
+  const int64_t total = op.g.owned_elems();
   ProfScope prof(sizeof(T) == 8 ? "jacobi_zero_c128" : "jacobi_zero_c64",
-                 double(op.g.nodes) * ((double(sizeof(In)) + sizeof(cplx_t<T>)) * op.g.k + sizeof(cplx_t<T>)), s);
+                 double(op.g.owned_nodes()) * ((double(sizeof(In)) + sizeof(cplx_t<T>)) * op.g.k + sizeof(cplx_t<T>)), s);
   jacobi_zero_kernel<T, In><<<grid_for(total, kBlock), kBlock, 0, s>>>(op.g, op.inv_diag, wj, b, xout);
   HZ_LAUNCH_CHECK();
 }
 template <class T>
 void launch_restrict(const LevelGeom& gf, const LevelGeom& gc, int ndim, const cplx_t<T>* r,
                      cplx_t<T>* bc, cudaStream_t s) {
-  const int grid = grid_for(int64_t(gc.nodes) * gc.k, kBlock);
+  const int grid = grid_for(gc.owned_elems(), kBlock);
   ProfScope prof(sizeof(T) == 8 ? "restrict_c128" : "restrict_c64",
-                 (double(gf.nodes) + gc.nodes) * gf.k * sizeof(cplx_t<T>), s);
+                 (double(gf.nodes) * gc.owned_nodes() / gc.nodes + gc.owned_nodes()) * gf.k * sizeof(cplx_t<T>), s);
   if (ndim == 3)
     restrict_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, r, bc);
   else
@@ -516,9 +516,9 @@ void launch_restrict(const LevelGeom& gf, const LevelGeom& gc, int ndim, const c
 template <class T>
 void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
                             const cplx_t<T>* ec, cplx_t<T>* x, cudaStream_t s) {
-  const int grid = grid_for(int64_t(gf.nodes) * gf.k, kBlock);
+  const int grid = grid_for(gf.owned_elems(), kBlock);
   ProfScope prof(sizeof(T) == 8 ? "prolong_correct_c128" : "prolong_correct_c64",
-                 (2.0 * gf.nodes + gc.nodes) * gf.k * sizeof(cplx_t<T>), s);
+                 (2.0 * gf.owned_nodes() + gc.nodes * double(gf.owned_nodes()) / gf.nodes) * gf.k * sizeof(cplx_t<T>), s);
   if (ndim == 3)
     prolong_correct_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
   else

@@ -1,0 +1,123 @@
+"""GPU tier: slab decomposition along the slow axis.
+
+Parts are cut on the slow axis; every part computes its own planes and reads
+the neighbour faces through the global layout (on several GPUs, peer memory
+over NVLink). On this one-GPU tier the parts are separate streams on one GPU,
+ordered only by the slab events, which exercises the same partitioning and
+synchronisation. A cycle does the same arithmetic per element whatever the
+partition, so slab cycles must equal the single-stream cycle BITWISE; a slab
+FGMRES solve differs only in the grouping of its Gram partial sums."""
+import numpy as np
+import pytest
+
+from hzt_util import rel_err
+from paper_1607_00968_b200 import configs
+
+pytestmark = pytest.mark.gpu
+hz = pytest.importorskip("paper_1607_00968_b200")
+
+
+def _cfg3d():
+    return configs.config3(nlevels=3, n=(65, 65, 33), sgrid=2, layer=8)
+
+
+def _solver(cfg, precision="c128", kind="V", nlevels=None):
+    P = hz.HelmholtzProblem.from_config(cfg)
+    o = hz.HelmholtzSolveOptions.from_config(cfg)
+    o.method = "MgFgmres"
+    o.cycle = hz.CycleSpec(kind)
+    o.precond_precision = precision
+    if nlevels:
+        o.nlevels = nlevels
+    return hz.HelmholtzSolver(P, o)
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+@pytest.mark.parametrize("kind", ["V", "W"])
+def test_slab_cycle_3d_bitwise_equals_single_domain(precision, kind):
+    cfg = _cfg3d()
+    S = _solver(cfg, precision, kind)
+    b = configs.random_block(cfg.num_nodes, 8, seed=11)
+    x1 = S.cycle(b)
+    for parts in (2, 4, 8):
+        S.set_slabs(parts)
+        xs = S.cycle(b)
+        assert np.array_equal(xs, x1), f"{parts} parts"
+    S.set_slabs(1)
+    assert np.array_equal(S.cycle(b), x1)
+
+
+def test_slab_cycle_2d_bitwise_equals_single_domain():
+    cfg = configs.config1(nlevels=4, nx=129, k=4)
+    S = _solver(cfg, "c128", "W", nlevels=4)
+    b = configs.random_block(cfg.num_nodes, 4, seed=3)
+    x1 = S.cycle(b)
+    for parts in (2, 3, 4):
+        S.set_slabs(parts)
+        assert np.array_equal(S.cycle(b), x1), f"{parts} parts"
+
+
+def test_slab_info_cuts_follow_coarsening():
+    cfg = _cfg3d()
+    S = _solver(cfg)
+    S.set_slabs(4)
+    P, agg, planes = S.slab_info()
+    assert P == 4
+    assert planes.shape == (3, 5)
+    assert list(planes[0]) == [0, 8, 16, 24, 33]
+    assert list(planes[1]) == [0, 4, 8, 12, 17]
+    assert list(planes[2]) == [0, 2, 4, 6, 9]
+    assert agg == 2  # the coarsest level is solved on part 0
+    S.set_slabs(8)
+    P, agg, planes = S.slab_info()
+    assert list(planes[0]) == [0, 4, 8, 12, 16, 20, 24, 28, 33]
+    assert agg == 2
+
+
+@pytest.mark.parametrize("precision", ["c128", "c64"])
+def test_slab_fgmres_solve_matches_single_domain_and_reference(ref, precision):
+    cfg = _cfg3d()
+    S = _solver(cfg, precision)
+    B = cfg.rhs_block()
+    X1, r1 = S.solve_block(B)
+    S.set_slabs(4)
+    X4, r4 = S.solve_block(B)
+    assert r1.all_converged() and r4.all_converged()
+    assert abs(r4.cycles - r1.cycles) <= 1
+    assert np.all(r4.rel_residual <= 1e-6)
+    for j in range(B.shape[1]):
+        assert rel_err(X4[:, j], X1[:, j]) <= 1e-6
+    R = ref.RefProblem.from_config(cfg)
+    H = ref.RefHierarchy(R, 3, cfg.shift)
+    Xr, rr = ref.krylov_solve(R, H, B, method="fgmres", kind="V", restart=cfg.restart, tol=1e-6,
+                              max_cycles=cfg.max_cycles)
+    for j in range(B.shape[1]):
+        assert rel_err(X4[:, j], Xr[:, j]) <= 1e-5
+
+
+def test_slab_device_tensor_solve():
+    import torch
+    cfg = _cfg3d()
+    S = _solver(cfg, "c64")
+    S.set_slabs(2)
+    B = cfg.rhs_block()
+    Xh, rh = S.solve_block(B)
+    Xd, rd = S.solve_block(torch.from_numpy(B).cuda())
+    assert rh.cycles == rd.cycles
+    assert np.array_equal(Xh, Xd.cpu().numpy())
+
+
+def test_slab_mode_validation():
+    cfg = _cfg3d()
+    P = hz.HelmholtzProblem.from_config(cfg)
+    bic = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgBicgstab", nlevels=3))
+    with pytest.raises(hz.ValidationError):
+        bic.set_slabs(2)
+    kc = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmresK", nlevels=3))
+    with pytest.raises(hz.ValidationError):
+        kc.set_slabs(2)
+    S = _solver(cfg)
+    with pytest.raises(hz.ValidationError):
+        S.set_slabs(17)  # fewer than 2 fine planes per part
+    with pytest.raises(hz.ValidationError):
+        S.set_slabs(2, devices=[0, 99])
