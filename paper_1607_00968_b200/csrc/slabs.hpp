@@ -91,6 +91,7 @@ class Slabs {
 // Spanning allocation helper for DevBuf (see Slabs::alloc).
 template <class E>
 void alloc_span(DevBuf<E>& b, const Slabs& sl, int l, int k) {
+  b.release();  // free first: these blocks are large and HBM may be nearly full
   b.adopt(sl.alloc(l, sizeof(E) * size_t(k)), size_t(sl.rows(l)) * k);
 }
 

@@ -43,14 +43,20 @@ if __name__ == "__main__":
         torch.cuda.synchronize()
         setup = time.time() - t
         B = torch.from_numpy(cfg.rhs_block()).cuda()
-        torch.cuda.synchronize(); t = time.time()
-        X, rep = S.solve_block(B)
-        torch.cuda.synchronize(); dt = time.time() - t
-        out = dict(config=c, name=cfg.name, n=cfg.n, k=cfg.k, nlevels=cfg.nlevels, shift=cfg.shift,
-                   restart=cfg.restart, prec=cfg.precond_precision, setup_s=round(setup, 2), solve_s=round(dt, 3),
-                   cycles=rep.cycles, converged=rep.all_converged(), worst_res=float(rep.rel_residual.max()),
-                   rhs_per_s=round(cfg.k / dt, 3), ms_per_cycle=round(1e3 * dt / max(rep.cycles, 1), 3))
-        print(json.dumps(out), flush=True)
+        # HZ_SLABS="1,8": solve once per slab count (parts as streams on this GPU)
+        for slabs in [int(x) for x in os.environ.get("HZ_SLABS", "1").split(",")]:
+            S.set_slabs(slabs)
+            torch.cuda.synchronize(); t = time.time()
+            X, rep = S.solve_block(B)
+            torch.cuda.synchronize(); dt = time.time() - t
+            out = dict(config=c, name=cfg.name, n=cfg.n, k=cfg.k, nlevels=cfg.nlevels, shift=cfg.shift,
+                       restart=cfg.restart, prec=cfg.precond_precision, slabs=slabs, setup_s=round(setup, 2),
+                       solve_s=round(dt, 3), cycles=rep.cycles, converged=rep.all_converged(),
+                       worst_res=float(rep.rel_residual.max()), rhs_per_s=round(cfg.k / dt, 3),
+                       ms_per_cycle=round(1e3 * dt / max(rep.cycles, 1), 3))
+            print(json.dumps(out), flush=True)
+            if slabs > 1:
+                S.set_slabs(1)
         if prof:
             with hz.kernel_profile() as p:
                 S.solve_block(B)
