@@ -95,6 +95,7 @@ typedef struct hz_report {
 
 typedef struct hz_problem hz_problem;
 typedef struct hz_solver hz_solver;
+typedef struct hz_sampling hz_sampling;
 
 HZ_API int hz_abi_version(void);
 HZ_API const char* hz_last_error_message(void);
@@ -182,6 +183,56 @@ HZ_API int hz_sensitivity_accumulate_device(hz_problem* p, int64_t n, int k, con
 
 /* number of this library's kernel launches so far (process-wide) */
 HZ_API int64_t hz_kernel_launch_count(void);
+
+/* ---- FWI path either side of the solve ----------------
+ * SamplingOperator(AcquisitionGeometry, grid) (inc/acquisition.hpp:30-62,
+ * src/acquisition.cpp:33-62): receivers at physical points xyz[r][3] on the
+ * problem's grid with the given origin (NULL: 0); multilinear weights over the
+ * <= 2^ndim enclosing nodes. ValidationError if a receiver is off the grid. */
+HZ_API int hz_sampling_create(const hz_problem* p, const double origin[3], int64_t nrec, const double* xyz,
+                              hz_sampling** out);
+HZ_API int hz_sampling_destroy(hz_sampling* s);
+HZ_API int64_t hz_sampling_num_receivers(const hz_sampling* s);
+/* receiver_nodes / receiver_weights (inc/acquisition.hpp:64-65) */
+HZ_API int hz_sampling_receiver(const hz_sampling* s, int64_t r, int64_t nodes[8], double weights[8], int* count);
+/* SamplingOperator::sample (inc/acquisition.hpp:40-51): D[nrec][k] = P^T U[n][k] */
+HZ_API int hz_sample_device(hz_sampling* s, int k, const void* U_dev, void* D_dev, void* stream);
+HZ_API int hz_sample(hz_sampling* s, int k, const double* U, double* D);
+/* SamplingOperator::sample_adjoint (inc/acquisition.hpp:53-61): U = P D, or
+ * P conj(D) when conj != 0; same summation order as the reference */
+HZ_API int hz_sample_adjoint_device(hz_sampling* s, int k, const void* D_dev, void* U_dev, int conj, void* stream);
+HZ_API int hz_sample_adjoint(hz_sampling* s, int k, const double* D, double* U, int conj);
+/* fwi_sensitivity_rhs (src/helmholtz_solver.cpp:95-101) for k fields:
+ * R = -w^2 (1 - i gamma/w) U v, v real [n] */
+HZ_API int hz_fwi_sensitivity_rhs_device(hz_problem* p, int64_t n, int k, const void* U_dev, const void* v_dev,
+                                         void* R_dev, void* stream);
+/* fwi_jacobian_vec (src/helmholtz_solver.cpp:113-125) for k stored fields
+ * U[n][k] at once (one block solve): D[nrec][k] = P^T A^{-1}(-w^2 gf U v).
+ * HZ_CONVERGENCE if the solve misses tol (report still filled). k = 1 is the
+ * reference function exactly. */
+HZ_API int hz_fwi_jacobian_vec(hz_solver* s, hz_sampling* P, int64_t n, int k, const double* U, const double* v,
+                               double* D, hz_report* rep);
+HZ_API int hz_fwi_jacobian_vec_device(hz_solver* s, hz_sampling* P, int64_t n, int k, const void* U_dev,
+                                      const void* v_dev, void* D_dev, hz_report* rep);
+/* fwi_jacobian_transpose_vec (src/helmholtz_solver.cpp:127-139) summed over
+ * k sources: g[n] (+)= sum_s Re(-w^2 gf u_s lambda_s), lambda_s = A^{-1} P conj(W_s) */
+HZ_API int hz_fwi_jacobian_transpose_vec(hz_solver* s, hz_sampling* P, int64_t n, int k, const double* U,
+                                         const double* W, double* g, int accumulate, hz_report* rep);
+HZ_API int hz_fwi_jacobian_transpose_vec_device(hz_solver* s, hz_sampling* P, int64_t n, int k, const void* U_dev,
+                                                const void* W_dev, double* g_dev, int accumulate, hz_report* rep);
+
+/* ---- wavefield output -----------------------------------
+ * WavefieldBatch::append with StoragePrecision::Compact16
+ * (src/helmholtz.cpp:137-151) for k columns of X[n][k] on the device:
+ * scales[c] = 2^ceil(log2 max|re,im|) (host array), Q = source-major
+ * [k][n][2] binary16 (re, im) of X / scale, round-to-nearest-even. */
+HZ_API int hz_compact16_device(int64_t n, int k, const void* X_dev, void* Q_dev, double* scales, void* stream);
+HZ_API int hz_compact16(int64_t n, int k, const double* X, uint16_t* Q, double* scales);
+/* solve_helmholtz(..., Compact16) (src/helmholtz_solver.cpp:81-93): solve,
+ * HZ_CONVERGENCE if any column misses tol, then quantise on the device and
+ * return only the 4-byte-per-entry compact fields to the host. */
+HZ_API int hz_solve_helmholtz_compact16(hz_solver* s, int64_t n, int k, const double* B, uint16_t* Q,
+                                        double* scales, hz_report* rep);
 
 /* Per-kernel CUDA-event profiling of this library's launches (measurement
  * support for bench.py): begin clears and enables, end disables, report

@@ -10,9 +10,13 @@
 // libhz_b200.so on the GPU; this header only marshals.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
+#include <cstring>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -79,6 +83,7 @@ struct RegularGrid {
   int ndim = 2;
   std::array<std::int64_t, 3> n{1, 1, 1};
   std::array<double, 3> h{1.0, 1.0, 1.0};
+  std::array<double, 3> origin{0.0, 0.0, 0.0};
   std::int64_t num_nodes() const { return n[0] * n[1] * n[2]; }
 };
 
@@ -253,6 +258,7 @@ class HelmholtzSolver {
     rep.history = std::move(hist);
     return {std::move(X), std::move(rep)};
   }
+  hz_solver* handle() const { return h_.get(); }
   std::pair<CField, SolveReport> solve(const CField& rhs) const {
     BlockVec<cplx> B(static_cast<std::int64_t>(rhs.size()), 1);
     B.set_col(0, rhs);
@@ -266,20 +272,351 @@ class HelmholtzSolver {
   std::shared_ptr<hz_solver> h_;
 };
 
-// solve_helmholtz (src/helmholtz_solver.cpp:81-93), Full storage: one
-// solution field per right-hand side; ConvergenceError if any column misses tol.
-inline std::vector<CField> solve_helmholtz(const HelmholtzSolver& solver, const std::vector<CField>& rhs,
-                                           SolveReport* report = nullptr) {
+// ---- acquisition (acquisition.hpp:9-62): receivers sampled on the GPU
+struct AcquisitionGeometry {
+  std::vector<std::array<double, 3>> sources;
+  std::vector<std::array<double, 3>> receivers;
+  double offset_min = 0.0;
+  double offset_max = 0.0;
+  std::vector<std::vector<std::uint8_t>> active;  // [source][receiver]
+  AcquisitionGeometry() = default;
+  AcquisitionGeometry(std::vector<std::array<double, 3>> src, std::vector<std::array<double, 3>> rec, double omin,
+                      double omax, const RegularGrid& core_grid)
+      : sources(std::move(src)), receivers(std::move(rec)), offset_min(omin), offset_max(omax) {
+    if (omin < 0.0 || omax < omin) throw ValidationError("acquisition: bad offset range");
+    auto inside = [&](const std::array<double, 3>& x) {
+      for (int a = 0; a < core_grid.ndim; ++a) {
+        const double lo = core_grid.origin[a] - 1e-9 * core_grid.h[a];
+        const double hi = core_grid.origin[a] + (core_grid.n[a] - 1) * core_grid.h[a] + 1e-9 * core_grid.h[a];
+        if (x[a] < lo || x[a] > hi) return false;
+      }
+      return true;
+    };
+    for (std::size_t i = 0; i < sources.size(); ++i)
+      if (!inside(sources[i])) throw ValidationError("acquisition: source " + std::to_string(i) + " outside core grid");
+    for (std::size_t i = 0; i < receivers.size(); ++i)
+      if (!inside(receivers[i]))
+        throw ValidationError("acquisition: receiver " + std::to_string(i) + " outside core grid");
+    active.assign(sources.size(), std::vector<std::uint8_t>(receivers.size(), 0));
+    for (std::size_t a = 0; a < sources.size(); ++a)
+      for (std::size_t r = 0; r < receivers.size(); ++r) {
+        double d2 = 0.0;
+        for (int c = 0; c < core_grid.ndim; ++c) {
+          const double dx = sources[a][c] - receivers[r][c];
+          d2 += dx * dx;
+        }
+        const double d = std::sqrt(d2);
+        active[a][r] = (d >= offset_min && d <= offset_max) ? 1 : 0;
+      }
+  }
+  std::size_t num_sources() const { return sources.size(); }
+  std::size_t num_receivers() const { return receivers.size(); }
+  bool is_active(std::size_t a, std::size_t r) const { return active[a][r] != 0; }
+};
+
+// SamplingOperator: P^T u / P d as GPU gathers (node-major transpose for the
+// scatter, so the sum order is the reference's without atomics).
+class SamplingOperator {
+ public:
+  SamplingOperator(const AcquisitionGeometry& geom, const HelmholtzProblem& problem) : grid_(problem.grid()) {
+    std::vector<double> xyz;
+    for (const auto& r : geom.receivers) xyz.insert(xyz.end(), r.begin(), r.end());
+    hz_sampling* p = nullptr;
+    check(hz_sampling_create(problem.handle(), grid_.origin.data(), static_cast<std::int64_t>(geom.receivers.size()),
+                             xyz.data(), &p));
+    h_.reset(p, [](hz_sampling* q) { hz_sampling_destroy(q); });
+  }
+  std::size_t num_receivers() const { return static_cast<std::size_t>(hz_sampling_num_receivers(h_.get())); }
+  const RegularGrid& grid() const { return grid_; }
+  std::vector<cplx> sample(const CField& u) const {
+    if (static_cast<std::int64_t>(u.size()) != grid_.num_nodes())
+      throw ValidationError("sample: field size does not match grid");
+    std::vector<cplx> d(num_receivers());
+    check(hz_sample(h_.get(), 1, reinterpret_cast<const double*>(u.data()), reinterpret_cast<double*>(d.data())));
+    return d;
+  }
+  CField sample_adjoint(const std::vector<cplx>& d) const {
+    if (d.size() != num_receivers()) throw ValidationError("sample_adjoint: receiver count mismatch");
+    CField u(static_cast<std::size_t>(grid_.num_nodes()));
+    check(hz_sample_adjoint(h_.get(), 1, reinterpret_cast<const double*>(d.data()), reinterpret_cast<double*>(u.data()),
+                            0));
+    return u;
+  }
+  std::vector<std::int64_t> receiver_nodes(std::size_t r) const {
+    std::int64_t nd[8];
+    double w[8];
+    int c = 0;
+    check(hz_sampling_receiver(h_.get(), static_cast<std::int64_t>(r), nd, w, &c));
+    return std::vector<std::int64_t>(nd, nd + c);
+  }
+  std::vector<double> receiver_weights(std::size_t r) const {
+    std::int64_t nd[8];
+    double w[8];
+    int c = 0;
+    check(hz_sampling_receiver(h_.get(), static_cast<std::int64_t>(r), nd, w, &c));
+    return std::vector<double>(w, w + c);
+  }
+  hz_sampling* handle() const { return h_.get(); }
+
+ private:
+  RegularGrid grid_;
+  std::shared_ptr<hz_sampling> h_;
+};
+
+namespace detail {
+inline hz_report make_report(std::vector<int>& cc, std::vector<double>& rr, std::vector<int>& cv,
+                             std::vector<double>& hist) {
+  hz_report r{};
+  r.col_cycles = cc.data();
+  r.rel_residual = rr.data();
+  r.converged = cv.data();
+  r.history = hist.data();
+  r.history_cap = static_cast<int>(hist.size());
+  return r;
+}
+}  // namespace detail
+
+// fwi_jacobian_vec (src/helmholtz_solver.cpp:113-125)
+inline std::vector<cplx> fwi_jacobian_vec(const HelmholtzSolver& solver, const CField& u_s, const SamplingOperator& P,
+                                          const Field& v) {
   const std::int64_t n = solver.problem().grid().num_nodes();
-  BlockVec<cplx> B(n, static_cast<int>(rhs.size()));
-  for (std::size_t s = 0; s < rhs.size(); ++s) B.set_col(static_cast<int>(s), rhs[s]);
-  auto res = solver.solve_block(B);
-  if (!res.second.all_converged())
-    throw ConvergenceError("helmholtz solve: tolerance not met within cycle cap", res.second.history);
-  std::vector<CField> out(rhs.size());
-  for (std::size_t s = 0; s < rhs.size(); ++s) out[s] = res.first.col(static_cast<int>(s));
-  if (report) *report = res.second;
+  if (static_cast<std::int64_t>(u_s.size()) != n) throw StateError("fwi_jacobian_vec: stored field does not match grid");
+  if (v.size() != u_s.size()) throw ValidationError("fwi_jacobian_vec: model vector size mismatch");
+  std::vector<cplx> d(P.num_receivers());
+  std::vector<int> cc(1), cv(1);
+  std::vector<double> rr(1), hist(static_cast<std::size_t>(solver.options().max_cycles) + 8);
+  hz_report r = detail::make_report(cc, rr, cv, hist);
+  const int st = hz_fwi_jacobian_vec(solver.handle(), P.handle(), n, 1, reinterpret_cast<const double*>(u_s.data()),
+                                     v.data(), reinterpret_cast<double*>(d.data()), &r);
+  hist.resize(std::min<std::size_t>(hist.size(), static_cast<std::size_t>(r.history_len)));
+  check(st, hist);
+  return d;
+}
+
+// fwi_jacobian_transpose_vec (src/helmholtz_solver.cpp:127-139)
+inline Field fwi_jacobian_transpose_vec(const HelmholtzSolver& solver, const CField& u_s, const SamplingOperator& P,
+                                        const std::vector<cplx>& w) {
+  const std::int64_t n = solver.problem().grid().num_nodes();
+  if (static_cast<std::int64_t>(u_s.size()) != n)
+    throw StateError("fwi_jacobian_transpose_vec: stored field does not match grid");
+  if (w.size() != P.num_receivers()) throw ValidationError("sample_adjoint: receiver count mismatch");
+  Field g(static_cast<std::size_t>(n));
+  std::vector<int> cc(1), cv(1);
+  std::vector<double> rr(1), hist(static_cast<std::size_t>(solver.options().max_cycles) + 8);
+  hz_report r = detail::make_report(cc, rr, cv, hist);
+  const int st = hz_fwi_jacobian_transpose_vec(solver.handle(), P.handle(), n, 1,
+                                               reinterpret_cast<const double*>(u_s.data()),
+                                               reinterpret_cast<const double*>(w.data()), g.data(), 0, &r);
+  hist.resize(std::min<std::size_t>(hist.size(), static_cast<std::size_t>(r.history_len)));
+  check(st, hist);
+  return g;
+}
+
+// ---- wavefield output (helmholtz.hpp:59-91)
+enum class StoragePrecision { Full32, Compact16 };
+
+namespace detail {
+// IEEE binary16 <-> binary32, round to nearest even (host side of the
+// JSWF1 f16 payload; the solve's own quantisation runs on the GPU)
+inline std::uint16_t f32_to_f16(float x) {
+  std::uint32_t b;
+  std::memcpy(&b, &x, 4);
+  const std::uint16_t sgn = static_cast<std::uint16_t>((b >> 16) & 0x8000u);
+  const std::uint32_t ex = (b >> 23) & 0xffu, fr = b & 0x7fffffu;
+  if (ex == 0xffu) return static_cast<std::uint16_t>(sgn | (fr ? 0x7e00u : 0x7c00u));
+  const int e = static_cast<int>(ex) - 112;  // rebias 127 -> 15
+  if (e >= 31) return static_cast<std::uint16_t>(sgn | 0x7c00u);
+  std::uint32_t m, shift;
+  if (e <= 0) {  // half subnormal (or zero)
+    if (e < -10) return sgn;
+    m = fr | 0x800000u;
+    shift = static_cast<std::uint32_t>(14 - e);
+  } else {
+    m = (static_cast<std::uint32_t>(e) << 23) | fr;  // exponent rides above the mantissa
+    shift = 13;
+  }
+  std::uint32_t q = m >> shift;
+  const std::uint32_t rest = m & ((1u << shift) - 1u), half = 1u << (shift - 1u);
+  if (rest > half || (rest == half && (q & 1u))) ++q;  // a carry into the exponent is correct
+  return static_cast<std::uint16_t>(sgn | q);
+}
+inline float f16_to_f32(std::uint16_t v) {
+  const std::uint32_t sgn = static_cast<std::uint32_t>(v & 0x8000u) << 16;
+  const std::uint32_t ex = (v >> 10) & 0x1fu, fr = v & 0x3ffu;
+  float out;
+  if (ex == 0) {
+    out = std::ldexp(static_cast<float>(fr), -24);  // zero / subnormal, exact
+    return sgn ? -out : out;
+  }
+  const std::uint32_t bits = ex == 0x1fu ? (sgn | 0x7f800000u | (fr << 13)) : (sgn | ((ex + 112u) << 23) | (fr << 13));
+  std::memcpy(&out, &bits, 4);
   return out;
+}
+}  // namespace detail
+
+class WavefieldBatch {
+ public:
+  WavefieldBatch() = default;
+  WavefieldBatch(RegularGrid grid, StoragePrecision precision) : grid_(std::move(grid)), precision_(precision) {}
+  // Compact16 quantisation runs on the GPU (hz_compact16)
+  void append(int source_id, const CField& u) {
+    if (static_cast<std::int64_t>(u.size()) != grid_.num_nodes())
+      throw ValidationError("wavefield batch: field size mismatch");
+    source_ids_.push_back(source_id);
+    if (precision_ == StoragePrecision::Full32) {
+      full_.push_back(u);
+      return;
+    }
+    const std::int64_t n = grid_.num_nodes();
+    Compact c;
+    c.re_im.resize(2 * static_cast<std::size_t>(n));
+    check(hz_compact16(n, 1, reinterpret_cast<const double*>(u.data()), c.re_im.data(), &c.scale));
+    compact_.push_back(std::move(c));
+  }
+  // k solved columns already quantised on the device (solve_helmholtz)
+  void append_compact(int source_id, double scale, std::vector<std::uint16_t> re_im) {
+    source_ids_.push_back(source_id);
+    compact_.push_back(Compact{scale, std::move(re_im)});
+  }
+  CField field(std::size_t idx) const {
+    if (idx >= source_ids_.size()) throw StateError("wavefield batch: no stored field at index");
+    if (precision_ == StoragePrecision::Full32) return full_[idx];
+    const Compact& c = compact_[idx];
+    CField u(c.re_im.size() / 2);
+    for (std::size_t i = 0; i < u.size(); ++i)
+      u[i] = cplx(detail::f16_to_f32(c.re_im[2 * i]) * c.scale, detail::f16_to_f32(c.re_im[2 * i + 1]) * c.scale);
+    return u;
+  }
+  int source_id(std::size_t idx) const { return source_ids_[idx]; }
+  std::size_t size() const { return source_ids_.size(); }
+  StoragePrecision precision() const { return precision_; }
+  const RegularGrid& grid() const { return grid_; }
+  // JSWF1: "JSWF1 <nsrc> <nnodes> <f32|f16>\n" + per-source little-endian (re, im)
+  void save(const std::string& path) const {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw IoError("cannot open for write: " + path);
+    const bool f32 = precision_ == StoragePrecision::Full32;
+    bool ok = std::fprintf(f, "JSWF1 %zu %lld %s\n", size(), static_cast<long long>(grid_.num_nodes()),
+                           f32 ? "f32" : "f16") > 0;
+    for (std::size_t a = 0; a < size() && ok; ++a) {
+      const CField u = field(a);
+      if (f32) {
+        std::vector<float> b(2 * u.size());
+        for (std::size_t i = 0; i < u.size(); ++i) {
+          b[2 * i] = static_cast<float>(u[i].real());
+          b[2 * i + 1] = static_cast<float>(u[i].imag());
+        }
+        ok = std::fwrite(b.data(), sizeof(float), b.size(), f) == b.size();
+      } else {
+        std::vector<std::uint16_t> b(2 * u.size());
+        for (std::size_t i = 0; i < u.size(); ++i) {
+          b[2 * i] = detail::f32_to_f16(static_cast<float>(u[i].real()));
+          b[2 * i + 1] = detail::f32_to_f16(static_cast<float>(u[i].imag()));
+        }
+        ok = std::fwrite(b.data(), sizeof(std::uint16_t), b.size(), f) == b.size();
+      }
+    }
+    ok = (std::fclose(f) == 0) && ok;
+    if (!ok) throw IoError("short write: " + path);
+  }
+  static WavefieldBatch load(const std::string& path, RegularGrid grid) {
+    std::FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) throw IoError("cannot open: " + path);
+    char magic[16] = {0}, tok[16] = {0};
+    std::size_t nsrc = 0;
+    long long nn = 0;
+    if (std::fscanf(f, "%15s %zu %lld %15s", magic, &nsrc, &nn, tok) != 4 || std::string(magic) != "JSWF1" ||
+        std::fgetc(f) != '\n') {
+      std::fclose(f);
+      throw IoError("bad JSWF1 header: " + path);
+    }
+    if (nn != grid.num_nodes()) {
+      std::fclose(f);
+      throw IoError("JSWF1 node count does not match grid: " + path);
+    }
+    const std::string t(tok);
+    if (t != "f16" && t != "f32") {
+      std::fclose(f);
+      throw IoError("bad JSWF1 precision token: " + path);
+    }
+    WavefieldBatch b(std::move(grid), StoragePrecision::Full32);
+    CField u(static_cast<std::size_t>(nn));
+    for (std::size_t a = 0; a < nsrc; ++a) {
+      if (t == "f16") {
+        std::vector<std::uint16_t> buf(2 * static_cast<std::size_t>(nn));
+        if (std::fread(buf.data(), 2, buf.size(), f) != buf.size()) {
+          std::fclose(f);
+          throw IoError("truncated JSWF1 payload: " + path);
+        }
+        for (long long i = 0; i < nn; ++i)
+          u[i] = cplx(detail::f16_to_f32(buf[2 * i]), detail::f16_to_f32(buf[2 * i + 1]));
+      } else {
+        std::vector<float> buf(2 * static_cast<std::size_t>(nn));
+        if (std::fread(buf.data(), 4, buf.size(), f) != buf.size()) {
+          std::fclose(f);
+          throw IoError("truncated JSWF1 payload: " + path);
+        }
+        for (long long i = 0; i < nn; ++i) u[i] = cplx(buf[2 * i], buf[2 * i + 1]);
+      }
+      b.append(static_cast<int>(a), u);
+    }
+    std::fclose(f);
+    return b;
+  }
+
+ private:
+  struct Compact {
+    double scale = 1.0;
+    std::vector<std::uint16_t> re_im;
+  };
+  RegularGrid grid_;
+  StoragePrecision precision_ = StoragePrecision::Full32;
+  std::vector<int> source_ids_;
+  std::vector<CField> full_;
+  std::vector<Compact> compact_;
+};
+
+// solve_helmholtz (src/helmholtz_solver.cpp:81-93): one block solve;
+// Compact16 batches are quantised on the GPU and only the 4-byte entries
+// come back to the host.
+inline WavefieldBatch solve_helmholtz(const HelmholtzSolver& solver, const std::vector<CField>& rhs,
+                                      StoragePrecision precision = StoragePrecision::Full32,
+                                      SolveReport* report = nullptr) {
+  const std::int64_t n = solver.problem().grid().num_nodes();
+  const int k = static_cast<int>(rhs.size());
+  BlockVec<cplx> B(n, k);
+  for (int a = 0; a < k; ++a) B.set_col(a, rhs[a]);
+  WavefieldBatch batch(solver.problem().grid(), precision);
+  if (precision == StoragePrecision::Full32) {
+    auto res = solver.solve_block(B);
+    if (!res.second.all_converged())
+      throw ConvergenceError("helmholtz solve: tolerance not met within cycle cap", res.second.history);
+    for (int a = 0; a < k; ++a) batch.append(a, res.first.col(a));
+    if (report) *report = res.second;
+    return batch;
+  }
+  std::vector<std::uint16_t> q(2 * static_cast<std::size_t>(n) * k);
+  std::vector<double> scales(k);
+  std::vector<int> cc(k), cv(k);
+  std::vector<double> rr(k), hist(static_cast<std::size_t>(solver.options().max_cycles) + 8);
+  hz_report r = detail::make_report(cc, rr, cv, hist);
+  const int st = hz_solve_helmholtz_compact16(solver.handle(), n, k, reinterpret_cast<const double*>(B.a.data()),
+                                              q.data(), scales.data(), &r);
+  hist.resize(std::min<std::size_t>(hist.size(), static_cast<std::size_t>(r.history_len)));
+  check(st, hist);
+  for (int a = 0; a < k; ++a)
+    batch.append_compact(a, scales[a], std::vector<std::uint16_t>(q.begin() + 2 * n * a, q.begin() + 2 * n * (a + 1)));
+  if (report) {
+    report->cycles = r.cycles;
+    report->col_cycles = cc;
+    report->rel_residual = rr;
+    report->converged.assign(cv.begin(), cv.end());
+    report->history = hist;
+    report->wall_s = r.wall_s;
+    report->qr_factorizations = r.qr_factorizations;
+    report->block_gram_products = r.block_gram_products;
+  }
+  return batch;
 }
 
 }  // namespace hzb

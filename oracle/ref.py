@@ -303,3 +303,89 @@ def attenuation_ramp(ndim, n, lo, hi) -> np.ndarray:
     out = np.empty(int(np.prod(nn)), dtype=np.float64)
     _check(lib().ref_attenuation_ramp(C.c_int(ndim), _p(nn), _p(lo_), _p(hi_), _p(out)))
     return out
+
+
+# ---- FWI path either side of the solve
+class RefSampling:
+    """seistomo::SamplingOperator over receivers at physical points
+    (inc/acquisition.hpp:30-62, src/acquisition.cpp:33-62)."""
+
+    def __init__(self, ndim, n, h, receivers_xyz, origin=(0.0, 0.0, 0.0)):
+        nn = np.asarray(list(n) + [1] * (3 - len(n)), dtype=np.int64)
+        hh = np.asarray(list(h) + [1.0] * (3 - len(h)), dtype=np.float64)
+        oo = np.asarray(list(origin) + [0.0] * (3 - len(origin)), dtype=np.float64)
+        xyz = np.ascontiguousarray(receivers_xyz, dtype=np.float64).reshape(-1, 3)
+        self.nrec = xyz.shape[0]
+        self.n = int(nn.prod())
+        out = C.c_void_p()
+        _check(lib().ref_sampling_create(C.c_int(ndim), _p(nn), _p(hh), _p(oo), C.c_longlong(self.nrec),
+                                         _p(xyz), C.byref(out)))
+        self._h = out
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ref_sampling_destroy(self._h)
+            self._h = None
+
+    def receiver(self, r):
+        nodes = np.zeros(8, np.int64)
+        w = np.zeros(8, np.float64)
+        c = lib().ref_sampling_receiver(self._h, C.c_longlong(r), _p(nodes), _p(w))
+        return nodes[:c].copy(), w[:c].copy()
+
+    def sample(self, u):
+        u = np.ascontiguousarray(u, dtype=np.complex128).reshape(-1)
+        d = np.empty(self.nrec, np.complex128)
+        _check(lib().ref_sample(self._h, _p(u), _p(d)))
+        return d
+
+    def sample_adjoint(self, d):
+        d = np.ascontiguousarray(d, dtype=np.complex128).reshape(-1)
+        u = np.empty(self.n, np.complex128)
+        _check(lib().ref_sample_adjoint(self._h, _p(d), _p(u)))
+        return u
+
+
+def fwi_sensitivity_rhs(problem: RefProblem, u, v):
+    u = np.ascontiguousarray(u, dtype=np.complex128).reshape(-1)
+    v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
+    out = np.empty_like(u)
+    _check(lib().ref_fwi_sensitivity_rhs(problem._h, _p(u), _p(v), _p(out)))
+    return out
+
+
+def fwi_jacobian_vec(solver: RefSolver, u, sampling: RefSampling, v):
+    u = np.ascontiguousarray(u, dtype=np.complex128).reshape(-1)
+    v = np.ascontiguousarray(v, dtype=np.float64).reshape(-1)
+    d = np.empty(sampling.nrec, np.complex128)
+    _check(lib().ref_fwi_jacobian_vec(solver._h, sampling._h, _p(u), _p(v), _p(d)))
+    return d
+
+
+def fwi_jacobian_transpose_vec(solver: RefSolver, u, sampling: RefSampling, w):
+    u = np.ascontiguousarray(u, dtype=np.complex128).reshape(-1)
+    w = np.ascontiguousarray(w, dtype=np.complex128).reshape(-1)
+    g = np.empty(u.size, np.float64)
+    _check(lib().ref_fwi_jacobian_transpose_vec(solver._h, sampling._h, _p(u), _p(w), _p(g)))
+    return g
+
+
+# ---- wavefield output (SURVEY §8f.3)
+def wavefield_roundtrip(fields, dims2d, compact: bool, path: str = ""):
+    """WavefieldBatch append (Full32 / Compact16) -> field(s); optional JSWF1
+    save (src/helmholtz.cpp:137-195). fields: [nsrc][n] complex."""
+    F = np.ascontiguousarray(fields, dtype=np.complex128)
+    nsrc, n = F.shape
+    out = np.empty_like(F)
+    _check(lib().ref_wavefield_roundtrip(C.c_longlong(dims2d[0]), C.c_longlong(dims2d[1]), C.c_int(nsrc), _p(F),
+                                         C.c_int(1 if compact else 0), _p(out), path.encode()))
+    return out
+
+
+def wavefield_load(path: str, dims2d, max_src: int):
+    n = dims2d[0] * dims2d[1]
+    out = np.zeros((max_src, n), np.complex128)
+    ns = C.c_int(0)
+    _check(lib().ref_wavefield_load(path.encode(), C.c_longlong(dims2d[0]), C.c_longlong(dims2d[1]),
+                                    C.c_int(max_src), _p(out), C.byref(ns)))
+    return out[:ns.value]

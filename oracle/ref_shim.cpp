@@ -18,6 +18,7 @@
 #include <string>
 #include <vector>
 
+#include "seistomo/acquisition.hpp"
 #include "seistomo/attenuation.hpp"
 #include "seistomo/errors.hpp"
 #include "seistomo/grid.hpp"
@@ -381,6 +382,142 @@ int ref_attenuation_ramp(int ndim, const long long* n, const int* lo, const int*
     }
     AttenuationField f = assemble_attenuation(g, 0.0, w);
     std::memcpy(ramp, f.ramp.data(), sizeof(double) * f.ramp.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// ---- FWI path either side of the solve
+// SamplingOperator(AcquisitionGeometry, grid) (src/acquisition.cpp:10-62):
+// receivers only (no sources), full offset range.
+int ref_sampling_create(int ndim, const long long* n, const double* h, const double* origin, long long nrec,
+                        const double* xyz, void** out) {
+  try {
+    RegularGrid g(ndim, {n[0], n[1], n[2]}, {h[0], h[1], h[2]}, {origin[0], origin[1], origin[2]});
+    std::vector<std::array<double, 3>> rec(nrec);
+    for (long long r = 0; r < nrec; ++r) rec[r] = {xyz[3 * r], xyz[3 * r + 1], xyz[3 * r + 2]};
+    AcquisitionGeometry geom({}, rec, 0.0, 1e300, g);
+    *out = new SamplingOperator(geom, g);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+void ref_sampling_destroy(void* s) { delete static_cast<SamplingOperator*>(s); }
+int ref_sampling_receiver(void* s, long long r, long long* nodes, double* w) {
+  const auto* P = static_cast<SamplingOperator*>(s);
+  const auto& nd = P->receiver_nodes(r);
+  const auto& ww = P->receiver_weights(r);
+  for (size_t q = 0; q < nd.size(); ++q) {
+    nodes[q] = nd[q];
+    w[q] = ww[q];
+  }
+  return int(nd.size());
+}
+// SamplingOperator::sample / sample_adjoint (inc/acquisition.hpp:40-61), one field
+int ref_sample(void* s, const double* u, double* d) {
+  try {
+    const auto* P = static_cast<SamplingOperator*>(s);
+    const std::int64_t n = P->grid().num_nodes();
+    CField U(reinterpret_cast<const cplx*>(u), reinterpret_cast<const cplx*>(u) + n);
+    auto D = P->sample(U);
+    std::memcpy(d, D.data(), sizeof(cplx) * D.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+int ref_sample_adjoint(void* s, const double* d, double* u) {
+  try {
+    const auto* P = static_cast<SamplingOperator*>(s);
+    std::vector<cplx> D(reinterpret_cast<const cplx*>(d), reinterpret_cast<const cplx*>(d) + P->num_receivers());
+    auto U = P->sample_adjoint(D);
+    std::memcpy(u, U.data(), sizeof(cplx) * U.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+// fwi_sensitivity_rhs (src/helmholtz_solver.cpp:95-101)
+int ref_fwi_sensitivity_rhs(void* p, const double* u, const double* v, double* rhs) {
+  try {
+    const HelmholtzProblem& prob = *static_cast<RefProblem*>(p)->p;
+    const std::int64_t n = prob.grid().num_nodes();
+    CField U(reinterpret_cast<const cplx*>(u), reinterpret_cast<const cplx*>(u) + n);
+    Field V(v, v + n);
+    CField R = fwi_sensitivity_rhs(prob, U, V);
+    std::memcpy(rhs, R.data(), sizeof(cplx) * n);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+// fwi_jacobian_vec / fwi_jacobian_transpose_vec (src/helmholtz_solver.cpp:113-139)
+int ref_fwi_jacobian_vec(void* solver, void* sampling, const double* u, const double* v, double* d) {
+  try {
+    const HelmholtzSolver& S = *static_cast<RefSolver*>(solver)->s;
+    const auto* P = static_cast<SamplingOperator*>(sampling);
+    const std::int64_t n = S.problem().grid().num_nodes();
+    CField U(reinterpret_cast<const cplx*>(u), reinterpret_cast<const cplx*>(u) + n);
+    Field V(v, v + n);
+    auto D = fwi_jacobian_vec(S, U, *P, V);
+    std::memcpy(d, D.data(), sizeof(cplx) * D.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+int ref_fwi_jacobian_transpose_vec(void* solver, void* sampling, const double* u, const double* w, double* g) {
+  try {
+    const HelmholtzSolver& S = *static_cast<RefSolver*>(solver)->s;
+    const auto* P = static_cast<SamplingOperator*>(sampling);
+    const std::int64_t n = S.problem().grid().num_nodes();
+    CField U(reinterpret_cast<const cplx*>(u), reinterpret_cast<const cplx*>(u) + n);
+    std::vector<cplx> W(reinterpret_cast<const cplx*>(w), reinterpret_cast<const cplx*>(w) + P->num_receivers());
+    Field G = fwi_jacobian_transpose_vec(S, U, *P, W);
+    std::memcpy(g, G.data(), sizeof(double) * n);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// ---- wavefield output: WavefieldBatch (src/helmholtz.cpp:137-233)
+// fields[s] (n0 x n1 2D grid) -> append (Full32 or Compact16) -> field(s)
+// into out[s][n];
+// optionally save(path) as JSWF1.
+int ref_wavefield_roundtrip(long long n0, long long n1, int nsrc, const double* fields, int compact, double* out,
+                            const char* path) {
+  try {
+    RegularGrid g(2, {n0, n1, 1}, {1.0, 1.0, 1.0});
+    const long long n = n0 * n1;
+    WavefieldBatch b(g, compact ? StoragePrecision::Compact16 : StoragePrecision::Full32);
+    for (int s = 0; s < nsrc; ++s) {
+      const cplx* f = reinterpret_cast<const cplx*>(fields) + size_t(s) * n;
+      b.append(s, CField(f, f + n));
+    }
+    for (int s = 0; s < nsrc; ++s) {
+      CField u = b.field(s);
+      std::memcpy(out + 2 * size_t(s) * n, u.data(), sizeof(cplx) * n);
+    }
+    if (path && path[0]) b.save(path);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+// WavefieldBatch::load (src/helmholtz.cpp:197-233) -> out[s][n]
+int ref_wavefield_load(const char* path, long long n0, long long n1, int max_src, double* out, int* nsrc) {
+  try {
+    RegularGrid g(2, {n0, n1, 1}, {1.0, 1.0, 1.0});
+    const long long n = n0 * n1;
+    WavefieldBatch b = WavefieldBatch::load(path, g);
+    *nsrc = int(b.size());
+    for (int s = 0; s < int(b.size()) && s < max_src; ++s) {
+      CField u = b.field(s);
+      std::memcpy(out + 2 * size_t(s) * n, u.data(), sizeof(cplx) * n);
+    }
     return 0;
   } catch (...) {
     return map_exception();

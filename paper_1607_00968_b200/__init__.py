@@ -29,7 +29,9 @@ __all__ = [
     "ValidationError", "ConvergenceError", "BreakdownError", "FactorizationError", "StateError",
     "IoError", "CudaError", "NcclError", "AttenuationField", "HelmholtzProblem",
     "HelmholtzSolveOptions", "CycleSpec", "HelmholtzSolver", "SolveReport", "solve_helmholtz",
-    "fwi_sensitivity_output", "kernel_launch_count", "device_count",
+    "fwi_sensitivity_output", "kernel_launch_count", "device_count", "SamplingOperator",
+    "fwi_sensitivity_rhs", "fwi_jacobian_vec", "fwi_jacobian_transpose_vec", "WavefieldBatch", "Full32",
+    "Compact16", "compact16",
 ]
 
 
@@ -469,19 +471,6 @@ class HelmholtzSolver:
         return x
 
 
-def solve_helmholtz(solver: HelmholtzSolver, rhs: List[np.ndarray], report: Optional[list] = None):
-    """solve_helmholtz (src/helmholtz_solver.cpp:81-93): one block solve,
-    ConvergenceError (with the residual history) if any column misses tol.
-    Returns the [n][k] solution block (Full storage)."""
-    B = np.stack([np.asarray(q, dtype=np.complex128).reshape(-1) for q in rhs], axis=1)
-    X, rep = solver.solve_block(B)
-    if not rep.all_converged():
-        raise ConvergenceError("helmholtz solve: tolerance not met within cycle cap", rep.history)
-    if report is not None:
-        report.append(rep)
-    return X
-
-
 def fwi_sensitivity_output(problem: HelmholtzProblem, U, L, g=None):
     """sum_s fwi_sensitivity_output(problem, u_s, lambda_s)
     (src/helmholtz_solver.cpp:103-111): g[i] = sum_s Re(-w^2 (1 - i gamma/w) u_s lambda_s).
@@ -507,3 +496,8 @@ def fwi_sensitivity_output(problem: HelmholtzProblem, U, L, g=None):
     _check(_native.lib().hz_sensitivity_accumulate(problem._h, n, U.shape[1], U.ctypes.data, L.ctypes.data,
                                                    g.ctypes.data, 1 if acc else 0))
     return g
+
+
+# FWI path either side of the solve and wavefield output
+from .fwi import (Compact16, Full32, SamplingOperator, WavefieldBatch, compact16,  # noqa: E402
+                  fwi_jacobian_transpose_vec, fwi_jacobian_vec, fwi_sensitivity_rhs, solve_helmholtz)

@@ -22,6 +22,11 @@ EXPORTS = (
     "hz_hierarchy_level_dims", "hz_hierarchy_level_coefficients", "hz_sensitivity_accumulate",
     "hz_sensitivity_accumulate_device", "hz_kernel_launch_count", "hz_profile_begin",
     "hz_profile_end", "hz_profile_report", "hz_solver_set_slabs", "hz_solver_slab_info",
+    "hz_sampling_create", "hz_sampling_destroy", "hz_sampling_num_receivers", "hz_sampling_receiver",
+    "hz_sample_device", "hz_sample", "hz_sample_adjoint_device", "hz_sample_adjoint",
+    "hz_fwi_sensitivity_rhs_device", "hz_fwi_jacobian_vec", "hz_fwi_jacobian_vec_device",
+    "hz_fwi_jacobian_transpose_vec", "hz_fwi_jacobian_transpose_vec_device", "hz_compact16_device",
+    "hz_solve_helmholtz_compact16", "hz_compact16",
 )
 
 
@@ -81,6 +86,24 @@ def lib():
         L.hz_options_default.argtypes = [C.POINTER(hz_options)]
         L.hz_solver_set_slabs.argtypes = [vp, i32, vp]
         L.hz_solver_slab_info.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), vp, i32]
+        L.hz_sampling_create.argtypes = [vp, vp, i64, vp, C.POINTER(vp)]
+        L.hz_sampling_destroy.argtypes = [vp]
+        L.hz_sampling_num_receivers.restype = i64
+        L.hz_sampling_num_receivers.argtypes = [vp]
+        L.hz_sampling_receiver.argtypes = [vp, i64, vp, vp, C.POINTER(i32)]
+        L.hz_sample_device.argtypes = [vp, i32, vp, vp, vp]
+        L.hz_sample.argtypes = [vp, i32, vp, vp]
+        L.hz_sample_adjoint_device.argtypes = [vp, i32, vp, vp, i32, vp]
+        L.hz_sample_adjoint.argtypes = [vp, i32, vp, vp, i32]
+        L.hz_fwi_sensitivity_rhs_device.argtypes = [vp, i64, i32, vp, vp, vp, vp]
+        L.hz_fwi_jacobian_vec.argtypes = [vp, vp, i64, i32, vp, vp, vp, C.POINTER(hz_report)]
+        L.hz_fwi_jacobian_vec_device.argtypes = [vp, vp, i64, i32, vp, vp, vp, C.POINTER(hz_report)]
+        L.hz_fwi_jacobian_transpose_vec.argtypes = [vp, vp, i64, i32, vp, vp, vp, i32, C.POINTER(hz_report)]
+        L.hz_fwi_jacobian_transpose_vec_device.argtypes = [vp, vp, i64, i32, vp, vp, vp, i32,
+                                                           C.POINTER(hz_report)]
+        L.hz_compact16_device.argtypes = [i64, i32, vp, vp, vp, vp]
+        L.hz_compact16.argtypes = [i64, i32, vp, vp, vp]
+        L.hz_solve_helmholtz_compact16.argtypes = [vp, i64, i32, vp, vp, vp, C.POINTER(hz_report)]
         _lib = L
     return _lib
 

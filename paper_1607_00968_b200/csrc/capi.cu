@@ -8,6 +8,7 @@
 #include <string>
 
 #include "../../include/hz_b200.h"
+#include "acquisition.hpp"
 #include "solver.hpp"
 
 #include <map>
@@ -60,6 +61,10 @@ struct hz_problem {
   std::shared_ptr<Problem> p;
 };
 
+struct hz_sampling {
+  std::unique_ptr<Sampling> s;
+};
+
 struct hz_solver {
   std::shared_ptr<Problem> prob;
   hz_options opts{};
@@ -81,6 +86,10 @@ struct hz_solver {
   std::map<int, std::unique_ptr<Hierarchy<double>>> rep64;
   std::map<int, std::unique_ptr<Hierarchy<float>>> rep32;
   std::map<int, DevBuf<double2>> center_rep;
+  // FWI / wavefield-output scratch (grow-only)
+  DevBuf<double2> fU, fR, fX, fD;
+  DevBuf<double> fv, fpart, fmax;
+  DevBuf<uint32_t> fQ;
   int span_k = 0;  // k the spanning dB/dX/b32/x32 are laid out for
   const double2* center_on(int device) const {
     if (device == prob->device) return prob->d_center.get();
@@ -732,6 +741,282 @@ int hz_sensitivity_accumulate(hz_problem* p, int64_t n, int k, const double* U, 
     launch_sensitivity(n, k, p->p->omega * p->p->omega, p->p->d_gf.get(), du.get(), dl.get(),
                        dg_.get(), accumulate, nullptr);
     HZ_CUDA(cudaMemcpy(g, dg_.get(), n * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+// ---------------------------------------------------------------- FWI path
+int hz_sampling_create(const hz_problem* p, const double origin[3], int64_t nrec, const double* xyz,
+                       hz_sampling** out) {
+  return guarded([&] {
+    if (!p || !out || (nrec > 0 && !xyz)) throw HzError(kValidation, "hz_sampling_create: null argument");
+    const Problem& P = *p->p;
+    const double zero[3] = {0, 0, 0};
+    auto* hs = new hz_sampling;
+    try {
+      hs->s = std::make_unique<Sampling>(P.ndim, P.n.data(), P.h.data(), origin ? origin : zero, nrec, xyz,
+                                         P.device);
+    } catch (...) {
+      delete hs;
+      throw;
+    }
+    *out = hs;
+  });
+}
+
+int hz_sampling_destroy(hz_sampling* s) {
+  return guarded([&] {
+    if (s) {
+      DeviceGuard dg(s->s->device);
+      delete s;
+    }
+  });
+}
+
+int64_t hz_sampling_num_receivers(const hz_sampling* s) { return s ? s->s->nrec : 0; }
+
+int hz_sampling_receiver(const hz_sampling* s, int64_t r, int64_t nodes[8], double weights[8], int* count) {
+  return guarded([&] {
+    if (!s || !nodes || !weights || !count) throw HzError(kValidation, "null argument");
+    const Sampling& S = *s->s;
+    if (r < 0 || r >= S.nrec) throw HzError(kValidation, "receiver index out of range");
+    *count = int(S.rp[r + 1] - S.rp[r]);
+    for (int q = 0; q < *count; ++q) {
+      nodes[q] = S.nodes[S.rp[r] + q];
+      weights[q] = S.w[S.rp[r] + q];
+    }
+  });
+}
+
+int hz_sample_device(hz_sampling* s, int k, const void* U, void* D, void* stream) {
+  return guarded([&] {
+    if (!s || !U || (!D && s->s->nrec)) throw HzError(kValidation, "null argument");
+    if (k < 1) throw HzError(kValidation, "sample: k must be >= 1");
+    DeviceGuard dg(s->s->device);
+    launch_sample(*s->s, k, static_cast<const double2*>(U), static_cast<double2*>(D),
+                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hz_sample_adjoint_device(hz_sampling* s, int k, const void* D, void* U, int conj, void* stream) {
+  return guarded([&] {
+    if (!s || !U || (!D && s->s->nrec)) throw HzError(kValidation, "null argument");
+    if (k < 1) throw HzError(kValidation, "sample_adjoint: k must be >= 1");
+    DeviceGuard dg(s->s->device);
+    launch_sample_adjoint(*s->s, k, static_cast<const double2*>(D), static_cast<double2*>(U), conj != 0,
+                          static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hz_sample(hz_sampling* s, int k, const double* U, double* D) {
+  return guarded([&] {
+    if (!s || !U || (!D && s->s->nrec)) throw HzError(kValidation, "null argument");
+    if (k < 1) throw HzError(kValidation, "sample: k must be >= 1");
+    const Sampling& S = *s->s;
+    DeviceGuard dg(S.device);
+    DevBuf<double2> du(size_t(S.n) * k), dd(std::max<size_t>(size_t(S.nrec) * k, 1));
+    HZ_CUDA(cudaMemcpy(du.get(), U, du.bytes(), cudaMemcpyHostToDevice));
+    launch_sample(S, k, du.get(), dd.get(), nullptr);
+    if (S.nrec) HZ_CUDA(cudaMemcpy(D, dd.get(), sizeof(double2) * S.nrec * k, cudaMemcpyDeviceToHost));
+  });
+}
+
+int hz_sample_adjoint(hz_sampling* s, int k, const double* D, double* U, int conj) {
+  return guarded([&] {
+    if (!s || !U || (!D && s->s->nrec)) throw HzError(kValidation, "null argument");
+    if (k < 1) throw HzError(kValidation, "sample_adjoint: k must be >= 1");
+    const Sampling& S = *s->s;
+    DeviceGuard dg(S.device);
+    DevBuf<double2> du(size_t(S.n) * k), dd(std::max<size_t>(size_t(S.nrec) * k, 1));
+    if (S.nrec) HZ_CUDA(cudaMemcpy(dd.get(), D, sizeof(double2) * S.nrec * k, cudaMemcpyHostToDevice));
+    launch_sample_adjoint(S, k, dd.get(), du.get(), conj != 0, nullptr);
+    HZ_CUDA(cudaMemcpy(U, du.get(), du.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+int hz_fwi_sensitivity_rhs_device(hz_problem* p, int64_t n, int k, const void* U, const void* v, void* R,
+                                  void* stream) {
+  return guarded([&] {
+    if (!p || !U || !v || !R) throw HzError(kValidation, "null argument");
+    check_block(*p->p, n, k);
+    DeviceGuard dg(p->p->device);
+    launch_sens_rhs(n, k, p->p->omega * p->p->omega, p->p->d_gf.get(), static_cast<const double2*>(U),
+                    static_cast<const double*>(v), static_cast<double2*>(R), static_cast<cudaStream_t>(stream));
+  });
+}
+
+namespace {
+void require_converged(const Report& r, const char* what) {
+  for (char c : r.converged)
+    if (!c) throw HzError(kConvergence, what);
+}
+// fwi_jacobian_vec (src/helmholtz_solver.cpp:113-125) for k stored fields at
+// once: D = P^T A^{-1} (-w^2 gf U v), one block solve
+void jacobian_vec(hz_solver* s, hz_sampling* smp, int k, const double2* U, const double* v, double2* D,
+                  Report& rep) {
+  const Problem& P = *s->prob;
+  const int64_t n = P.num_nodes();
+  s->fR.ensure(size_t(n) * k);
+  s->fX.ensure(size_t(n) * k);
+  launch_sens_rhs(n, k, P.omega * P.omega, P.d_gf.get(), U, v, s->fR.get(), s->stream);
+  rep = run_solve(s, k, s->fR.get(), s->fX.get());
+  launch_sample(*smp->s, k, s->fX.get(), D, s->stream);
+}
+// fwi_jacobian_transpose_vec (src/helmholtz_solver.cpp:127-139) for k
+// sources: g (+)= sum_s Re(-w^2 gf u_s lambda_s), lambda = A^{-1} P conj(w_s)
+void jacobian_transpose_vec(hz_solver* s, hz_sampling* smp, int k, const double2* U, const double2* W, double* g,
+                            int accumulate, Report& rep) {
+  const Problem& P = *s->prob;
+  const int64_t n = P.num_nodes();
+  s->fR.ensure(size_t(n) * k);
+  s->fX.ensure(size_t(n) * k);
+  launch_sample_adjoint(*smp->s, k, W, s->fR.get(), true, s->stream);
+  rep = run_solve(s, k, s->fR.get(), s->fX.get());
+  launch_sensitivity(n, k, P.omega * P.omega, P.d_gf.get(), U, s->fX.get(), g, accumulate, s->stream);
+}
+void check_fwi(hz_solver* s, hz_sampling* smp, int64_t n, int k) {
+  if (!s || !smp) throw HzError(kValidation, "null argument");
+  if (s->slabs) throw HzError(kState, "FWI block functions run on a single-domain solver");
+  check_block(*s->prob, n, k);
+  if (smp->s->n != n) throw HzError(kValidation, "sampling operator does not match the grid");
+  if (smp->s->device != s->prob->device) throw HzError(kValidation, "sampling operator on another GPU");
+}
+}  // namespace
+
+int hz_fwi_jacobian_vec_device(hz_solver* s, hz_sampling* smp, int64_t n, int k, const void* U, const void* v,
+                               void* D, hz_report* rep) {
+  return guarded([&] {
+    check_fwi(s, smp, n, k);
+    if (!U || !v || (!D && smp->s->nrec)) throw HzError(kValidation, "null argument");
+    DeviceGuard dg(s->prob->device);
+    Report r;
+    jacobian_vec(s, smp, k, static_cast<const double2*>(U), static_cast<const double*>(v),
+                 static_cast<double2*>(D), r);
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+    require_converged(r, "fwi_jacobian_vec: sensitivity solve did not converge");
+  });
+}
+
+int hz_fwi_jacobian_vec(hz_solver* s, hz_sampling* smp, int64_t n, int k, const double* U, const double* v,
+                        double* D, hz_report* rep) {
+  return guarded([&] {
+    check_fwi(s, smp, n, k);
+    if (!U || !v || (!D && smp->s->nrec)) throw HzError(kValidation, "null argument");
+    DeviceGuard dg(s->prob->device);
+    const int64_t nr = smp->s->nrec;
+    s->fU.ensure(size_t(n) * k);
+    s->fv.ensure(size_t(n));
+    s->fD.ensure(std::max<size_t>(size_t(nr) * k, 1));
+    HZ_CUDA(cudaMemcpyAsync(s->fU.get(), U, sizeof(double2) * n * k, cudaMemcpyHostToDevice, s->stream));
+    HZ_CUDA(cudaMemcpyAsync(s->fv.get(), v, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    Report r;
+    jacobian_vec(s, smp, k, s->fU.get(), s->fv.get(), s->fD.get(), r);
+    if (nr) HZ_CUDA(cudaMemcpyAsync(D, s->fD.get(), sizeof(double2) * nr * k, cudaMemcpyDeviceToHost, s->stream));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+    require_converged(r, "fwi_jacobian_vec: sensitivity solve did not converge");
+  });
+}
+
+int hz_fwi_jacobian_transpose_vec_device(hz_solver* s, hz_sampling* smp, int64_t n, int k, const void* U,
+                                         const void* W, double* g, int accumulate, hz_report* rep) {
+  return guarded([&] {
+    check_fwi(s, smp, n, k);
+    if (!U || !g || (!W && smp->s->nrec)) throw HzError(kValidation, "null argument");
+    DeviceGuard dg(s->prob->device);
+    Report r;
+    jacobian_transpose_vec(s, smp, k, static_cast<const double2*>(U), static_cast<const double2*>(W), g,
+                           accumulate, r);
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+    require_converged(r, "fwi_jacobian_transpose_vec: adjoint solve did not converge");
+  });
+}
+
+int hz_fwi_jacobian_transpose_vec(hz_solver* s, hz_sampling* smp, int64_t n, int k, const double* U,
+                                  const double* W, double* g, int accumulate, hz_report* rep) {
+  return guarded([&] {
+    check_fwi(s, smp, n, k);
+    if (!U || !g || (!W && smp->s->nrec)) throw HzError(kValidation, "null argument");
+    DeviceGuard dg(s->prob->device);
+    const int64_t nr = smp->s->nrec;
+    s->fU.ensure(size_t(n) * k);
+    s->fD.ensure(std::max<size_t>(size_t(nr) * k, 1));
+    s->fv.ensure(size_t(n));
+    HZ_CUDA(cudaMemcpyAsync(s->fU.get(), U, sizeof(double2) * n * k, cudaMemcpyHostToDevice, s->stream));
+    if (nr) HZ_CUDA(cudaMemcpyAsync(s->fD.get(), W, sizeof(double2) * nr * k, cudaMemcpyHostToDevice, s->stream));
+    if (accumulate) HZ_CUDA(cudaMemcpyAsync(s->fv.get(), g, sizeof(double) * n, cudaMemcpyHostToDevice, s->stream));
+    Report r;
+    jacobian_transpose_vec(s, smp, k, s->fU.get(), s->fD.get(), s->fv.get(), accumulate, r);
+    HZ_CUDA(cudaMemcpyAsync(g, s->fv.get(), sizeof(double) * n, cudaMemcpyDeviceToHost, s->stream));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+    require_converged(r, "fwi_jacobian_transpose_vec: adjoint solve did not converge");
+  });
+}
+
+// ---------------------------------------------------------------- Compact16
+namespace {
+// WavefieldBatch::append Compact16 (src/helmholtz.cpp:143-151) for k
+// columns: scale_c = 2^ceil(log2(peak_c)) (1 when the column is zero)
+void compact16(int64_t n, int k, const double2* X, uint32_t* Q, double* scales, DevBuf<double>& part,
+               DevBuf<double>& mx, cudaStream_t st) {
+  const int nslots = int(std::min<int64_t>(4 * kNumSMs, std::max<int64_t>(1, n / 1024)));
+  part.ensure(size_t(nslots) * k);
+  mx.ensure(2 * size_t(k));
+  launch_colmax(n, k, X, part.get(), nslots, mx.get(), st);
+  std::vector<double> peak(k), inv(k);
+  HZ_CUDA(cudaMemcpyAsync(peak.data(), mx.get(), sizeof(double) * k, cudaMemcpyDeviceToHost, st));
+  HZ_CUDA(cudaStreamSynchronize(st));
+  for (int c = 0; c < k; ++c) {
+    scales[c] = peak[c] > 0.0 ? std::exp2(std::ceil(std::log2(peak[c]))) : 1.0;
+    inv[c] = 1.0 / scales[c];  // exact: scales are powers of two
+  }
+  HZ_CUDA(cudaMemcpyAsync(mx.get() + k, inv.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st));
+  launch_quantize16(n, k, X, mx.get() + k, Q, st);
+  HZ_CUDA(cudaStreamSynchronize(st));  // inv lives on this stack frame
+}
+}  // namespace
+
+int hz_compact16_device(int64_t n, int k, const void* X, void* Q, double* scales, void* stream) {
+  return guarded([&] {
+    if (!X || !Q || !scales) throw HzError(kValidation, "null argument");
+    if (n < 1 || k < 1) throw HzError(kValidation, "compact16: empty block");
+    DevBuf<double> part, mx;
+    compact16(n, k, static_cast<const double2*>(X), static_cast<uint32_t*>(Q), scales, part, mx,
+              static_cast<cudaStream_t>(stream));
+  });
+}
+
+int hz_compact16(int64_t n, int k, const double* X, uint16_t* Q, double* scales) {
+  return guarded([&] {
+    if (!X || !Q || !scales) throw HzError(kValidation, "null argument");
+    if (n < 1 || k < 1) throw HzError(kValidation, "compact16: empty block");
+    require_device();
+    DevBuf<double2> dx(size_t(n) * k);
+    DevBuf<uint32_t> dq(size_t(n) * k);
+    DevBuf<double> part, mx;
+    HZ_CUDA(cudaMemcpy(dx.get(), X, dx.bytes(), cudaMemcpyHostToDevice));
+    compact16(n, k, dx.get(), dq.get(), scales, part, mx, nullptr);
+    HZ_CUDA(cudaMemcpy(Q, dq.get(), dq.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+int hz_solve_helmholtz_compact16(hz_solver* s, int64_t n, int k, const double* B, uint16_t* Q, double* scales,
+                                 hz_report* rep) {
+  return guarded([&] {
+    if (!s || !B || !Q || !scales) throw HzError(kValidation, "null argument");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    s->ensure_blocks(k);
+    upload_rows(s, k, B, s->dB.get());
+    Report r = run_solve(s, k, s->dB.get(), s->dX.get());
+    if (s->slabs) s->slabs->join();
+    fill_report(r, k, rep);
+    require_converged(r, "helmholtz solve: tolerance not met within cycle cap");
+    s->fQ.ensure(size_t(n) * k);
+    compact16(n, k, s->dX.get(), s->fQ.get(), scales, s->fpart, s->fmax, s->stream);
+    HZ_CUDA(cudaMemcpy(Q, s->fQ.get(), sizeof(uint32_t) * n * k, cudaMemcpyDeviceToHost));
   });
 }
 
