@@ -57,44 +57,50 @@ class GradientResult:
     adjoint_cycles: int
 
 
-def fwi_gradient(problem, solver, source_nodes: Sequence[int], receiver_nodes: np.ndarray,
+def fwi_gradient(problem, solver, source_nodes: Sequence[int], receivers,
                  d_obs_fn: Callable[[np.ndarray], np.ndarray], rank: int = 0, world: int = 1,
                  device: Optional[str] = None) -> GradientResult:
     """Sharded FWI gradient for one frequency.
 
-    Rank `rank` solves the forward block U = A^{-1} Q for its sources, forms
-    the adjoint right-hand sides P conj(P^T u_s - d_s) (receivers at grid
-    nodes: P is the node restriction, the multilinear SamplingOperator of
-    inc/acquisition.hpp:40-62 with unit weights), solves the adjoint block
-    with the same hierarchy (A is complex symmetric,
-    inc/helmholtz_solver.hpp:26-29), accumulates the gradient on the device
-    (hz_sensitivity_accumulate_device) and all-reduces gradient and misfit.
-    d_obs_fn(local_source_ids) -> [n_rec, k_local] complex observed data.
+    Rank `rank` solves the forward block U = A^{-1} Q for its sources, samples
+    the receivers (SamplingOperator::sample, inc/acquisition.hpp:40-51), forms
+    the residuals r_s = P^T u_s - d_s and accumulates sum_s J_s^T r_s with ONE
+    adjoint block solve (fwi_jacobian_transpose_vec,
+    src/helmholtz_solver.cpp:127-139: lambda = A^{-1} P conj(r),
+    g += Re(-w^2 (1 - i gamma/w) u lambda)), then all-reduces gradient and
+    misfit. `receivers` is a SamplingOperator or an array of receiver grid
+    nodes (unit weights). d_obs_fn(local_source_ids) -> [n_rec, k_local]
+    complex observed data.
     """
     import torch
-    from . import fwi_sensitivity_output
+    from . import SamplingOperator, fwi_jacobian_transpose_vec
 
     dev = device or f"cuda:{problem.device}"
+    if isinstance(receivers, SamplingOperator):
+        Ps = receivers
+    else:
+        nodes = np.asarray(receivers, dtype=np.int64)
+        n0, n1 = problem.n[0], problem.n[1]
+        xyz = np.stack([(nodes % n0) * problem.h[0], ((nodes // n0) % n1) * problem.h[1],
+                        (nodes // (n0 * n1)) * problem.h[2]], axis=1).astype(np.float64)
+        Ps = SamplingOperator(problem, xyz)
     mine = shard_sources(len(source_nodes), rank, world)
-    nodes = np.asarray(source_nodes, dtype=np.int64)[mine]
+    src = np.asarray(source_nodes, dtype=np.int64)[mine]
     n = problem.num_nodes
-    k = len(nodes)
+    k = len(src)
     g = torch.zeros(n, dtype=torch.float64, device=dev)
     misfit = torch.zeros(1, dtype=torch.float64, device=dev)
     fcyc = acyc = 0
     if k > 0:
         Q = torch.zeros((n, k), dtype=torch.complex128, device=dev)
-        Q[torch.as_tensor(nodes, device=dev), torch.arange(k, device=dev)] = 1.0
+        Q[torch.as_tensor(src, device=dev), torch.arange(k, device=dev)] = 1.0
         U, rep_f = solver.solve_block(Q)
-        rec = torch.as_tensor(np.asarray(receiver_nodes, dtype=np.int64), device=dev)
-        d = torch.as_tensor(d_obs_fn(mine), dtype=torch.complex128, device=dev)
-        r = U[rec] - d
+        d = torch.as_tensor(d_obs_fn(mine), dtype=torch.complex128, device=dev).reshape(Ps.num_receivers, k)
+        r = Ps.sample(U) - d
         misfit += 0.5 * torch.sum(torch.abs(r) ** 2)
-        L_rhs = torch.zeros_like(U)
-        L_rhs[rec] = torch.conj(r)
-        Lam, rep_a = solver.solve_block(L_rhs)
-        fwi_sensitivity_output(problem, U, Lam, g)
-        fcyc, acyc = rep_f.cycles, rep_a.cycles
+        reps = []
+        fwi_jacobian_transpose_vec(solver, U, Ps, r, g=g, report=reps)
+        fcyc, acyc = rep_f.cycles, reps[0].cycles
     allreduce_sum(g)
     allreduce_sum(misfit)
     return GradientResult(g, float(misfit.item()), mine, fcyc, acyc)

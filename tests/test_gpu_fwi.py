@@ -178,3 +178,70 @@ def test_solve_helmholtz_compact16_end_to_end():
     Q, scales = hz.compact16(X)
     for s in range(4):
         assert np.array_equal(Q[s], comp._q[s]) and scales[s] == comp._scale[s]
+
+
+CPP_FWI = r"""
+#include <cstdio>
+#include <cmath>
+#include "hz_b200.hpp"
+using namespace hzb;
+int main(int argc, char** argv) {
+  RegularGrid g; g.ndim = 2; g.n = {65, 33, 1};
+  const std::int64_t n = g.num_nodes();
+  SlownessSquaredModel m{g, Field(n, 0.25)};
+  const double omega = 2 * M_PI * 2.0 / 10.0 * (1 - 1e-9);
+  AttenuationField a{g, 0.01 * omega, Field(n, 0.0)};
+  auto prob = std::make_shared<HelmholtzProblem>(m, omega, a);
+  HelmholtzSolveOptions o;
+  HelmholtzSolver solver(prob, o);
+  std::vector<std::array<double, 3>> rec;
+  for (int i = 0; i < 20; ++i) rec.push_back({2.0 + 3.0 * i + 0.25, 1.5, 0.0});
+  AcquisitionGeometry geom({{32.0, 0.0, 0.0}}, rec, 0.0, 1e9, g);
+  SamplingOperator P(geom, *prob);
+  CField q(n, cplx(0.0));
+  q[32] = 1.0;
+  SolveReport rep;
+  WavefieldBatch fw = solve_helmholtz(solver, {q}, StoragePrecision::Full32, &rep);
+  WavefieldBatch cw = solve_helmholtz(solver, {q}, StoragePrecision::Compact16);
+  const CField u = fw.field(0), uc = cw.field(0);
+  double peak = 0, err = 0;
+  for (std::int64_t i = 0; i < n; ++i) {
+    peak = std::max({peak, std::abs(u[i].real()), std::abs(u[i].imag())});
+    err = std::max({err, std::abs(u[i].real() - uc[i].real()), std::abs(u[i].imag() - uc[i].imag())});
+  }
+  Field v(n, 0.0);
+  for (std::int64_t i = 0; i < n; ++i) v[i] = 1e-3 * std::sin(0.1 * i);
+  auto d = fwi_jacobian_vec(solver, u, P, v);
+  std::vector<cplx> w(P.num_receivers(), cplx(1.0, -0.5));
+  Field gr = fwi_jacobian_transpose_vec(solver, u, P, w);
+  // adjoint identity up to solver tolerance (A complex symmetric):
+  // Re sum_r conj(w_r) (J v)_r = sum_i v_i (J^T w)_i
+  double lhs = 0, rhs = 0;
+  for (std::size_t r = 0; r < d.size(); ++r) lhs += (std::conj(w[r]) * d[r]).real();
+  for (std::int64_t i = 0; i < n; ++i) rhs += v[i] * gr[i];
+  cw.save(argv[1]);
+  WavefieldBatch back = WavefieldBatch::load(argv[1], g);
+  const CField ub = back.field(0);
+  double ferr = 0;
+  for (std::int64_t i = 0; i < n; ++i) ferr = std::max(ferr, std::abs(ub[i] - uc[i]));
+  std::printf("cycles %d qerr %.3e peak %.3e adj %.6e %.6e ferr %.3e\n", rep.cycles, err, peak, lhs, rhs, ferr);
+  const bool ok = rep.all_converged() && err <= 2 * std::ldexp(peak, -10) &&
+                  std::abs(lhs - rhs) <= 1e-4 * std::abs(lhs) && ferr <= 1e-3 * peak;
+  return ok ? 0 : 1;
+}
+"""
+
+
+def test_cpp_dropin_fwi_and_wavefield_output():
+    import subprocess
+    from paper_1607_00968_b200 import _native
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with tempfile.TemporaryDirectory() as d:
+        src, exe = os.path.join(d, "fwi.cpp"), os.path.join(d, "fwi")
+        open(src, "w").write(CPP_FWI)
+        libdir = os.path.dirname(_native.LIB_PATH)
+        r = subprocess.run(["g++", "-std=c++17", "-O1", src, "-I", os.path.join(root, "include"), "-L", libdir,
+                            "-lhz_b200", f"-Wl,-rpath,{libdir}", "-o", exe], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        r = subprocess.run([exe, os.path.join(d, "w.jswf")], capture_output=True, text=True, timeout=120)
+        assert r.returncode == 0, r.stdout + r.stderr
