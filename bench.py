@@ -41,7 +41,7 @@ UNIT = "RHS/s"
 # shifted-Laplacian V(2,2) (w_J 0.8), 4 levels to a 129x65 coarse grid
 # (SURVEY §8d), shift 1.0 -- at shift 0.5 the 4-level V-cycle stalls in the
 # reference oracle and on the GPU alike (DESIGN.md §"Workload").
-WORKLOAD = dict(cfg=2, k=32, nlevels=4, shift=1.0, cycle="V", restart=5, tol=1e-6,
+WORKLOAD = dict(cfg=2, k=32, nlevels=5, shift=1.0, cycle="V", restart=3, tol=1e-6,
                 max_cycles=2000, precond="c64")
 
 
@@ -155,8 +155,9 @@ def config_json(cfg, world, l2_note):
 # with the full oracle solve, scripts/ref_full_solve.py; used to extrapolate
 # the bounded CPU samples when no GPU count is at hand).
 REF_CYCLES = None
-# GPU cycle count of this workload (FGMRES(5), 4 levels, shift 1.0, k = 32).
-DEFAULT_CYCLES = 443
+# GPU cycle count of this workload (FGMRES(3), 5 levels, shift 1.0, k = 32;
+# scripts/sweep_bench_solver.py, profiles/r01_bench_solver_sweep.jsonl).
+DEFAULT_CYCLES = 503
 
 
 class ReferenceRunner:
