@@ -9,6 +9,9 @@
 // fetched moments earlier by neighbouring CTAs and hit the 126 MB L2, so HBM
 // sees (close to) one read per input and one write per output: these kernels
 // are HBM-bandwidth bound.
+#include <cstdlib>
+#include <type_traits>
+
 #include "kernels.hpp"
 #include "profile.hpp"
 
@@ -205,6 +208,161 @@ stencil_mc_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
   }
 }
 
+// CPT = 4 consecutive columns of one node with 16-byte loads / stores
+__device__ __forceinline__ void ld4(const float2* __restrict__ p, float2 (&v)[4]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  v[0] = make_float2(a.x, a.y);
+  v[1] = make_float2(a.z, a.w);
+  v[2] = make_float2(b.x, b.y);
+  v[3] = make_float2(b.z, b.w);
+}
+__device__ __forceinline__ void ld4(const double2* __restrict__ p, double2 (&v)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) v[c] = __ldg(p + c);
+}
+__device__ __forceinline__ void st4(float2* p, const float2 (&v)[4]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+}
+__device__ __forceinline__ void st4(double2* p, const double2 (&v)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) p[c] = v[c];
+}
+
+// Galerkin level kernel, 4 columns per thread, with every load of a group of
+// G neighbours (G = 9: a whole plane; G = 3: one row) issued before its FMAs
+// and 16-byte vector loads: the one-load-then-FMA form leaves the kernel
+// latency bound (~1.7 TB/s at level 1 of config 2). Same
+// accumulation order as stencil_mc_kernel, so the results are bitwise equal.
+template <class T, int NDIM, int MODE, int G>
+__global__ void __launch_bounds__(kBlock)
+stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
+                  cplx_t<T>* __restrict__ out, T wj) {
+  using V = cplx_t<T>;
+  constexpr int CPT = 4;
+  const LevelGeom& g = op.g;
+  const uint32_t t = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t e0 = g.e_begin() + t * CPT;
+  if (e0 >= g.e_end()) return;
+  uint32_t node, col, i, j, kz;
+  g.div_k.divmod(e0, node, col);
+  g.unpack(node, i, j, kz);
+  const int64_t sx = g.k, sy = int64_t(g.n0) * g.k, sz = int64_t(g.n0) * g.n1 * g.k;
+  const V* __restrict__ cf = op.coef + node;
+  V acc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) acc[c] = czero<V>();
+  constexpr int S = NDIM == 3 ? 27 : 9;
+#pragma unroll
+  for (int s0 = 0; s0 < S; s0 += G) {
+    V av[G], xv[G][CPT];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int s = s0 + q;
+      const int dz = NDIM == 3 ? s / 9 - 1 : 0, dy = (s / 3) % 3 - 1, dx = s % 3 - 1;
+      const bool okz = NDIM == 2 || (dz < 0 ? kz > 0 : (dz > 0 ? kz + 1 < g.n2 : true));
+      const bool oky = dy < 0 ? j > 0 : (dy > 0 ? j + 1 < g.n1 : true);
+      const bool okx = dx < 0 ? i > 0 : (dx > 0 ? i + 1 < g.n0 : true);
+      const int64_t off = (okz && oky && okx) ? dz * sz + dy * sy + dx * sx : 0;
+      av[q] = __ldg(&cf[int64_t(s) * g.nodes]);
+      ld4(x + int64_t(e0) + off, xv[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) acc[c] = cfma(av[q], xv[q][c], acc[c]);
+  }
+  V o[CPT];
+  if (MODE == 0) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[c] = acc[c];
+  } else if (MODE == 1) {
+    V bv[CPT];
+    ld4(b + e0, bv);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[c] = csub(bv[c], acc[c]);
+  } else {
+    V bv[CPT], xc[CPT];
+    ld4(b + e0, bv);
+    ld4(x + e0, xc);
+    const V d = __ldg(&op.inv_diag[node]);
+    const V wd = mk(wj * d.x, wj * d.y);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[c] = cadd(xc[c], cmul(wd, csub(bv[c], acc[c])));
+  }
+  st4(out + e0, o);
+}
+
+// Fine 5/7-point level kernel, 4 columns per thread with 16-byte loads (all
+// loads issued first); same per-column arithmetic and order as fine_ax.
+template <class T, int NDIM, int MODE>
+__global__ void __launch_bounds__(kBlock)
+fine_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
+               cplx_t<T>* __restrict__ out, T wj) {
+  using V = cplx_t<T>;
+  constexpr int CPT = 4;
+  constexpr bool CSR = MODE != 0;
+  const LevelGeom& g = op.g;
+  const uint32_t t = blockIdx.x * kBlock + threadIdx.x;
+  const uint32_t e0 = g.e_begin() + t * CPT;
+  if (e0 >= g.e_end()) return;
+  uint32_t node, col, i, j, kz;
+  g.div_k.divmod(e0, node, col);
+  g.unpack(node, i, j, kz);
+  const uint32_t sx = g.k, sy = g.n0 * g.k, sz = g.n0 * g.n1 * g.k;
+  const bool xm = i > 0, xp = i + 1 < g.n0, ym = j > 0, yp = j + 1 < g.n1;
+  const bool zm = NDIM == 3 && kz > 0, zp = NDIM == 3 && kz + 1 < g.n2;
+  const V c = __ldg(&op.center[node]);
+  V u0[CPT], uxm[CPT], uxp[CPT], uym[CPT], uyp[CPT], uzm[CPT], uzp[CPT];
+  ld4(x + e0, u0);
+  ld4(x + (xm ? e0 - sx : e0), uxm);
+  ld4(x + (xp ? e0 + sx : e0), uxp);
+  ld4(x + (ym ? e0 - sy : e0), uym);
+  ld4(x + (yp ? e0 + sy : e0), uyp);
+  if (NDIM == 3) {
+    ld4(x + (zm ? e0 - sz : e0), uzm);
+    ld4(x + (zp ? e0 + sz : e0), uzp);
+  }
+  V bv[CPT];
+  if (MODE != 0) ld4(b + e0, bv);
+  V dv = czero<V>();
+  if (MODE == 2) dv = __ldg(&op.inv_diag[node]);
+  const T wx = op.w[0], wy = op.w[1], wz = op.w[2];
+  V o[CPT];
+#pragma unroll
+  for (int q = 0; q < CPT; ++q) {
+    V acc;
+    if (!CSR) {
+      acc = cmul(c, u0[q]);
+      if (xm) acc = crfma(wx, uxm[q], acc);
+      if (xp) acc = crfma(wx, uxp[q], acc);
+      if (ym) acc = crfma(wy, uym[q], acc);
+      if (yp) acc = crfma(wy, uyp[q], acc);
+      if (zm) acc = crfma(wz, uzm[q], acc);
+      if (zp) acc = crfma(wz, uzp[q], acc);
+    } else {
+      acc = czero<V>();
+      if (zm) acc = crfma(wz, uzm[q], acc);
+      if (ym) acc = crfma(wy, uym[q], acc);
+      if (xm) acc = crfma(wx, uxm[q], acc);
+      acc = cfma(c, u0[q], acc);
+      if (xp) acc = crfma(wx, uxp[q], acc);
+      if (yp) acc = crfma(wy, uyp[q], acc);
+      if (zp) acc = crfma(wz, uzp[q], acc);
+    }
+    if (MODE == 0) {
+      o[q] = acc;
+    } else if (MODE == 1) {
+      o[q] = csub(bv[q], acc);
+    } else {
+      const V wd = mk(wj * dv.x, wj * dv.y);
+      o[q] = cadd(u0[q], cmul(wd, csub(bv[q], acc)));
+    }
+  }
+  st4(out + e0, o);
+}
+
 template <class T, class In>
 __global__ void __launch_bounds__(kBlock)
 jacobi_zero_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj,
@@ -305,6 +463,106 @@ prolong_correct_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__
       for (int a = 0; a < 2; ++a)
         if (wv[c][b][a] != T(0)) corr = crfma(wv[c][b][a], ev[c][b][a], corr);
   x[e] = cadd(xe, corr);
+}
+
+// ---- 4-columns-per-thread forms of the transfers and the zero-start sweep
+// (16-byte loads, complex64 with k % 4 == 0); per-column arithmetic and
+// order exactly as the one-column kernels above.
+template <class T, int NDIM>
+__global__ void __launch_bounds__(kBlock)
+restrict_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r, cplx_t<T>* __restrict__ bc) {
+  using V = cplx_t<T>;
+  const uint32_t e0 = gc.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  if (e0 >= gc.e_end()) return;
+  uint32_t node, col, I, J, K;
+  gc.div_k.divmod(e0, node, col);
+  gc.unpack(node, I, J, K);
+  const int64_t k = gf.k;
+  constexpr int S = NDIM == 3 ? 27 : 9;
+  V rv[S][4];
+  T wv[S];
+  const int64_t fc = (2 * int64_t(I) + int64_t(gf.n0) * (2 * int64_t(J) + int64_t(gf.n1) * 2 * K)) * k + col;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int ez = NDIM == 3 ? s / 9 - 1 : 0, ey = (s / 3) % 3 - 1, ex = s % 3 - 1;
+    const int64_t fz = 2 * int64_t(K) + ez, fy = 2 * int64_t(J) + ey, fx = 2 * int64_t(I) + ex;
+    const bool ok = fz >= 0 && fz < gf.n2 && fy >= 0 && fy < gf.n1 && fx >= 0 && fx < gf.n0;
+    wv[s] = ok ? (ex == 0 ? T(1) : T(0.5)) * (ey == 0 ? T(1) : T(0.5)) * (ez == 0 ? T(1) : T(0.5)) : T(0);
+    const int64_t off = (int64_t(ex) + int64_t(gf.n0) * (ey + int64_t(gf.n1) * ez)) * k;
+    ld4(r + (ok ? fc + off : fc), rv[s]);
+  }
+  V o[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    V acc = czero<V>();
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+      if (wv[s] != T(0)) acc = crfma(wv[s], rv[s][c], acc);
+    o[c] = acc;
+  }
+  st4(bc + e0, o);
+}
+
+template <class T, int NDIM>
+__global__ void __launch_bounds__(kBlock)
+prolong_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec, cplx_t<T>* __restrict__ x) {
+  using V = cplx_t<T>;
+  const uint32_t e0 = gf.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  if (e0 >= gf.e_end()) return;
+  uint32_t node, col, i, j, kz;
+  gf.div_k.divmod(e0, node, col);
+  gf.unpack(node, i, j, kz);
+  const int64_t k = gf.k;
+  const uint32_t cx0 = i >> 1, cx1 = (i + 1) >> 1, cy0 = j >> 1, cy1 = (j + 1) >> 1;
+  const uint32_t cz0 = NDIM == 3 ? (kz >> 1) : 0, cz1 = NDIM == 3 ? ((kz + 1) >> 1) : 0;
+  const T wx0 = (i & 1u) ? T(0.5) : T(1), wx1 = (i & 1u) ? T(0.5) : T(0);
+  const T wy0 = (j & 1u) ? T(0.5) : T(1), wy1 = (j & 1u) ? T(0.5) : T(0);
+  const T wz0 = NDIM == 3 && (kz & 1u) ? T(0.5) : T(1), wz1 = NDIM == 3 && (kz & 1u) ? T(0.5) : T(0);
+  constexpr int NZ = NDIM == 3 ? 2 : 1;
+  V ev[NZ][2][2][4];
+  T wv[NZ][2][2];
+#pragma unroll
+  for (int c = 0; c < NZ; ++c)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        const int64_t C = (a ? cx1 : cx0) + int64_t(gc.n0) * ((b ? cy1 : cy0) + int64_t(gc.n1) * (c ? cz1 : cz0));
+        ld4(ec + C * k + col, ev[c][b][a]);
+        wv[c][b][a] = (a ? wx1 : wx0) * (b ? wy1 : wy0) * (c ? wz1 : wz0);
+      }
+  V xe[4], o[4];
+  ld4(x + e0, xe);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    V corr = czero<V>();
+#pragma unroll
+    for (int c = 0; c < NZ; ++c)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+          if (wv[c][b][a] != T(0)) corr = crfma(wv[c][b][a], ev[c][b][a][q], corr);
+    o[q] = cadd(xe[q], corr);
+  }
+  st4(x + e0, o);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock)
+jacobi_zero_v4_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj, const cplx_t<T>* __restrict__ b,
+                      cplx_t<T>* __restrict__ out) {
+  using V = cplx_t<T>;
+  const uint32_t e0 = g.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  if (e0 >= g.e_end()) return;
+  const uint32_t node = g.div_k.div(e0);
+  const V d = __ldg(&inv_diag[node]);
+  const V wd = mk(wj * d.x, wj * d.y);
+  V bv[4], o[4];
+  ld4(b + e0, bv);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) o[q] = cmul(wd, bv[q]);
+  st4(out + e0, o);
 }
 
 // ---------------------------------------------------------------- Galerkin
@@ -457,17 +715,45 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
   const int64_t total = op.g.owned_elems();
   const int grid = grid_for(total, kBlock);
   ProfScope prof(level_name<T, MODE>(op.kind), level_bytes(op, MODE), s);
-  if (op.kind == kFine) {
+  static const bool fine_v4 = [] {
+    const char* e = std::getenv("HZ_FINE_V4");
+    return !(e && e[0] == '0');
+  }();
+  // c64 only: for c128 the 4-column form needs 7 x 64 B per thread in
+  // registers and runs slower than one column per thread
+  if (op.kind == kFine && fine_v4 && sizeof(T) == 4 && op.g.k % 4 == 0) {
+    const int g4 = grid_for(total / 4, kBlock);
+    if (op.ndim == 3)
+      fine_v4_kernel<T, 3, MODE><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+    else
+      fine_v4_kernel<T, 2, MODE><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+  } else if (op.kind == kFine) {
     if (op.ndim == 3)
       level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
     else
       level_kernel<T, 2, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
   } else if (op.g.k % 4 == 0) {
     const int g4 = grid_for(total / 4, kBlock);
-    if (op.ndim == 3)
-      stencil_mc_kernel<T, 3, MODE, 4><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
-    else
-      stencil_mc_kernel<T, 2, MODE, 4><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+    static const int variant = [] {
+      const char* e = std::getenv("HZ_STENCIL_VARIANT");
+      return e ? std::atoi(e) : 1;
+    }();
+    if (variant == 0) {
+      if (op.ndim == 3)
+        stencil_mc_kernel<T, 3, MODE, 4><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+      else
+        stencil_mc_kernel<T, 2, MODE, 4><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+    } else if (variant == 2 || (sizeof(T) == 8 && variant != 3)) {
+      if (op.ndim == 3)
+        stencil_v4_kernel<T, 3, MODE, 3><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+      else
+        stencil_v4_kernel<T, 2, MODE, 3><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+    } else {
+      if (op.ndim == 3)
+        stencil_v4_kernel<T, 3, MODE, 9><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+      else
+        stencil_v4_kernel<T, 2, MODE, 9><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
+    }
   } else {
     if (op.ndim == 3)
       level_kernel<T, 3, kStencil, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
@@ -498,6 +784,13 @@ void launch_jacobi_zero(const LevelOp<T>& op, T wj, const In* b, cplx_t<T>* xout
   const int64_t total = op.g.owned_elems();
   ProfScope prof(sizeof(T) == 8 ? "jacobi_zero_c128" : "jacobi_zero_c64",
                  double(op.g.owned_nodes()) * ((double(sizeof(In)) + sizeof(cplx_t<T>)) * op.g.k + sizeof(cplx_t<T>)), s);
+  if constexpr (std::is_same<In, cplx_t<T>>::value && sizeof(T) == 4) {
+    if (op.g.k % 4 == 0) {
+      jacobi_zero_v4_kernel<T><<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op.g, op.inv_diag, wj, b, xout);
+      HZ_LAUNCH_CHECK();
+      return;
+    }
+  }
   jacobi_zero_kernel<T, In><<<grid_for(total, kBlock), kBlock, 0, s>>>(op.g, op.inv_diag, wj, b, xout);
   HZ_LAUNCH_CHECK();
 }
@@ -507,10 +800,17 @@ void launch_restrict(const LevelGeom& gf, const LevelGeom& gc, int ndim, const c
   const int grid = grid_for(gc.owned_elems(), kBlock);
   ProfScope prof(sizeof(T) == 8 ? "restrict_c128" : "restrict_c64",
                  (double(gf.nodes) * gc.owned_nodes() / gc.nodes + gc.owned_nodes()) * gf.k * sizeof(cplx_t<T>), s);
-  if (ndim == 3)
+  if (sizeof(T) == 4 && gf.k % 4 == 0) {
+    const int g4 = grid_for(gc.owned_elems() / 4, kBlock);
+    if (ndim == 3)
+      restrict_v4_kernel<T, 3><<<g4, kBlock, 0, s>>>(gf, gc, r, bc);
+    else
+      restrict_v4_kernel<T, 2><<<g4, kBlock, 0, s>>>(gf, gc, r, bc);
+  } else if (ndim == 3) {
     restrict_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, r, bc);
-  else
+  } else {
     restrict_kernel<T, 2><<<grid, kBlock, 0, s>>>(gf, gc, r, bc);
+  }
   HZ_LAUNCH_CHECK();
 }
 template <class T>
@@ -519,10 +819,17 @@ void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
   const int grid = grid_for(gf.owned_elems(), kBlock);
   ProfScope prof(sizeof(T) == 8 ? "prolong_correct_c128" : "prolong_correct_c64",
                  (2.0 * gf.owned_nodes() + gc.nodes * double(gf.owned_nodes()) / gf.nodes) * gf.k * sizeof(cplx_t<T>), s);
-  if (ndim == 3)
+  if (sizeof(T) == 4 && gf.k % 4 == 0) {
+    const int g4 = grid_for(gf.owned_elems() / 4, kBlock);
+    if (ndim == 3)
+      prolong_v4_kernel<T, 3><<<g4, kBlock, 0, s>>>(gf, gc, ec, x);
+    else
+      prolong_v4_kernel<T, 2><<<g4, kBlock, 0, s>>>(gf, gc, ec, x);
+  } else if (ndim == 3) {
     prolong_correct_kernel<T, 3><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
-  else
+  } else {
     prolong_correct_kernel<T, 2><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
+  }
   HZ_LAUNCH_CHECK();
 }
 
