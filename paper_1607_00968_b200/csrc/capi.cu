@@ -77,7 +77,6 @@ struct hz_solver {
   std::unique_ptr<Fgmres<double>> fgm;
   std::unique_ptr<Bicgstab> bicg;
   DevBuf<double2> dB, dX;
-  DevBuf<float2> b32, x32;
   // DenseLuSmall: explicit inverse of the unshifted operator
   DevBuf<double2> dense_ainvT;
   // slab decomposition (slabs.hpp): per-GPU copies of the fine centre and of
@@ -90,7 +89,7 @@ struct hz_solver {
   DevBuf<double2> fU, fR, fX, fD;
   DevBuf<double> fv, fpart, fmax;
   DevBuf<uint32_t> fQ;
-  int span_k = 0;  // k the spanning dB/dX/b32/x32 are laid out for
+  int span_k = 0;  // k the spanning dB/dX are laid out for
   const double2* center_on(int device) const {
     if (device == prob->device) return prob->d_center.get();
     return center_rep.at(device).get();
@@ -101,19 +100,11 @@ struct hz_solver {
     if (!slabs) {
       dB.ensure(e);
       dX.ensure(e);
-      if (opts.precond_precision == HZ_C64) {
-        b32.ensure(e);
-        x32.ensure(e);
-      }
       return;
     }
     if (span_k == k) return;
     alloc_span(dB, *slabs, 0, k);
     alloc_span(dX, *slabs, 0, k);
-    if (opts.precond_precision == HZ_C64) {
-      alloc_span(b32, *slabs, 0, k);
-      alloc_span(x32, *slabs, 0, k);
-    }
     span_k = k;
   }
   ~hz_solver() {
@@ -195,15 +186,8 @@ DevOp<double> make_slab_op(hz_solver* s, int k) {
     });
   };
   if (s->opts.precond_precision == HZ_C64) {
-    s->ensure_blocks(k);
-    op.prec = [s, sl](const double2* in, double2* out, int kk, cudaStream_t st) {
-      sl->each(0, [&](int, int64_t r0, int64_t nr, cudaStream_t pst) {
-        launch_cast<float2, double2>(nr * kk, in + r0 * kk, s->b32.get() + r0 * kk, pst);
-      });
-      s->h32->cycle(s->spec, kk, s->b32.get(), s->x32.get(), true, st);
-      sl->each(0, [&](int, int64_t r0, int64_t nr, cudaStream_t pst) {
-        launch_cast<double2, float2>(nr * kk, s->x32.get() + r0 * kk, out + r0 * kk, pst);
-      });
+    op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
+      s->h32->cycle_cast(s->spec, kk, in, out, st);
     };
   } else {
     op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
@@ -222,14 +206,8 @@ DevOp<double> make_op(hz_solver* s, int k) {
     launch_apply<double>(P->fine_op(kk), in, out, st);
   };
   if (s->opts.precond_precision == HZ_C64) {
-    const size_t e = size_t(op.n) * k;
-    s->b32.ensure(e);
-    s->x32.ensure(e);
     op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
-      const int64_t cnt = s->prob->num_nodes() * kk;
-      launch_cast<float2, double2>(cnt, in, s->b32.get(), st);
-      s->h32->cycle(s->spec, kk, s->b32.get(), s->x32.get(), true, st);
-      launch_cast<double2, float2>(cnt, s->x32.get(), out, st);
+      s->h32->cycle_cast(s->spec, kk, in, out, st);
     };
   } else {
     op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
@@ -518,8 +496,6 @@ int hz_solver_set_slabs(hz_solver* s, int nparts, const int* devices) {
       if (s->fgm) s->fgm->set_slabs(nullptr);
       s->dB.release();
       s->dX.release();
-      s->b32.release();
-      s->x32.release();
       s->span_k = 0;
       s->slabs.reset();
       s->rep32.clear();

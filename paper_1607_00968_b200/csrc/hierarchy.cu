@@ -11,6 +11,9 @@
 #include <cstring>
 #include <string>
 
+#include <cstdlib>
+#include <type_traits>
+
 #include "solver.hpp"
 
 namespace hz {
@@ -441,7 +444,7 @@ void Hierarchy<T>::ensure_ws(int k) {
       else
         b.alloc(e);
     };
-    if (l > 0) {
+    if (l > 0 || std::is_same<T, float>::value) {  // level 0: cycle_cast's b32 / x
       get(wx_[l]);
       get(wb_[l]);
     }
@@ -519,6 +522,22 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
   V* other = wt_[l].get();
   bool cur_zero = x_zero;
   relax(l, spec, spec.pre, k, b, cur, other, cur_zero, s);
+  const size_t rowb = size_t(k) * sizeof(V);
+  coarse_correction(l, spec, k, b, cur, cur_zero, s);
+  cur_zero = false;
+  relax(l, spec, spec.post, k, b, cur, other, cur_zero, s);
+  if (cur != x)
+    on_level(l, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
+      HZ_CUDA(cudaMemcpyAsync(x + r0 * k, cur + r0 * k, size_t(nr) * rowb, cudaMemcpyDeviceToDevice, st));
+    });
+}
+
+// the middle of cycle_rec: residual, restriction, coarse visit(s) and the
+// prolongated correction of cur (zeroed first when cur_zero)
+template <class T>
+void Hierarchy<T>::coarse_correction(int l, const CycleSpec& spec, int k, const V* b, V* cur, bool cur_zero,
+                                     cudaStream_t s) {
+  const int L = num_levels();
   const bool sl = slab_level(l);
   const size_t rowb = size_t(k) * sizeof(V);
   if (cur_zero)
@@ -569,12 +588,54 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
   on_level(l, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
     launch_prolong_correct<T>(o.g, gc, ndim_, ec, cur, st);
   });
-  cur_zero = false;
-  relax(l, spec, spec.post, k, b, cur, other, cur_zero, s);
-  if (cur != x)
-    on_level(l, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
-      HZ_CUDA(cudaMemcpyAsync(x + r0 * k, cur + r0 * k, size_t(nr) * rowb, cudaMemcpyDeviceToDevice, st));
+}
+
+// One cycle of the complex64 hierarchy applied to a complex128 block (the
+// mixed-precision preconditioner): b64 -> x64 with the casts fused into the
+// first two and the last fine-level sweeps when the fine level allows it;
+// otherwise cast, cycle, cast.
+template <class T>
+void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, double2* x64, cudaStream_t s) {
+  if constexpr (!std::is_same<T, float>::value) {
+    throw HzError(kState, "cycle_cast: complex64 hierarchies only");
+  } else {
+    ensure_ws(k);
+    const int L = num_levels();
+    V* b32 = wb_[0].get();
+    V* x = wx_[0].get();
+    static const bool allow = [] {  // HZ_FUSED_CAST=0: unfused reference path
+      const char* e = std::getenv("HZ_FUSED_CAST");
+      return !(e && e[0] == '0');
+    }();
+    const bool fused = allow && L > 1 && fused_fine_ok(op(0, k)) && cast_zero_ok(op(0, k)) && spec.pre >= 1 &&
+                       spec.post >= 1;
+    if (!fused) {
+      on_level(0, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
+        launch_cast<float2, double2>(nr * k, b64 + r0 * k, b32 + r0 * k, st);
+      });
+      cycle_rec(0, spec, k, b32, x, true, s);
+      on_level(0, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
+        launch_cast<double2, float2>(nr * k, x + r0 * k, x64 + r0 * k, st);
+      });
+      return;
+    }
+    const bool sl = slab_level(0);
+    const T wj = T(spec.jacobi_weight);
+    if (sl) sl_->neighbours();
+    on_level(0, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
+      launch_jacobi_zero_cast(o, wj, b64, b32, x, st);
     });
+    V* cur = x;
+    V* other = wt_[0].get();
+    bool cur_zero = false;
+    relax(0, spec, spec.pre - 1, k, b32, cur, other, cur_zero, s);
+    coarse_correction(0, spec, k, b32, cur, false, s);
+    relax(0, spec, spec.post - 1, k, b32, cur, other, cur_zero, s);
+    if (sl) sl_->neighbours();
+    on_level(0, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
+      launch_jacobi_out64(o, wj, cur, b32, x64, st);
+    });
+  }
 }
 
 // kcycle_coarse (src/multigrid.cpp:138-160): k_inner block FGMRES iterations

@@ -57,6 +57,18 @@ void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
 void launch_galerkin(const LevelOp<double>& fine, const LevelGeom& gc, double2* coef_c,
                      cudaStream_t s);
 
+// complex64 preconditioner of a complex128 block, finest level: the
+// zero-start sweep fused with the c128 -> c64 cast of the right-hand side
+// (b32 is written for the rest of the cycle; k % 4 == 0) ...
+bool cast_zero_ok(const LevelOp<float>& op);
+void launch_jacobi_zero_cast(const LevelOp<float>& op, float wj, const double2* b64, float2* b32, float2* x1,
+                             cudaStream_t s);
+// ... and the last post-smoothing sweep writing the c128 result directly
+// (kFine, k % 4 == 0)
+bool fused_fine_ok(const LevelOp<float>& op);
+void launch_jacobi_out64(const LevelOp<float>& op, float wj, const float2* x, const float2* b, double2* out,
+                         cudaStream_t s);
+
 // elementwise casts / copies
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);

@@ -97,6 +97,9 @@ class Hierarchy {
   // application does, src/helmholtz_solver.cpp:65-68).
   void cycle(const CycleSpec& spec, int k, const V* b, V* x, bool x_zero, cudaStream_t s);
   void coarse_solve(int k, const V* b, V* x, cudaStream_t s);
+  // complex64 hierarchy as the preconditioner of a complex128 block (casts
+  // fused into the fine-level sweeps where possible)
+  void cycle_cast(const CycleSpec& spec, int k, const double2* b64, double2* x64, cudaStream_t s);
   // Galerkin planes / diagonal of level l (host copy, f64) for parity checks
   void download_level(int l, std::vector<cplx>& coef_or_center) const;
   // copy of the level operators (not the coarsest solver) on another GPU
@@ -125,6 +128,8 @@ class Hierarchy {
   void relax(int l, const CycleSpec& spec, int sweeps, int k, const V* b, V*& cur, V*& other,
              bool& cur_zero, cudaStream_t s);
   void kcycle_coarse(int l, const CycleSpec& spec, int k, const V* b, V* x, cudaStream_t s);
+  void coarse_correction(int l, const CycleSpec& spec, int k, const V* b, V* cur, bool cur_zero,
+                         cudaStream_t s);
   bool slab_level(int l) const { return sl_ && l < sl_->agg_level(); }
   // f(op, stream, row0, rows) once per part owning level l (slab levels), or
   // once on stream s over the whole grid

@@ -296,10 +296,10 @@ stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
 
 // Fine 5/7-point level kernel, 4 columns per thread with 16-byte loads (all
 // loads issued first); same per-column arithmetic and order as fine_ax.
-template <class T, int NDIM, int MODE>
+template <class T, int NDIM, int MODE, class Out = cplx_t<T>>
 __global__ void __launch_bounds__(kBlock)
 fine_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
-               cplx_t<T>* __restrict__ out, T wj) {
+               Out* __restrict__ out, T wj) {
   using V = cplx_t<T>;
   constexpr int CPT = 4;
   constexpr bool CSR = MODE != 0;
@@ -360,6 +360,36 @@ fine_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* 
       o[q] = cadd(u0[q], cmul(wd, csub(bv[q], acc)));
     }
   }
+  if constexpr (std::is_same<Out, cplx_t<T>>::value) {
+    st4(out + e0, o);
+  } else {
+    Out w[CPT];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) w[q] = ccast<Out>(o[q]);
+    st4(out + e0, w);
+  }
+}
+
+// Zero-start sweep fused with the c128 -> c64 cast of the right-hand side
+// (complex64 preconditioner): b32 = (c64) b64, x1 = wD^{-1} b32; 4 columns
+// per thread, the same per-column operations as cast + jacobi_zero.
+__global__ void __launch_bounds__(kBlock)
+jacobi_zero_cast_kernel(LevelGeom g, const float2* __restrict__ inv_diag, float wj, const double2* __restrict__ b64,
+                        float2* __restrict__ b32, float2* __restrict__ out) {
+  const uint32_t e0 = g.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  if (e0 >= g.e_end()) return;
+  const uint32_t node = g.div_k.div(e0);
+  const float2 d = __ldg(&inv_diag[node]);
+  const float2 wd = mk(wj * d.x, wj * d.y);
+  double2 bb[4];
+  ld4(b64 + e0, bb);
+  float2 bv[4], o[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    bv[q] = ccast<float2>(bb[q]);
+    o[q] = cmul(wd, bv[q]);
+  }
+  st4(b32 + e0, bv);
   st4(out + e0, o);
 }
 
@@ -830,6 +860,30 @@ void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
   } else {
     prolong_correct_kernel<T, 2><<<grid, kBlock, 0, s>>>(gf, gc, ec, x);
   }
+  HZ_LAUNCH_CHECK();
+}
+
+bool fused_fine_ok(const LevelOp<float>& op) { return op.kind == kFine && op.g.k % 4 == 0; }
+bool cast_zero_ok(const LevelOp<float>& op) { return op.g.k % 4 == 0; }
+
+void launch_jacobi_zero_cast(const LevelOp<float>& op, float wj, const double2* b64, float2* b32, float2* x1,
+                             cudaStream_t s) {
+  const int64_t total = op.g.owned_elems();
+  const double n = double(op.g.owned_nodes()), k = op.g.k;
+  ProfScope prof("jacobi_zero_cast_c64", n * (k * (16.0 + 8.0 + 8.0) + 8.0), s);
+  jacobi_zero_cast_kernel<<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op.g, op.inv_diag, wj, b64, b32, x1);
+  HZ_LAUNCH_CHECK();
+}
+
+void launch_jacobi_out64(const LevelOp<float>& op, float wj, const float2* x, const float2* b, double2* out,
+                         cudaStream_t s) {
+  const int64_t total = op.g.owned_elems();
+  const double n = double(op.g.owned_nodes()), k = op.g.k;
+  ProfScope prof("jacobi_out64_fine_c64", n * (k * (8.0 + 8.0 + 16.0) + 8.0 + 8.0), s);
+  if (op.ndim == 3)
+    fine_v4_kernel<float, 3, 2, double2><<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op, x, b, out, wj);
+  else
+    fine_v4_kernel<float, 2, 2, double2><<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op, x, b, out, wj);
   HZ_LAUNCH_CHECK();
 }
 

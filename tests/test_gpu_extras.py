@@ -219,3 +219,25 @@ def test_config3_three_levels_block_tridiagonal(ref):
     assert abs(rep.cycles - rr.cycles) <= 0.05 * rr.cycles + 2
     for j in range(B.shape[1]):
         assert rel_err(X[:, j], Xr[:, j]) <= 1e-5
+
+
+def test_fused_c64_cycle_matches_unfused():
+    """The complex64 preconditioner with the casts fused into the fine-level
+    sweeps (cycle_cast) against cast + cycle + cast (HZ_FUSED_CAST=0), in a
+    fresh process each (the switch is read once)."""
+    import subprocess, sys
+    code = (
+        "import sys; sys.path.insert(0, '.'); import numpy as np\n"
+        "import paper_1607_00968_b200 as hz; from paper_1607_00968_b200 import configs\n"
+        "cfg = configs.config2(nlevels=4, k=8, nx=257, nz=129); cfg.precond_precision = 'c64'\n"
+        "S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))\n"
+        "np.save(sys.argv[1], S.cycle(configs.random_block(cfg.num_nodes, 8, seed=4)))\n")
+    with tempfile.TemporaryDirectory() as d:
+        outs = []
+        for flag in ("1", "0"):
+            path = os.path.join(d, f"x{flag}.npy")
+            env = dict(os.environ, HZ_FUSED_CAST=flag)
+            r = subprocess.run([sys.executable, "-c", code, path], cwd=ROOT, env=env, capture_output=True, text=True)
+            assert r.returncode == 0, r.stderr
+            outs.append(np.load(path))
+        assert rel_err(outs[0], outs[1]) <= 1e-5
