@@ -247,62 +247,125 @@ frob2_kernel(int64_t count, const cplx_t<T>* __restrict__ Tt, const cplx_t<T>* _
   }
 }
 
+// ---- k x k factorisations on one CTA (k <= 64, up to 1024 threads).
+// In-place right-looking Cholesky of the Hermitian A (upper triangle) in
+// shared memory, A <- R (upper, real positive diagonal). Element (a, c) is
+// owned by thread (a k + c) mod nt for the whole factorisation, so step j
+// needs ONE barrier: every thread reads the pivot and row j, updates its own
+// trailing elements in place, and the row-j owners publish the scaled row
+// after the barrier. Pivot test: PIP -- stop at the first d_j < thr G_jj;
+// else (CholQR) collapse the column (zero row of R) and go on. Returns the
+// first failing column + 1 (0: none).
+template <class T, bool PIP>
+__device__ int chol_upper_smem(cplx_t<T>* A, int k, const cplx_t<T>* G, T thr) {
+  using V = cplx_t<T>;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  constexpr int MAXE = 4;  // owned elements per thread: k^2 <= 4 * nt
+  int fail = 0;
+  int ea[MAXE], ec[MAXE], ne = 0;
+#pragma unroll
+  for (int q = 0; q < MAXE; ++q) {
+    const int e = tid + q * nt;
+    if (e < k * k) {
+      ea[q] = e / k;
+      ec[q] = e - ea[q] * k;
+      ne = q + 1;
+    }
+  }
+  for (int j = 0; j < k; ++j) {
+    const T d = A[j * k + j].x;
+    const T g0 = G[j * k + j].x;
+    const bool dead = PIP ? (!(d >= thr * g0) || !(d > T(0)))
+                          : (!(d > thr * (g0 > T(0) ? g0 : T(1))) || !(d > T(0)));
+    if (dead && fail == 0) fail = j + 1;
+    if (PIP && dead) return fail;  // the same decision in every thread
+    const T piv = dead ? T(0) : sqrt(d);
+    const T inv = piv > T(0) ? T(1) / piv : T(0);
+    V rowv[MAXE];
+    int rowc[MAXE];
+    int nrow = 0;
+#pragma unroll
+    for (int q = 0; q < MAXE; ++q) {
+      if (q >= ne) break;
+      const int a = ea[q], c = ec[q], e = a * k + c;
+      if (a == j && c >= j) {
+        rowv[nrow] = c == j ? mk(piv, T(0)) : cscale(inv, A[e]);
+        rowc[nrow++] = c;
+      } else if (a > j && c >= a) {
+        const V ra = cscale(inv, A[j * k + a]), rc = cscale(inv, A[j * k + c]);
+        A[e] = csub(A[e], cmulc(ra, rc));
+      }
+    }
+    __syncthreads();
+    for (int q = 0; q < nrow; ++q) A[j * k + rowc[q]] = rowv[q];
+  }
+  __syncthreads();
+  return fail;
+}
+
+template <class V>
+__device__ __forceinline__ V warp_allsum(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+  }
+  return v;
+}
+
+// Ri = R^{-1} for upper R in shared memory (k <= 64): one warp per column,
+// column-oriented back substitution (x = e_c; for l = c..0: x_l /= d_l, then
+// every lane i < l subtracts A[i][l] x_l) -- one shuffle per step, no
+// reductions on the dependency chain. A column whose pivot is not positive
+// (collapsed) is zero, as are rows with d_i <= 0.
+template <class T>
+__device__ void tri_inv_upper(const cplx_t<T>* A, cplx_t<T>* Ri, int k) {
+  using V = cplx_t<T>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // reciprocal pivots of this lane's rows (0 for non-positive pivots)
+  const T d0 = lane < k ? A[lane * k + lane].x : T(0);
+  const T d1 = lane + 32 < k ? A[(lane + 32) * k + lane + 32].x : T(0);
+  const T r0 = d0 > T(0) ? T(1) / d0 : T(0), r1 = d1 > T(0) ? T(1) / d1 : T(0);
+  for (int c = warp; c < k; c += nw) {
+    const bool live = A[c * k + c].x > T(0);
+    V x0 = (lane == c && live) ? mk(T(1), T(0)) : czero<V>();
+    V x1 = (lane + 32 == c && live) ? mk(T(1), T(0)) : czero<V>();
+    for (int l = c; l >= 0 && live; --l) {
+      // finalise x_l on its lane, then broadcast it
+      if (lane == l) x0 = cscale(r0, x0);
+      if (lane + 32 == l) x1 = cscale(r1, x1);
+      const V src = l < 32 ? x0 : x1;
+      V xl;
+      xl.x = __shfl_sync(0xffffffffu, src.x, l & 31);
+      xl.y = __shfl_sync(0xffffffffu, src.y, l & 31);
+      if (lane < l) x0 = csub(x0, cmul(A[lane * k + l], xl));
+      if (lane + 32 < l) x1 = csub(x1, cmul(A[(lane + 32) * k + l], xl));
+    }
+    if (lane < k) Ri[lane * k + c] = x0;
+    if (lane + 32 < k) Ri[(lane + 32) * k + c] = x1;
+  }
+}
+
 // Single-CTA Cholesky G = R^H R (upper R, real positive diagonal) and R^{-1}.
 // flag = first column j whose pivot fails d_j > rel_tol^2 * G_jj (+1), else 0.
 template <class T>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 small_cholesky_kernel(int k, const cplx_t<T>* __restrict__ G, cplx_t<T>* __restrict__ R,
                       cplx_t<T>* __restrict__ Rinv, int* flag, T rel_tol) {
   using V = cplx_t<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* A = reinterpret_cast<V*>(smem_raw);  // [k][k]
-  __shared__ int fl;
+  V* Ri = A + k * k;                      // [k][k]
   const int tid = threadIdx.x;
   for (int e = tid; e < k * k; e += blockDim.x) A[e] = G[e];
-  if (tid == 0) fl = 0;
   __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    if (tid == 0) {
-      const T d = A[j * k + j].x;
-      const T g0 = G[j * k + j].x;
-      const bool dead = !(d > rel_tol * rel_tol * (g0 > T(0) ? g0 : T(1))) || !(d > T(0));
-      if (dead && fl == 0) fl = j + 1;
-      A[j * k + j] = dead ? czero<V>() : mk(sqrt(d), T(0));
-    }
-    __syncthreads();
-    const T piv = A[j * k + j].x;
-    const T inv = piv > T(0) ? T(1) / piv : T(0);  // collapsed column: zero row of R
-    for (int c = j + 1 + tid; c < k; c += blockDim.x) A[j * k + c] = cscale(inv, A[j * k + c]);
-    __syncthreads();
-    // trailing update A[a][c] -= conj(A[j][a]) A[j][c], j < a <= c
-    const int m = k - j - 1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-      const int a = j + 1 + e / m, c = j + 1 + e % m;
-      if (c >= a) {
-        const V ra = A[j * k + a], rc = A[j * k + c];
-        A[a * k + c] = csub(A[a * k + c], cmulc(ra, rc));
-      }
-    }
-    __syncthreads();
-  }
-  // R = upper(A)
+  const int fl = chol_upper_smem<T, false>(A, k, G, rel_tol * rel_tol);
+  tri_inv_upper<T>(A, Ri, k);
+  __syncthreads();
   for (int e = tid; e < k * k; e += blockDim.x) {
-    const int a = e / k, c = e % k;
+    const int a = e / k, c = e - a * k;
     R[e] = c >= a ? A[e] : czero<V>();
-  }
-  __syncthreads();
-  // Rinv by back substitution, one column per thread
-  for (int c = tid; c < k; c += blockDim.x) {
-    for (int i = k - 1; i >= 0; --i) {
-      V s = (i == c) ? mk(T(1), T(0)) : czero<V>();
-      if (i <= c) {
-        for (int l = i + 1; l <= c; ++l) s = csub(s, cmul(A[i * k + l], Rinv[l * k + c]));
-        const T d = A[i * k + i].x;
-        Rinv[i * k + c] = (d > T(0) && A[c * k + c].x > T(0)) ? cscale(T(1) / d, s) : czero<V>();
-      } else {
-        Rinv[i * k + c] = czero<V>();
-      }
-    }
+    Rinv[e] = Ri[e];
   }
   if (tid == 0) *flag = fl;
 }
@@ -421,14 +484,12 @@ pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __
   V* A = reinterpret_cast<V*>(smem_raw);  // [k][k] S, then R
   V* Ri = A + kk;                         // [k][k] R^{-1}
   V* Hs = Ri + kk;                        // [nb+1][k][k] when staged
-  __shared__ int fl;
   const int tid = threadIdx.x, nt = blockDim.x;
   const V* H = Hc;
   if (staged) {
     for (int e = tid; e < (nb + 1) * kk; e += nt) Hs[e] = Hc[e];
     H = Hs;
   }
-  if (tid == 0) fl = 0;
   __syncthreads();
   const V* G = H + int64_t(nb) * kk;
   for (int e = tid; e < kk; e += nt) {
@@ -443,40 +504,13 @@ pip_factor_kernel(int k, int nb, const cplx_t<T>* __restrict__ Hc, cplx_t<T>* __
     A[e] = s;
   }
   __syncthreads();
-  for (int j = 0; j < k; ++j) {
-    // every pivot (squared norm of column j after projecting out V and the
-    // earlier columns) must keep eta2 of the column's norm^2
-    if (tid == 0) {
-      const T d = A[j * k + j].x;
-      if (!(d >= eta2 * G[j * k + j].x) || !(d > T(0))) fl = 1;
-      A[j * k + j] = mk(sqrt(d > T(0) ? d : T(1)), T(0));
-    }
-    __syncthreads();
-    if (fl) {
-      if (tid == 0) *flag = 1;
-      return;
-    }
-    const T inv = T(1) / A[j * k + j].x;
-    for (int c = j + 1 + tid; c < k; c += nt) A[j * k + c] = cscale(inv, A[j * k + c]);
-    __syncthreads();
-    const int m = k - j - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int a = j + 1 + e / m, c = j + 1 + e % m;
-      if (c >= a) A[a * k + c] = csub(A[a * k + c], cmulc(A[j * k + a], A[j * k + c]));
-    }
-    __syncthreads();
+  // every pivot (squared norm of column j after projecting out V and the
+  // earlier columns) must keep eta2 of the column's norm^2
+  if (chol_upper_smem<T, true>(A, k, G, eta2)) {
+    if (tid == 0) *flag = 1;
+    return;
   }
-  // R^{-1}: column c solved by one warp-strided thread group (back substitution)
-  for (int c = tid; c < k; c += nt)
-    for (int i = k - 1; i >= 0; --i) {
-      if (i > c) {
-        Ri[i * k + c] = czero<V>();
-        continue;
-      }
-      V s = (i == c) ? mk(T(1), T(0)) : czero<V>();
-      for (int l = i + 1; l <= c; ++l) s = csub(s, cmul(A[i * k + l], Ri[l * k + c]));
-      Ri[i * k + c] = cscale(T(1) / A[i * k + i].x, s);
-    }
+  tri_inv_upper<T>(A, Ri, k);
   __syncthreads();
   for (int e = tid; e < kk; e += nt) {
     const int a = e / k, c = e % k;
@@ -705,12 +739,13 @@ void launch_frob2_partial(int64_t count, const cplx_t<T>* Tt, const cplx_t<T>* S
 template <class T>
 void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* Rinv, int* flag,
                            T rel_tol, cudaStream_t s) {
-  const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
+  if (k > 64) throw HzError(kValidation, "small_cholesky: k > 64");
+  const size_t smem = 2 * sizeof(cplx_t<T>) * size_t(k) * k;
   auto kern = small_cholesky_kernel<T>;
   if (smem > 48 * 1024)
     HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   ProfScope prof("small_cholesky", 4.0 * k * k * sizeof(cplx_t<T>), s);
-  kern<<<1, 256, smem, s>>>(k, G, R, Rinv, flag, rel_tol);
+  kern<<<1, 1024, smem, s>>>(k, G, R, Rinv, flag, rel_tol);
   HZ_LAUNCH_CHECK();
 }
 
