@@ -739,6 +739,17 @@ const char* level_name(int kind) {
   return names[kind][MODE][sizeof(T) == 8 ? 0 : 1];
 }
 
+// Below this many (node, column) elements a Galerkin level is latency bound
+// and one column per thread (4x the threads in flight) beats the 4-column
+// form (HZ_V4_MIN_ELEMS overrides).
+int64_t stencil_v4_min_elems() {
+  static const int64_t v = [] {
+    const char* e = std::getenv("HZ_V4_MIN_ELEMS");
+    return e ? int64_t(std::atoll(e)) : int64_t(0);
+  }();
+  return v;
+}
+
 template <class T, int MODE>
 void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out,
                     T wj, cudaStream_t s) {
@@ -762,7 +773,7 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
       level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
     else
       level_kernel<T, 2, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
-  } else if (op.g.k % 4 == 0) {
+  } else if (op.g.k % 4 == 0 && total >= stencil_v4_min_elems()) {
     const int g4 = grid_for(total / 4, kBlock);
     static const int variant = [] {
       const char* e = std::getenv("HZ_STENCIL_VARIANT");
