@@ -240,7 +240,13 @@ class Fgmres {
                int max_cycles, cudaStream_t s);
   // slab mode: B, X and the basis span the parts; s must be part 0's stream
   void set_slabs(const Slabs* sl) {
-    if (sl != sl_) n_ = 0;
+    if (sl != sl_) {  // re-laid out at the next solve: free the old basis now
+      n_ = 0;
+      Vb_.clear();
+      Zb_.clear();
+      R_.release();
+      alg_.tmp_blk.release();
+    }
     sl_ = sl;
   }
 

@@ -45,6 +45,8 @@ if __name__ == "__main__":
         B = torch.from_numpy(cfg.rhs_block()).cuda()
         # HZ_SLABS="1,8": solve once per slab count (parts as streams on this GPU)
         for slabs in [int(x) for x in os.environ.get("HZ_SLABS", "1").split(",")]:
+            X = None
+            torch.cuda.empty_cache()
             S.set_slabs(slabs)
             if os.environ.get("HZ_WARM", "1") == "1" and cfg.num_nodes * cfg.k < 2 ** 27:
                 S.solve_block(B)  # warm-up solve (first-launch costs), not timed
