@@ -35,13 +35,13 @@ sys.path.insert(0, ROOT)
 METRIC = "Helmholtz RHS solved/sec to 1e-6 residual"
 UNIT = "RHS/s"
 
-# The BASELINE config-2 solver (config 2 leaves levels / shift / Krylov
-# unstated): c128 block FGMRES(5) (restart = the reference's
-# HelmholtzSolveOptions default, inc/helmholtz_solver.hpp:21) + c64
-# shifted-Laplacian V(2,2) (w_J 0.8), 4 levels to a 129x65 coarse grid
-# (SURVEY §8d), shift 1.0 -- at shift 0.5 the 4-level V-cycle stalls in the
-# reference oracle and on the GPU alike (DESIGN.md §"Workload").
-WORKLOAD = dict(cfg=2, k=32, nlevels=5, shift=1.0, cycle="V", restart=3, tol=1e-6,
+# The BASELINE config-2 solver (config 2 leaves levels / shift / cycle /
+# Krylov unstated): c128 block FGMRES(3) + c64 shifted-Laplacian V(2,2),
+# 5 levels to a 65x33 coarse grid, shift 0.9, damped-Jacobi weight 0.6 --
+# the fastest converging setting of the GPU sweeps (DESIGN.md §5,
+# profiles/r01_sweep_cycle_cfg2*.jsonl); at shift 0.5 / w_J 0.8 the V-cycle
+# stalls in the reference oracle and on the GPU alike.
+WORKLOAD = dict(cfg=2, k=32, nlevels=5, shift=0.9, jacobi_weight=0.6, cycle="V", restart=3, tol=1e-6,
                 max_cycles=2000, precond="c64")
 
 
@@ -133,6 +133,7 @@ def build_workload(rank, world, k):
     cfg = configs.config2(nlevels=WORKLOAD["nlevels"], k=k)
     cfg.source_nodes = rank_sources(cfg, rank, world, k)
     cfg.shift = WORKLOAD["shift"]
+    cfg.jacobi_weight = WORKLOAD["jacobi_weight"]
     cfg.cycle = WORKLOAD["cycle"]
     cfg.restart = WORKLOAD["restart"]
     cfg.tol = WORKLOAD["tol"]
@@ -155,9 +156,9 @@ def config_json(cfg, world, l2_note):
 # with the full oracle solve, scripts/ref_full_solve.py; used to extrapolate
 # the bounded CPU samples when no GPU count is at hand).
 REF_CYCLES = None
-# GPU cycle count of this workload (FGMRES(3), 5 levels, shift 1.0, k = 32;
-# scripts/sweep_bench_solver.py, profiles/r01_bench_solver_sweep.jsonl).
-DEFAULT_CYCLES = 503
+# GPU cycle count of this workload (FGMRES(3), 5 levels, shift 0.9, w_J 0.6,
+# k = 32; scripts/sweep_cycle_cfg2.py, profiles/r01_sweep_cycle_cfg2b.jsonl).
+DEFAULT_CYCLES = 429
 
 
 class ReferenceRunner:
@@ -313,22 +314,51 @@ def run_ours(args):
     total_ms = sum(r["ms"] for r in kern.values()) or 1.0
     for name, r in kern.items():
         table[name]["share"] = round(r["ms"] / total_ms, 4)
-    # dominant HBM-roofline kernel: the grid stencil / smoother with the largest share
-    stencil = {n_: r for n_, r in kern.items() if n_.startswith(("jacobi", "residual", "apply", "restrict",
-                                                                  "prolong"))}
-    dom = max(stencil or kern, key=lambda n_: kern[n_]["ms"])
-    r = kern[dom]
-    achieved = r["bytes"] / (r["ms"] / 1e3) / 1e9
-    traffic = None
+    # roofline of the dominant kernel (largest share of the step): the FP64
+    # tall-skinny Gram / block update at k = 32 are bound by the FP64 tensor
+    # pipe (DMMA; 8 flop/B > the FP64 ridge), the grid kernels by HBM
+    traffic_tab = {}
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(dom)
+            traffic_tab = json.load(open(tfile))
         except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "algorithmic_bytes_per_launch": r["bytes"] / r["count"], "peak_source": peak_kind}
+            traffic_tab = {}
+    try:
+        fp64_peak, fp64_src = hz.measure_fp64_peak(), "measured live (hz_measure_fp64_peak, DMMA m8n8k4)"
+    except Exception:
+        fp64_peak, fp64_src = 37.1, "fallback: scripts/micro/fp64_peak.cu measurement on this pool"
+
+    def roof(name):
+        r = kern[name]
+        secs = r["ms"] / 1e3
+        gbs = r["bytes"] / secs / 1e9
+        per = {"kernel": name, "launches": r["count"],
+               "algorithmic_bytes_per_launch": r["bytes"] / r["count"],
+               "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
+               "traffic": (traffic_tab.get(name) or {}).get("dram_bytes_per_launch"),
+               "traffic_note": (traffic_tab.get(name) or {}).get("note")}
+        if r.get("flops", 0) > 0:
+            tf = r["flops"] / secs / 1e12
+            per.update({"bound": "tensor", "achieved": round(tf, 2), "peak": round(fp64_peak, 2),
+                        "unit": "TFLOP/s", "frac": round(tf / fp64_peak, 4), "peak_source": fp64_src,
+                        "flops_note": "algorithmic complex flops 8nk^2 per block; issued real flops are 3/4 of "
+                                      "that (3-multiplication complex product)",
+                        "issued_frac": round(0.75 * tf / fp64_peak, 4)})
+        else:
+            per.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(gbs / peak, 4), "peak_source": peak_kind})
+        return per
+
+    dom = max(kern, key=lambda n_: kern[n_]["ms"])
+    roofline = roof(dom)
+    roofline["share"] = table[dom]["share"]
+    stencil = [n_ for n_ in kern if n_.startswith(("jacobi", "residual", "apply", "restrict", "prolong"))]
+    roof_st = None
+    if stencil:
+        dst = max(stencil, key=lambda n_: kern[n_]["ms"])
+        roof_st = roof(dst)
+        roof_st["share"] = table[dst]["share"]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128",
@@ -337,7 +367,7 @@ def run_ours(args):
             "cycles_per_solve": statistics.mean(cycles), "setup_s": round(setup_s, 3),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B_host.nbytes),
                     "d2h_bytes_per_step": int(B_host.nbytes)},
-            "roofline": roofline, "kernels": table, "gpu_launches": int(launches),
+            "roofline": roofline, "roofline_stencil": roof_st, "kernels": table, "gpu_launches": int(launches),
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:

@@ -242,6 +242,11 @@ HZ_API int hz_solve_helmholtz_compact16(hz_solver* s, int64_t n, int k, const do
 HZ_API int hz_profile_begin(void);
 HZ_API int hz_profile_end(void);
 HZ_API int64_t hz_profile_report(char* buf, int64_t cap);
+/* Diagnostic (no reference counterpart): the FP64 tensor-pipe (DMMA,
+   mma.sync m8n8k4 f64) peak of the current device in TFLOP/s, measured by a
+   ~50 ms register-only kernel -- the roofline denominator of the FP64-bound
+   Gram / block-update kernels (MEASURED_PEAKS.json has no FP64 figure). */
+HZ_API int hz_measure_fp64_peak(double* tflops);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,14 @@ def device_count() -> int:
     return int(_native.lib().hz_device_count())
 
 
+def measure_fp64_peak() -> float:
+    """FP64 tensor-pipe (DMMA) peak of the current device, TFLOP/s, measured
+    live (the denominator of the FP64-bound Gram / block-update kernels)."""
+    v = C.c_double()
+    _check(_native.lib().hz_measure_fp64_peak(C.byref(v)))
+    return float(v.value)
+
+
 class kernel_profile:
     """Context manager: CUDA-event timing of every library kernel launched
     inside the block. `.result` maps kernel name -> {count, ms, bytes, flops}

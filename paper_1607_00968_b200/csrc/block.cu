@@ -10,6 +10,7 @@
 #include "profile.hpp"
 #include "block_tiled.cuh"
 #include "block_dmma.cuh"
+#include "devbuf.hpp"
 
 #include <cstdlib>
 #include <type_traits>
@@ -795,5 +796,51 @@ void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const do
 HZ_INST(double)
 HZ_INST(float)
 #undef HZ_INST
+
+namespace {
+// 4 independent DMMA accumulator chains per warp, operands in registers
+__global__ void __launch_bounds__(256) dmma_peak_kernel(double* out, int iters) {
+  const double a = threadIdx.x * 1e-9, b = 1.0;
+  double d[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) dmma::mma884(d[c][0], d[c][1], a, b);
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = d[0][0] + d[0][1] + d[1][0] + d[1][1] + d[2][0] + d[2][1] +
+                                               d[3][0] + d[3][1];
+}
+}  // namespace
+
+double measure_dmma_tflops() {
+  int dev = 0, sms = 0;
+  HZ_CUDA(cudaGetDevice(&dev));
+  HZ_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int blocks = sms * 8, threads = 256, iters = 400;
+  DevBuf<double> out;
+  out.alloc(size_t(blocks) * threads);
+  cudaEvent_t e0, e1;
+  HZ_CUDA(cudaEventCreate(&e0));
+  HZ_CUDA(cudaEventCreate(&e1));
+  dmma_peak_kernel<<<blocks, threads>>>(out.get(), 20);  // warm-up / clocks up
+  HZ_LAUNCH_CHECK();
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    HZ_CUDA(cudaEventRecord(e0));
+    dmma_peak_kernel<<<blocks, threads>>>(out.get(), iters);
+    HZ_LAUNCH_CHECK();
+    HZ_CUDA(cudaEventRecord(e1));
+    HZ_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    HZ_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    best = ms < best ? ms : best;
+  }
+  HZ_CUDA(cudaEventDestroy(e0));
+  HZ_CUDA(cudaEventDestroy(e1));
+  // 2 * 8*8*4 flops per mma, 64 mma per iteration per warp
+  const double flops = 2.0 * 256 * 64.0 * iters * (double(blocks) * threads / 32);
+  return flops / (double(best) * 1e-3) / 1e12;
+}
 
 }  // namespace hz

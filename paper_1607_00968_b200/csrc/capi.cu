@@ -48,6 +48,17 @@ cudaEvent_t profile_event() {
   return g_prof_pool[g_prof_next++];
 }
 
+const char* profile_name_level(const char* base, int level) {
+  if (!g_prof_on) return base;
+  static std::mutex mu;
+  static std::map<std::string, std::unique_ptr<std::string>> names;
+  std::string key = std::string(base) + "_L" + std::to_string(level);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& slot = names[key];
+  if (!slot) slot = std::make_unique<std::string>(key);
+  return slot->c_str();
+}
+
 void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   g_prof_recs.push_back({name, bytes, flops, a, b});
@@ -290,6 +301,13 @@ int hz_device_count(void) {
   return n;
 }
 int64_t hz_kernel_launch_count(void) { return g_launches.load(); }
+
+int hz_measure_fp64_peak(double* tflops) {
+  return guarded([&] {
+    if (!tflops) throw HzError(kValidation, "hz_measure_fp64_peak: null output");
+    *tflops = measure_dmma_tflops();
+  });
+}
 
 int hz_profile_begin(void) {
   return guarded([&] {

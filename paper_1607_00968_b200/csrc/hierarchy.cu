@@ -356,6 +356,7 @@ LevelOp<T> Hierarchy<T>::op(int l, int k) const {
   o.coef = L.coef.get();
   o.inv_diag = L.inv_diag.get();
   for (int a = 0; a < 3; ++a) o.w[a] = L.w[a];
+  o.level = l;
   return o;
 }
 
@@ -537,7 +538,6 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
 template <class T>
 void Hierarchy<T>::coarse_correction(int l, const CycleSpec& spec, int k, const V* b, V* cur, bool cur_zero,
                                      cudaStream_t s) {
-  const int L = num_levels();
   const bool sl = slab_level(l);
   const size_t rowb = size_t(k) * sizeof(V);
   if (cur_zero)
@@ -562,10 +562,23 @@ void Hierarchy<T>::coarse_correction(int l, const CycleSpec& spec, int k, const 
     launch_restrict<T>(op(l, k).g, gc, ndim_, wr_[l].get(), wb_[l + 1].get(), s);
   }
   V* ec = wx_[l + 1].get();
-  const V* rc = wb_[l + 1].get();
   // the first agglomerated level runs on part 0 alone
   const bool agg = sl && !slab_level(l + 1);
   if (agg) sl_->join();
+  coarse_visit(l, spec, k, s);
+  if (agg) sl_->fork();
+  if (sl) sl_->neighbours();
+  on_level(l, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
+    launch_prolong_correct<T>(o.g, gc, ndim_, ec, cur, st);
+  });
+}
+
+template <class T>
+void Hierarchy<T>::coarse_visit(int l, const CycleSpec& spec, int k, cudaStream_t s) {
+  const int L = num_levels();
+  const bool sl = slab_level(l);
+  V* ec = wx_[l + 1].get();
+  const V* rc = wb_[l + 1].get();
   switch (spec.kind) {
     case CycleKind::V:
       cycle_rec(l + 1, spec, k, rc, ec, true, s);
@@ -583,11 +596,6 @@ void Hierarchy<T>::coarse_correction(int l, const CycleSpec& spec, int k, const 
         kcycle_coarse(l + 1, spec, k, rc, ec, s);
       break;
   }
-  if (agg) sl_->fork();
-  if (sl) sl_->neighbours();
-  on_level(l, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
-    launch_prolong_correct<T>(o.g, gc, ndim_, ec, cur, st);
-  });
 }
 
 // One cycle of the complex64 hierarchy applied to a complex128 block (the

@@ -26,6 +26,7 @@ struct LevelOp {
   const V* coef = nullptr;     // kStencil: [S][nodes]
   const V* inv_diag = nullptr; // Jacobi D^{-1} per node
   T w[3] = {0, 0, 0};          // kFine off-diagonal weights (0 on flat axes)
+  int level = 0;               // multigrid level (profiling names only)
 };
 
 // out = A u                                    (K1: apply_block)
@@ -170,6 +171,9 @@ void launch_mgs_qr(int64_t n, int k, cplx_t<T>* W, cplx_t<T>* R, cplx_t<T>* dbuf
 template <class T>
 void launch_pip_factor(int k, int nb, const cplx_t<T>* Hc, cplx_t<T>* R, cplx_t<T>* Rinv,
                        cplx_t<T>* C, int* flag, T eta2, cudaStream_t s);
+
+// FP64 tensor-pipe (DMMA) peak of the current device, TFLOP/s (diagnostic)
+double measure_dmma_tflops();
 
 // sensitivity: g[i] (+)= sum_s Re(-omega^2 gf[i] u[i][s] lam[i][s])  (K13)
 void launch_sensitivity(int64_t n, int k, double w2, const double2* gf, const double2* U,

@@ -14,6 +14,8 @@ namespace hz {
 bool profiling_enabled();
 void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b);
 cudaEvent_t profile_event();
+// interned "<base>_L<level>" (stable pointer for the profile records)
+const char* profile_name_level(const char* base, int level);
 
 class ProfScope {
  public:

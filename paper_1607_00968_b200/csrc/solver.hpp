@@ -130,6 +130,9 @@ class Hierarchy {
   void kcycle_coarse(int l, const CycleSpec& spec, int k, const V* b, V* x, cudaStream_t s);
   void coarse_correction(int l, const CycleSpec& spec, int k, const V* b, V* cur, bool cur_zero,
                          cudaStream_t s);
+  // the coarse visit(s) of level l's correction: level l+1 solved from
+  // wb_[l+1] into wx_[l+1] (V / W / K per spec.kind)
+  void coarse_visit(int l, const CycleSpec& spec, int k, cudaStream_t s);
   bool slab_level(int l) const { return sl_ && l < sl_->agg_level(); }
   // f(op, stream, row0, rows) once per part owning level l (slab levels), or
   // once on stream s over the whole grid

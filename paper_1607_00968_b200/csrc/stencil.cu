@@ -730,13 +730,17 @@ double level_bytes(const LevelOp<T>& op, int mode) {
 }
 
 template <class T, int MODE>
-const char* level_name(int kind) {
+const char* level_name(int kind, int level) {
   static const char* names[2][3][2] = {
       {{"apply_fine_c128", "apply_fine_c64"}, {"residual_fine_c128", "residual_fine_c64"},
        {"jacobi_fine_c128", "jacobi_fine_c64"}},
       {{"apply_stencil_c128", "apply_stencil_c64"}, {"residual_stencil_c128", "residual_stencil_c64"},
        {"jacobi_stencil_c128", "jacobi_stencil_c64"}}};
-  return names[kind][MODE][sizeof(T) == 8 ? 0 : 1];
+  const char* base = names[kind][MODE][sizeof(T) == 8 ? 0 : 1];
+  if (kind == kFine) return base;
+  // Galerkin levels by level index: level 1 streams from HBM, deeper levels
+  // are L2-resident and launch/latency bound, so they are reported apart
+  return profile_name_level(base, level);
 }
 
 // Below this many (node, column) elements a Galerkin level is latency bound
@@ -755,7 +759,7 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
                     T wj, cudaStream_t s) {
   const int64_t total = op.g.owned_elems();
   const int grid = grid_for(total, kBlock);
-  ProfScope prof(level_name<T, MODE>(op.kind), level_bytes(op, MODE), s);
+  ProfScope prof(level_name<T, MODE>(op.kind, op.level), level_bytes(op, MODE), s);
   static const bool fine_v4 = [] {
     const char* e = std::getenv("HZ_FINE_V4");
     return !(e && e[0] == '0');
