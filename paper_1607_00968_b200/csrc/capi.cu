@@ -196,6 +196,15 @@ DevOp<double> make_slab_op(hz_solver* s, int k) {
       launch_apply<double>(o, in, out, st);
     });
   };
+  op.resid = [s, P, sl](const double2* x, const double2* b, double2* r, int kk, cudaStream_t) {
+    sl->neighbours();
+    sl->each(0, [&](int p, int64_t, int64_t, cudaStream_t st) {
+      LevelOp<double> o = P->fine_op(kk);
+      o.center = s->center_on(sl->part(p).device);
+      o.g = o.g.slab(sl->z0(0, p), sl->z1(0, p));
+      launch_apply_residual<double>(o, x, b, r, st);
+    });
+  };
   if (s->opts.precond_precision == HZ_C64) {
     op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
       s->h32->cycle_cast(s->spec, kk, in, out, st);
@@ -215,6 +224,9 @@ DevOp<double> make_op(hz_solver* s, int k) {
   op.n = P->num_nodes();
   op.apply = [P](const double2* in, double2* out, int kk, cudaStream_t st) {
     launch_apply<double>(P->fine_op(kk), in, out, st);
+  };
+  op.resid = [P](const double2* x, const double2* b, double2* r, int kk, cudaStream_t st) {
+    launch_apply_residual<double>(P->fine_op(kk), x, b, r, st);
   };
   if (s->opts.precond_precision == HZ_C64) {
     op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {

@@ -36,6 +36,12 @@ void launch_apply(const LevelOp<T>& op, const cplx_t<T>* u, cplx_t<T>* out, cuda
 template <class T>
 void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
                      cudaStream_t s);
+// r = b - A x for the fine operator with A x in apply_block order: the
+// fused, bitwise-identical form of apply + axpby(-1, r, 1, b) (the true
+// residual of block_fgmres / finalize, src/krylov.cpp:35-37,270-271)
+template <class T>
+void launch_apply_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
+                           cudaStream_t s);
 // xout = x + (wj D^{-1}) (b - A x)             (K2: relax, src/multigrid.cpp:119-136)
 template <class T>
 void launch_jacobi(const LevelOp<T>& op, T wj, const cplx_t<T>* x, const cplx_t<T>* b,

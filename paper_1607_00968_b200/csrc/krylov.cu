@@ -256,7 +256,7 @@ void BlockAlgebra<T>::ensure(int64_t n_, int k_, int max_blocks, const Slabs* sl
   rnorm.ensure(k);
   flags.ensure(2);
   h_norm.ensure(k);
-  h_R.ensure(2 * size_t(k) * k);
+  h_R.ensure(3 * size_t(k) * k);
   h_flags.ensure(2);
 }
 
@@ -334,6 +334,81 @@ void BlockAlgebra<T>::thin_qr_enqueue(V* W, cudaStream_t s) {
 }
 
 template <class T>
+void BlockAlgebra<T>::self_gram_norms(const V* W, std::vector<double>& out, cudaStream_t s) {
+  BlockTab<T> t{};
+  t.p[0] = W;
+  gram(t, 1, W, G.get(), s);
+  const size_t kk = size_t(k) * k;
+  HZ_CUDA(cudaMemcpyAsync(h_R.get() + 2 * kk, G.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  out.resize(k);
+  for (int j = 0; j < k; ++j) out[j] = std::sqrt(std::max(0.0, double(h_R[2 * kk + size_t(j) * (k + 1)].x)));
+}
+
+template <class T>
+void BlockAlgebra<T>::thin_qr_from(const V* src, V* dst, std::vector<cplx>& R, bool& deficient, double eta2,
+                                   cudaStream_t s) {
+  const size_t kk = size_t(k) * k;
+  const T tol = std::is_same<T, double>::value ? T(1e-5) : T(1e-3);
+  launch_small_cholesky<T>(k, G.get(), R1.get(), R1i.get(), flags.get(), tol, s);
+  HZ_CUDA(cudaMemcpyAsync(h_R.get(), R1.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaMemcpyAsync(h_flags.get(), flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  R.assign(kk, cplx{});
+  if (h_flags[0] != 0) {
+    // near rank deficiency: the column Gram-Schmidt on a copy of src
+    each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+      HZ_CUDA(cudaMemcpyAsync(dst + r0 * k, src + r0 * k, size_t(nr) * k * sizeof(V), cudaMemcpyDeviceToDevice, st));
+    });
+    join();
+    dbuf.ensure(192);
+    launch_mgs_qr<T>(n, k, dst, R1.get(), dbuf.get(), partials.get(), nslots, flags.get(), s);
+    HZ_CUDA(cudaMemcpyAsync(h_R.get(), R1.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaMemcpyAsync(h_flags.get(), flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    HZ_CUDA(cudaStreamSynchronize(s));
+    fork();
+    for (size_t e = 0; e < kk; ++e) R[e] = to_c(h_R[e]);
+    deficient = h_flags[0] != 0;
+    mgs_used = true;
+    return;
+  }
+  mgs_used = false;
+  // smallest pivot^2 / column norm^2 (G's diagonal is in h_R[2kk..] when
+  // self_gram_norms produced G; otherwise fetch it)
+  double worst = 1.0;
+  for (int j = 0; j < k; ++j) {
+    const double d = double(h_R[size_t(j) * (k + 1)].x);
+    const double g = double(h_R[2 * kk + size_t(j) * (k + 1)].x);
+    if (g > 0) worst = std::min(worst, d * d / g);
+  }
+  BlockTab<T> t{};
+  t.p[0] = src;
+  fork();
+  if (worst >= eta2) {
+    update(1, t, R1i.get(), nullptr, dst, T(1), s);
+    for (size_t e = 0; e < kk; ++e) R[e] = to_c(h_R[e]);
+    deficient = false;
+    return;
+  }
+  update(1, t, R1i.get(), nullptr, tmp_blk.get(), T(1), s);
+  t.p[0] = tmp_blk.get();
+  gram(t, 1, tmp_blk.get(), G.get(), s);
+  launch_small_cholesky<T>(k, G.get(), R2.get(), R2i.get(), flags.get() + 1, tol, s);
+  fork();
+  update(1, t, R2i.get(), nullptr, dst, T(1), s);
+  HZ_CUDA(cudaMemcpyAsync(h_R.get() + kk, R2.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaMemcpyAsync(h_flags.get() + 1, flags.get() + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HZ_CUDA(cudaStreamSynchronize(s));
+  for (int p = 0; p < k; ++p)
+    for (int q = p; q < k; ++q) {
+      cplx v{};
+      for (int l = p; l <= q; ++l) v += to_c(h_R[kk + size_t(p) * k + l]) * to_c(h_R[size_t(l) * k + q]);
+      R[size_t(p) * k + q] = v;
+    }
+  deficient = h_flags[1] != 0;
+}
+
+template <class T>
 void BlockAlgebra<T>::thin_qr_finish(std::vector<cplx>& R, bool& deficient) {
   const size_t kk = size_t(k) * k;
   R.assign(kk, cplx{});
@@ -371,6 +446,7 @@ void Fgmres<T>::ensure(int64_t n, int k, int restart) {
   for (auto& b : Vb_) get(b);
   for (auto& b : Zb_) get(b);
   get(R_);
+  get(Qs_);
   hcol1_.alloc(size_t(restart + 2) * k * k);
   ccoef_.alloc(size_t(restart + 2) * k * k);
   hcol2_.alloc(size_t(restart + 1) * k * k);
@@ -425,13 +501,33 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
   std::vector<std::vector<std::vector<cplx>>> H(m);  // H[j] = tiles i = 0..j+1
   std::vector<double> res;
   std::vector<cplx> Rk;
+  // true residual R = B - A X (fused kernel when the operator provides it)
+  auto true_residual = [&]() {
+    if (op.resid) {
+      op.resid(X, B, R_.get(), k, s);
+      return;
+    }
+    op.apply(X, R_.get(), k, s);
+    alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
+      launch_axpby<T>(nr * k, mk(T(-1), T(0)), R_.get() + r0 * k, mk(T(1), T(0)), B + r0 * k, st);
+    });
+  };
+  // one-pass CholQR of the restart residual when well conditioned (every
+  // pivot keeps qr_eta2 of its column norm^2), else CholQR2 (thin_qr_from)
+  const double qr_eta2 = [] {
+    const char* e = std::getenv("HZ_QR_ETA2");
+    return e ? std::atof(e) : 1e-4;
+  }();
+  bool have_gram = false;  // alg_.G holds R^H R of the current R_
   while (!done && rep.cycles < max_cycles) {
-    // Arnoldi from the current residual: V_0 = thin_qr(R)
-    copy_blk(Vb_[0].get(), R_.get());
-    alg_.thin_qr_enqueue(Vb_[0].get(), s);
-    HZ_CUDA(cudaStreamSynchronize(s));
+    // Arnoldi from the current residual: V_0 = thin_qr(R) (src/krylov.cpp:196-200)
+    if (!have_gram) {
+      std::vector<double> unused;
+      alg_.self_gram_norms(R_.get(), unused, s);
+    }
+    have_gram = false;
     bool rd = false;
-    alg_.thin_qr_finish(Rk, rd);
+    alg_.thin_qr_from(R_.get(), Vb_[0].get(), Rk, rd, qr_eta2, s);
     ++rep.qr_factorizations;
     lsq.reset(k, m, Rk);
     int j = 0;
@@ -470,14 +566,31 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
         HZ_CUDA(cudaMemcpyAsync(alg_.h_flags.get(), alg_.flags.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
         HZ_CUDA(cudaMemcpyAsync(h_hcol_.get(), hcol1_.get(), sizeof(V) * hc, cudaMemcpyDeviceToHost, s));
         HZ_CUDA(cudaMemcpyAsync(alg_.h_R.get(), alg_.R1.get(), sizeof(V) * kk, cudaMemcpyDeviceToHost, s));
-        HZ_CUDA(cudaStreamSynchronize(s));
+        HZ_CUDA(cudaEventRecord(ev_.get(), s));
+        // Speculate acceptance (the common case): Q = (W - V H) R^{-1} into
+        // the spare block and the next step's preconditioner + matvec from
+        // it, queued behind the flag copies; the host decides meanwhile. A
+        // rejected step leaves W untouched and the speculative results are
+        // overwritten by the CGS2 path and its own next-step enqueue.
+        const bool spec_next = j + 1 < m && rep.cycles < max_cycles;
+        alg_.fork();
+        alg_.update(j + 2, vtab_, ccoef_.get(), nullptr, Qs_.get(), T(1), s);
+        if (spec_next) {
+          V* Zn = Zb_[j + 1].get();
+          if (op.prec)
+            op.prec(Qs_.get(), Zn, k, s);
+          else
+            copy_blk(Zn, Qs_.get());
+          op.apply(Zn, Vb_[j + 2].get(), k, s);
+        }
+        HZ_CUDA(cudaEventSynchronize(ev_.get()));
         if (alg_.h_flags[0] == 0) {
           accepted = true;
           ++pip_accepted_;
-          // W <- sum_i V_i C_i + W C_{j+1} = (W - V H) R^{-1}  (in place: each
-          // CTA stages its rows of every block before writing them)
-          alg_.fork();
-          alg_.update(j + 2, vtab_, ccoef_.get(), nullptr, W, T(1), s);
+          std::swap(Vb_[j + 1], Qs_);
+          vtab_.p[j + 1] = Vb_[j + 1].get();
+          W = Vb_[j + 1].get();
+          prefetched = spec_next;
           for (int i = 0; i <= j; ++i)
             for (size_t e = 0; e < kk; ++e) H[j][i][e] = cplx{} + to_c(h_hcol_[i * kk + e]);
           for (size_t e = 0; e < kk; ++e) H[j][j + 1][e] = to_c(alg_.h_R[e]);
@@ -510,7 +623,7 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
         ++j;
         break;  // happy breakdown
       }
-      if (j + 1 < m && rep.cycles < max_cycles) {
+      if (!accepted && j + 1 < m && rep.cycles < max_cycles) {
         enqueue_step(j + 1);
         prefetched = true;
       }
@@ -530,22 +643,18 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
                             cudaMemcpyHostToDevice, s));
     alg_.fork();
     alg_.update(j, ztab_, ydev_.get(), X, X, T(1), s);
-    // true residual for the restart / convergence decision
-    op.apply(X, R_.get(), k, s);
-    alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
-      launch_axpby<T>(nr * k, mk(T(-1), T(0)), R_.get() + r0 * k, mk(T(1), T(0)), B + r0 * k, st);
-    });
+    // true residual for the restart / convergence decision; its norms come
+    // from the Gram the next restart's QR starts from
+    true_residual();
     std::vector<double> rn;
-    alg_.col_norms(R_.get(), rn, s);
+    alg_.self_gram_norms(R_.get(), rn, s);
+    have_gram = true;
     double worst = 0.0;
     for (int c = 0; c < k; ++c) worst = std::max(worst, rn[c] / bnorm[c]);
     if (worst <= tol) done = true;
   }
   // finalize (src/krylov.cpp:33-46)
-  op.apply(X, R_.get(), k, s);
-  alg_.each(s, [&](int, int64_t r0, int64_t nr, cudaStream_t st) {
-    launch_axpby<T>(nr * k, mk(T(-1), T(0)), R_.get() + r0 * k, mk(T(1), T(0)), B + r0 * k, st);
-  });
+  true_residual();
   std::vector<double> rn;
   alg_.col_norms(R_.get(), rn, s);
   rep.rel_residual.resize(k);

@@ -172,6 +172,8 @@ struct DevOp {
   int64_t n = 0;
   std::function<void(const V* in, V* out, int k, cudaStream_t)> apply;
   std::function<void(const V* in, V* out, int k, cudaStream_t)> prec;  // optional
+  // optional fused true residual r = b - A x (bitwise apply + axpby)
+  std::function<void(const V* x, const V* b, V* r, int k, cudaStream_t)> resid;
 };
 
 // Device block algebra shared by the Krylov methods.
@@ -190,6 +192,15 @@ class BlockAlgebra {
   // available after sync in host_R()/host_deficient().
   void thin_qr_enqueue(V* W, cudaStream_t s);
   void thin_qr_finish(std::vector<cplx>& R, bool& deficient);  // after stream sync
+  // G = W^H W on device (kept for thin_qr_from) and the column 2-norms
+  // sqrt(diag G) to host: one pass over W instead of col_norms + a QR Gram
+  void self_gram_norms(const V* W, std::vector<double>& out, cudaStream_t s);
+  // thin QR of src into dst (dst != src) from the Gram G = src^H src
+  // already on device: one CholQR pass when every Cholesky pivot keeps eta2
+  // of its column's norm^2 (then Q^H Q = I to ~eps/eta2), else CholQR2, or
+  // the column Gram-Schmidt for near rank deficiency; R / deficient as
+  // thin_qr_finish. Synchronises the stream.
+  void thin_qr_from(const V* src, V* dst, std::vector<cplx>& R, bool& deficient, double eta2, cudaStream_t s);
 
   int64_t n = 0;
   int k = 0;
@@ -200,7 +211,7 @@ class BlockAlgebra {
   DevBuf<V> dbuf;         // column Gram-Schmidt dot products
   bool mgs_used = false;  // last thin_qr took the column Gram-Schmidt path
   PinnedBuf<T> h_norm;
-  PinnedBuf<V> h_R;     // [R1 | R2]
+  PinnedBuf<V> h_R;     // [R1 | R2 | G]
   PinnedBuf<int> h_flags;
 
   // ---- slab mode: row-local work runs per part on the part's rows; the
@@ -248,6 +259,7 @@ class Fgmres {
       Vb_.clear();
       Zb_.clear();
       R_.release();
+      Qs_.release();
       alg_.tmp_blk.release();
     }
     sl_ = sl;
@@ -260,7 +272,20 @@ class Fgmres {
   int k_ = 0, m_ = 0;
   std::vector<DevBuf<V>> Vb_, Zb_;
   DevBuf<V> R_;
+  DevBuf<V> Qs_;  // spare block: the speculative one-pass Q of an Arnoldi step
   BlockTab<T> vtab_{}, ztab_{};
+  // marks the D2H copies of a step's acceptance flag / H column, so the host
+  // waits for them without draining the speculative work behind them
+  struct Event {
+    cudaEvent_t e = nullptr;
+    ~Event() {
+      if (e) cudaEventDestroy(e);
+    }
+    cudaEvent_t get() {
+      if (!e) HZ_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      return e;
+    }
+  } ev_;
   DevBuf<V> hcol1_, hcol2_, ydev_, ccoef_;
   // Pythagorean one-pass orthogonalisation with CGS2 fallback (HZ_ORTHO=cgs2
   // forces the two-pass path everywhere)

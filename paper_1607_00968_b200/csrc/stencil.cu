@@ -132,6 +132,8 @@ __device__ __forceinline__ cplx_t<T> level_ax(const LevelOp<T>& op, const cplx_t
 }
 
 // MODE 0: out = A x ; 1: out = b - A x ; 2: out = x + (wj dinv)(b - A x)
+// MODE 3: out = b - A x with A x in apply_block order (the fused form of
+// apply + axpby(-1, r, 1, b): bitwise the same values)
 template <class T, int NDIM, int KIND, int MODE>
 __global__ void __launch_bounds__(kBlock)
 level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
@@ -140,10 +142,10 @@ level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __
   const uint32_t e = op.g.e_begin() + blockIdx.x * kBlock + threadIdx.x;
   Elem<T> el;
   if (!decode(op.g, e, el)) return;
-  const V ax = level_ax<T, NDIM, KIND, MODE != 0>(op, x, e, el);
+  const V ax = level_ax<T, NDIM, KIND, MODE == 1 || MODE == 2>(op, x, e, el);
   if (MODE == 0) {
     out[e] = ax;
-  } else if (MODE == 1) {
+  } else if (MODE == 1 || MODE == 3) {
     out[e] = csub(__ldg(&b[e]), ax);
   } else {
     const V d = __ldg(&op.inv_diag[el.node]);
@@ -302,7 +304,7 @@ fine_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* 
                Out* __restrict__ out, T wj) {
   using V = cplx_t<T>;
   constexpr int CPT = 4;
-  constexpr bool CSR = MODE != 0;
+  constexpr bool CSR = MODE == 1 || MODE == 2;
   const LevelGeom& g = op.g;
   const uint32_t t = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t e0 = g.e_begin() + t * CPT;
@@ -353,7 +355,7 @@ fine_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* 
     }
     if (MODE == 0) {
       o[q] = acc;
-    } else if (MODE == 1) {
+    } else if (MODE == 1 || MODE == 3) {
       o[q] = csub(bv[q], acc);
     } else {
       const V wd = mk(wj * dv.x, wj * dv.y);
@@ -820,6 +822,25 @@ void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* 
   dispatch_level<T, 1>(op, x, b, r, T(0), s);
 }
 template <class T>
+void launch_apply_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
+                           cudaStream_t s) {
+  if (op.kind != kFine) throw HzError(kState, "apply_residual: fine operator only");
+  const int64_t total = op.g.owned_elems();
+  ProfScope prof(sizeof(T) == 8 ? "apply_residual_fine_c128" : "apply_residual_fine_c64", level_bytes(op, 1), s);
+  if (sizeof(T) == 4 && op.g.k % 4 == 0) {
+    const int g4 = grid_for(total / 4, kBlock);
+    if (op.ndim == 3)
+      fine_v4_kernel<T, 3, 3><<<g4, kBlock, 0, s>>>(op, x, b, r, T(0));
+    else
+      fine_v4_kernel<T, 2, 3><<<g4, kBlock, 0, s>>>(op, x, b, r, T(0));
+  } else if (op.ndim == 3) {
+    level_kernel<T, 3, kFine, 3><<<grid_for(total, kBlock), kBlock, 0, s>>>(op, x, b, r, T(0));
+  } else {
+    level_kernel<T, 2, kFine, 3><<<grid_for(total, kBlock), kBlock, 0, s>>>(op, x, b, r, T(0));
+  }
+  HZ_LAUNCH_CHECK();
+}
+template <class T>
 void launch_jacobi(const LevelOp<T>& op, T wj, const cplx_t<T>* x, const cplx_t<T>* b,
                    cplx_t<T>* xout, cudaStream_t s) {
   dispatch_level<T, 2>(op, x, b, xout, wj, s);
@@ -930,6 +951,8 @@ void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s) {
   template void launch_apply<T>(const LevelOp<T>&, const cplx_t<T>*, cplx_t<T>*, cudaStream_t);   \
   template void launch_residual<T>(const LevelOp<T>&, const cplx_t<T>*, const cplx_t<T>*,         \
                                    cplx_t<T>*, cudaStream_t);                                     \
+  template void launch_apply_residual<T>(const LevelOp<T>&, const cplx_t<T>*, const cplx_t<T>*,   \
+                                         cplx_t<T>*, cudaStream_t);                               \
   template void launch_jacobi<T>(const LevelOp<T>&, T, const cplx_t<T>*, const cplx_t<T>*,        \
                                  cplx_t<T>*, cudaStream_t);                                       \
   template void launch_restrict<T>(const LevelGeom&, const LevelGeom&, int, const cplx_t<T>*,     \
