@@ -152,6 +152,17 @@ HZ_API int hz_solve_block(hz_solver* s, int64_t n, int k, const double* B, doubl
 /* device-resident variant (double2*) */
 HZ_API int hz_solve_block_device(hz_solver* s, int64_t n, int k, const void* B_dev, void* X_dev,
                           hz_report* rep);
+/* Multi-frequency batching (no reference counterpart -- the
+   reference solves one (m, omega) at a time): `count` independent block
+   solves, one per solver (each solver owns its hierarchy, stream and Krylov
+   workspace, e.g. one per frequency of a frequency-continuation stage), run
+   concurrently from one host thread each so their kernels overlap on the GPU.
+   Results equal `count` hz_solve_block calls. Solvers must be distinct. The
+   first failing solve's status / message is returned. reps may be NULL. */
+HZ_API int hz_solve_blocks_multi(int count, hz_solver* const* solvers, const int64_t* n, const int* k,
+                                 const double* const* B, double* const* X, hz_report* reps);
+HZ_API int hz_solve_blocks_multi_device(int count, hz_solver* const* solvers, const int64_t* n, const int* k,
+                                        const void* const* B_dev, void* const* X_dev, hz_report* reps);
 
 /* solve_helmholtz contract (src/helmholtz_solver.cpp:81-93): like
  * hz_solve_block but returns HZ_CONVERGENCE if any column misses tol. */

@@ -102,6 +102,78 @@ def measure_fp64_peak() -> float:
     return float(v.value)
 
 
+def solve_blocks_multi(solvers: Sequence["HelmholtzSolver"], Bs, outs=None):
+    """Multi-frequency batching: solvers[i].solve_block(Bs[i])
+    for every i, run concurrently (hz_solve_blocks_multi[_device]: one host
+    thread per solve, kernels overlapping on the GPU). Each solver owns its
+    (m, omega) hierarchy, stream and Krylov workspace -- typically one per
+    frequency of a frequency-continuation stage. Results
+    equal the sequential solves. Bs: all numpy (host) or all torch (device)."""
+    cnt = len(solvers)
+    if len(Bs) != cnt:
+        raise ValidationError("solve_blocks_multi: one right-hand-side block per solver")
+    if len({id(s) for s in solvers}) != cnt:
+        raise ValidationError("solve_blocks_multi: solvers must be distinct")
+    if cnt == 0:
+        return [], []
+    dev = _is_torch(Bs[0])
+    Xs, reps, bufs, ptrB, ptrX, ns, ks = [], [], [], [], [], [], []
+    for i, (S, B) in enumerate(zip(solvers, Bs)):
+        n = S.problem.num_nodes
+        if dev:
+            B = _dev_block(B, n)
+            import torch
+            X = outs[i] if outs is not None else torch.empty_like(B)
+            ptrB.append(B.data_ptr())
+            ptrX.append(X.data_ptr())
+        else:
+            B = _host_block(B, n)
+            X = outs[i] if outs is not None else np.empty_like(B)
+            ptrB.append(B.ctypes.data)
+            ptrX.append(X.ctypes.data)
+        r, b = S._report(B.shape[1], S.options.max_cycles + 8)
+        Xs.append(X)
+        reps.append(r)
+        bufs.append((b, B))
+        ns.append(n)
+        ks.append(B.shape[1])
+    if dev:
+        import torch
+        torch.cuda.synchronize()
+    L = _native.lib()
+    hs = (C.c_void_p * cnt)(*[S._h for S in solvers])
+    rep_arr = (hz_report * cnt)(*reps)
+    nn = (C.c_int64 * cnt)(*ns)
+    kk = (C.c_int * cnt)(*ks)
+    pb = (C.c_void_p * cnt)(*ptrB)
+    px = (C.c_void_p * cnt)(*ptrX)
+    fn = L.hz_solve_blocks_multi_device if dev else L.hz_solve_blocks_multi
+    _check(fn(cnt, hs, nn, kk, pb, px, rep_arr))
+    return Xs, [S._finish(rep_arr[i], bufs[i][0]) for i, S in enumerate(solvers)]
+
+
+class MultiFrequencySolver:
+    """Several (m, omega) hierarchies resident on one GPU: one
+    HelmholtzProblem + HelmholtzSolver per frequency over the same slowness
+    squared m and attenuation, solved as one concurrent batch. The caller is
+    the frequency-continuation loop (Algorithm 1)."""
+
+    def __init__(self, ndim, n, h, m, omegas: Sequence[float], gamma: "AttenuationField",
+                 options: Optional["HelmholtzSolveOptions"] = None, allow_coarse_ppw: bool = False,
+                 device: int = 0):
+        self.omegas = [float(w) for w in omegas]
+        self.problems = [HelmholtzProblem(ndim, n, h, m, w, gamma, allow_coarse_ppw=allow_coarse_ppw,
+                                          device=device) for w in self.omegas]
+        self.solvers = [HelmholtzSolver(P, options) for P in self.problems]
+
+    def __len__(self):
+        return len(self.solvers)
+
+    def solve_blocks(self, Bs, outs=None):
+        """X_f = A(m, omega_f)^{-1} B_f for every frequency f, concurrently."""
+        return solve_blocks_multi(self.solvers, Bs, outs)
+
+
 class kernel_profile:
     """Context manager: CUDA-event timing of every library kernel launched
     inside the block. `.result` maps kernel name -> {count, ms, bytes, flops}

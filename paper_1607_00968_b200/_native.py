@@ -21,7 +21,7 @@ EXPORTS = (
     "hz_cycle", "hz_cycle_device", "hz_coarse_solve", "hz_hierarchy_num_levels",
     "hz_hierarchy_level_dims", "hz_hierarchy_level_coefficients", "hz_sensitivity_accumulate",
     "hz_sensitivity_accumulate_device", "hz_kernel_launch_count", "hz_profile_begin",
-    "hz_profile_end", "hz_profile_report", "hz_measure_fp64_peak", "hz_solver_set_slabs", "hz_solver_slab_info",
+    "hz_profile_end", "hz_profile_report", "hz_measure_fp64_peak", "hz_solve_blocks_multi", "hz_solve_blocks_multi_device", "hz_solver_set_slabs", "hz_solver_slab_info",
     "hz_sampling_create", "hz_sampling_destroy", "hz_sampling_num_receivers", "hz_sampling_receiver",
     "hz_sample_device", "hz_sample", "hz_sample_adjoint_device", "hz_sample_adjoint",
     "hz_fwi_sensitivity_rhs_device", "hz_fwi_jacobian_vec", "hz_fwi_jacobian_vec_device",

@@ -6,6 +6,8 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "../../include/hz_b200.h"
 #include "acquisition.hpp"
@@ -636,6 +638,77 @@ int hz_solve_block(hz_solver* s, int64_t n, int k, const double* B, double* X, h
     Report r = run_solve(s, k, s->dB.get(), s->dX.get());
     download_rows(s, k, s->dX.get(), X);
     fill_report(r, k, rep);
+  });
+}
+
+}  // extern "C"
+
+namespace {
+std::string thread_error() { return g_err; }
+void set_thread_error(const std::string& m) { g_err = m; }
+// one host thread per solve: every solve keeps its own host control flow
+// (syncs included) while the kernels of all of them share the GPU
+template <class F>
+int run_concurrent(int count, hz_solver* const* solvers, F&& one) {
+  if (count < 0) {
+    set_thread_error("multi solve: negative count");
+    return kValidation;
+  }
+  if (count > 0 && !solvers) {
+    set_thread_error("null argument");
+    return kValidation;
+  }
+  for (int i = 0; i < count; ++i) {
+    if (!solvers[i]) {
+      set_thread_error("multi solve: null solver");
+      return kValidation;
+    }
+    for (int j = 0; j < i; ++j)
+      if (solvers[j] == solvers[i]) {
+        set_thread_error("multi solve: solvers must be distinct (each owns its stream and workspace)");
+        return kValidation;
+      }
+  }
+  std::vector<int> st(size_t(count), kOk);
+  std::vector<std::string> errs(static_cast<size_t>(count));
+  std::vector<std::thread> th;
+  th.reserve(size_t(count));
+  for (int i = 0; i < count; ++i)
+    th.emplace_back([&st, &errs, &one, i] {
+      st[i] = one(i);
+      if (st[i] != kOk) errs[i] = thread_error();
+    });
+  for (auto& t : th) t.join();
+  for (int i = 0; i < count; ++i)
+    if (st[i] != kOk) {
+      set_thread_error("multi solve " + std::to_string(i) + ": " + errs[i]);
+      return st[i];
+    }
+  return kOk;
+}
+}  // namespace
+
+extern "C" {
+
+int hz_solve_blocks_multi(int count, hz_solver* const* solvers, const int64_t* n, const int* k,
+                          const double* const* B, double* const* X, hz_report* reps) {
+  if (count > 0 && (!n || !k || !B || !X)) {
+    g_err = "null argument";
+    return kValidation;
+  }
+  return run_concurrent(count, solvers, [&](int i) {
+    return hz_solve_block(solvers[i], n[i], k[i], B[i], X[i], reps ? &reps[i] : nullptr);
+  });
+}
+
+int hz_solve_blocks_multi_device(int count, hz_solver* const* solvers, const int64_t* n, const int* k,
+                                 const void* const* B, void* const* X, hz_report* reps) {
+  if (count > 0 && (!n || !k || !B || !X)) {
+    g_err = "null argument";
+    return kValidation;
+  }
+  return run_concurrent(count, solvers, [&](int i) {
+    return hz_solve_block_device(solvers[i], n[i], k[i], B[i], X[i], reps ? &reps[i] : nullptr);
   });
 }
 

@@ -104,3 +104,99 @@ def fwi_gradient(problem, solver, source_nodes: Sequence[int], receivers,
     allreduce_sum(g)
     allreduce_sum(misfit)
     return GradientResult(g, float(misfit.item()), mine, fcyc, acyc)
+
+
+@dataclasses.dataclass
+class MultiGradientResult:
+    gradient: object              # [n] float64: sum over frequencies (and ranks)
+    misfit: float                 # sum over frequencies of the per-frequency misfits
+    per_frequency: list           # [GradientResult-like (gradient, misfit, cycles)] per frequency
+    local_sources: np.ndarray
+
+
+def fwi_gradient_multi(problems, solvers, source_nodes: Sequence[int], receivers,
+                       d_obs_fn: Callable[[int, np.ndarray], np.ndarray], rank: int = 0, world: int = 1,
+                       device: Optional[str] = None) -> MultiGradientResult:
+    """Multi-frequency FWI gradient: the misfit of one
+    frequency-continuation stage is the sum over its frequencies (PAPER.md
+    Algorithm 1 uses the data of omega_1..omega_k), so its gradient is the sum
+    of the per-frequency gradients of fwi_gradient. All frequencies' forward
+    block solves run as ONE concurrent batch (hz_solve_blocks_multi: one
+    hierarchy / stream per frequency on this GPU), then their adjoint solves
+    run concurrently the same way; per-frequency gradients are summed in
+    frequency order and all-reduced once. d_obs_fn(f, local_source_ids) ->
+    [n_rec, k_local] observed data of frequency f."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from . import SamplingOperator, fwi_jacobian_transpose_vec, solve_blocks_multi
+
+    nf = len(solvers)
+    if len(problems) != nf or nf == 0:
+        raise ValueError("fwi_gradient_multi: one problem per solver, at least one frequency")
+    P0 = problems[0]
+    dev = device or f"cuda:{P0.device}"
+    samplers = []
+    for P in problems:
+        if isinstance(receivers, SamplingOperator):
+            samplers.append(receivers)
+            continue
+        nodes = np.asarray(receivers, dtype=np.int64)
+        n0, n1 = P.n[0], P.n[1]
+        xyz = np.stack([(nodes % n0) * P.h[0], ((nodes // n0) % n1) * P.h[1],
+                        (nodes // (n0 * n1)) * P.h[2]], axis=1).astype(np.float64)
+        samplers.append(SamplingOperator(P, xyz))
+    mine = shard_sources(len(source_nodes), rank, world)
+    src = np.asarray(source_nodes, dtype=np.int64)[mine]
+    n = P0.num_nodes
+    k = len(src)
+    g_f = [torch.zeros(n, dtype=torch.float64, device=dev) for _ in range(nf)]
+    mis_f = [0.0] * nf
+    cyc = [(0, 0)] * nf
+    if k > 0:
+        Q = torch.zeros((n, k), dtype=torch.complex128, device=dev)
+        Q[torch.as_tensor(src, device=dev), torch.arange(k, device=dev)] = 1.0
+        Us, reps_f = solve_blocks_multi(solvers, [Q] * nf)
+        Rs = []
+        for f in range(nf):
+            d = torch.as_tensor(d_obs_fn(f, mine), dtype=torch.complex128, device=dev)
+            r = samplers[f].sample(Us[f]) - d.reshape(samplers[f].num_receivers, k)
+            mis_f[f] = float(0.5 * torch.sum(torch.abs(r) ** 2).item())
+            Rs.append(r)
+        torch.cuda.synchronize()
+
+        def adjoint(f):
+            reps = []
+            fwi_jacobian_transpose_vec(solvers[f], Us[f], samplers[f], Rs[f], g=g_f[f], report=reps)
+            return reps[0].cycles
+
+        with ThreadPoolExecutor(max_workers=nf) as ex:  # ctypes releases the GIL: solves overlap
+            acyc = list(ex.map(adjoint, range(nf)))
+        cyc = [(reps_f[f].cycles, acyc[f]) for f in range(nf)]
+    g = torch.zeros(n, dtype=torch.float64, device=dev)
+    for f in range(nf):  # fixed frequency order
+        g += g_f[f]
+    misfit = torch.tensor([sum(mis_f)], dtype=torch.float64, device=dev)
+    allreduce_sum(g)
+    allreduce_sum(misfit)
+    per = [{"misfit_local": mis_f[f], "forward_cycles": cyc[f][0], "adjoint_cycles": cyc[f][1]} for f in range(nf)]
+    return MultiGradientResult(g, float(misfit.item()), per, mine)
+
+
+def frequency_continuation(m0, omegas: Sequence[float], stage_solve: Callable, start: int = 1):
+    """Frequency continuation, PAPER.md:96-107 (Algorithm 1): with
+    omega_1 < ... < omega_nf, stage k solves the inversion with the data of
+    omega_1..omega_k starting from the previous stage's model:
+        m_k = stage_solve(m_{k-1}, omegas[:k]).
+    stage_solve is the caller's inner inversion (e.g. gradient / Gauss-Newton
+    steps built on MultiFrequencySolver and fwi_gradient_multi; the
+    reference's inversion layer itself is absent). Returns
+    the list of stage models [m_start, ..., m_nf]."""
+    om = [float(w) for w in omegas]
+    if any(b <= a for a, b in zip(om, om[1:])):
+        raise ValueError("frequency_continuation: frequencies must be increasing")
+    models = [m0]
+    m = m0
+    for kk in range(start, len(om) + 1):
+        m = stage_solve(m, om[:kk])
+        models.append(m)
+    return models
