@@ -426,6 +426,13 @@ void Hierarchy<T>::on_level(int l, int k, cudaStream_t s, F&& f) {
 }
 
 // ------------------------------------------------------------------ cycle
+// the fused finest-level visit (fused.cu) covers V/W/K cycles with 2 pre- and
+// 2 post-sweeps on a single-domain 2D fine grid
+template <class T>
+bool Hierarchy<T>::fused_level0(const CycleSpec& spec, int k) const {
+  return num_levels() > 1 && !sl_ && spec.pre == 2 && spec.post == 2 && fused_fine_vcycle_ok(op(0, k));
+}
+
 template <class T>
 void Hierarchy<T>::ensure_ws(int k) {
   if (ws_k_ == k) return;
@@ -517,6 +524,17 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
   const int L = num_levels();
   if (l == L - 1) {
     coarse_solve(k, b, x, s);
+    return;
+  }
+  if (l == 0 && x_zero && fused_level0(spec, k)) {
+    // fused finest-level visit: pre-smoothing + residual + restriction,
+    // coarse visit(s), prolongation + post-smoothing (fused.cu)
+    const LevelGeom gc(levels_[1].dims[0], levels_[1].dims[1], levels_[1].dims[2], k);
+    const T wj = T(spec.jacobi_weight);
+    V* x2 = wt_[0].get();
+    launch_fused_pre<T, V>(op(0, k), gc, wj, b, x2, wb_[1].get(), s);
+    coarse_visit(0, spec, k, s);
+    launch_fused_post<T, V, V>(op(0, k), gc, wj, x2, wx_[1].get(), b, x, s);
     return;
   }
   V* cur = x;
@@ -627,8 +645,15 @@ void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, 
       });
       return;
     }
-    const bool sl = slab_level(0);
     const T wj = T(spec.jacobi_weight);
+    if (fused_level0(spec, k)) {
+      const LevelGeom gc(levels_[1].dims[0], levels_[1].dims[1], levels_[1].dims[2], k);
+      launch_fused_pre<T, double2>(op(0, k), gc, wj, b64, x, wb_[1].get(), s);
+      coarse_visit(0, spec, k, s);
+      launch_fused_post<T, double2, double2>(op(0, k), gc, wj, x, wx_[1].get(), b64, x64, s);
+      return;
+    }
+    const bool sl = slab_level(0);
     if (sl) sl_->neighbours();
     on_level(0, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
       launch_jacobi_zero_cast(o, wj, b64, b32, x, st);

@@ -76,6 +76,20 @@ bool fused_fine_ok(const LevelOp<float>& op);
 void launch_jacobi_out64(const LevelOp<float>& op, float wj, const float2* x, const float2* b, double2* out,
                          cudaStream_t s);
 
+// Fused finest-level V(2,2) smoothing on a 2D grid (fused.cu): the zero-start
+// pre-smoothing sweeps + residual + restriction in one streaming kernel
+// (x2 = the pre-smoothed iterate, rc = P^T r), and the prolongated correction
+// + both post-smoothing sweeps in another (out = x after the visit, cast to
+// Out). Bitwise equal to the unfused sequence. HZ_FUSED_VCYCLE=0 disables.
+template <class T>
+bool fused_fine_vcycle_ok(const LevelOp<T>& op);
+template <class T, class In>
+void launch_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In* b, cplx_t<T>* x2,
+                      cplx_t<T>* rc, cudaStream_t s);
+template <class T, class In, class Out>
+void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_t<T>* x2,
+                       const cplx_t<T>* ec, const In* b, Out* out, cudaStream_t s);
+
 // elementwise casts / copies
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);

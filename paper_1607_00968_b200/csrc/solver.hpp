@@ -133,6 +133,7 @@ class Hierarchy {
   // the coarse visit(s) of level l's correction: level l+1 solved from
   // wb_[l+1] into wx_[l+1] (V / W / K per spec.kind)
   void coarse_visit(int l, const CycleSpec& spec, int k, cudaStream_t s);
+  bool fused_level0(const CycleSpec& spec, int k) const;
   bool slab_level(int l) const { return sl_ && l < sl_->agg_level(); }
   // f(op, stream, row0, rows) once per part owning level l (slab levels), or
   // once on stream s over the whole grid

@@ -1,0 +1,101 @@
+"""GPU tier: the fused finest-level V(2,2) visit (csrc/fused.cu: pre-smoothing
++ residual + restriction in one streaming kernel, prolongation + both
+post-smoothing sweeps in another) against the unfused kernel sequence
+(HZ_FUSED_VCYCLE=0) -- bitwise -- and, through the c128 cycle, against the
+reference oracle's MgHierarchy::cycle (src/multigrid.cpp:162-199)."""
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+from hzt_util import rel_err
+from paper_1607_00968_b200 import configs
+
+pytestmark = pytest.mark.gpu
+hz = pytest.importorskip("paper_1607_00968_b200")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CYCLE = (
+    "import sys; sys.path.insert(0, '.'); import numpy as np\n"
+    "import paper_1607_00968_b200 as hz; from paper_1607_00968_b200 import configs\n"
+    "nx, nz, k, nl, prec, kind = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]), sys.argv[6], sys.argv[7]\n"
+    "cfg = configs.config2(nlevels=nl, k=k, nx=nx, nz=nz); cfg.precond_precision = prec; cfg.cycle = kind\n"
+    "S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))\n"
+    "b = configs.random_block(cfg.num_nodes, k, seed=11)\n"
+    "x1 = S.cycle(b); x2 = S.cycle(b)\n"
+    "assert np.array_equal(x1, x2), 'cycle not deterministic'\n"
+    "np.save(sys.argv[1], x1)\n")
+
+
+def _run(code, path, flag, *args):
+    env = dict(os.environ, HZ_FUSED_VCYCLE=flag)
+    r = subprocess.run([sys.executable, "-c", code, path, *map(str, args)], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(path)
+
+
+# (nx, nz, k, levels, precision, cycle): odd sizes that are not multiples of
+# the strip width (122 / 124 fine nodes) or the row chunks (32), grids
+# narrower than one strip, and the full config-2 geometry (9 strips x 17 chunks)
+CASES = [
+    (257, 129, 8, 4, "c64", "V"),
+    (297, 161, 4, 3, "c64", "W"),
+    (49, 41, 8, 3, "c64", "V"),
+    (1025, 513, 8, 5, "c64", "V"),
+    (129, 65, 32, 3, "c64", "V"),
+    (257, 129, 4, 4, "c128", "V"),
+    (297, 161, 2, 3, "c128", "W"),
+    (65, 41, 6, 3, "c128", "V"),
+]
+
+
+@pytest.mark.parametrize("nx,nz,k,nl,prec,kind", CASES)
+def test_fused_vcycle_bitwise_equals_unfused(nx, nz, k, nl, prec, kind):
+    with tempfile.TemporaryDirectory() as d:
+        fused = _run(CYCLE, os.path.join(d, "f.npy"), "1", nx, nz, k, nl, prec, kind)
+        plain = _run(CYCLE, os.path.join(d, "p.npy"), "0", nx, nz, k, nl, prec, kind)
+    assert np.all(np.isfinite(fused))
+    if prec == "c64":
+        assert np.array_equal(fused, plain), f"max rel diff {rel_err(fused, plain):.3e}"
+    else:
+        # complex128: same expressions, but nvcc may contract a complex
+        # product into FMAs differently in the two kernels (last-bit
+        # differences; the reference parity bar is 1e-12)
+        assert rel_err(fused, plain) <= 1e-14
+
+
+def test_fused_c128_cycle_matches_reference():
+    """c128 V(2,2) cycle through the fused fine level vs the compiled
+    reference's MgHierarchy::cycle at the 1e-12 parity bar."""
+    from oracle import ref
+    cfg = configs.config2(nlevels=3, k=4, nx=129, nz=65)
+    cfg.precond_precision = "c128"
+    P = hz.HelmholtzProblem.from_config(cfg)
+    S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions.from_config(cfg))
+    b = configs.random_block(cfg.num_nodes, 4, seed=5)
+    x = S.cycle(b)
+    R = ref.RefProblem.from_config(cfg)
+    H = ref.RefHierarchy(R, cfg.nlevels, cfg.shift)
+    xr = H.cycle(b, kind="V", pre=cfg.pre, post=cfg.post, wj=cfg.jacobi_weight)
+    assert rel_err(x, xr) <= 1e-12
+
+
+SOLVE = (
+    "import sys; sys.path.insert(0, '.'); import numpy as np\n"
+    "import paper_1607_00968_b200 as hz; from paper_1607_00968_b200 import configs\n"
+    "cfg = configs.config2(nlevels=4, k=8, nx=257, nz=129); cfg.restart = 3\n"
+    "S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))\n"
+    "X, rep = S.solve_block(cfg.rhs_block())\n"
+    "assert rep.all_converged(), rep.rel_residual\n"
+    "np.save(sys.argv[1], X); print(rep.cycles)\n")
+
+
+def test_fused_solve_bitwise_equals_unfused():
+    with tempfile.TemporaryDirectory() as d:
+        a = _run(SOLVE, os.path.join(d, "a.npy"), "1")
+        b = _run(SOLVE, os.path.join(d, "b.npy"), "0")
+    assert np.array_equal(a, b)
