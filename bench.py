@@ -1,8 +1,9 @@
 #!/usr/bin/env python
 """Benchmark: Helmholtz right-hand sides solved per second to 1e-6 relative
 residual (BASELINE.json metric) on BASELINE config 2 -- 2D 1025x513 layered
-model, k = 32 surface sources per GPU, complex128 block FGMRES(10) with a
-complex64 shifted-Laplacian V(2,2) multigrid preconditioner.
+model, k = 32 surface sources per GPU, complex128 block FGMRES with a
+complex64 shifted-Laplacian V(2,2) multigrid preconditioner; the 32 sources
+are solved as 4 concurrent independent blocks of 8 (hz_options.rhs_block).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -13,7 +14,8 @@ data-path collective). `value` = all ranks' RHS / max-over-ranks device time.
 
 The JSON line also carries: `e2e` (same metric through the C ABI with host
 buffers, H2D/D2H inside the timed region), `roofline` (dominant kernel's
-algorithmic GB/s from CUDA events in a profiled pass over the same steps),
+algorithmic GB/s from CUDA events in a profiled pass: one RHS block solved
+alone, so concurrent kernels do not share each other's event windows),
 `kernels` (all kernels), `cpu_baseline` (the reference C++ solver timed on
 this host on a bounded sample, rank 0, N = 1), `clocks`, `gpu_launches`.
 """
@@ -36,13 +38,18 @@ METRIC = "Helmholtz RHS solved/sec to 1e-6 residual"
 UNIT = "RHS/s"
 
 # The BASELINE config-2 solver (config 2 leaves levels / shift / cycle /
-# Krylov unstated): c128 block FGMRES(3) + c64 shifted-Laplacian V(2,2),
-# 5 levels to a 65x33 coarse grid, shift 0.9, damped-Jacobi weight 0.6 --
-# the fastest converging setting of the GPU sweeps (DESIGN.md §5,
-# profiles/r01_sweep_cycle_cfg2*.jsonl); at shift 0.5 / w_J 0.8 the V-cycle
-# stalls in the reference oracle and on the GPU alike.
-WORKLOAD = dict(cfg=2, k=32, nlevels=5, shift=0.9, jacobi_weight=0.6, cycle="V", restart=3, tol=1e-6,
-                max_cycles=2000, precond="c64")
+# Krylov / RHS blocking unstated): c128 block FGMRES(5) + c64
+# shifted-Laplacian V(2,2), 5 levels to a 65x33 coarse grid, shift 0.9,
+# damped-Jacobi weight 0.6, the 32 sources solved as 4 independent blocks of
+# 8 columns running concurrently (hz_options.rhs_block = 8) -- the fastest
+# converging setting of the GPU sweeps (DESIGN.md §5,
+# profiles/r01_sweep_rhs_block.jsonl). Cycle counts barely depend on the
+# block width here (390-430 for blocks of 1-32) while the block Krylov cost
+# grows with it (8k^2 flops per row), so 8-column blocks turn the FP64-bound
+# Gram/update of a 32-column block into HBM-bound ones. At shift 0.5 /
+# w_J 0.8 the V-cycle stalls in the reference oracle and on the GPU alike.
+WORKLOAD = dict(cfg=2, k=32, nlevels=5, shift=0.9, jacobi_weight=0.6, cycle="V", restart=5, tol=1e-6,
+                max_cycles=2000, precond="c64", krylov_block=8)
 
 
 def peaks():
@@ -139,6 +146,7 @@ def build_workload(rank, world, k):
     cfg.tol = WORKLOAD["tol"]
     cfg.max_cycles = WORKLOAD["max_cycles"]
     cfg.precond_precision = WORKLOAD["precond"]
+    cfg.krylov_block = WORKLOAD["krylov_block"]
     return cfg
 
 
@@ -147,6 +155,8 @@ def config_json(cfg, world, l2_note):
             "grid": list(cfg.n[:2]), "rhs_per_gpu": cfg.k, "global_rhs": cfg.k * world,
             "solver": f"block FGMRES({cfg.restart}) + {cfg.cycle}({cfg.pre},{cfg.post}) MG, "
                       f"{cfg.nlevels} levels, shift {cfg.shift}, w_J {cfg.jacobi_weight}",
+            "rhs_blocking": (f"{-(-cfg.k // cfg.krylov_block)} concurrent block solves of {cfg.krylov_block} columns"
+                             if 0 < cfg.krylov_block < cfg.k else f"one block of {cfg.k} columns"),
             "precision": "c128 Krylov / c64 preconditioner", "tol": cfg.tol,
             "parallelism": f"rhs-sharded x{world}", "l2": l2_note}
 
@@ -156,19 +166,22 @@ def config_json(cfg, world, l2_note):
 # with the full oracle solve, scripts/ref_full_solve.py; used to extrapolate
 # the bounded CPU samples when no GPU count is at hand).
 REF_CYCLES = None
-# GPU cycle count of this workload (FGMRES(3), 5 levels, shift 0.9, w_J 0.6,
-# k = 32; scripts/sweep_cycle_cfg2.py, profiles/r01_sweep_cycle_cfg2b.jsonl).
-DEFAULT_CYCLES = 429
+# GPU cycle count of this workload per 8-column block (mean over the 4
+# blocks; FGMRES(5), 5 levels, shift 0.9, w_J 0.6; scripts/sweep_rhs_block.py,
+# profiles/r01_sweep_rhs_block.jsonl).
+DEFAULT_CYCLES = 390
 
 
 class ReferenceRunner:
     """The reference C++ solver (oracle/_ref, stock-contraction build) driven
     through its public API -- build_hierarchy + MgHierarchy::cycle +
     block_fgmres -- with all host threads. Setup is done once
-    (excluded); a step is a bounded sample of
-    `sample_cycles` FGMRES iterations of the same k-column block (c128
-    preconditioner: the reference has no c64 path), extrapolated to the
-    cycle count of a full solve: RHS/s = k / (s_per_cycle x cycles)."""
+    (excluded). The workload's k sources are solved the way
+    our arm blocks them: ceil(k/b) independent block_fgmres solves of b
+    columns (b = krylov_block; one k-column block when 0). A step is a bounded
+    sample of `sample_cycles` FGMRES iterations of one such block (c128
+    preconditioner: the reference has no c64 path), extrapolated to full
+    solves of all blocks: RHS/s = k / (blocks x s_per_cycle x cycles)."""
 
     def __init__(self, cfg, threads=None):
         os.environ["HZ_REF_VARIANT"] = "fast"
@@ -177,7 +190,9 @@ class ReferenceRunner:
         self.cfg = cfg
         self.threads = threads or os.cpu_count() or 1
         ref.set_num_threads(self.threads)
-        self.B = cfg.rhs_block()
+        b = cfg.krylov_block if 0 < cfg.krylov_block < cfg.k else cfg.k
+        self.block, self.nblocks = b, -(-cfg.k // b)
+        self.B = cfg.rhs_block()[:, :b].copy()
         t0 = time.perf_counter()
         self.R = ref.RefProblem.from_config(cfg)
         self.H = ref.RefHierarchy(self.R, cfg.nlevels, cfg.shift)
@@ -191,19 +206,22 @@ class ReferenceRunner:
                                        restart=cfg.restart, tol=cfg.tol, max_cycles=sample_cycles)
         return (time.perf_counter() - t0) / max(rep.cycles, 1), rep.cycles
 
+    def rhs_per_s(self, per_cycle, cycles_target):
+        return self.cfg.k / (self.nblocks * per_cycle * cycles_target)
+
     def describe(self, sample_cycles, cycles_target):
         cfg = self.cfg
-        return (f"{sample_cycles} FGMRES({cfg.restart}) iterations (V-cycle + Arnoldi + LS) per step of the "
-                f"same k={cfg.k} block on the reference C++ solver (oracle/_ref, {self.threads} threads, "
-                f"c128 preconditioner), setup excluded; RHS/s = k / (s_per_cycle x {cycles_target:.0f} cycles "
-                f"to 1e-6)")
+        return (f"{sample_cycles} FGMRES({cfg.restart}) iterations (V-cycle + Arnoldi + LS) per step of one "
+                f"{self.block}-column block of the workload ({self.nblocks} blocks) on the reference C++ solver "
+                f"(oracle/_ref, {self.threads} threads, c128 preconditioner), setup excluded; RHS/s = "
+                f"k / (blocks x s_per_cycle x {cycles_target:.0f} cycles to 1e-6)")
 
 
 def reference_sample(cfg, cycles_target, sample_cycles, threads=None):
     run = ReferenceRunner(cfg, threads)
     per_cycle, _ = run.step(sample_cycles)
-    return cfg.k / (per_cycle * cycles_target), {"cores": run.threads, "s_per_cycle": per_cycle,
-                                                 "sample": run.describe(sample_cycles, cycles_target)}
+    return run.rhs_per_s(per_cycle, cycles_target), {"cores": run.threads, "s_per_cycle": per_cycle,
+                                                     "sample": run.describe(sample_cycles, cycles_target)}
 
 
 def run_reference(args):
@@ -217,7 +235,7 @@ def run_reference(args):
     for i in range(args.warmup + args.steps):
         per_cycle, _ = run.step(args.ref_sample_cycles)
         if i >= args.warmup:
-            vals.append(cfg.k / (per_cycle * cycles_target))
+            vals.append(run.rhs_per_s(per_cycle, cycles_target))
     info = {"cores": run.threads, "sample": run.describe(args.ref_sample_cycles, cycles_target)}
     value = statistics.mean(vals)
     ms = 1e3 * cfg.k / value
@@ -233,6 +251,17 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- our arm
+def block_cycles(rep, cfg):
+    """Mean over the RHS blocks of each block solve's cycle count (the
+    slowest column of the block); the cycle count of the solve when unblocked."""
+    import numpy as np
+    b = cfg.krylov_block
+    if not 0 < b < cfg.k:
+        return float(rep.cycles)
+    cc = np.asarray(rep.col_cycles)
+    return float(np.mean([cc[i:i + b].max() for i in range(0, cfg.k, b)]))
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -280,7 +309,7 @@ def run_ours(args):
         ev0.record(stream)
         for _ in range(args.steps):
             _, rep = S.solve_block(Bd, out=Xd)  # library stream; synchronised on return
-            cycles.append(rep.cycles)
+            cycles.append(block_cycles(rep, cfg))
             if not rep.all_converged():
                 raise RuntimeError(f"solve did not converge: {rep.rel_residual}")
         ev1.record(stream)
@@ -300,9 +329,16 @@ def run_ours(args):
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e = ws * k * args.steps / e2e_s
     # ---- profiled pass (same steps) for the per-kernel roofline
+    # (blocked workload: one block solved alone -- the concurrent blocks run
+    # the same kernels at the same shapes, but overlapping kernels would
+    # share HBM inside each other's event windows)
+    b = cfg.krylov_block if 0 < cfg.krylov_block < k else k
+    Sp = S if b == k else hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions.from_config(cfg, rhs_block=0))
+    Bp1 = Bd[:, :b].contiguous()
+    Sp.solve_block(Bp1)
     with hz.kernel_profile() as prof:
         for _ in range(max(1, min(args.steps, 3))):
-            S.solve_block(Bd, out=Xd)
+            Sp.solve_block(Bp1)
     kern = prof.result
     peak, peak_kind = peaks()
     table = {}
@@ -363,7 +399,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded, SURVEY §8d; random-free point sources)",
-            "config": config_json(cfg, ws, "inputs larger than L2 (269 MB block, 5.6 GB Krylov basis)"),
+            "config": config_json(cfg, ws, "inputs larger than L2 (269 MB block, 3.5 GB Krylov bases)"),
             "cycles_per_solve": statistics.mean(cycles), "setup_s": round(setup_s, 3),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B_host.nbytes),
                     "d2h_bytes_per_step": int(B_host.nbytes)},

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define HZ_ABI_VERSION 1
+#define HZ_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define HZ_API __attribute__((visibility("default")))
@@ -76,6 +76,11 @@ typedef struct hz_options {
   int fgmres_restart;      /* 5 */
   int64_t dense_threshold; /* 3000 */
   int precond_precision;   /* hz_precision of the multigrid cycle; HZ_C128 */
+  int rhs_block;           /* 0: one Krylov block over all k columns (solve_block,
+                              src/helmholtz_solver.cpp:61-79); b > 0: the k columns
+                              solved as ceil(k/b) independent blocks of <= b
+                              contiguous columns, run concurrently (each equals
+                              solve_block on its columns); default 0 */
 } hz_options;
 
 /* SolveReport (include/seistomo/krylov.hpp:19-40). Arrays are caller-owned

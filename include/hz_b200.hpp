@@ -145,6 +145,7 @@ struct HelmholtzSolveOptions {
   std::int64_t dense_threshold = 3000;
   bool allow_coarse_ppw = false;
   PreconditionerPrecision precond_precision = PreconditionerPrecision::C128;
+  int rhs_block = 0;  // hz_options.rhs_block: 0 = one Krylov block over all columns
 };
 
 struct SolveReport {
@@ -224,6 +225,7 @@ class HelmholtzSolver {
     o.fgmres_restart = opts.fgmres_restart;
     o.dense_threshold = opts.dense_threshold;
     o.precond_precision = opts.precond_precision == PreconditionerPrecision::C64 ? HZ_C64 : HZ_C128;
+    o.rhs_block = opts.rhs_block;
     hz_solver* s = nullptr;
     check(hz_solver_create(problem_->handle(), &o, &s));
     h_.reset(s, [](hz_solver* q) { hz_solver_destroy(q); });

@@ -369,6 +369,10 @@ class HelmholtzSolveOptions:
     dense_threshold: int = 3000
     allow_coarse_ppw: bool = False
     precond_precision: str = "c128"
+    # 0: one block Krylov solve over all k columns (the reference's
+    # solve_block); b > 0: ceil(k/b) independent block solves of <= b
+    # contiguous columns, run concurrently on the GPU (hz_options.rhs_block)
+    rhs_block: int = 0
 
     def to_c(self) -> hz_options:
         o = hz_options()
@@ -391,6 +395,9 @@ class HelmholtzSolveOptions:
         o.fgmres_restart = self.fgmres_restart
         o.dense_threshold = self.dense_threshold
         o.precond_precision = 0 if self.precond_precision == "c128" else 1
+        if self.rhs_block < 0:
+            raise ValidationError("rhs_block must be >= 0")
+        o.rhs_block = self.rhs_block
         return o
 
     @classmethod
@@ -399,7 +406,8 @@ class HelmholtzSolveOptions:
         method = "MgFgmres" if cfg.method == "fgmres" else "MgBicgstabCycle"
         o = cls(method=method, tol=cfg.tol, max_cycles=cfg.max_cycles, nlevels=cfg.nlevels,
                 shift_factor=cfg.shift, cycle=CycleSpec(kind, cfg.pre, cfg.post, cfg.jacobi_weight),
-                fgmres_restart=cfg.restart, precond_precision=cfg.precond_precision)
+                fgmres_restart=cfg.restart, precond_precision=cfg.precond_precision,
+                rhs_block=cfg.krylov_block)
         for k, v in over.items():
             setattr(o, k, v)
         return o

@@ -35,7 +35,8 @@ class hz_options(C.Structure):
                 ("nlevels", C.c_int), ("shift_factor", C.c_double), ("cycle_kind", C.c_int),
                 ("pre", C.c_int), ("post", C.c_int), ("jacobi_weight", C.c_double),
                 ("k_inner", C.c_int), ("fgmres_restart", C.c_int),
-                ("dense_threshold", C.c_int64), ("precond_precision", C.c_int)]
+                ("dense_threshold", C.c_int64), ("precond_precision", C.c_int),
+                ("rhs_block", C.c_int)]
 
 
 class hz_report(C.Structure):

@@ -58,6 +58,7 @@ class HelmholtzConfig:
     tol: float = 1e-6
     max_cycles: int = 400
     precond_precision: str = "c128"
+    krylov_block: int = 0             # HelmholtzSolveOptions.rhs_block (0 = one block)
     note: str = ""
 
     @property

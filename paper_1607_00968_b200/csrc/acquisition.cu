@@ -172,8 +172,7 @@ void launch_colmax(int64_t n, int k, const double2* X, double* part, int nslots,
 void launch_quantize16(int64_t n, int k, const double2* X, const double* inv_scale, uint32_t* Q, cudaStream_t st) {
   ProfScope prof("quantize16", double(n) * k * (16 + 4), st);
   const size_t smem = sizeof(uint32_t) * size_t(k) * 33;
-  if (smem > 48 * 1024)
-    HZ_CUDA(cudaFuncSetAttribute(quantize_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  allow_dyn_smem(reinterpret_cast<const void*>(quantize_kernel), int(smem));
   quantize_kernel<<<grid_for(n, 32), kBlk, smem, st>>>(n, k, X, inv_scale, Q);
   HZ_LAUNCH_CHECK();
 }

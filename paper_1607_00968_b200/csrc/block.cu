@@ -556,8 +556,7 @@ void gram_launch(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>
   const int groups = std::max(1, kBlk / tiles);
   const size_t smem = groups > 1 ? sizeof(cplx_t<T>) * size_t(groups) * k * k : 0;
   auto kern = multi_gram_kernel<T, TP, TQ>;
-  if (smem > 48 * 1024)
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   dim3 grid(nb, nslots);
   kern<<<grid, kBlk, smem, s>>>(n, k, X, Y, partials, nslots);
 }
@@ -584,11 +583,7 @@ void gram_dmma_launch(int64_t n, int nb, const BlockTab<double>& X, const double
                       int nslots, cudaStream_t s) {
   const size_t smem = dmma::gram_smem<K>();
   auto kern = dmma::gram_kernel<K>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   kern<<<dim3(nb, nslots), 256, smem, s>>>(n, X, Y, partials, nslots);
 }
 
@@ -597,11 +592,7 @@ void update_dmma_launch(int64_t n, int nb, const BlockTab<double>& X, const doub
                         double2* Yout, double sign, cudaStream_t s) {
   const size_t smem = dmma::update_smem<K>();
   auto kern = dmma::update_kernel<K>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   kern<<<grid_for(n, dmma::UpdateCfg<K>::RC), dmma::UpdateCfg<K>::THREADS, smem, s>>>(n, nb, X, H, Yin, Yout,
                                                                                     sign);
 }
@@ -614,11 +605,7 @@ void gram_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T>*
   }
   const size_t smem = tiled::gram_smem<T, K>();
   auto kern = tiled::gram_kernel<T, K>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   kern<<<dim3(nb, nslots), 256, smem, s>>>(n, X, Y, partials, nslots);
 }
 
@@ -631,11 +618,7 @@ void update_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T
   constexpr int RC = tiled::update_rows<K>();
   const size_t smem = tiled::update_smem<T, K>();
   auto kern = tiled::update_kernel<T, K>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   kern<<<grid_for(n, RC), 256, smem, s>>>(n, nb, X, H, Yin, Yout, sign);
 }
 
@@ -686,8 +669,7 @@ void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const c
   } else {
     const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
     auto kern = multi_update_kernel<T>;
-    if (smem > 48 * 1024)
-      HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
     kern<<<grid_for(n * k, kBlk), kBlk, smem, s>>>(n, k, nb, X, H, Yin, Yout, sign);
   }
   HZ_LAUNCH_CHECK();
@@ -743,8 +725,7 @@ void launch_small_cholesky(int k, const cplx_t<T>* G, cplx_t<T>* R, cplx_t<T>* R
   if (k > 64) throw HzError(kValidation, "small_cholesky: k > 64");
   const size_t smem = 2 * sizeof(cplx_t<T>) * size_t(k) * k;
   auto kern = small_cholesky_kernel<T>;
-  if (smem > 48 * 1024)
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   ProfScope prof("small_cholesky", 4.0 * k * k * sizeof(cplx_t<T>), s);
   kern<<<1, 1024, smem, s>>>(k, G, R, Rinv, flag, rel_tol);
   HZ_LAUNCH_CHECK();
@@ -758,7 +739,7 @@ void launch_pip_factor(int k, int nb, const cplx_t<T>* Hc, cplx_t<T>* R, cplx_t<
   const int staged = full <= 200 * 1024 ? 1 : 0;
   const size_t smem = staged ? full : base;
   auto kern = pip_factor_kernel<T>;
-  HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), 200 * 1024);
   ProfScope prof("pip_factor", double(nb + 2) * k * k * sizeof(cplx_t<T>), s);
   kern<<<1, 1024, smem, s>>>(k, nb, Hc, R, Rinv, C, flag, eta2, staged);
   HZ_LAUNCH_CHECK();

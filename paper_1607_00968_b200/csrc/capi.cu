@@ -1,7 +1,9 @@
 // extern "C" boundary (include/hz_b200.h). Maps the reference's exception
 // classes to status codes and owns the device-side state behind the opaque
 // hz_problem / hz_solver handles.
+#include <algorithm>
 #include <atomic>
+#include <exception>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -78,6 +80,25 @@ struct hz_sampling {
   std::unique_ptr<Sampling> s;
 };
 
+// One RHS group of a blocked solve (hz_options.rhs_block): its own stream,
+// hierarchy views (shared operators, private cycle workspace), Krylov
+// workspace and column-gathered [n][kg] blocks.
+struct RhsGroup {
+  cudaStream_t stream = nullptr;
+  std::unique_ptr<Hierarchy<double>> h64;
+  std::unique_ptr<Hierarchy<float>> h32;
+  std::unique_ptr<Fgmres<double>> fgm;
+  std::unique_ptr<Bicgstab> bicg;
+  DevBuf<double2> B, X;
+  ~RhsGroup() {
+    fgm.reset();
+    bicg.reset();
+    h32.reset();
+    h64.reset();
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
 struct hz_solver {
   std::shared_ptr<Problem> prob;
   hz_options opts{};
@@ -90,6 +111,7 @@ struct hz_solver {
   std::unique_ptr<Fgmres<double>> fgm;
   std::unique_ptr<Bicgstab> bicg;
   DevBuf<double2> dB, dX;
+  std::vector<std::unique_ptr<RhsGroup>> groups;  // blocked solves (rhs_block > 0)
   // DenseLuSmall: explicit inverse of the unshifted operator
   DevBuf<double2> dense_ainvT;
   // slab decomposition (slabs.hpp): per-GPU copies of the fine centre and of
@@ -121,6 +143,7 @@ struct hz_solver {
     span_k = k;
   }
   ~hz_solver() {
+    groups.clear();  // views of h64 / h32
     fgm.reset();
     h32.reset();
     h64.reset();
@@ -219,8 +242,8 @@ DevOp<double> make_slab_op(hz_solver* s, int k) {
   return op;
 }
 
-DevOp<double> make_op(hz_solver* s, int k) {
-  if (s->slabs) return make_slab_op(s, k);
+// the unpreconditioned fine operator + the cycle of hierarchy h64 / h32
+DevOp<double> make_op_with(hz_solver* s, Hierarchy<double>* h64, Hierarchy<float>* h32) {
   DevOp<double> op;
   Problem* P = s->prob.get();
   op.n = P->num_nodes();
@@ -230,16 +253,21 @@ DevOp<double> make_op(hz_solver* s, int k) {
   op.resid = [P](const double2* x, const double2* b, double2* r, int kk, cudaStream_t st) {
     launch_apply_residual<double>(P->fine_op(kk), x, b, r, st);
   };
-  if (s->opts.precond_precision == HZ_C64) {
-    op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
-      s->h32->cycle_cast(s->spec, kk, in, out, st);
+  const CycleSpec* spec = &s->spec;
+  if (s->opts.precond_precision == HZ_C64)
+    op.prec = [spec, h32](const double2* in, double2* out, int kk, cudaStream_t st) {
+      h32->cycle_cast(*spec, kk, in, out, st);
     };
-  } else {
-    op.prec = [s](const double2* in, double2* out, int kk, cudaStream_t st) {
-      s->h64->cycle(s->spec, kk, in, out, true, st);
+  else
+    op.prec = [spec, h64](const double2* in, double2* out, int kk, cudaStream_t st) {
+      h64->cycle(*spec, kk, in, out, true, st);
     };
-  }
   return op;
+}
+
+DevOp<double> make_op(hz_solver* s, int k) {
+  if (s->slabs) return make_slab_op(s, k);
+  return make_op_with(s, s->h64.get(), s->h32.get());
 }
 
 // host <-> solver block copies, one per part (each part's rows live on its GPU)
@@ -269,8 +297,11 @@ void download_rows(hz_solver* s, int k, const double2* dev, double* host) {
   HZ_CUDA(cudaStreamSynchronize(s->stream));
 }
 
+Report run_grouped(hz_solver* s, int k, const double2* B, double2* X);
+
 Report run_solve(hz_solver* s, int k, const double2* B, double2* X) {
   Report rep;
+  if (!s->dense && s->opts.rhs_block > 0 && k > s->opts.rhs_block) return run_grouped(s, k, B, X);
   if (s->dense) {
     // DenseLuSmall (src/helmholtz_solver.cpp:38-59): direct solve, then the
     // reported residuals
@@ -301,6 +332,87 @@ Report run_solve(hz_solver* s, int k, const double2* B, double2* X) {
   if (!s->fgm) s->fgm = std::make_unique<Fgmres<double>>();
   return s->fgm->solve(op, k, B, X, s->opts.fgmres_restart, s->opts.tol, s->opts.max_cycles,
                        s->stream);
+}
+
+// Blocked solve (hz_options.rhs_block = b): the k columns of B are solved as
+// ceil(k/b) independent block Krylov solves of <= b contiguous columns --
+// each exactly the reference's block_fgmres / block_bicgstab on its columns
+// (src/krylov.cpp:60-280), i.e. solve_block called per column group. The
+// groups run concurrently (one host thread + stream each, hierarchy views
+// sharing the operators). B and X are level-0 device blocks [n][k], ready on
+// s->stream; X is complete when this returns.
+Report run_grouped(hz_solver* s, int k, const double2* B, double2* X) {
+  if (s->slabs) throw HzError(kValidation, "rhs_block: blocked solves are not supported in slab mode");
+  const int kb = s->opts.rhs_block;
+  const int G = (k + kb - 1) / kb;
+  const int64_t n = s->prob->num_nodes();
+  while (int(s->groups.size()) < G) {
+    auto g = std::make_unique<RhsGroup>();
+    HZ_CUDA(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->h64 = s->h64->share();
+    if (s->h32) g->h32 = s->h32->share();
+    s->groups.push_back(std::move(g));
+  }
+  cudaEvent_t ready = nullptr;
+  HZ_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  std::shared_ptr<void> ev_guard(ready, [](void* e) { cudaEventDestroy(static_cast<cudaEvent_t>(e)); });
+  HZ_CUDA(cudaEventRecord(ready, s->stream));
+  std::vector<Report> reps(static_cast<size_t>(G));
+  std::vector<std::exception_ptr> errs(static_cast<size_t>(G));
+  auto one = [&](int i) {
+    try {
+      DeviceGuard dg(s->prob->device);
+      RhsGroup& g = *s->groups[i];
+      const int c0 = i * kb, kg = std::min(kb, k - c0);
+      const size_t pitch = size_t(k) * sizeof(double2), gp = size_t(kg) * sizeof(double2);
+      g.B.ensure(size_t(n) * kg);
+      g.X.ensure(size_t(n) * kg);
+      HZ_CUDA(cudaStreamWaitEvent(g.stream, ready, 0));
+      HZ_CUDA(cudaMemcpy2DAsync(g.B.get(), gp, B + c0, pitch, gp, size_t(n), cudaMemcpyDeviceToDevice, g.stream));
+      DevOp<double> op = make_op_with(s, g.h64.get(), g.h32.get());
+      if (s->bicgstab) {
+        if (!g.bicg) g.bicg = std::make_unique<Bicgstab>();
+        reps[i] = g.bicg->solve(op, kg, g.B.get(), g.X.get(), s->opts.tol, s->opts.max_cycles, g.stream);
+      } else {
+        if (!g.fgm) g.fgm = std::make_unique<Fgmres<double>>();
+        reps[i] = g.fgm->solve(op, kg, g.B.get(), g.X.get(), s->opts.fgmres_restart, s->opts.tol,
+                               s->opts.max_cycles, g.stream);
+      }
+      HZ_CUDA(cudaMemcpy2DAsync(X + c0, pitch, g.X.get(), gp, gp, size_t(n), cudaMemcpyDeviceToDevice, g.stream));
+      HZ_CUDA(cudaStreamSynchronize(g.stream));
+    } catch (...) {
+      errs[i] = std::current_exception();
+    }
+  };
+  if (G == 1) {
+    one(0);
+  } else {
+    std::vector<std::thread> th;
+    th.reserve(size_t(G));
+    for (int i = 0; i < G; ++i) th.emplace_back(one, i);
+    for (auto& t : th) t.join();
+  }
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  // merged report: columns in order; cycles / wall = slowest group; the
+  // history is the worst column estimate over the groups per cycle
+  Report rep;
+  size_t hl = 0;
+  for (const Report& r : reps) {
+    rep.cycles = std::max(rep.cycles, r.cycles);
+    rep.wall_s = std::max(rep.wall_s, r.wall_s);
+    rep.qr_factorizations += r.qr_factorizations;
+    rep.block_gram_products += r.block_gram_products;
+    rep.col_cycles.insert(rep.col_cycles.end(), r.col_cycles.begin(), r.col_cycles.end());
+    rep.rel_residual.insert(rep.rel_residual.end(), r.rel_residual.begin(), r.rel_residual.end());
+    rep.converged.insert(rep.converged.end(), r.converged.begin(), r.converged.end());
+    hl = std::max(hl, r.history.size());
+  }
+  rep.history.assign(hl, 0.0);
+  for (const Report& r : reps)
+    for (size_t t = 0; t < hl && !r.history.empty(); ++t)
+      rep.history[t] = std::max(rep.history[t], r.history[std::min(t, r.history.size() - 1)]);
+  return rep;
 }
 
 }  // namespace
@@ -392,6 +504,7 @@ void hz_options_default(hz_options* o) {
   o->fgmres_restart = 5;
   o->dense_threshold = 3000;
   o->precond_precision = HZ_C128;
+  o->rhs_block = 0;
 }
 
 int hz_problem_create(int ndim, const int64_t n[3], const double h[3], const double* m,
@@ -467,6 +580,7 @@ int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** out) {
     const hz_options& o = s->opts;
     if (o.precond_precision != HZ_C128 && o.precond_precision != HZ_C64)
       throw HzError(kValidation, "precond_precision must be HZ_C128 or HZ_C64");
+    if (o.rhs_block < 0) throw HzError(kValidation, "rhs_block must be >= 0");
     HZ_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     s->spec.pre = o.pre;
     s->spec.post = o.post;

@@ -281,11 +281,7 @@ void coarse_gemm_launch(int64_t n, const cplx_t<T>* ainvT, int64_t ld, const cpl
   constexpr int TI = CoarseTile<T, K>::TI, TL = CoarseTile<T, K>::TL;
   const size_t smem = sizeof(V) * 2 * (TL * TI + TL * K);
   auto kern = coarse_gemm_kernel<T, K>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
   const int tiles = grid_for(n, TI);
   nsplit = std::min(nsplit, split_for_tiles(tiles));
   if (nsplit > 1 && part == nullptr) nsplit = 1;
@@ -342,7 +338,7 @@ void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, co
   const size_t smem = sizeof(V) * (TL * 16 + TL * size_t(k));
   const int grid = grid_for(n, ti);
   auto go = [&](auto kern) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
     kern<<<grid, 256, smem, s>>>(n, k, ainvT, ld, b, x, c_in, sign);
   };
   if (ti == 16)

@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -47,6 +50,23 @@ void count_launch();
     ::hz::count_launch();                                                              \
     ::hz::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__);         \
   } while (0)
+
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` on the
+// current device. Monotonic and serialised: concurrent solves (RHS groups,
+// frequencies) launching the same kernel with different sizes never lower
+// the limit under one another's launch; per device, so slab parts on other
+// GPUs get it too.
+inline void allow_dyn_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  int& cur = done[{kern, dev}];
+  if (cur >= bytes) return;
+  HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  cur = bytes;
+}
 
 // ---------------------------------------------------------------- complex
 template <class T> struct CT;

@@ -471,11 +471,7 @@ void run_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In* b,
   constexpr int MINB = int(std::min<size_t>(8, (227 * 1024) / (P::BYTES + 1024)));
   const dim3 grid(unsigned((gc.n0 + TC - 1) / TC), unsigned(op.g.k / C), unsigned((gc.n1 + crows - 1) / crows));
   auto kern = fused_pre_kernel<T, In, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB)>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P::BYTES)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
   kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, b, x2, rc, crows);
 }
 
@@ -487,11 +483,7 @@ void run_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_
   constexpr int MINB = int(std::min<size_t>(8, (227 * 1024) / (P::BYTES + 1024)));
   const dim3 grid(unsigned((op.g.n0 + W - 1) / W), unsigned(op.g.k / C), unsigned((op.g.n1 + frows - 1) / frows));
   auto kern = fused_post_kernel<T, In, Out, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB)>;
-  static bool attr = false;
-  if (!attr) {
-    HZ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P::BYTES)));
-    attr = true;
-  }
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
   kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, x2, ec, b, out, frows);
 }
 

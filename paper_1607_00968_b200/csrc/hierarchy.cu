@@ -400,6 +400,38 @@ std::unique_ptr<Hierarchy<T>> Hierarchy<T>::replica(int device, cudaStream_t s) 
   return H;
 }
 
+// A view of the same operators with its own cycle workspace: the hierarchy is
+// immutable after build and only the workspaces are written by a cycle
+// (inc/multigrid.hpp:37-39: distinct blocks may cycle concurrently), so
+// views on different streams run concurrently. The view must not outlive
+// this hierarchy.
+template <class T>
+std::unique_ptr<Hierarchy<T>> Hierarchy<T>::share() const {
+  if (sl_) throw HzError(kState, "hierarchy views of a slab-decomposed hierarchy are not supported");
+  auto H = std::make_unique<Hierarchy<T>>();
+  H->ndim_ = ndim_;
+  H->band_ = band_;
+  H->bt_ = bt_;
+  auto alias = [](const auto& src, auto& dst) {
+    if (src.size()) dst.adopt(std::shared_ptr<void>(static_cast<void*>(src.get()), [](void*) {}), src.size());
+  };
+  H->levels_.resize(levels_.size());
+  for (size_t l = 0; l < levels_.size(); ++l) {
+    const auto& A = levels_[l];
+    auto& B = H->levels_[l];
+    B.dims = A.dims;
+    B.kind = A.kind;
+    for (int a = 0; a < 3; ++a) B.w[a] = A.w[a];
+    alias(A.center, B.center);
+    alias(A.coef, B.coef);
+    alias(A.inv_diag, B.inv_diag);
+  }
+  alias(ainvT_, H->ainvT_);
+  alias(bt_ET_, H->bt_ET_);
+  alias(bt_FT_, H->bt_FT_);
+  return H;
+}
+
 template <class T>
 void Hierarchy<T>::attach_slabs(const Slabs* sl, std::vector<const Hierarchy<T>*> reps) {
   if (sl && sl->levels() != num_levels()) throw HzError(kValidation, "slabs: level count mismatch");

@@ -104,6 +104,9 @@ class Hierarchy {
   void download_level(int l, std::vector<cplx>& coef_or_center) const;
   // copy of the level operators (not the coarsest solver) on another GPU
   std::unique_ptr<Hierarchy<T>> replica(int device, cudaStream_t s) const;
+  // same operators (aliased, not copied), private cycle workspace: one per
+  // concurrently cycling RHS group
+  std::unique_ptr<Hierarchy<T>> share() const;
   // Slab mode (slabs.hpp): levels below sl->agg_level() run on every part,
   // each part computing its own planes with the operators of reps[p] (a
   // hierarchy resident on part p's GPU); coarser levels and the coarsest

@@ -46,8 +46,8 @@ def test_options_default_mirror_reference():
     _native.lib().hz_options_default(C.byref(o))
     assert (o.method, o.tol, o.max_cycles, o.nlevels, o.shift_factor) == (0, 1e-6, 200, 3, 0.2)
     assert (o.cycle_kind, o.pre, o.post, o.jacobi_weight, o.k_inner) == (1, 2, 2, 0.8, 2)
-    assert (o.fgmres_restart, o.dense_threshold, o.precond_precision) == (5, 3000, 0)
-    assert _native.lib().hz_abi_version() == 1
+    assert (o.fgmres_restart, o.dense_threshold, o.precond_precision, o.rhs_block) == (5, 3000, 0, 0)
+    assert _native.lib().hz_abi_version() == 2
 
 
 @pytest.mark.skipif(__import__("torch").cuda.is_available(), reason="only meaningful without a GPU")
@@ -66,6 +66,8 @@ def test_python_mirror_validates_before_the_device():
         hz.HelmholtzSolveOptions(method="Nope").to_c()
     with pytest.raises(hz.ValidationError):
         hz.HelmholtzSolveOptions(precond_precision="c32").to_c()
+    with pytest.raises(hz.ValidationError):
+        hz.HelmholtzSolveOptions(rhs_block=-1).to_c()
     with pytest.raises(hz.ValidationError):
         hz.HelmholtzProblem(2, (17, 17), (1.0, 1.0), np.ones(10), 1.0,
                             hz.AttenuationField(0.0, np.zeros(10)))
