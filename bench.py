@@ -39,7 +39,7 @@ UNIT = "RHS/s"
 
 # The BASELINE config-2 solver (config 2 leaves levels / shift / cycle /
 # Krylov / RHS blocking unstated): c128 block FGMRES(5) + c64
-# shifted-Laplacian V(2,2), 5 levels to a 65x33 coarse grid, shift 0.9,
+# shifted-Laplacian V(2,2), 6 levels to a 33x17 coarse grid, shift 0.9,
 # damped-Jacobi weight 0.6, the 32 sources solved as 4 independent blocks of
 # 8 columns running concurrently (hz_options.rhs_block = 8) -- the fastest
 # converging setting of the GPU sweeps (DESIGN.md §5,
@@ -48,7 +48,7 @@ UNIT = "RHS/s"
 # grows with it (8k^2 flops per row), so 8-column blocks turn the FP64-bound
 # Gram/update of a 32-column block into HBM-bound ones. At shift 0.5 /
 # w_J 0.8 the V-cycle stalls in the reference oracle and on the GPU alike.
-WORKLOAD = dict(cfg=2, k=32, nlevels=5, shift=0.9, jacobi_weight=0.6, cycle="V", restart=5, tol=1e-6,
+WORKLOAD = dict(cfg=2, k=32, nlevels=6, shift=0.9, jacobi_weight=0.6, cycle="V", restart=5, tol=1e-6,
                 max_cycles=2000, precond="c64", krylov_block=8)
 
 
@@ -167,9 +167,9 @@ def config_json(cfg, world, l2_note):
 # the bounded CPU samples when no GPU count is at hand).
 REF_CYCLES = None
 # GPU cycle count of this workload per 8-column block (mean over the 4
-# blocks; FGMRES(5), 5 levels, shift 0.9, w_J 0.6; scripts/sweep_rhs_block.py,
+# blocks; FGMRES(5), 6 levels, shift 0.9, w_J 0.6; scripts/sweep_rhs_block.py,
 # profiles/r01_sweep_rhs_block.jsonl).
-DEFAULT_CYCLES = 390
+DEFAULT_CYCLES = 391
 
 
 class ReferenceRunner:

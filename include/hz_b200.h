@@ -169,6 +169,18 @@ HZ_API int hz_solve_blocks_multi(int count, hz_solver* const* solvers, const int
 HZ_API int hz_solve_blocks_multi_device(int count, hz_solver* const* solvers, const int64_t* n, const int* k,
                                         const void* const* B_dev, void* const* X_dev, hz_report* reps);
 
+/* Block algebra of the Arnoldi step on caller device blocks ([n][k]
+ * complex128, current device; synchronous), for kernel-level parity:
+ *   hz_block_gram_device:       G_i = X_i^H Y for i < nb, G on the host as nb
+ *                               row-major k x k tiles (gram,
+ *                               include/seistomo/block.hpp:51-74, batched);
+ *   hz_block_add_scaled_device: Y += sum_i X_i C_i, C on the host as nb
+ *                               row-major k x k tiles (add_block_scaled,
+ *                               include/seistomo/block.hpp:76-88, batched). */
+HZ_API int hz_block_gram_device(int64_t n, int k, int nb, const void* const* X_dev, const void* Y_dev, double* G);
+HZ_API int hz_block_add_scaled_device(int64_t n, int k, int nb, const void* const* X_dev, const double* C,
+                                      void* Y_dev);
+
 /* solve_helmholtz contract (src/helmholtz_solver.cpp:81-93): like
  * hz_solve_block but returns HZ_CONVERGENCE if any column misses tol. */
 HZ_API int hz_solve_helmholtz(hz_solver* s, int64_t n, int k, const double* B, double* X,

@@ -152,6 +152,49 @@ def solve_blocks_multi(solvers: Sequence["HelmholtzSolver"], Bs, outs=None):
     return Xs, [S._finish(rep_arr[i], bufs[i][0]) for i, S in enumerate(solvers)]
 
 
+def _dev_blocks(Xs):
+    import torch
+    Xs = [x.contiguous() for x in Xs]
+    if not Xs or any(x.dtype != torch.complex128 or not x.is_cuda or x.dim() != 2 for x in Xs):
+        raise ValidationError("block algebra: complex128 [n][k] CUDA tensors expected")
+    if any(x.shape != Xs[0].shape for x in Xs):
+        raise ValidationError("block algebra: all blocks must have the same shape")
+    return Xs
+
+
+def block_gram(Xs, Y):
+    """G_i = X_i^H Y for every block X_i (gram, inc/block.hpp:51-74, batched
+    over the blocks as the Arnoldi step uses it): [nb, k, k] complex128 numpy."""
+    import torch
+    Xs = _dev_blocks(Xs)
+    Y = _dev_blocks([Y])[0]
+    n, k = Xs[0].shape
+    nb = len(Xs)
+    G = np.empty((nb, k, k), dtype=np.complex128)
+    ptrs = (C.c_void_p * nb)(*[x.data_ptr() for x in Xs])
+    torch.cuda.synchronize()
+    with torch.cuda.device(Y.device):
+        _check(_native.lib().hz_block_gram_device(n, k, nb, ptrs, Y.data_ptr(), G.ctypes.data))
+    return G
+
+
+def block_add_scaled(Y, Xs, Cs):
+    """Y += sum_i X_i C_i in place (add_block_scaled, inc/block.hpp:76-88,
+    batched); Y a contiguous complex128 CUDA tensor, Cs [nb, k, k]."""
+    import torch
+    Xs = _dev_blocks(Xs)
+    if not Y.is_contiguous():
+        raise ValidationError("block_add_scaled: Y must be contiguous")
+    n, k = Xs[0].shape
+    nb = len(Xs)
+    Cs = np.ascontiguousarray(np.asarray(Cs, dtype=np.complex128).reshape(nb, k, k))
+    ptrs = (C.c_void_p * nb)(*[x.data_ptr() for x in Xs])
+    torch.cuda.synchronize()
+    with torch.cuda.device(Y.device):
+        _check(_native.lib().hz_block_add_scaled_device(n, k, nb, ptrs, Cs.ctypes.data, Y.data_ptr()))
+    return Y
+
+
 class MultiFrequencySolver:
     """Several (m, omega) hierarchies resident on one GPU: one
     HelmholtzProblem + HelmholtzSolver per frequency over the same slowness

@@ -26,7 +26,7 @@ EXPORTS = (
     "hz_sample_device", "hz_sample", "hz_sample_adjoint_device", "hz_sample_adjoint",
     "hz_fwi_sensitivity_rhs_device", "hz_fwi_jacobian_vec", "hz_fwi_jacobian_vec_device",
     "hz_fwi_jacobian_transpose_vec", "hz_fwi_jacobian_transpose_vec_device", "hz_compact16_device",
-    "hz_solve_helmholtz_compact16", "hz_compact16",
+    "hz_solve_helmholtz_compact16", "hz_compact16", "hz_block_gram_device", "hz_block_add_scaled_device",
 )
 
 
@@ -77,6 +77,8 @@ def lib():
         L.hz_solve_block_device.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report)]
         L.hz_solve_helmholtz.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report)]
         L.hz_cycle.argtypes = [vp, i64, i32, vp, vp]
+        L.hz_block_gram_device.argtypes = [i64, i32, i32, vp, vp, vp]
+        L.hz_block_add_scaled_device.argtypes = [i64, i32, i32, vp, vp, vp]
         L.hz_cycle_device.argtypes = [vp, i64, i32, vp, vp]
         L.hz_coarse_solve.argtypes = [vp, i64, i32, vp, vp]
         L.hz_hierarchy_num_levels.argtypes = [vp, C.POINTER(i32)]

@@ -10,6 +10,7 @@
 #include "profile.hpp"
 #include "block_tiled.cuh"
 #include "block_dmma.cuh"
+#include "block_k8.cuh"
 #include "devbuf.hpp"
 
 #include <cstdlib>
@@ -622,6 +623,67 @@ void update_tiled_launch(int64_t n, int nb, const BlockTab<T>& X, const cplx_t<T
   kern<<<grid_for(n, RC), 256, smem, s>>>(n, nb, X, H, Yin, Yout, sign);
 }
 
+// K = 8 register-direct DMMA kernels (block_k8.cuh) for nb <= kK8MaxNb
+constexpr int kK8MaxNb = 12;
+
+template <int NB>
+void gram8_dispatch(int nb, int64_t n, const BlockTab<double>& X, const double2* Y, double2* partials, int nslots,
+                    cudaStream_t s) {
+  if constexpr (NB <= kK8MaxNb) {
+    if (nb == NB) {
+      k8::gram8_kernel<NB><<<nslots, k8::kThreads, 0, s>>>(n, X, Y, partials);
+      return;
+    }
+    gram8_dispatch<NB + 1>(nb, n, X, Y, partials, nslots, s);
+  }
+}
+
+template <int NB, class TT>
+void update8_dispatch(int nb, int64_t n, const BlockTab<TT>& X, const double2* H, const double2* Yin,
+                      double2* Yout, double sign, cudaStream_t s) {
+  if constexpr (NB <= kK8MaxNb) {
+    if (nb == NB) {
+      const int64_t tiles = (n + 7) / 8;
+      const int grid = int(std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, (tiles + 7) / 8)));
+      k8::update8_kernel<NB, TT><<<grid, k8::kThreads, 0, s>>>(n, X, H, Yin, Yout, sign);
+      return;
+    }
+    update8_dispatch<NB + 1, TT>(nb, n, X, H, Yin, Yout, sign, s);
+  }
+}
+
+// Y += sum_i Z_i H_i, Z_i complex64 (widened), any k: one thread per output
+// element, H tiles in shared memory, complex products in the reference's
+// order (sum over i, then the k entries of a row)
+__global__ void __launch_bounds__(kBlk)
+update_lo_kernel(int64_t n, int k, int nb, const BlockTab<float> Z, const double2* __restrict__ H, double2* Y) {
+  extern __shared__ double2 hsm[];
+  for (int e = threadIdx.x; e < nb * k * k; e += kBlk) hsm[e] = H[e];
+  __syncthreads();
+  const int64_t e = int64_t(blockIdx.x) * kBlk + threadIdx.x;
+  if (e >= n * k) return;
+  const int64_t row = e / k;
+  const int q = int(e - row * k);
+  double2 acc = Y[e];
+  for (int i = 0; i < nb; ++i) {
+    const float2* z = Z.p[i] + row * k;
+    const double2* h = hsm + size_t(i) * k * k;
+    for (int p = 0; p < k; ++p) {
+      const float2 zf = __ldg(z + p);
+      acc = cfma(make_double2(double(zf.x), double(zf.y)), h[p * k + q], acc);
+    }
+  }
+  Y[e] = acc;
+}
+
+bool use_k8() {
+  static const bool on = [] {
+    const char* e = std::getenv("HZ_K8");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class T>
 int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx_t<T>* Y,
                       cplx_t<T>* partials, int max_slots, cudaStream_t s) {
@@ -632,6 +694,16 @@ int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx
   // ~4 CTAs per SM in total over the nb blocks; at least 32 rows per slot
   // exactly one wave of resident CTAs (3 per SM for the tiled / DMMA Grams)
   // over the nb blocks: a partial last wave would idle up to 2/3 of the GPU
+  if constexpr (std::is_same<T, double>::value) {
+    if (k == 8 && nb >= 1 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
+      // one pass over all nb blocks per CTA: one wave of 2 CTAs per SM
+      int64_t want = std::min<int64_t>(2 * kNumSMs, (n + 31) / 32);
+      const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(want, max_slots)));
+      gram8_dispatch<1>(nb, n, X, Y, partials, nslots, s);
+      HZ_LAUNCH_CHECK();
+      return nslots;
+    }
+  }
   int64_t want = std::max<int64_t>(1, (3 * kNumSMs) / nb);
   want = std::min<int64_t>(want, (n + 31) / 32);
   const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(want, max_slots)));
@@ -665,12 +737,34 @@ void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const c
   } else if (k == 64) {
     update_tiled_launch<T, 64>(n, nb, X, H, Yin, Yout, sign, s);
   } else if (k == 8) {
-    update_tiled_launch<T, 8>(n, nb, X, H, Yin, Yout, sign, s);
+    bool done = false;
+    if constexpr (std::is_same<T, double>::value) {
+      if (nb >= 1 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
+        update8_dispatch<1, double>(nb, n, X, H, Yin, Yout, sign, s);
+        done = true;
+      }
+    }
+    if (!done) update_tiled_launch<T, 8>(n, nb, X, H, Yin, Yout, sign, s);
   } else {
     const size_t smem = sizeof(cplx_t<T>) * size_t(k) * k;
     auto kern = multi_update_kernel<T>;
     allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
     kern<<<grid_for(n * k, kBlk), kBlk, smem, s>>>(n, k, nb, X, H, Yin, Yout, sign);
+  }
+  HZ_LAUNCH_CHECK();
+}
+
+void launch_update_lo(int64_t n, int k, int nb, const BlockTab<float>& Z, const double2* H, double2* Y,
+                      cudaStream_t s) {
+  ProfScope prof("multi_update_lo_c128", double(nb) * n * k * 8.0 + 2.0 * n * k * 16.0, s,
+                 8.0 * double(n) * k * k * nb);
+  if (nb < 1) return;
+  if (k == 8 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
+    update8_dispatch<1, float>(nb, n, Z, H, Y, Y, 1.0, s);
+  } else {
+    const size_t smem = sizeof(double2) * size_t(nb) * k * k;
+    allow_dyn_smem(reinterpret_cast<const void*>(update_lo_kernel), int(smem));
+    update_lo_kernel<<<grid_for(n * k, kBlk), kBlk, smem, s>>>(n, k, nb, Z, H, Y);
   }
   HZ_LAUNCH_CHECK();
 }

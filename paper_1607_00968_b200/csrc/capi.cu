@@ -254,10 +254,17 @@ DevOp<double> make_op_with(hz_solver* s, Hierarchy<double>* h64, Hierarchy<float
     launch_apply_residual<double>(P->fine_op(kk), x, b, r, st);
   };
   const CycleSpec* spec = &s->spec;
-  if (s->opts.precond_precision == HZ_C64)
+  if (s->opts.precond_precision == HZ_C64) {
     op.prec = [spec, h32](const double2* in, double2* out, int kk, cudaStream_t st) {
       h32->cycle_cast(*spec, kk, in, out, st);
     };
+    op.prec_lo = [spec, h32](const double2* in, float2* out, int kk, cudaStream_t st) {
+      h32->cycle_cast(*spec, kk, in, out, st);
+    };
+    op.apply_lo = [P](const float2* in, double2* out, int kk, cudaStream_t st) {
+      launch_apply_lo(P->fine_op(kk), in, out, st);
+    };
+  }
   else
     op.prec = [spec, h64](const double2* in, double2* out, int kk, cudaStream_t st) {
       h64->cycle(*spec, kk, in, out, true, st);
@@ -823,6 +830,37 @@ int hz_solve_blocks_multi_device(int count, hz_solver* const* solvers, const int
   }
   return run_concurrent(count, solvers, [&](int i) {
     return hz_solve_block_device(solvers[i], n[i], k[i], B[i], X[i], reps ? &reps[i] : nullptr);
+  });
+}
+
+// Block algebra of the Arnoldi step on caller device blocks (current
+// device, synchronous), for kernel-level parity with the reference.
+int hz_block_gram_device(int64_t n, int k, int nb, const void* const* X, const void* Y, double* G) {
+  return guarded([&] {
+    if (!X || !Y || !G) throw HzError(kValidation, "null argument");
+    if (n < 1 || nb < 1 || nb > kMaxBlocks) throw HzError(kValidation, "block gram: bad n / nb");
+    BlockAlgebra<double> alg;
+    alg.ensure(n, k, nb);
+    BlockTab<double> tab{};
+    for (int i = 0; i < nb; ++i) tab.p[i] = static_cast<const double2*>(X[i]);
+    DevBuf<double2> out(size_t(nb) * k * k);
+    alg.gram(tab, nb, static_cast<const double2*>(Y), out.get(), nullptr);
+    HZ_CUDA(cudaMemcpy(G, out.get(), out.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+int hz_block_add_scaled_device(int64_t n, int k, int nb, const void* const* X, const double* C, void* Y) {
+  return guarded([&] {
+    if (!X || !C || !Y) throw HzError(kValidation, "null argument");
+    if (n < 1 || nb < 1 || nb > kMaxBlocks) throw HzError(kValidation, "block update: bad n / nb");
+    if (k < 1 || k > 64) throw HzError(kValidation, "block width must be in [1, 64]");
+    BlockTab<double> tab{};
+    for (int i = 0; i < nb; ++i) tab.p[i] = static_cast<const double2*>(X[i]);
+    DevBuf<double2> c(size_t(nb) * k * k);
+    HZ_CUDA(cudaMemcpy(c.get(), C, c.bytes(), cudaMemcpyHostToDevice));
+    auto* y = static_cast<double2*>(Y);
+    launch_multi_update<double>(n, k, nb, tab, c.get(), y, y, 1.0, nullptr);
+    HZ_CUDA(cudaDeviceSynchronize());
   });
 }
 

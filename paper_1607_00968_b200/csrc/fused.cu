@@ -545,6 +545,9 @@ template void launch_fused_pre<double, double2>(const LevelOp<double>&, const Le
 template void launch_fused_post<float, double2, double2>(const LevelOp<float>&, const LevelGeom&, float,
                                                          const float2*, const float2*, const double2*, double2*,
                                                          cudaStream_t);
+template void launch_fused_post<float, double2, float2>(const LevelOp<float>&, const LevelGeom&, float,
+                                                        const float2*, const float2*, const double2*, float2*,
+                                                        cudaStream_t);
 template void launch_fused_post<float, float2, float2>(const LevelOp<float>&, const LevelGeom&, float,
                                                        const float2*, const float2*, const float2*, float2*,
                                                        cudaStream_t);

@@ -652,8 +652,11 @@ void Hierarchy<T>::coarse_visit(int l, const CycleSpec& spec, int k, cudaStream_
 // mixed-precision preconditioner): b64 -> x64 with the casts fused into the
 // first two and the last fine-level sweeps when the fine level allows it;
 // otherwise cast, cycle, cast.
+// XO = float2: the cycle's complex64 result without the up-cast (exact: the
+// c128 value would be its widening), for FGMRES's complex64 Z blocks.
 template <class T>
-void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, double2* x64, cudaStream_t s) {
+template <class XO>
+void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, XO* x64, cudaStream_t s) {
   if constexpr (!std::is_same<T, float>::value) {
     throw HzError(kState, "cycle_cast: complex64 hierarchies only");
   } else {
@@ -673,7 +676,11 @@ void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, 
       });
       cycle_rec(0, spec, k, b32, x, true, s);
       on_level(0, k, s, [&](const LevelOp<T>&, cudaStream_t st, int64_t r0, int64_t nr) {
-        launch_cast<double2, float2>(nr * k, x + r0 * k, x64 + r0 * k, st);
+        if constexpr (std::is_same<XO, double2>::value)
+          launch_cast<double2, float2>(nr * k, x + r0 * k, x64 + r0 * k, st);
+        else
+          HZ_CUDA(cudaMemcpyAsync(x64 + r0 * k, x + r0 * k, size_t(nr) * k * sizeof(float2),
+                                  cudaMemcpyDeviceToDevice, st));
       });
       return;
     }
@@ -682,7 +689,7 @@ void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, 
       const LevelGeom gc(levels_[1].dims[0], levels_[1].dims[1], levels_[1].dims[2], k);
       launch_fused_pre<T, double2>(op(0, k), gc, wj, b64, x, wb_[1].get(), s);
       coarse_visit(0, spec, k, s);
-      launch_fused_post<T, double2, double2>(op(0, k), gc, wj, x, wx_[1].get(), b64, x64, s);
+      launch_fused_post<T, double2, XO>(op(0, k), gc, wj, x, wx_[1].get(), b64, x64, s);
       return;
     }
     const bool sl = slab_level(0);
@@ -698,7 +705,10 @@ void Hierarchy<T>::cycle_cast(const CycleSpec& spec, int k, const double2* b64, 
     relax(0, spec, spec.post - 1, k, b32, cur, other, cur_zero, s);
     if (sl) sl_->neighbours();
     on_level(0, k, s, [&](const LevelOp<T>& o, cudaStream_t st, int64_t, int64_t) {
-      launch_jacobi_out64(o, wj, cur, b32, x64, st);
+      if constexpr (std::is_same<XO, double2>::value)
+        launch_jacobi_out64(o, wj, cur, b32, x64, st);
+      else
+        launch_jacobi<T>(o, wj, cur, b32, x64, st);
     });
   }
 }
@@ -725,5 +735,7 @@ void Hierarchy<T>::kcycle_coarse(int l, const CycleSpec& spec, int k, const V* b
 
 template class Hierarchy<double>;
 template class Hierarchy<float>;
+template void Hierarchy<float>::cycle_cast<double2>(const CycleSpec&, int, const double2*, double2*, cudaStream_t);
+template void Hierarchy<float>::cycle_cast<float2>(const CycleSpec&, int, const double2*, float2*, cudaStream_t);
 
 }  // namespace hz

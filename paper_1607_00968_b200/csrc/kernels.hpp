@@ -32,6 +32,9 @@ struct LevelOp {
 // out = A u                                    (K1: apply_block)
 template <class T>
 void launch_apply(const LevelOp<T>& op, const cplx_t<T>* u, cplx_t<T>* out, cudaStream_t s);
+// complex128 fine apply of a complex64 block (widened on load; the values
+// and arithmetic of launch_apply<double> on the widened block)
+void launch_apply_lo(const LevelOp<double>& op, const float2* u, double2* out, cudaStream_t s);
 // r = b - A x                                  (residual, src/multigrid.cpp:173-175)
 template <class T>
 void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
@@ -131,6 +134,10 @@ template <class T>
 struct BlockTab {
   const cplx_t<T>* p[kMaxBlocks];
 };
+// Y += sum_i Z_i H_i with complex64 blocks Z_i widened on load (FGMRES's
+// restart update X += Z Y over complex64 Z blocks)
+void launch_update_lo(int64_t n, int k, int nb, const BlockTab<float>& Z, const double2* H, double2* Y,
+                      cudaStream_t s);
 // Stage 1 of a deterministic two-stage reduction: per-CTA partial Grams
 // G_i = X_i^H Y for nb blocks X_i against one Y (k x k each).
 // Returns the number of partial slices written to `partials`

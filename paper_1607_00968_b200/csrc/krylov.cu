@@ -429,14 +429,20 @@ void BlockAlgebra<T>::thin_qr_finish(std::vector<cplx>& R, bool& deficient) {
 
 // ---------------------------------------------------------------- FGMRES
 template <class T>
-void Fgmres<T>::ensure(int64_t n, int k, int restart) {
+void Fgmres<T>::ensure(int64_t n, int k, int restart, bool lo) {
   if (restart < 1) throw HzError(kValidation, "fgmres: restart must be >= 1");
   if (restart + 2 > kMaxBlocks) throw HzError(kValidation, "fgmres: restart too large");
-  if (n == n_ && k == k_ && restart == m_) return;
+  if (n == n_ && k == k_ && restart == m_ && lo == lo_) return;
   Vb_.clear();
   Zb_.clear();
+  Zlo_.clear();
   Vb_.resize(restart + 1);
-  Zb_.resize(restart);
+  Zb_.resize(lo ? 0 : restart);
+  Zlo_.resize(lo ? restart : 0);
+  for (auto& b : Zlo_) b.alloc(size_t(n) * k);
+  zlotab_ = BlockTab<float>{};
+  for (int i = 0; i < int(Zlo_.size()); ++i) zlotab_.p[i] = Zlo_[i].get();
+  lo_ = lo;
   auto get = [&](DevBuf<V>& b) {
     if (sl_)
       alloc_span(b, *sl_, 0, k);
@@ -456,7 +462,7 @@ void Fgmres<T>::ensure(int64_t n, int k, int restart) {
   vtab_ = BlockTab<T>{};
   ztab_ = BlockTab<T>{};
   for (int i = 0; i <= restart; ++i) vtab_.p[i] = Vb_[i].get();
-  for (int i = 0; i < restart; ++i) ztab_.p[i] = Zb_[i].get();
+  for (int i = 0; i < int(Zb_.size()); ++i) ztab_.p[i] = Zb_[i].get();
   alg_.ensure(n, k, restart + 1, sl_);
   n_ = n;
   k_ = k;
@@ -468,7 +474,16 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
                         int max_cycles, cudaStream_t s) {
   const auto t0 = Clock::now();
   const int64_t n = op.n;
-  ensure(n, k, restart);
+  // complex64 Z blocks when the preconditioner is a complex64 cycle (exact;
+  // HZ_ZLO=0 keeps them in complex128); the restart update stages the k x k
+  // coefficient tiles in shared memory
+  static const bool zlo_env = [] {
+    const char* e = std::getenv("HZ_ZLO");
+    return !(e && e[0] == '0');
+  }();
+  const bool lo = zlo_env && !sl_ && op.prec_lo && op.apply_lo &&
+                  size_t(restart) * k * k * sizeof(V) <= 192 * 1024;
+  ensure(n, k, restart, lo);
   {
     const char* o = std::getenv("HZ_ORTHO");
     pip_ = !(o && std::string(o) == "cgs2");
@@ -532,14 +547,20 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     lsq.reset(k, m, Rk);
     int j = 0;
     // Z_j = M^{-1} V_j ; V_{j+1} <- A Z_j  (enqueue only)
-    auto enqueue_step = [&](int jj) {
+    auto precond_apply = [&](const V* v, int jj, V* w) {
+      if (lo_) {
+        op.prec_lo(v, Zlo_[jj].get(), k, s);
+        op.apply_lo(Zlo_[jj].get(), w, k, s);
+        return;
+      }
       V* Zj = Zb_[jj].get();
       if (op.prec)
-        op.prec(Vb_[jj].get(), Zj, k, s);
+        op.prec(v, Zj, k, s);
       else
-        copy_blk(Zj, Vb_[jj].get());
-      op.apply(Zj, Vb_[jj + 1].get(), k, s);
+        copy_blk(Zj, v);
+      op.apply(Zj, w, k, s);
     };
+    auto enqueue_step = [&](int jj) { precond_apply(Vb_[jj].get(), jj, Vb_[jj + 1].get()); };
     // The next step's preconditioner + matvec depend only on V_{j+1}, not on
     // the host least-squares update of step j, so they are enqueued before
     // the host LS and overlap it; if step j converges, the speculative work
@@ -575,14 +596,7 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
         const bool spec_next = j + 1 < m && rep.cycles < max_cycles;
         alg_.fork();
         alg_.update(j + 2, vtab_, ccoef_.get(), nullptr, Qs_.get(), T(1), s);
-        if (spec_next) {
-          V* Zn = Zb_[j + 1].get();
-          if (op.prec)
-            op.prec(Qs_.get(), Zn, k, s);
-          else
-            copy_blk(Zn, Qs_.get());
-          op.apply(Zn, Vb_[j + 2].get(), k, s);
-        }
+        if (spec_next) precond_apply(Qs_.get(), j + 1, Vb_[j + 2].get());
         HZ_CUDA(cudaEventSynchronize(ev_.get()));
         if (alg_.h_flags[0] == 0) {
           accepted = true;
@@ -642,7 +656,14 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     HZ_CUDA(cudaMemcpyAsync(ydev_.get(), h_y_.get(), sizeof(V) * size_t(j) * kk,
                             cudaMemcpyHostToDevice, s));
     alg_.fork();
-    alg_.update(j, ztab_, ydev_.get(), X, X, T(1), s);
+    if constexpr (std::is_same<T, double>::value) {
+      if (lo_)
+        launch_update_lo(n, k, j, zlotab_, ydev_.get(), X, s);
+      else
+        alg_.update(j, ztab_, ydev_.get(), X, X, T(1), s);
+    } else {
+      alg_.update(j, ztab_, ydev_.get(), X, X, T(1), s);
+    }
     // true residual for the restart / convergence decision; its norms come
     // from the Gram the next restart's QR starts from
     true_residual();

@@ -99,7 +99,9 @@ class Hierarchy {
   void coarse_solve(int k, const V* b, V* x, cudaStream_t s);
   // complex64 hierarchy as the preconditioner of a complex128 block (casts
   // fused into the fine-level sweeps where possible)
-  void cycle_cast(const CycleSpec& spec, int k, const double2* b64, double2* x64, cudaStream_t s);
+  // (XO = double2: widened result; XO = float2: the complex64 result as is)
+  template <class XO>
+  void cycle_cast(const CycleSpec& spec, int k, const double2* b64, XO* x64, cudaStream_t s);
   // Galerkin planes / diagonal of level l (host copy, f64) for parity checks
   void download_level(int l, std::vector<cplx>& coef_or_center) const;
   // copy of the level operators (not the coarsest solver) on another GPU
@@ -178,6 +180,11 @@ struct DevOp {
   std::function<void(const V* in, V* out, int k, cudaStream_t)> prec;  // optional
   // optional fused true residual r = b - A x (bitwise apply + axpby)
   std::function<void(const V* x, const V* b, V* r, int k, cudaStream_t)> resid;
+  // optional complex64 preconditioner output (a c64 cycle's result before
+  // its exact widening) + the operator applied to such a block: FGMRES then
+  // keeps its Z blocks in complex64 -- the same values at half the bytes
+  std::function<void(const V* in, float2* out, int k, cudaStream_t)> prec_lo;
+  std::function<void(const float2* in, V* out, int k, cudaStream_t)> apply_lo;
 };
 
 // Device block algebra shared by the Krylov methods.
@@ -262,6 +269,7 @@ class Fgmres {
       n_ = 0;
       Vb_.clear();
       Zb_.clear();
+      Zlo_.clear();
       R_.release();
       Qs_.release();
       alg_.tmp_blk.release();
@@ -270,11 +278,14 @@ class Fgmres {
   }
 
  private:
-  void ensure(int64_t n, int k, int restart);
+  void ensure(int64_t n, int k, int restart, bool lo);
   const Slabs* sl_ = nullptr;
   int64_t n_ = 0;
   int k_ = 0, m_ = 0;
   std::vector<DevBuf<V>> Vb_, Zb_;
+  std::vector<DevBuf<float2>> Zlo_;  // complex64 Z blocks (DevOp::prec_lo)
+  bool lo_ = false;
+  BlockTab<float> zlotab_{};
   DevBuf<V> R_;
   DevBuf<V> Qs_;  // spare block: the speculative one-pass Q of an Arnoldi step
   BlockTab<T> vtab_{}, ztab_{};

@@ -39,8 +39,19 @@ __device__ __forceinline__ bool decode(const LevelGeom& g, uint32_t e, Elem<T>& 
 //            x-, x+, y-, y+, z-, z+ (src/helmholtz.cpp:85-98).
 // CSR=true : Csr::mul_block order over the sorted row -- z-, y-, x-, centre,
 //            x+, y+, z+ (inc/csr.hpp:43-53), used by the multigrid levels.
-template <class T, int NDIM, bool CSR>
-__device__ __forceinline__ cplx_t<T> fine_ax(const LevelOp<T>& op, const cplx_t<T>* __restrict__ x,
+// widening load: XV = the level's complex type, or complex64 read into complex128
+template <class V, class XV>
+__device__ __forceinline__ V ldw(const XV* p) {
+  if constexpr (std::is_same<V, XV>::value) {
+    return __ldg(p);
+  } else {
+    const XV v = __ldg(p);
+    return mk(double(v.x), double(v.y));
+  }
+}
+
+template <class T, int NDIM, bool CSR, class XV = cplx_t<T>>
+__device__ __forceinline__ cplx_t<T> fine_ax(const LevelOp<T>& op, const XV* __restrict__ x,
                                              uint32_t e, const Elem<T>& el) {
   using V = cplx_t<T>;
   const LevelGeom& g = op.g;
@@ -52,13 +63,13 @@ __device__ __forceinline__ cplx_t<T> fine_ax(const LevelOp<T>& op, const cplx_t<
   const bool xm = el.i > 0, xp = el.i + 1 < g.n0, ym = el.j > 0, yp = el.j + 1 < g.n1;
   const bool zm = NDIM == 3 && el.kz > 0, zp = NDIM == 3 && el.kz + 1 < g.n2;
   const V c = __ldg(&op.center[el.node]);
-  const V u0 = __ldg(&x[e]);
-  const V uxm = __ldg(&x[xm ? e - sx : e]), uxp = __ldg(&x[xp ? e + sx : e]);
-  const V uym = __ldg(&x[ym ? e - sy : e]), uyp = __ldg(&x[yp ? e + sy : e]);
+  const V u0 = ldw<V>(&x[e]);
+  const V uxm = ldw<V>(&x[xm ? e - sx : e]), uxp = ldw<V>(&x[xp ? e + sx : e]);
+  const V uym = ldw<V>(&x[ym ? e - sy : e]), uyp = ldw<V>(&x[yp ? e + sy : e]);
   V uzm = u0, uzp = u0;
   if (NDIM == 3) {
-    uzm = __ldg(&x[zm ? e - sz : e]);
-    uzp = __ldg(&x[zp ? e + sz : e]);
+    uzm = ldw<V>(&x[zm ? e - sz : e]);
+    uzp = ldw<V>(&x[zp ? e + sz : e]);
   }
   const T wx = op.w[0], wy = op.w[1], wz = op.w[2];
   V acc;
@@ -152,6 +163,18 @@ level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __
     const V wd = mk(wj * d.x, wj * d.y);
     out[e] = cadd(__ldg(&x[e]), cmul(wd, csub(__ldg(&b[e]), ax)));
   }
+}
+
+// out = A x for the complex128 fine operator with x a complex64 block
+// (widened on load, exact): the apply_block arithmetic of level_kernel
+// MODE 0 on the same values, reading half the bytes of x.
+template <int NDIM>
+__global__ void __launch_bounds__(kBlock)
+apply_lo_kernel(LevelOp<double> op, const float2* __restrict__ x, double2* __restrict__ out) {
+  const uint32_t e = op.g.e_begin() + blockIdx.x * kBlock + threadIdx.x;
+  Elem<double> el;
+  if (!decode(op.g, e, el)) return;
+  out[e] = fine_ax<double, NDIM, false, float2>(op, x, e, el);
 }
 
 // Galerkin 9/27-point level kernel, CPT consecutive columns per thread: the
@@ -816,6 +839,18 @@ template <class T>
 void launch_apply(const LevelOp<T>& op, const cplx_t<T>* u, cplx_t<T>* out, cudaStream_t s) {
   dispatch_level<T, 0>(op, u, nullptr, out, T(0), s);
 }
+void launch_apply_lo(const LevelOp<double>& op, const float2* u, double2* out, cudaStream_t s) {
+  if (op.kind != kFine) throw HzError(kState, "apply_lo: fine operator only");
+  const double n = double(op.g.owned_nodes()), k = op.g.k;
+  ProfScope prof("apply_fine_c128", n * (k * (8.0 + 16.0) + 16.0), s);
+  const int grid = grid_for(op.g.owned_elems(), kBlock);
+  if (op.ndim == 3)
+    apply_lo_kernel<3><<<grid, kBlock, 0, s>>>(op, u, out);
+  else
+    apply_lo_kernel<2><<<grid, kBlock, 0, s>>>(op, u, out);
+  HZ_LAUNCH_CHECK();
+}
+
 template <class T>
 void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
                      cudaStream_t s) {

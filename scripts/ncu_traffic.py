@@ -16,6 +16,10 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def name_of(k):
+    if "fused_pre_kernel<float" in k:
+        return "fused_pre_fine_c64"
+    if "fused_post_kernel<float" in k:
+        return "fused_post_fine_c64"
     if "update_kernel" in k:
         return "multi_update_c128"
     if "gram_kernel" in k:

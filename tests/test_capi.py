@@ -81,3 +81,16 @@ def test_cpp_header_compiles():
     r = subprocess.run(["g++", "-std=c++17", "-fsyntax-only", "-x", "c++", src, "-I", os.path.join(ROOT, "include")],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_library_has_no_undefined_internal_symbols():
+    """Every hz:: template the library uses is instantiated in it (a missing
+    explicit instantiation only shows up as a load failure on the GPU box)."""
+    import shutil
+    import subprocess
+    from paper_1607_00968_b200 import _native
+    if not shutil.which("nm"):
+        pytest.skip("nm not available")
+    out = subprocess.run(["nm", "-C", "--undefined-only", _native.LIB_PATH], capture_output=True, text=True).stdout
+    missing = [ln for ln in out.splitlines() if "hz::" in ln]
+    assert not missing, missing

@@ -95,3 +95,60 @@ def test_blocked_solve_3d_one_column_groups():
         xj, rj = S1.solve_block(np.ascontiguousarray(B[:, j:j + 1]))
         assert np.array_equal(X[:, j:j + 1], xj)
         assert rep.col_cycles[j] == rj.col_cycles[0]
+
+
+# ---- the Arnoldi block algebra on its own (K = 8 register-direct DMMA
+# kernels, block_k8.cuh; other widths through the staged kernels)
+@pytest.mark.parametrize("n,k,nb", [(525825, 8, 1), (525825, 8, 2), (100003, 8, 6), (4097, 8, 12),
+                                    (13, 8, 3), (70001, 8, 13), (9001, 16, 3), (5003, 4, 2)])
+def test_block_gram_and_update_match_numpy(n, k, nb):
+    rng = np.random.default_rng(n + k + nb)
+    Xh = [rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)) for _ in range(nb)]
+    Yh = rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k))
+    Cs = rng.standard_normal((nb, k, k)) + 1j * rng.standard_normal((nb, k, k))
+    Xd = [torch.from_numpy(x).cuda() for x in Xh]
+    Yd = torch.from_numpy(Yh).cuda()
+    G = hz.block_gram(Xd, Yd)
+    for i in range(nb):
+        ref_g = Xh[i].conj().T @ Yh
+        assert rel_err(G[i], ref_g) <= 1e-13
+    hz.block_add_scaled(Yd, Xd, Cs)
+    ref_y = Yh + sum(Xh[i] @ Cs[i] for i in range(nb))
+    assert rel_err(Yd.cpu().numpy(), ref_y) <= 1e-14
+
+
+ZLO_SOLVE = (
+    "import sys; sys.path.insert(0, '.'); import numpy as np\n"
+    "import paper_1607_00968_b200 as hz; from paper_1607_00968_b200 import configs\n"
+    "cfg = configs.config2(nlevels=4, k=int(sys.argv[2]), nx=257, nz=129); cfg.restart = 4\n"
+    "cfg.shift, cfg.jacobi_weight, cfg.precond_precision, cfg.max_cycles = 0.9, 0.6, 'c64', 400\n"
+    "S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))\n"
+    "X, rep = S.solve_block(cfg.rhs_block())\n"
+    "assert rep.all_converged(), rep.rel_residual\n"
+    "np.save(sys.argv[1], X)\n")
+
+
+@pytest.mark.parametrize("k", [8, 4])
+def test_complex64_z_blocks_match_complex128_z_blocks(k):
+    """FGMRES keeps the preconditioned blocks Z_j of a complex64 cycle in
+    complex64 (HZ_ZLO, default on): the values are the c128 ones before their
+    exact widening, so the K = 8 path (same DMMA update kernel) is bitwise
+    equal to the c128-Z run; other widths differ by the restart update's
+    rounding only."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    with tempfile.TemporaryDirectory() as d:
+        for flag in ("1", "0"):
+            path = os.path.join(d, f"x{flag}.npy")
+            r = subprocess.run([sys.executable, "-c", ZLO_SOLVE, path, str(k)], cwd=root,
+                               env=dict(os.environ, HZ_ZLO=flag), capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+    if k == 8:
+        assert np.array_equal(outs[0], outs[1])
+    else:
+        assert rel_err(outs[0], outs[1]) <= 1e-8
