@@ -374,7 +374,11 @@ def run_ours(args):
                "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
                "traffic": (traffic_tab.get(name) or {}).get("dram_bytes_per_launch"),
                "traffic_note": (traffic_tab.get(name) or {}).get("note")}
-        if r.get("flops", 0) > 0:
+        # the binding roofline: FP64 tensor pipe when the kernel's flops at
+        # the DMMA peak take longer than its bytes at the HBM peak (the
+        # 32-column Gram / update), else HBM (8-column blocks, stencils)
+        flops_bound = r.get("flops", 0) > 0 and 0.75 * r["flops"] / (fp64_peak * 1e12) > r["bytes"] / (peak * 1e9)
+        if flops_bound:
             tf = r["flops"] / secs / 1e12
             per.update({"bound": "tensor", "achieved": round(tf, 2), "peak": round(fp64_peak, 2),
                         "unit": "TFLOP/s", "frac": round(tf / fp64_peak, 4), "peak_source": fp64_src,
@@ -384,6 +388,8 @@ def run_ours(args):
         else:
             per.update({"bound": "hbm", "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s",
                         "frac": round(gbs / peak, 4), "peak_source": peak_kind})
+            if r.get("flops", 0) > 0:
+                per["fp64_tflops"] = round(r["flops"] / secs / 1e12, 2)
         return per
 
     dom = max(kern, key=lambda n_: kern[n_]["ms"])

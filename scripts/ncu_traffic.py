@@ -16,6 +16,12 @@ scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
 def name_of(k):
+    if "update8_kernel" in k:
+        return "multi_update_lo_c128" if ", float>" in k else "multi_update_c128"
+    if "gram8_kernel" in k:
+        return "multi_gram_c128"
+    if "apply_lo_kernel" in k:
+        return "apply_fine_c128"
     if "fused_pre_kernel<float" in k:
         return "fused_pre_fine_c64"
     if "fused_post_kernel<float" in k:
