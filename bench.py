@@ -155,7 +155,7 @@ def config_json(cfg, world, l2_note):
             "grid": list(cfg.n[:2]), "rhs_per_gpu": cfg.k, "global_rhs": cfg.k * world,
             "solver": f"block FGMRES({cfg.restart}) + {cfg.cycle}({cfg.pre},{cfg.post}) MG, "
                       f"{cfg.nlevels} levels, shift {cfg.shift}, w_J {cfg.jacobi_weight}",
-            "rhs_blocking": (f"{-(-cfg.k // cfg.krylov_block)} concurrent block solves of {cfg.krylov_block} columns"
+            "rhs_blocking": (f"{-(-cfg.k // cfg.krylov_block)} independent block solves of {cfg.krylov_block} columns"
                              if 0 < cfg.krylov_block < cfg.k else f"one block of {cfg.k} columns"),
             "precision": "c128 Krylov / c64 preconditioner", "tol": cfg.tol,
             "parallelism": f"rhs-sharded x{world}", "l2": l2_note}

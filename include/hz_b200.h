@@ -270,6 +270,9 @@ HZ_API int hz_solve_helmholtz_compact16(hz_solver* s, int64_t n, int k, const do
 HZ_API int hz_profile_begin(void);
 HZ_API int hz_profile_end(void);
 HZ_API int64_t hz_profile_report(char* buf, int64_t cap);
+/* per-launch timeline of the last profiled region: JSON [[name, stream,
+ * start_ms, dur_ms, bytes], ...]; same size protocol as hz_profile_report */
+HZ_API int64_t hz_profile_trace(char* buf, int64_t cap);
 /* Diagnostic (no reference counterpart): the FP64 tensor-pipe (DMMA,
    mma.sync m8n8k4 f64) peak of the current device in TFLOP/s, measured by a
    ~50 ms register-only kernel -- the roofline denominator of the FP64-bound

@@ -220,7 +220,12 @@ class MultiFrequencySolver:
 class kernel_profile:
     """Context manager: CUDA-event timing of every library kernel launched
     inside the block. `.result` maps kernel name -> {count, ms, bytes, flops}
-    (summed event durations and algorithmic bytes / flops)."""
+    (summed event durations and algorithmic bytes / flops); with
+    trace=True, `.trace` lists [name, stream, start_ms, dur_ms, bytes] per
+    launch (hz_profile_trace)."""
+
+    def __init__(self, trace: bool = False):
+        self.want_trace = trace
 
     def __enter__(self):
         _check(_native.lib().hz_profile_begin())
@@ -237,6 +242,11 @@ class kernel_profile:
         buf = C.create_string_buffer(int(need))
         L.hz_profile_report(buf, need)
         self.result = json.loads(buf.value.decode())
+        if getattr(self, "want_trace", False):
+            need = L.hz_profile_trace(None, 0)
+            buf = C.create_string_buffer(int(need))
+            L.hz_profile_trace(buf, need)
+            self.trace = json.loads(buf.value.decode())
         return False
 
 

@@ -26,7 +26,7 @@ EXPORTS = (
     "hz_sample_device", "hz_sample", "hz_sample_adjoint_device", "hz_sample_adjoint",
     "hz_fwi_sensitivity_rhs_device", "hz_fwi_jacobian_vec", "hz_fwi_jacobian_vec_device",
     "hz_fwi_jacobian_transpose_vec", "hz_fwi_jacobian_transpose_vec_device", "hz_compact16_device",
-    "hz_solve_helmholtz_compact16", "hz_compact16", "hz_block_gram_device", "hz_block_add_scaled_device",
+    "hz_solve_helmholtz_compact16", "hz_compact16", "hz_block_gram_device", "hz_block_add_scaled_device", "hz_profile_trace",
 )
 
 
@@ -63,6 +63,8 @@ def lib():
         L.hz_kernel_launch_count.restype = C.c_int64
         L.hz_profile_report.restype = C.c_int64
         L.hz_profile_report.argtypes = [C.c_char_p, C.c_int64]
+        L.hz_profile_trace.restype = C.c_int64
+        L.hz_profile_trace.argtypes = [C.c_char_p, C.c_int64]
         vp, i64, dbl, i32 = C.c_void_p, C.c_int64, C.c_double, C.c_int
         L.hz_problem_create.argtypes = [i32, vp, vp, vp, dbl, dbl, vp, i32, i32, C.POINTER(vp)]
         L.hz_problem_destroy.argtypes = [vp]

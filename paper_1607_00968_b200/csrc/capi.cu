@@ -32,24 +32,30 @@ struct ProfRec {
   const char* name;
   double bytes, flops;
   cudaEvent_t a, b;
+  cudaStream_t s;
 };
 std::mutex g_prof_mu;
 bool g_prof_on = false;
+// events are created up front (hz_profile_begin) and handed out by an atomic
+// index, so concurrent solves do not serialise on the profiler
+constexpr size_t kProfPool = size_t(1) << 17;
 std::vector<cudaEvent_t> g_prof_pool;
-size_t g_prof_next = 0;
+std::atomic<size_t> g_prof_next{0};
+std::vector<cudaEvent_t> g_prof_extra;
 std::vector<ProfRec> g_prof_recs;
 }  // namespace
 
 bool profiling_enabled() { return g_prof_on; }
 
 cudaEvent_t profile_event() {
+  const size_t i = g_prof_next.fetch_add(1);
+  if (i < g_prof_pool.size()) return g_prof_pool[i];  // never resized while profiling
+  // pool exhausted: fresh events kept apart (destroyed at the next begin)
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  if (g_prof_next == g_prof_pool.size()) {
-    cudaEvent_t e;
-    HZ_CUDA(cudaEventCreate(&e));
-    g_prof_pool.push_back(e);
-  }
-  return g_prof_pool[g_prof_next++];
+  cudaEvent_t e;
+  HZ_CUDA(cudaEventCreate(&e));
+  g_prof_extra.push_back(e);
+  return e;
 }
 
 const char* profile_name_level(const char* base, int level) {
@@ -63,9 +69,10 @@ const char* profile_name_level(const char* base, int level) {
   return slot->c_str();
 }
 
-void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b) {
+void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b,
+                    cudaStream_t s) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
-  g_prof_recs.push_back({name, bytes, flops, a, b});
+  g_prof_recs.push_back({name, bytes, flops, a, b, s});
 }
 
 }  // namespace hz
@@ -445,7 +452,16 @@ int hz_measure_fp64_peak(double* tflops) {
 int hz_profile_begin(void) {
   return guarded([&] {
     std::lock_guard<std::mutex> lk(g_prof_mu);
+    HZ_CUDA(cudaDeviceSynchronize());
     g_prof_recs.clear();
+    g_prof_recs.reserve(kProfPool / 2);
+    for (cudaEvent_t e : g_prof_extra) cudaEventDestroy(e);
+    g_prof_extra.clear();
+    while (g_prof_pool.size() < kProfPool) {
+      cudaEvent_t e;
+      HZ_CUDA(cudaEventCreate(&e));
+      g_prof_pool.push_back(e);
+    }
     g_prof_next = 0;
     g_prof_on = true;
   });
@@ -453,6 +469,39 @@ int hz_profile_begin(void) {
 
 int hz_profile_end(void) {
   return guarded([&] { g_prof_on = false; });
+}
+
+// Per-launch timeline of the profiled region: JSON list of
+// [name, stream, start_ms, dur_ms, bytes] with start relative to the first
+// recorded launch (events on different streams of one device compare).
+int64_t hz_profile_trace(char* buf, int64_t cap) {
+  std::string js;
+  const int st = guarded([&] {
+    HZ_CUDA(cudaDeviceSynchronize());
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    std::map<cudaStream_t, int> sid;
+    std::ostringstream os;
+    os.precision(9);
+    os << "[";
+    for (size_t i = 0; i < g_prof_recs.size(); ++i) {
+      const auto& r = g_prof_recs[i];
+      float t0 = 0, d = 0;
+      HZ_CUDA(cudaEventElapsedTime(&t0, g_prof_recs[0].a, r.a));
+      HZ_CUDA(cudaEventElapsedTime(&d, r.a, r.b));
+      const int id = sid.emplace(r.s, int(sid.size())).first->second;
+      os << (i ? "," : "") << "[\"" << r.name << "\"," << id << "," << t0 << "," << d << "," << r.bytes << "]";
+    }
+    os << "]";
+    js = os.str();
+  });
+  if (st != kOk) return -1;
+  const int64_t need = int64_t(js.size()) + 1;
+  if (buf && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, int64_t(js.size()));
+    std::memcpy(buf, js.data(), size_t(n));
+    buf[n] = 0;
+  }
+  return need;
 }
 
 int64_t hz_profile_report(char* buf, int64_t cap) {

@@ -558,6 +558,17 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
     coarse_solve(k, b, x, s);
     return;
   }
+  {  // timing experiments only (wrong preconditioner): HZ_DEBUG_CUT_LEVEL=c
+     // replaces the visits of levels >= c by a zero correction
+    static const int cut = [] {
+      const char* e = std::getenv("HZ_DEBUG_CUT_LEVEL");
+      return e ? std::atoi(e) : 0;
+    }();
+    if (cut > 0 && l >= cut) {
+      HZ_CUDA(cudaMemsetAsync(x, 0, size_t(levels_[l].nodes()) * k * sizeof(V), s));
+      return;
+    }
+  }
   if (l == 0 && x_zero && fused_level0(spec, k)) {
     // fused finest-level visit: pre-smoothing + residual + restriction,
     // coarse visit(s), prolongation + post-smoothing (fused.cu)
@@ -623,8 +634,59 @@ void Hierarchy<T>::coarse_correction(int l, const CycleSpec& spec, int k, const 
   });
 }
 
+// The coarse part of the cycle (levels > l0, HZ_PRIO_FROM, default 0) runs on
+// a high-priority stream forked from / joined to the caller's: its many small,
+// latency-bound kernels then take SMs ahead of the large fine-level and
+// Krylov kernels that concurrent solves (RHS groups, frequencies) keep queued,
+// instead of waiting behind them. Same kernels, same order: bitwise equal.
+// Off by default (HZ_PRIO=1 enables): no gain measured at the bench blocking
+// (1.309 vs 1.323 ms per cycle, profiles/r01_prio_variants.txt).
+namespace {
+bool prio_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HZ_PRIO");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+int prio_from() {
+  static const int l0 = [] {
+    const char* e = std::getenv("HZ_PRIO_FROM");
+    return e ? std::atoi(e) : 0;
+  }();
+  return l0;
+}
+}  // namespace
+
+template <class T>
+Hierarchy<T>::~Hierarchy() {
+  if (hp_fork_) cudaEventDestroy(hp_fork_);
+  if (hp_join_) cudaEventDestroy(hp_join_);
+  if (hp_) cudaStreamDestroy(hp_);
+}
+
 template <class T>
 void Hierarchy<T>::coarse_visit(int l, const CycleSpec& spec, int k, cudaStream_t s) {
+  if (l == prio_from() && !sl_ && prio_enabled()) {
+    if (!hp_) {
+      int lo = 0, hi = 0;
+      HZ_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      HZ_CUDA(cudaStreamCreateWithPriority(&hp_, cudaStreamNonBlocking, hi));
+      HZ_CUDA(cudaEventCreateWithFlags(&hp_fork_, cudaEventDisableTiming));
+      HZ_CUDA(cudaEventCreateWithFlags(&hp_join_, cudaEventDisableTiming));
+    }
+    HZ_CUDA(cudaEventRecord(hp_fork_, s));
+    HZ_CUDA(cudaStreamWaitEvent(hp_, hp_fork_, 0));
+    coarse_visit_on(l, spec, k, hp_);
+    HZ_CUDA(cudaEventRecord(hp_join_, hp_));
+    HZ_CUDA(cudaStreamWaitEvent(s, hp_join_, 0));
+    return;
+  }
+  coarse_visit_on(l, spec, k, s);
+}
+
+template <class T>
+void Hierarchy<T>::coarse_visit_on(int l, const CycleSpec& spec, int k, cudaStream_t s) {
   const int L = num_levels();
   const bool sl = slab_level(l);
   V* ec = wx_[l + 1].get();

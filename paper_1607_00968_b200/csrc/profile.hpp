@@ -12,7 +12,8 @@
 namespace hz {
 
 bool profiling_enabled();
-void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b);
+void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b,
+                    cudaStream_t s = nullptr);
 cudaEvent_t profile_event();
 // interned "<base>_L<level>" (stable pointer for the profile records)
 const char* profile_name_level(const char* base, int level);
@@ -30,7 +31,7 @@ class ProfScope {
   ~ProfScope() {
     if (a_) {
       cudaEventRecord(b_, s_);
-      profile_record(name_, bytes_, flops_, a_, b_);
+      profile_record(name_, bytes_, flops_, a_, b_, s_);
     }
   }
 

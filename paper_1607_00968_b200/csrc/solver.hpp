@@ -79,6 +79,10 @@ template <class T>
 class Hierarchy {
  public:
   using V = cplx_t<T>;
+  Hierarchy() = default;
+  Hierarchy(const Hierarchy&) = delete;
+  Hierarchy& operator=(const Hierarchy&) = delete;
+  ~Hierarchy();
   // Build from f64 setup data (the f64 hierarchy is always built first; the
   // c64 one is a rounded copy so both apply the same operators).
   static std::unique_ptr<Hierarchy<double>> build(const Problem& p, int nlevels, double shift,
@@ -138,6 +142,7 @@ class Hierarchy {
   // the coarse visit(s) of level l's correction: level l+1 solved from
   // wb_[l+1] into wx_[l+1] (V / W / K per spec.kind)
   void coarse_visit(int l, const CycleSpec& spec, int k, cudaStream_t s);
+  void coarse_visit_on(int l, const CycleSpec& spec, int k, cudaStream_t s);
   bool fused_level0(const CycleSpec& spec, int k) const;
   bool slab_level(int l) const { return sl_ && l < sl_->agg_level(); }
   // f(op, stream, row0, rows) once per part owning level l (slab levels), or
@@ -149,6 +154,9 @@ class Hierarchy {
   int ws_k_ = 0;
   std::vector<DevBuf<V>> wx_, wt_, wb_, wr_;  // per level: solution, ping-pong, rhs, residual
   std::vector<std::unique_ptr<Fgmres<T>>> kfgm_;
+  // high-priority stream of the coarse part of the cycle (coarse_visit)
+  cudaStream_t hp_ = nullptr;
+  cudaEvent_t hp_fork_ = nullptr, hp_join_ = nullptr;
 };
 
 // explicit inverse of the unshifted operator (HelmholtzMethod::DenseLuSmall)
