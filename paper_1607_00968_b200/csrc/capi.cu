@@ -271,6 +271,10 @@ DevOp<double> make_op_with(hz_solver* s, Hierarchy<double>* h64, Hierarchy<float
     op.apply_lo = [P](const float2* in, double2* out, int kk, cudaStream_t st) {
       launch_apply_lo(P->fine_op(kk), in, out, st);
     };
+    op.apply_lo_gram = [P](const float2* Z, double2* W, const BlockTab<double>& X, int nb, double2* part,
+                           int max_slots, cudaStream_t st) {
+      return launch_gram8_apply(P->fine_op(8), nb, X, Z, W, part, max_slots, st);
+    };
   }
   else
     op.prec = [spec, h64](const double2* in, double2* out, int kk, cudaStream_t st) {

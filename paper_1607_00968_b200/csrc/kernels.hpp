@@ -134,6 +134,11 @@ template <class T>
 struct BlockTab {
   const cplx_t<T>* p[kMaxBlocks];
 };
+// W = A Z (fine complex128 operator, Z complex64, k = 8) fused with the
+// partial Grams of [X_0..X_{nb-2}, W]^H W (gram8 slot layout); returns the
+// number of partial slots written (<= max_slots)
+int launch_gram8_apply(const LevelOp<double>& op, int nb, const BlockTab<double>& X, const float2* Z, double2* W,
+                       double2* partials, int max_slots, cudaStream_t s);
 // Y += sum_i Z_i H_i with complex64 blocks Z_i widened on load (FGMRES's
 // restart update X += Z Y over complex64 Z blocks)
 void launch_update_lo(int64_t n, int k, int nb, const BlockTab<float>& Z, const double2* H, double2* Y,

@@ -282,6 +282,14 @@ void BlockAlgebra<T>::update(int nb, const BlockTab<T>& X, const V* H, const V* 
 }
 
 template <class T>
+void BlockAlgebra<T>::gram_apply(const DevOp<T>& op, const BlockTab<T>& tab, int nb, const float2* Z, V* W, V* out,
+                                 cudaStream_t s) {
+  if (sl) throw HzError(kState, "gram_apply: not in slab mode");
+  const int used = op.apply_lo_gram(Z, W, tab, nb, partials.get(), pslots[0], s);
+  launch_reduce_partials<T>(int64_t(nb) * k * k, used, partials.get(), out, s);
+}
+
+template <class T>
 void BlockAlgebra<T>::col_norms(const V* X, std::vector<double>& out, cudaStream_t s) {
   int used = 0;
   each(s, [&](int p, int64_t r0, int64_t nr, cudaStream_t st) {
@@ -454,6 +462,7 @@ void Fgmres<T>::ensure(int64_t n, int k, int restart, bool lo) {
   get(R_);
   get(Qs_);
   hcol1_.alloc(size_t(restart + 2) * k * k);
+  hcol_next_.alloc(size_t(restart + 2) * k * k);
   ccoef_.alloc(size_t(restart + 2) * k * k);
   hcol2_.alloc(size_t(restart + 1) * k * k);
   ydev_.alloc(size_t(restart) * k * k);
@@ -484,6 +493,15 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
   const bool lo = zlo_env && !sl_ && op.prec_lo && op.apply_lo &&
                   size_t(restart) * k * k * sizeof(V) <= 192 * 1024;
   ensure(n, k, restart, lo);
+  // off by default (HZ_GRAM_APPLY=1 enables): the fused kernel took 90 us
+  // against 27 + 53 us for apply_lo + gram8 alone, and 1.33 vs 1.30 ms per
+  // cycle at the bench blocking (profiles/r01_gram_apply.txt)
+  static const bool ga_env = [] {
+    const char* e = std::getenv("HZ_GRAM_APPLY");
+    return e && e[0] == '1';
+  }();
+  ga_ = ga_env && lo_ && k == 8 && restart + 1 <= 12 && bool(op.apply_lo_gram);
+  gram_next_ = false;
   {
     const char* o = std::getenv("HZ_ORTHO");
     pip_ = !(o && std::string(o) == "cgs2");
@@ -550,6 +568,14 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     auto precond_apply = [&](const V* v, int jj, V* w) {
       if (lo_) {
         op.prec_lo(v, Zlo_[jj].get(), k, s);
+        if (ga_) {  // W = A Z_jj and the step's Gram [V_0..V_jj, W]^H W in one pass
+          BlockTab<T> t = vtab_;
+          t.p[jj] = v;
+          t.p[jj + 1] = w;
+          alg_.gram_apply(op, t, jj + 2, Zlo_[jj].get(), w, hcol_next_.get(), s);
+          gram_next_ = true;
+          return;
+        }
         op.apply_lo(Zlo_[jj].get(), w, k, s);
         return;
       }
@@ -575,7 +601,12 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
       bool deficient = false;
       H[j].assign(j + 2, std::vector<cplx>(kk));
       // Pass 1: one Gram of [V_0..V_j, W]^H W gives H_{:,j} and W^H W.
-      alg_.gram(vtab_, j + 2, W, hcol1_.get(), s);
+      if (gram_next_) {  // computed with the matvec (precond_apply)
+        std::swap(hcol1_, hcol_next_);
+        gram_next_ = false;
+      } else {
+        alg_.gram(vtab_, j + 2, W, hcol1_.get(), s);
+      }
       rep.block_gram_products += j + 1;
       bool accepted = false;
       if (pip_) {

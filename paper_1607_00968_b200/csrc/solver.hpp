@@ -193,6 +193,10 @@ struct DevOp {
   // keeps its Z blocks in complex64 -- the same values at half the bytes
   std::function<void(const V* in, float2* out, int k, cudaStream_t)> prec_lo;
   std::function<void(const float2* in, V* out, int k, cudaStream_t)> apply_lo;
+  // optional apply_lo fused with the Arnoldi Gram: W = A Z and the partial
+  // Grams of [X_0..X_{nb-2}, W]^H W (k = 8); returns the slots written
+  std::function<int(const float2* Z, V* W, const BlockTab<T>& X, int nb, V* partials, int max_slots, cudaStream_t)>
+      apply_lo_gram;
 };
 
 // Device block algebra shared by the Krylov methods.
@@ -204,6 +208,9 @@ class BlockAlgebra {
   void ensure(int64_t n, int k, int max_blocks, const Slabs* sl = nullptr);
   // G_i = X_i^H Y for nb blocks, result on device (nb k^2, row-major tiles)
   void gram(const BlockTab<T>& tab, int nb, const V* Y, V* out, cudaStream_t s);
+  // W = A Z with the Gram [X_0..X_{nb-2}, W]^H W into out (op.apply_lo_gram)
+  void gram_apply(const DevOp<T>& op, const BlockTab<T>& tab, int nb, const float2* Z, V* W, V* out,
+                  cudaStream_t s);
   // per-column 2-norms to host
   void col_norms(const V* X, std::vector<double>& out, cudaStream_t s);
   // CholQR2 thin QR of W in place (inc/block.hpp:104-137 semantics):
@@ -310,6 +317,9 @@ class Fgmres {
     }
   } ev_;
   DevBuf<V> hcol1_, hcol2_, ydev_, ccoef_;
+  // Gram of the next step computed with its matvec (DevOp::apply_lo_gram)
+  DevBuf<V> hcol_next_;
+  bool gram_next_ = false, ga_ = false;
   // Pythagorean one-pass orthogonalisation with CGS2 fallback (HZ_ORTHO=cgs2
   // forces the two-pass path everywhere)
   bool pip_ = true;

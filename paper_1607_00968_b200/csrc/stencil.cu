@@ -14,6 +14,7 @@
 
 #include "kernels.hpp"
 #include "profile.hpp"
+#include "block_k8.cuh"
 
 namespace hz {
 
@@ -175,6 +176,97 @@ apply_lo_kernel(LevelOp<double> op, const float2* __restrict__ x, double2* __res
   Elem<double> el;
   if (!decode(op.g, e, el)) return;
   out[e] = fine_ax<double, NDIM, false, float2>(op, x, e, el);
+}
+
+// W = A Z (complex128 fine operator, Z complex64 widened on load, K = 8)
+// fused with the Gram [X_0..X_{NB-2}, W]^H W of the Arnoldi step: the
+// register-direct k8::gram8_kernel with its Y = X_{NB-1} operand computed in
+// the kernel (apply_lo_kernel's expression on the same values) and stored as
+// W, so W is written once and never re-read for the Gram. Rows go to warps
+// and slots exactly as in gram8_kernel: the partials are bitwise those of
+// apply_lo + gram8.
+template <int NB, int NDIM>
+__global__ void __launch_bounds__(k8::kThreads, k8::Gram8Cfg<NB>::MINB)
+gram8_apply_kernel(LevelOp<double> op, const float2* __restrict__ Z, double2* __restrict__ W,
+                   const BlockTab<double> X, double2* __restrict__ partials) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int slot = blockIdx.x, nslots = gridDim.x;
+  const int64_t n = op.g.nodes;
+  const int64_t groups = (n + k8::kRowsPerStep - 1) / k8::kRowsPerStep;
+  const int64_t per = (groups + nslots - 1) / nslots;
+  const int64_t g0 = int64_t(slot) * per;
+  const int64_t g1 = (g0 + per) < groups ? (g0 + per) : groups;
+  double acc[NB][3][2];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int m = 0; m < 3; ++m) acc[i][m][0] = acc[i][m][1] = 0.0;
+  constexpr int kUnroll = k8::Gram8Cfg<NB>::U;
+  for (int64_t rg = g0 + warp; rg < g1; rg += 8 * kUnroll) {
+    double2 y[kUnroll], x[kUnroll][NB];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t row = (rg + 8 * u) * k8::kRowsPerStep + t;
+      const bool ok = rg + 8 * u < g1 && row < n;
+      const uint32_t e = uint32_t(row * 8 + g);
+      y[u] = czero<double2>();
+      if (ok) {
+        Elem<double> el;
+        el.node = uint32_t(row);
+        el.col = uint32_t(g);
+        op.g.unpack(el.node, el.i, el.j, el.kz);
+        y[u] = fine_ax<double, NDIM, false, float2>(op, Z, e, el);
+        W[e] = y[u];
+      }
+#pragma unroll
+      for (int i = 0; i < NB - 1; ++i) x[u][i] = ok ? __ldg(X.p[i] + e) : czero<double2>();
+      x[u][NB - 1] = y[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const double b0 = y[u].x, b1 = y[u].y, b2 = y[u].x - y[u].y;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        dmma::mma884(acc[i][0][0], acc[i][0][1], x[u][i].x, b0);
+        dmma::mma884(acc[i][1][0], acc[i][1][1], x[u][i].y, b1);
+        dmma::mma884(acc[i][2][0], acc[i][2][1], x[u][i].x + x[u][i].y, b2);
+      }
+    }
+  }
+  __shared__ double2 red[NB * 64];
+  for (int w = 0; w < 8; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double2 v;
+          v.x = acc[i][0][h] + acc[i][1][h];
+          v.y = acc[i][0][h] - acc[i][1][h] - acc[i][2][h];
+          const int e = i * 64 + g * 8 + 2 * t + h;
+          red[e] = w == 0 ? v : cadd(red[e], v);
+        }
+    }
+    __syncthreads();
+  }
+  double2* out = partials + int64_t(slot) * NB * 64;
+  for (int e = threadIdx.x; e < NB * 64; e += k8::kThreads) out[e] = red[e];
+}
+
+template <int NB>
+void gram8_apply_dispatch(int nb, const LevelOp<double>& op, const float2* Z, double2* W, const BlockTab<double>& X,
+                          double2* partials, int nslots, cudaStream_t s) {
+  if constexpr (NB <= 12) {
+    if (nb == NB) {
+      if (op.ndim == 3)
+        gram8_apply_kernel<NB, 3><<<nslots, k8::kThreads, 0, s>>>(op, Z, W, X, partials);
+      else
+        gram8_apply_kernel<NB, 2><<<nslots, k8::kThreads, 0, s>>>(op, Z, W, X, partials);
+      return;
+    }
+    gram8_apply_dispatch<NB + 1>(nb, op, Z, W, X, partials, nslots, s);
+  }
 }
 
 // Galerkin 9/27-point level kernel, CPT consecutive columns per thread: the
@@ -849,6 +941,19 @@ void launch_apply_lo(const LevelOp<double>& op, const float2* u, double2* out, c
   else
     apply_lo_kernel<2><<<grid, kBlock, 0, s>>>(op, u, out);
   HZ_LAUNCH_CHECK();
+}
+
+int launch_gram8_apply(const LevelOp<double>& op, int nb, const BlockTab<double>& X, const float2* Z, double2* W,
+                       double2* partials, int max_slots, cudaStream_t s) {
+  if (op.kind != kFine || op.g.k != 8 || nb < 1 || nb > 12 || op.g.z0 != 0 || op.g.z1 != (op.ndim == 3 ? op.g.n2 : op.g.n1))
+    throw HzError(kState, "gram8_apply: 8-column whole-grid fine operator, nb in [1, 12]");
+  const double n = double(op.g.nodes);
+  ProfScope prof("apply_gram_c128", n * 8.0 * (8.0 + 16.0 + 16.0 * (nb - 1)) + n * 16.0, s, 8.0 * n * 64.0 * nb);
+  const int64_t want = std::min<int64_t>(2 * kNumSMs, (int64_t(op.g.nodes) + 31) / 32);
+  const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(want, max_slots)));
+  gram8_apply_dispatch<1>(nb, op, Z, W, X, partials, nslots, s);
+  HZ_LAUNCH_CHECK();
+  return nslots;
 }
 
 template <class T>

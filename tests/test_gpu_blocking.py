@@ -152,3 +152,40 @@ def test_complex64_z_blocks_match_complex128_z_blocks(k):
         assert np.array_equal(outs[0], outs[1])
     else:
         assert rel_err(outs[0], outs[1]) <= 1e-8
+
+
+GA_SOLVE = (
+    "import sys; sys.path.insert(0, '.'); import numpy as np\n"
+    "import paper_1607_00968_b200 as hz; from paper_1607_00968_b200 import configs\n"
+    "if sys.argv[2] == '2d':\n"
+    "    cfg = configs.config2(nlevels=4, k=16, nx=257, nz=129); cfg.shift, cfg.jacobi_weight = 0.9, 0.6\n"
+    "else:\n"
+    "    cfg = configs.config3(nlevels=3, n=(33, 33, 17), sgrid=4)\n"
+    "cfg.restart, cfg.precond_precision, cfg.max_cycles, cfg.krylov_block = 5, 'c64', 80, 8\n"
+    "S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))\n"
+    "X, rep = S.solve_block(cfg.rhs_block())\n"
+    "assert np.all(np.isfinite(X)) and rep.cycles > 0\n"
+    "np.save(sys.argv[1], X)\n")
+
+
+@pytest.mark.parametrize("dim", ["2d", "3d"])
+def test_fused_apply_gram_matches_unfused(dim):
+    """W = A Z fused with the Arnoldi Gram (gram8_apply_kernel, HZ_GRAM_APPLY=1,
+    off by default, for 8-column blocks with c64 Z): the same W and the same
+    partial Grams as apply_lo + gram8, so the blocked solves (2 groups of 8)
+    are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    with tempfile.TemporaryDirectory() as d:
+        for flag in ("1", "0"):
+            path = os.path.join(d, f"x{flag}.npy")
+            r = subprocess.run([sys.executable, "-c", GA_SOLVE, path, dim], cwd=root,
+                               env=dict(os.environ, HZ_GRAM_APPLY=flag), capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
