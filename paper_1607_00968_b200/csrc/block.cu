@@ -676,6 +676,32 @@ update_lo_kernel(int64_t n, int k, int nb, const BlockTab<float> Z, const double
   Y[e] = acc;
 }
 
+template <int NB>
+void gram16_dispatch(int nb, int64_t n, const BlockTab<double>& X, const double2* Y, double2* partials, int nslots,
+                     cudaStream_t s) {
+  if constexpr (NB <= kK8MaxNb) {
+    if (nb == NB) {
+      k16::gram16_kernel<NB><<<nslots, k8::kThreads, 0, s>>>(n, X, Y, partials);
+      return;
+    }
+    gram16_dispatch<NB + 1>(nb, n, X, Y, partials, nslots, s);
+  }
+}
+
+template <int NB, class TT>
+void update16_dispatch(int nb, int64_t n, const BlockTab<TT>& X, const double2* H, const double2* Yin,
+                       double2* Yout, double sign, cudaStream_t s) {
+  if constexpr (NB <= kK8MaxNb) {
+    if (nb == NB) {
+      const int64_t tiles = (n + 7) / 8;
+      const int grid = int(std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, (tiles + 7) / 8)));
+      k16::update16_kernel<NB, TT><<<grid, k8::kThreads, 0, s>>>(n, X, H, Yin, Yout, sign);
+      return;
+    }
+    update16_dispatch<NB + 1, TT>(nb, n, X, H, Yin, Yout, sign, s);
+  }
+}
+
 bool use_k8() {
   static const bool on = [] {
     const char* e = std::getenv("HZ_K8");
@@ -695,11 +721,14 @@ int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx
   // exactly one wave of resident CTAs (3 per SM for the tiled / DMMA Grams)
   // over the nb blocks: a partial last wave would idle up to 2/3 of the GPU
   if constexpr (std::is_same<T, double>::value) {
-    if (k == 8 && nb >= 1 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
+    if ((k == 8 || k == 16) && nb >= 1 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
       // one pass over all nb blocks per CTA: one wave of 2 CTAs per SM
       int64_t want = std::min<int64_t>(2 * kNumSMs, (n + 31) / 32);
       const int nslots = int(std::max<int64_t>(1, std::min<int64_t>(want, max_slots)));
-      gram8_dispatch<1>(nb, n, X, Y, partials, nslots, s);
+      if (k == 8)
+        gram8_dispatch<1>(nb, n, X, Y, partials, nslots, s);
+      else
+        gram16_dispatch<1>(nb, n, X, Y, partials, nslots, s);
       HZ_LAUNCH_CHECK();
       return nslots;
     }
@@ -733,7 +762,14 @@ void launch_multi_update(int64_t n, int k, int nb, const BlockTab<T>& X, const c
   if (k == 32) {
     update_tiled_launch<T, 32>(n, nb, X, H, Yin, Yout, sign, s);
   } else if (k == 16) {
-    update_tiled_launch<T, 16>(n, nb, X, H, Yin, Yout, sign, s);
+    bool done = false;
+    if constexpr (std::is_same<T, double>::value) {
+      if (nb >= 1 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
+        update16_dispatch<1, double>(nb, n, X, H, Yin, Yout, sign, s);
+        done = true;
+      }
+    }
+    if (!done) update_tiled_launch<T, 16>(n, nb, X, H, Yin, Yout, sign, s);
   } else if (k == 64) {
     update_tiled_launch<T, 64>(n, nb, X, H, Yin, Yout, sign, s);
   } else if (k == 8) {
@@ -761,6 +797,8 @@ void launch_update_lo(int64_t n, int k, int nb, const BlockTab<float>& Z, const 
   if (nb < 1) return;
   if (k == 8 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
     update8_dispatch<1, float>(nb, n, Z, H, Y, Y, 1.0, s);
+  } else if (k == 16 && nb <= kK8MaxNb && use_dmma() && use_k8()) {
+    update16_dispatch<1, float>(nb, n, Z, H, Y, Y, 1.0, s);
   } else {
     const size_t smem = sizeof(double2) * size_t(nb) * k * k;
     allow_dyn_smem(reinterpret_cast<const void*>(update_lo_kernel), int(smem));

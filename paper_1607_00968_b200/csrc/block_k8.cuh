@@ -154,3 +154,130 @@ update8_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, c
 
 }  // namespace k8
 }  // namespace hz
+
+namespace hz {
+namespace k16 {
+
+// K = 16 register-direct forms. Gram: warp w takes p-half a = w & 1 of every
+// 4-row group it visits (row groups go to the 4 warps of its half round
+// robin); lane (g, t) loads X[r][8a + g] (one 16-byte load per block) and
+// Y[r][8b + g] for both q-halves b, and accumulates the 8 x 8 tiles (a, b).
+template <int NB>
+struct Gram16Cfg {  // 24 NB accumulator registers per lane
+  static constexpr int MINB = NB <= 3 ? 2 : 1;
+};
+
+template <int NB>
+__global__ void __launch_bounds__(k8::kThreads, Gram16Cfg<NB>::MINB)
+gram16_kernel(int64_t n, const BlockTab<double> X, const double2* __restrict__ Y, double2* __restrict__ partials) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int a = warp & 1, wr = warp >> 1;  // p-half, row stream (4 per half)
+  const int slot = blockIdx.x, nslots = gridDim.x;
+  const int64_t groups = (n + 3) / 4;
+  const int64_t per = (groups + nslots - 1) / nslots;
+  const int64_t g0 = int64_t(slot) * per;
+  const int64_t g1 = (g0 + per) < groups ? (g0 + per) : groups;
+  double acc[NB][2][3][2];
+#pragma unroll
+  for (int i = 0; i < NB; ++i)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) acc[i][b][m][0] = acc[i][b][m][1] = 0.0;
+  for (int64_t rg = g0 + wr; rg < g1; rg += 4) {
+    const int64_t row = rg * 4 + t;
+    const bool ok = row < n;
+    const int64_t e = row * 16 + g;
+    double2 y[2], x[NB];
+#pragma unroll
+    for (int b = 0; b < 2; ++b) y[b] = ok ? __ldg(Y + e + 8 * b) : czero<double2>();
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = ok ? __ldg(X.p[i] + e + 8 * a) : czero<double2>();
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const double b0 = y[b].x, b1 = y[b].y, b2 = y[b].x - y[b].y;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        dmma::mma884(acc[i][b][0][0], acc[i][b][0][1], x[i].x, b0);
+        dmma::mma884(acc[i][b][1][0], acc[i][b][1][1], x[i].y, b1);
+        dmma::mma884(acc[i][b][2][0], acc[i][b][2][1], x[i].x + x[i].y, b2);
+      }
+    }
+  }
+  // fixed-order reduction over the 4 row streams of each half
+  __shared__ double2 red[NB * 256];
+  for (int w = 0; w < 4; ++w) {
+    if (wr == w) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double2 v;
+            v.x = acc[i][b][0][h] + acc[i][b][1][h];
+            v.y = acc[i][b][0][h] - acc[i][b][1][h] - acc[i][b][2][h];
+            const int e = i * 256 + (8 * a + g) * 16 + 8 * b + 2 * t + h;
+            red[e] = w == 0 ? v : cadd(red[e], v);
+          }
+    }
+    __syncthreads();
+  }
+  double2* out = partials + int64_t(slot) * NB * 256;
+  for (int e = threadIdx.x; e < NB * 256; e += k8::kThreads) out[e] = red[e];
+}
+
+// Yout = Yin + sign * sum_i X_i H_i, 16 columns; warps take 8-row tiles; per
+// block 4 k-steps (q0 = 4 s, A = X[r0+g][q0+t]) x 2 output halves.
+template <int NB, class TT = double>
+__global__ void __launch_bounds__(k8::kThreads, 2)
+update16_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, const double2* Yin, double2* Yout,
+                double sign) {
+  __shared__ double2 hs[NB * 256];
+  for (int e = threadIdx.x; e < NB * 256; e += k8::kThreads) hs[e] = H[e];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int64_t tiles = (n + 7) / 8;
+  for (int64_t tile = int64_t(blockIdx.x) * 8 + warp; tile < tiles; tile += int64_t(gridDim.x) * 8) {
+    const int64_t row = tile * 8 + g;
+    const bool ok = row < n;
+    double acc[2][3][2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) acc[b][m][0] = acc[b][m][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      double2 xa[4];
+#pragma unroll
+      for (int st = 0; st < 4; ++st) xa[st] = ok ? k8::ld_widen(X.p[i] + row * 16 + 4 * st + t) : czero<double2>();
+#pragma unroll
+      for (int st = 0; st < 4; ++st)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const double2 h = hs[i * 256 + (4 * st + t) * 16 + 8 * b + g];
+          dmma::mma884(acc[b][0][0], acc[b][0][1], xa[st].x, h.x);
+          dmma::mma884(acc[b][1][0], acc[b][1][1], xa[st].y, h.y);
+          dmma::mma884(acc[b][2][0], acc[b][2][1], xa[st].x + xa[st].y, h.x + h.y);
+        }
+    }
+    if (ok) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int64_t base = row * 16 + 8 * b + 2 * t;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double2 y = Yin ? Yin[base + h] : czero<double2>();
+          y.x += sign * (acc[b][0][h] - acc[b][1][h]);
+          y.y += sign * (acc[b][2][h] - acc[b][0][h] - acc[b][1][h]);
+          Yout[base + h] = y;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace k16
+}  // namespace hz

@@ -100,7 +100,9 @@ def test_blocked_solve_3d_one_column_groups():
 # ---- the Arnoldi block algebra on its own (K = 8 register-direct DMMA
 # kernels, block_k8.cuh; other widths through the staged kernels)
 @pytest.mark.parametrize("n,k,nb", [(525825, 8, 1), (525825, 8, 2), (100003, 8, 6), (4097, 8, 12),
-                                    (13, 8, 3), (70001, 8, 13), (9001, 16, 3), (5003, 4, 2)])
+                                    (13, 8, 3), (70001, 8, 13), (9001, 16, 3), (5003, 4, 2),
+                                    (262913, 16, 1), (100003, 16, 6), (4099, 16, 12), (11, 16, 2),
+                                    (20001, 16, 14), (3001, 32, 3)])
 def test_block_gram_and_update_match_numpy(n, k, nb):
     rng = np.random.default_rng(n + k + nb)
     Xh = [rng.standard_normal((n, k)) + 1j * rng.standard_normal((n, k)) for _ in range(nb)]
@@ -128,11 +130,11 @@ ZLO_SOLVE = (
     "np.save(sys.argv[1], X)\n")
 
 
-@pytest.mark.parametrize("k", [8, 4])
+@pytest.mark.parametrize("k", [8, 16, 4])
 def test_complex64_z_blocks_match_complex128_z_blocks(k):
     """FGMRES keeps the preconditioned blocks Z_j of a complex64 cycle in
     complex64 (HZ_ZLO, default on): the values are the c128 ones before their
-    exact widening, so the K = 8 path (same DMMA update kernel) is bitwise
+    exact widening, so the K = 8 / 16 paths (same DMMA update kernels) are bitwise
     equal to the c128-Z run; other widths differ by the restart update's
     rounding only."""
     import os
@@ -148,7 +150,7 @@ def test_complex64_z_blocks_match_complex128_z_blocks(k):
                                env=dict(os.environ, HZ_ZLO=flag), capture_output=True, text=True, timeout=600)
             assert r.returncode == 0, r.stderr[-2000:]
             outs.append(np.load(path))
-    if k == 8:
+    if k in (8, 16):
         assert np.array_equal(outs[0], outs[1])
     else:
         assert rel_err(outs[0], outs[1]) <= 1e-8
