@@ -18,6 +18,7 @@ def make(c):
         cfg = bench.build_workload(0, 1, 32)
     elif c == 3:
         cfg = configs.config3(nlevels=3)                   # coarsest 33x33x17: plane block-tridiagonal
+        cfg.precond_precision, cfg.krylov_block, cfg.restart = "c64", 8, 5  # 2 concurrent 8-column blocks
     elif c == 4:
         cfg = configs.config4(nlevels=3)                   # coarsest 65x65x33
         cfg.source_nodes = cfg.source_nodes[:8]            # k = 8 per GPU (64 RHS sharded 8 per GPU)
@@ -25,7 +26,7 @@ def make(c):
     elif c == 5:
         cfg = configs.config5(nlevels=4)                   # coarsest 65x65x33
         cfg.shift, cfg.restart = 1.5, 5
-    for key in ("nlevels", "shift", "restart", "max_cycles"):
+    for key in ("nlevels", "shift", "restart", "max_cycles", "precond_precision", "krylov_block", "jacobi_weight"):
         v = os.environ.get(f"HZ_CFG{c}_{key.upper()}")
         if v is not None:
             setattr(cfg, key, type(getattr(cfg, key))(v))
@@ -54,7 +55,8 @@ if __name__ == "__main__":
             X, rep = S.solve_block(B)
             torch.cuda.synchronize(); dt = time.time() - t
             out = dict(config=c, name=cfg.name, n=cfg.n, k=cfg.k, nlevels=cfg.nlevels, shift=cfg.shift,
-                       restart=cfg.restart, prec=cfg.precond_precision, slabs=slabs, setup_s=round(setup, 2),
+                       restart=cfg.restart, prec=cfg.precond_precision, rhs_block=cfg.krylov_block, slabs=slabs,
+                       setup_s=round(setup, 2),
                        solve_s=round(dt, 3), cycles=rep.cycles, converged=rep.all_converged(),
                        worst_res=float(rep.rel_residual.max()), rhs_per_s=round(cfg.k / dt, 3),
                        ms_per_cycle=round(1e3 * dt / max(rep.cycles, 1), 3))
