@@ -487,10 +487,14 @@ void run_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_
   kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, x2, ec, b, out, frows);
 }
 
-// strip width: HZ_FUSED_NT = 64 or 128 fine nodes (default 64: more resident CTAs)
-int fused_nt() {
-  static const int nt = env_int("HZ_FUSED_NT", 64) == 128 ? 128 : 64;
-  return nt;
+// strip width in fine nodes: HZ_FUSED_NT = 32, 64 or 128; default 64, and
+// 32 when a CTA's 4 columns cover the block in <= 2 CTAs (k <= 8): the
+// strips stream their rows sequentially, so narrow blocks need the extra
+// (narrower) strips to keep enough row chains in flight
+int fused_nt(int k, int cols_per_cta) {
+  static const int env = env_int("HZ_FUSED_NT", 0);
+  if (env == 32 || env == 64 || env == 128) return env;
+  return k / cols_per_cta <= 2 ? 32 : 64;
 }
 
 }  // namespace
@@ -513,7 +517,10 @@ void launch_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In*
   const double n = double(op.g.nodes), nc = double(gc.nodes), k = op.g.k, s_ = sizeof(cplx_t<T>);
   ProfScope prof(sizeof(T) == 8 ? "fused_pre_fine_c128" : "fused_pre_fine_c64",
                  n * (k * (sizeof(In) + s_) + 2.0 * s_) + nc * k * s_, s);
-  if (fused_nt() == 64)
+  const int nt = fused_nt(int(op.g.k), kTPN * cpt<T>());
+  if (nt == 32)
+    run_fused_pre<T, In, 32>(op, gc, wj, b, x2, rc, crows, s);
+  else if (nt == 64)
     run_fused_pre<T, In, 64>(op, gc, wj, b, x2, rc, crows, s);
   else
     run_fused_pre<T, In, 128>(op, gc, wj, b, x2, rc, crows, s);
@@ -527,7 +534,10 @@ void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cp
   const double n = double(op.g.nodes), nc = double(gc.nodes), k = op.g.k, s_ = sizeof(cplx_t<T>);
   ProfScope prof(sizeof(T) == 8 ? "fused_post_fine_c128" : "fused_post_fine_c64",
                  n * (k * (s_ + sizeof(In) + sizeof(Out)) + 2.0 * s_) + nc * k * s_, s);
-  if (fused_nt() == 64)
+  const int nt = fused_nt(int(op.g.k), kTPN * cpt<T>());
+  if (nt == 32)
+    run_fused_post<T, In, Out, 32>(op, gc, wj, x2, ec, b, out, frows, s);
+  else if (nt == 64)
     run_fused_post<T, In, Out, 64>(op, gc, wj, x2, ec, b, out, frows, s);
   else
     run_fused_post<T, In, Out, 128>(op, gc, wj, x2, ec, b, out, frows, s);
