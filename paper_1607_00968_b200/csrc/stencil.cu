@@ -346,20 +346,41 @@ __device__ __forceinline__ void st4(double2* p, const double2 (&v)[4]) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) p[c] = v[c];
 }
+// CG = true: coherent (L1-bypassing) loads, for data written earlier in the
+// same (persistent) kernel -- the read-only path may hold stale lines
+template <bool CG>
+__device__ __forceinline__ void ld4v(const float2* __restrict__ p, float2 (&v)[4]) {
+  if constexpr (CG) {
+    const float4 a = __ldcg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldcg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = make_float2(a.x, a.y);
+    v[1] = make_float2(a.z, a.w);
+    v[2] = make_float2(b.x, b.y);
+    v[3] = make_float2(b.z, b.w);
+  } else {
+    ld4(p, v);
+  }
+}
+template <bool CG>
+__device__ __forceinline__ void ld4v(const double2* __restrict__ p, double2 (&v)[4]) {
+  if constexpr (CG) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = __ldcg(p + c);
+  } else {
+    ld4(p, v);
+  }
+}
 
 // Galerkin level kernel, 4 columns per thread, with every load of a group of
 // G neighbours (G = 9: a whole plane; G = 3: one row) issued before its FMAs
 // and 16-byte vector loads: the one-load-then-FMA form leaves the kernel
 // latency bound (~1.7 TB/s at level 1 of config 2). Same
 // accumulation order as stencil_mc_kernel, so the results are bitwise equal.
-template <class T, int NDIM, int MODE, int G>
-__global__ void __launch_bounds__(kBlock)
-stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
-                  cplx_t<T>* __restrict__ out, T wj) {
+template <class T, int NDIM, int MODE, int G, bool CG = false>
+__device__ __forceinline__ void stencil_v4_item(const LevelOp<T>& op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b, cplx_t<T>* __restrict__ out, T wj, uint32_t t) {
   using V = cplx_t<T>;
   constexpr int CPT = 4;
   const LevelGeom& g = op.g;
-  const uint32_t t = blockIdx.x * kBlock + threadIdx.x;
   const uint32_t e0 = g.e_begin() + t * CPT;
   if (e0 >= g.e_end()) return;
   uint32_t node, col, i, j, kz;
@@ -383,7 +404,7 @@ stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
       const bool okx = dx < 0 ? i > 0 : (dx > 0 ? i + 1 < g.n0 : true);
       const int64_t off = (okz && oky && okx) ? dz * sz + dy * sy + dx * sx : 0;
       av[q] = __ldg(&cf[int64_t(s) * g.nodes]);
-      ld4(x + int64_t(e0) + off, xv[q]);
+      ld4v<CG>(x + int64_t(e0) + off, xv[q]);
     }
 #pragma unroll
     for (int q = 0; q < G; ++q)
@@ -396,19 +417,26 @@ stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
     for (int c = 0; c < CPT; ++c) o[c] = acc[c];
   } else if (MODE == 1) {
     V bv[CPT];
-    ld4(b + e0, bv);
+    ld4v<CG>(b + e0, bv);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) o[c] = csub(bv[c], acc[c]);
   } else {
     V bv[CPT], xc[CPT];
-    ld4(b + e0, bv);
-    ld4(x + e0, xc);
+    ld4v<CG>(b + e0, bv);
+    ld4v<CG>(x + e0, xc);
     const V d = __ldg(&op.inv_diag[node]);
     const V wd = mk(wj * d.x, wj * d.y);
 #pragma unroll
     for (int c = 0; c < CPT; ++c) o[c] = cadd(xc[c], cmul(wd, csub(bv[c], acc[c])));
   }
   st4(out + e0, o);
+}
+
+template <class T, int NDIM, int MODE, int G>
+__global__ void __launch_bounds__(kBlock)
+stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
+                  cplx_t<T>* __restrict__ out, T wj) {
+  stencil_v4_item<T, NDIM, MODE, G>(op, x, b, out, wj, blockIdx.x * kBlock + threadIdx.x);
 }
 
 // Fine 5/7-point level kernel, 4 columns per thread with 16-byte loads (all
@@ -615,11 +643,10 @@ prolong_correct_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__
 // ---- 4-columns-per-thread forms of the transfers and the zero-start sweep
 // (16-byte loads, complex64 with k % 4 == 0); per-column arithmetic and
 // order exactly as the one-column kernels above.
-template <class T, int NDIM>
-__global__ void __launch_bounds__(kBlock)
-restrict_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r, cplx_t<T>* __restrict__ bc) {
+template <class T, int NDIM, bool CG = false>
+__device__ __forceinline__ void restrict_v4_item(const LevelGeom& gf, const LevelGeom& gc, const cplx_t<T>* __restrict__ r, cplx_t<T>* __restrict__ bc, uint32_t t) {
   using V = cplx_t<T>;
-  const uint32_t e0 = gc.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  const uint32_t e0 = gc.e_begin() + t * 4;
   if (e0 >= gc.e_end()) return;
   uint32_t node, col, I, J, K;
   gc.div_k.divmod(e0, node, col);
@@ -636,7 +663,7 @@ restrict_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r, 
     const bool ok = fz >= 0 && fz < gf.n2 && fy >= 0 && fy < gf.n1 && fx >= 0 && fx < gf.n0;
     wv[s] = ok ? (ex == 0 ? T(1) : T(0.5)) * (ey == 0 ? T(1) : T(0.5)) * (ez == 0 ? T(1) : T(0.5)) : T(0);
     const int64_t off = (int64_t(ex) + int64_t(gf.n0) * (ey + int64_t(gf.n1) * ez)) * k;
-    ld4(r + (ok ? fc + off : fc), rv[s]);
+    ld4v<CG>(r + (ok ? fc + off : fc), rv[s]);
   }
   V o[4];
 #pragma unroll
@@ -652,9 +679,14 @@ restrict_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r, 
 
 template <class T, int NDIM>
 __global__ void __launch_bounds__(kBlock)
-prolong_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec, cplx_t<T>* __restrict__ x) {
+restrict_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ r, cplx_t<T>* __restrict__ bc) {
+  restrict_v4_item<T, NDIM>(gf, gc, r, bc, blockIdx.x * kBlock + threadIdx.x);
+}
+
+template <class T, int NDIM, bool CG = false>
+__device__ __forceinline__ void prolong_v4_item(const LevelGeom& gf, const LevelGeom& gc, const cplx_t<T>* __restrict__ ec, cplx_t<T>* __restrict__ x, uint32_t t) {
   using V = cplx_t<T>;
-  const uint32_t e0 = gf.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  const uint32_t e0 = gf.e_begin() + t * 4;
   if (e0 >= gf.e_end()) return;
   uint32_t node, col, i, j, kz;
   gf.div_k.divmod(e0, node, col);
@@ -675,11 +707,11 @@ prolong_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec, 
 #pragma unroll
       for (int a = 0; a < 2; ++a) {
         const int64_t C = (a ? cx1 : cx0) + int64_t(gc.n0) * ((b ? cy1 : cy0) + int64_t(gc.n1) * (c ? cz1 : cz0));
-        ld4(ec + C * k + col, ev[c][b][a]);
+        ld4v<CG>(ec + C * k + col, ev[c][b][a]);
         wv[c][b][a] = (a ? wx1 : wx0) * (b ? wy1 : wy0) * (c ? wz1 : wz0);
       }
   V xe[4], o[4];
-  ld4(x + e0, xe);
+  ld4v<CG>(x + e0, xe);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     V corr = czero<V>();
@@ -695,21 +727,32 @@ prolong_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec, 
   st4(x + e0, o);
 }
 
-template <class T>
+template <class T, int NDIM>
 __global__ void __launch_bounds__(kBlock)
-jacobi_zero_v4_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj, const cplx_t<T>* __restrict__ b,
-                      cplx_t<T>* __restrict__ out) {
+prolong_v4_kernel(LevelGeom gf, LevelGeom gc, const cplx_t<T>* __restrict__ ec, cplx_t<T>* __restrict__ x) {
+  prolong_v4_item<T, NDIM>(gf, gc, ec, x, blockIdx.x * kBlock + threadIdx.x);
+}
+
+template <class T, bool CG = false>
+__device__ __forceinline__ void jacobi_zero_v4_item(const LevelGeom& g, const cplx_t<T>* __restrict__ inv_diag, T wj, const cplx_t<T>* __restrict__ b, cplx_t<T>* __restrict__ out, uint32_t t) {
   using V = cplx_t<T>;
-  const uint32_t e0 = g.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 4;
+  const uint32_t e0 = g.e_begin() + t * 4;
   if (e0 >= g.e_end()) return;
   const uint32_t node = g.div_k.div(e0);
   const V d = __ldg(&inv_diag[node]);
   const V wd = mk(wj * d.x, wj * d.y);
   V bv[4], o[4];
-  ld4(b + e0, bv);
+  ld4v<CG>(b + e0, bv);
 #pragma unroll
   for (int q = 0; q < 4; ++q) o[q] = cmul(wd, bv[q]);
   st4(out + e0, o);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock)
+jacobi_zero_v4_kernel(LevelGeom g, const cplx_t<T>* __restrict__ inv_diag, T wj, const cplx_t<T>* __restrict__ b,
+                      cplx_t<T>* __restrict__ out) {
+  jacobi_zero_v4_item<T>(g, inv_diag, wj, b, out, blockIdx.x * kBlock + threadIdx.x);
 }
 
 // ---------------------------------------------------------------- Galerkin

@@ -101,3 +101,4 @@ def test_fused_solve_bitwise_equals_unfused():
         a = _run(SOLVE, os.path.join(d, "a.npy"), "1")
         b = _run(SOLVE, os.path.join(d, "b.npy"), "0")
     assert np.array_equal(a, b)
+
