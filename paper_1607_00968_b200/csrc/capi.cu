@@ -24,7 +24,14 @@
 namespace hz {
 
 static std::atomic<int64_t> g_launches{0};
-void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+// kernels enqueued while this thread captures a CUDA graph run only when the
+// graph is launched: counted then (add_launches), not at capture
+thread_local bool g_capturing = false;
+void count_launch() {
+  if (!g_capturing) g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void set_capturing(bool on) { g_capturing = on; }
 
 // ---- per-kernel event profiler (profile.hpp)
 namespace {
@@ -263,10 +270,10 @@ DevOp<double> make_op_with(hz_solver* s, Hierarchy<double>* h64, Hierarchy<float
   const CycleSpec* spec = &s->spec;
   if (s->opts.precond_precision == HZ_C64) {
     op.prec = [spec, h32](const double2* in, double2* out, int kk, cudaStream_t st) {
-      h32->cycle_cast(*spec, kk, in, out, st);
+      h32->cycle_cast_graph(*spec, kk, in, out, st);
     };
     op.prec_lo = [spec, h32](const double2* in, float2* out, int kk, cudaStream_t st) {
-      h32->cycle_cast(*spec, kk, in, out, st);
+      h32->cycle_cast_graph(*spec, kk, in, out, st);
     };
     op.apply_lo = [P](const float2* in, double2* out, int kk, cudaStream_t st) {
       launch_apply_lo(P->fine_op(kk), in, out, st);

@@ -44,19 +44,25 @@ constexpr int cpt() {
   return sizeof(T) == 4 ? 2 : 1;
 }
 
-template <class T>
+// QU complex values per thread unit (cpt<T>() = one 16-byte vector; 4 for
+// complex64 = two vectors, for narrow blocks: twice the columns per thread
+// amortise the per-row index math, barriers and per-node coefficients)
+template <class T, int QU = cpt<T>()>
 struct Unit {
-  cplx_t<T> v[cpt<T>()];
+  cplx_t<T> v[QU];
 };
 
 // one unit of consecutive columns from global memory (read-only path); In
 // may be wider than T (complex128 right-hand side of the c64 cycle)
 template <class V, int N>
 __device__ __forceinline__ void gload(const V* __restrict__ p, V (&v)[N]) {
-  if constexpr (sizeof(V) == 8 && N == 2) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = make_float2(a.x, a.y);
-    v[1] = make_float2(a.z, a.w);
+  if constexpr (sizeof(V) == 8 && N % 2 == 0) {
+#pragma unroll
+    for (int h = 0; h < N / 2; ++h) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(p) + h);
+      v[2 * h] = make_float2(a.x, a.y);
+      v[2 * h + 1] = make_float2(a.z, a.w);
+    }
   } else {
 #pragma unroll
     for (int c = 0; c < N; ++c) v[c] = __ldg(p + c);
@@ -64,8 +70,10 @@ __device__ __forceinline__ void gload(const V* __restrict__ p, V (&v)[N]) {
 }
 template <class V, int N>
 __device__ __forceinline__ void gstore(V* p, const V (&v)[N]) {
-  if constexpr (sizeof(V) == 8 && N == 2) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
+  if constexpr (sizeof(V) == 8 && N % 2 == 0) {
+#pragma unroll
+    for (int h = 0; h < N / 2; ++h)
+      reinterpret_cast<float4*>(p)[h] = make_float4(v[2 * h].x, v[2 * h].y, v[2 * h + 1].x, v[2 * h + 1].y);
   } else {
 #pragma unroll
     for (int c = 0; c < N; ++c) p[c] = v[c];
@@ -90,15 +98,15 @@ __device__ __forceinline__ V ax_csr(const V& c, T wx, T wy, bool xm, bool xp, bo
 // One stencil row from a ring (rows rm, r0, rp; [thread] units) at thread
 // index t (TPN threads per node): MODE 1: o = b - A u; MODE 2:
 // o = u + d (b - A u)  (d = wD^{-1}).
-template <int TPN, int MODE, class T>
-__device__ __forceinline__ void ring_stencil(const Unit<T>* rm, const Unit<T>* r0, const Unit<T>* rp, int t,
-                                             const cplx_t<T>& c, const cplx_t<T>& d, T wx, T wy, bool xm, bool xp,
-                                             bool ym, bool yp, const Unit<T>& b, Unit<T>& o) {
-  const Unit<T> u0 = r0[t];
-  const Unit<T> uxm = xm ? r0[t - TPN] : u0, uxp = xp ? r0[t + TPN] : u0;
-  const Unit<T> um = ym ? rm[t] : u0, up = yp ? rp[t] : u0;
+template <int TPN, int MODE, class T, int QU>
+__device__ __forceinline__ void ring_stencil(const Unit<T, QU>* rm, const Unit<T, QU>* r0, const Unit<T, QU>* rp,
+                                             int t, const cplx_t<T>& c, const cplx_t<T>& d, T wx, T wy, bool xm,
+                                             bool xp, bool ym, bool yp, const Unit<T, QU>& b, Unit<T, QU>& o) {
+  const Unit<T, QU> u0 = r0[t];
+  const Unit<T, QU> uxm = xm ? r0[t - TPN] : u0, uxp = xp ? r0[t + TPN] : u0;
+  const Unit<T, QU> um = ym ? rm[t] : u0, up = yp ? rp[t] : u0;
 #pragma unroll
-  for (int q = 0; q < cpt<T>(); ++q) {
+  for (int q = 0; q < QU; ++q) {
     const auto a = ax_csr(c, wx, wy, xm, xp, ym, yp, um.v[q], uxm.v[q], u0.v[q], uxp.v[q], up.v[q]);
     o.v[q] = MODE == 1 ? csub(b.v[q], a) : cadd(u0.v[q], cmul(d, csub(b.v[q], a)));
   }
@@ -130,36 +138,37 @@ __device__ __forceinline__ void cpa_wait() {
 // its 16-byte units of each streamed input plus the node's centre and
 // wD^{-1} (each thread stages its own copies, so a row is usable after the
 // thread's own cp.async.wait -- no barrier).
-template <class T, class In, int TPN, int NT, int PD>
+template <class T, class In, int TPN, int NT, int PD, int QU>
 struct PrePlan {
-  static constexpr int Q = cpt<T>(), TH = NT * TPN;
+  static constexpr int Q = QU, TH = NT * TPN;
   static constexpr int UIN = int(sizeof(In)) * Q / 16;  // b units per thread
-  static constexpr size_t RINGS = size_t(7) * TH * sizeof(Unit<T>);
+  static constexpr size_t RINGS = size_t(7) * TH * sizeof(Unit<T, QU>);
   static constexpr size_t SLOT = size_t(TH) * (UIN * 16 + 2 * sizeof(cplx_t<T>));
   static constexpr size_t BYTES = RINGS + PD * SLOT;
 };
-template <class T, class In, int TPN, int NT, int PD>
+template <class T, class In, int TPN, int NT, int PD, int QU>
 struct PostPlan {
-  static constexpr int Q = cpt<T>(), TH = NT * TPN;
+  static constexpr int Q = QU, TH = NT * TPN;
   static constexpr int UIN = int(sizeof(In)) * Q / 16;
+  static constexpr int XU = int(sizeof(Unit<T, QU>)) / 16;  // 16-byte vectors per unit
   static constexpr int NCN = NT / 2 + 1;  // coarse nodes under a strip
   static constexpr int CS = PD / 2 + 3;   // coarse-row ring slots
-  static constexpr size_t RINGS = size_t(6) * TH * sizeof(Unit<T>);
-  static constexpr size_t SLOT = size_t(TH) * (16 + UIN * 16 + 2 * sizeof(cplx_t<T>));
-  static constexpr size_t COARSE = size_t(CS) * NCN * TPN * 16;
+  static constexpr size_t RINGS = size_t(6) * TH * sizeof(Unit<T, QU>);
+  static constexpr size_t SLOT = size_t(TH) * (XU * 16 + UIN * 16 + 2 * sizeof(cplx_t<T>));
+  static constexpr size_t COARSE = size_t(CS) * NCN * TPN * sizeof(Unit<T, QU>);
   static constexpr size_t BYTES = RINGS + PD * SLOT + COARSE;
 };
 
 // Pre-smoothing of a zero-start visit: x1 = wD^{-1} b, x2 = x1 + wD^{-1}(b - A x1),
 // r = b - A x2, rc = P^T r. Strip: W = NT - 6 fine columns (halo 3 each side),
 // coarse columns [CX0, CX0 + W/2); chunk: coarse rows [CY0, CY0 + crows).
-template <class T, class In, int TPN, int NT, int PD, int MINB>
+template <class T, class In, int TPN, int NT, int PD, int MINB, int QU>
 __global__ void __launch_bounds__(NT * TPN, MINB)
 fused_pre_kernel(LevelOp<T> op, LevelGeom gc, T wj, const In* __restrict__ b, cplx_t<T>* __restrict__ x2out,
                  cplx_t<T>* __restrict__ rc, int crows) {
   using V = cplx_t<T>;
-  using U = Unit<T>;
-  using P = PrePlan<T, In, TPN, NT, PD>;
+  using U = Unit<T, QU>;
+  using P = PrePlan<T, In, TPN, NT, PD, QU>;
   constexpr int Q = P::Q, TH = P::TH, UIN = P::UIN, W = NT - 6, TC = W / 2;
   extern __shared__ __align__(16) unsigned char smraw[];
   U* x1s = reinterpret_cast<U*>(smraw);  // [3][TH]
@@ -308,19 +317,19 @@ fused_pre_kernel(LevelOp<T> op, LevelGeom gc, T wj, const In* __restrict__ b, cp
 // chunk: fine rows [Y0, Y0 + frows). The coarse correction rows under the
 // strip are staged too (coarse row J with fine row 2J-2, so the barrier of
 // that row publishes it before its first use by fine row 2J-1).
-template <class T, class In, class Out, int TPN, int NT, int PD, int MINB>
+template <class T, class In, class Out, int TPN, int NT, int PD, int MINB, int QU>
 __global__ void __launch_bounds__(NT * TPN, MINB)
 fused_post_kernel(LevelOp<T> op, LevelGeom gc, T wj, const cplx_t<T>* __restrict__ x2,
                   const cplx_t<T>* __restrict__ ec, const In* __restrict__ b, Out* __restrict__ out, int frows) {
   using V = cplx_t<T>;
-  using U = Unit<T>;
-  using P = PostPlan<T, In, TPN, NT, PD>;
-  constexpr int Q = P::Q, TH = P::TH, UIN = P::UIN, W = NT - 4, NCN = P::NCN, CS = P::CS;
+  using U = Unit<T, QU>;
+  using P = PostPlan<T, In, TPN, NT, PD, QU>;
+  constexpr int Q = P::Q, TH = P::TH, UIN = P::UIN, W = NT - 4, NCN = P::NCN, CS = P::CS, XU = P::XU;
   extern __shared__ __align__(16) unsigned char smraw[];
   U* x3s = reinterpret_cast<U*>(smraw);  // [3][TH]
   U* x4s = x3s + 3 * TH;                 // [3][TH]
-  uint4* xst = reinterpret_cast<uint4*>(smraw + P::RINGS);     // [PD][TH]
-  uint4* bst = xst + size_t(PD) * TH;                          // [PD][UIN][TH]
+  uint4* xst = reinterpret_cast<uint4*>(smraw + P::RINGS);     // [PD][XU][TH]
+  uint4* bst = xst + size_t(PD) * XU * TH;                     // [PD][UIN][TH]
   V* cds = reinterpret_cast<V*>(bst + size_t(PD) * UIN * TH);  // [PD][2][TH]
   U* ecs = reinterpret_cast<U*>(smraw + P::RINGS + PD * P::SLOT);  // [CS][NCN * TPN]
   const int n0 = int(op.g.n0), n1 = int(op.g.n1), k = int(op.g.k);
@@ -352,16 +361,22 @@ fused_post_kernel(LevelOp<T> op, LevelGeom gc, T wj, const cplx_t<T>* __restrict
   auto issue_coarse = [&](int J) {
     if (J < int(gc.n1) && t < NCN * TPN) {
       const int cx = cxa + t / TPN;
-      if (cx >= 0 && cx < int(gc.n0))
-        cpa16(ecs + (J % CS) * (NCN * TPN) + t,
-              ec + (int64_t(cx) + int64_t(gc.n0) * J) * k + (blockIdx.y * TPN + t % TPN) * Q);
+      if (cx >= 0 && cx < int(gc.n0)) {
+        char* dst = reinterpret_cast<char*>(ecs + (J % CS) * (NCN * TPN) + t);
+        const char* src =
+            reinterpret_cast<const char*>(ec + (int64_t(cx) + int64_t(gc.n0) * J) * k + (blockIdx.y * TPN + t % TPN) * Q);
+#pragma unroll
+        for (int u = 0; u < XU; ++u) cpa16(dst + 16 * u, src + 16 * u);
+      }
     }
   };
   auto issue = [&](int j) {
     if (j <= jend && j < n1) {
       const int sl = j % PD;
       if (inx) {
-        cpa16(xst + sl * TH + t, xp2 + j * rstride);
+#pragma unroll
+        for (int u = 0; u < XU; ++u)
+          cpa16(xst + (sl * XU + u) * TH + t, reinterpret_cast<const char*>(xp2 + j * rstride) + 16 * u);
 #pragma unroll
         for (int u = 0; u < UIN; ++u)
           cpa16(bst + (sl * UIN + u) * TH + t, bp + j * rstride * int64_t(sizeof(In)) + 16 * u);
@@ -398,8 +413,10 @@ fused_post_kernel(LevelOp<T> op, LevelGeom gc, T wj, const cplx_t<T>* __restrict
       U xr;
       In braw[Q];
       {
-        const uint4 a = xst[sl * TH + t];
-        memcpy(&xr, &a, sizeof(xr));
+        uint4 a[XU];
+#pragma unroll
+        for (int u = 0; u < XU; ++u) a[u] = xst[(sl * XU + u) * TH + t];
+        memcpy(&xr, a, sizeof(xr));
         uint4 raw[UIN];
 #pragma unroll
         for (int u = 0; u < UIN; ++u) raw[u] = bst[(sl * UIN + u) * TH + t];
@@ -462,27 +479,27 @@ int env_int(const char* name, int dflt) {
 // strip shape: NT nodes x 2 threads per node; c64: 4 columns per CTA
 constexpr int kTPN = 2, kPD = 3;
 
-template <class T, class In, int NT>
+template <class T, class In, int NT, int QU>
 void run_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In* b, cplx_t<T>* x2, cplx_t<T>* rc,
                    int crows, cudaStream_t s) {
-  using P = PrePlan<T, In, kTPN, NT, kPD>;
-  constexpr int TC = (NT - 6) / 2, C = kTPN * cpt<T>();
+  using P = PrePlan<T, In, kTPN, NT, kPD, QU>;
+  constexpr int TC = (NT - 6) / 2, C = kTPN * QU;
   // resident CTAs per SM: by shared memory (228 KB per SM)
   constexpr int MINB = int(std::min<size_t>(8, (227 * 1024) / (P::BYTES + 1024)));
   const dim3 grid(unsigned((gc.n0 + TC - 1) / TC), unsigned(op.g.k / C), unsigned((gc.n1 + crows - 1) / crows));
-  auto kern = fused_pre_kernel<T, In, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB)>;
+  auto kern = fused_pre_kernel<T, In, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB), QU>;
   allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
   kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, b, x2, rc, crows);
 }
 
-template <class T, class In, class Out, int NT>
+template <class T, class In, class Out, int NT, int QU>
 void run_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_t<T>* x2, const cplx_t<T>* ec,
                     const In* b, Out* out, int frows, cudaStream_t s) {
-  using P = PostPlan<T, In, kTPN, NT, kPD>;
-  constexpr int W = NT - 4, C = kTPN * cpt<T>();
+  using P = PostPlan<T, In, kTPN, NT, kPD, QU>;
+  constexpr int W = NT - 4, C = kTPN * QU;
   constexpr int MINB = int(std::min<size_t>(8, (227 * 1024) / (P::BYTES + 1024)));
   const dim3 grid(unsigned((op.g.n0 + W - 1) / W), unsigned(op.g.k / C), unsigned((op.g.n1 + frows - 1) / frows));
-  auto kern = fused_post_kernel<T, In, Out, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB)>;
+  auto kern = fused_post_kernel<T, In, Out, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB), QU>;
   allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
   kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, x2, ec, b, out, frows);
 }
@@ -491,6 +508,18 @@ void run_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_
 // 32 when a CTA's 4 columns cover the block in <= 2 CTAs (k <= 8): the
 // strips stream their rows sequentially, so narrow blocks need the extra
 // (narrower) strips to keep enough row chains in flight
+// two 16-byte vectors per thread unit (complex64 only, k % 8 == 0), opt-in
+// with HZ_FUSED_WIDE=1: at k = 8 it halves the threads and measured slower
+// (post 82 vs 60 us, 1.47 vs 1.31 ms per bench cycle,
+// profiles/r01_fused_wide_units.txt) -- these kernels need row chains in
+// flight more than per-row amortisation
+template <class T>
+bool fused_wide(int k) {
+  if (sizeof(T) != 4 || k % (kTPN * 2 * cpt<T>()) != 0) return false;
+  static const int env = env_int("HZ_FUSED_WIDE", 0);
+  return env != 0;
+}
+
 int fused_nt(int k, int cols_per_cta) {
   static const int env = env_int("HZ_FUSED_NT", 0);
   if (env == 32 || env == 64 || env == 128) return env;
@@ -517,13 +546,22 @@ void launch_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In*
   const double n = double(op.g.nodes), nc = double(gc.nodes), k = op.g.k, s_ = sizeof(cplx_t<T>);
   ProfScope prof(sizeof(T) == 8 ? "fused_pre_fine_c128" : "fused_pre_fine_c64",
                  n * (k * (sizeof(In) + s_) + 2.0 * s_) + nc * k * s_, s);
-  const int nt = fused_nt(int(op.g.k), kTPN * cpt<T>());
-  if (nt == 32)
-    run_fused_pre<T, In, 32>(op, gc, wj, b, x2, rc, crows, s);
-  else if (nt == 64)
-    run_fused_pre<T, In, 64>(op, gc, wj, b, x2, rc, crows, s);
-  else
-    run_fused_pre<T, In, 128>(op, gc, wj, b, x2, rc, crows, s);
+  if (fused_wide<T>(int(op.g.k))) {
+    constexpr int QW = 2 * cpt<T>();
+    const int nt = fused_nt(int(op.g.k), kTPN * QW);
+    if (nt == 32)
+      run_fused_pre<T, In, 32, QW>(op, gc, wj, b, x2, rc, crows, s);
+    else
+      run_fused_pre<T, In, 64, QW>(op, gc, wj, b, x2, rc, crows, s);
+  } else {
+    const int nt = fused_nt(int(op.g.k), kTPN * cpt<T>());
+    if (nt == 32)
+      run_fused_pre<T, In, 32, cpt<T>()>(op, gc, wj, b, x2, rc, crows, s);
+    else if (nt == 64)
+      run_fused_pre<T, In, 64, cpt<T>()>(op, gc, wj, b, x2, rc, crows, s);
+    else
+      run_fused_pre<T, In, 128, cpt<T>()>(op, gc, wj, b, x2, rc, crows, s);
+  }
   HZ_LAUNCH_CHECK();
 }
 
@@ -534,13 +572,22 @@ void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cp
   const double n = double(op.g.nodes), nc = double(gc.nodes), k = op.g.k, s_ = sizeof(cplx_t<T>);
   ProfScope prof(sizeof(T) == 8 ? "fused_post_fine_c128" : "fused_post_fine_c64",
                  n * (k * (s_ + sizeof(In) + sizeof(Out)) + 2.0 * s_) + nc * k * s_, s);
-  const int nt = fused_nt(int(op.g.k), kTPN * cpt<T>());
-  if (nt == 32)
-    run_fused_post<T, In, Out, 32>(op, gc, wj, x2, ec, b, out, frows, s);
-  else if (nt == 64)
-    run_fused_post<T, In, Out, 64>(op, gc, wj, x2, ec, b, out, frows, s);
-  else
-    run_fused_post<T, In, Out, 128>(op, gc, wj, x2, ec, b, out, frows, s);
+  if (fused_wide<T>(int(op.g.k))) {
+    constexpr int QW = 2 * cpt<T>();
+    const int nt = fused_nt(int(op.g.k), kTPN * QW);
+    if (nt == 32)
+      run_fused_post<T, In, Out, 32, QW>(op, gc, wj, x2, ec, b, out, frows, s);
+    else
+      run_fused_post<T, In, Out, 64, QW>(op, gc, wj, x2, ec, b, out, frows, s);
+  } else {
+    const int nt = fused_nt(int(op.g.k), kTPN * cpt<T>());
+    if (nt == 32)
+      run_fused_post<T, In, Out, 32, cpt<T>()>(op, gc, wj, x2, ec, b, out, frows, s);
+    else if (nt == 64)
+      run_fused_post<T, In, Out, 64, cpt<T>()>(op, gc, wj, x2, ec, b, out, frows, s);
+    else
+      run_fused_post<T, In, Out, 128, cpt<T>()>(op, gc, wj, x2, ec, b, out, frows, s);
+  }
   HZ_LAUNCH_CHECK();
 }
 

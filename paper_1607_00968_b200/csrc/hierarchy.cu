@@ -15,6 +15,7 @@
 #include <type_traits>
 
 #include "solver.hpp"
+#include "profile.hpp"
 
 namespace hz {
 
@@ -468,6 +469,7 @@ bool Hierarchy<T>::fused_level0(const CycleSpec& spec, int k) const {
 template <class T>
 void Hierarchy<T>::ensure_ws(int k) {
   if (ws_k_ == k) return;
+  clear_graphs();  // captured cycles reference the old workspaces
   const int L = num_levels();
   wx_.resize(L);
   wt_.resize(L);
@@ -659,7 +661,66 @@ int prio_from() {
 }  // namespace
 
 template <class T>
+void Hierarchy<T>::clear_graphs() {
+  for (auto& kv : graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  graphs_.clear();
+}
+
+template <class T>
+template <class XO>
+void Hierarchy<T>::cycle_cast_graph(const CycleSpec& spec, int k, const double2* b64, XO* x64, cudaStream_t s) {
+  static const bool on = [] {
+    const char* e = std::getenv("HZ_CYCLE_GRAPHS");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || sl_ || spec.kind == CycleKind::K || profiling_enabled()) {
+    cycle_cast(spec, k, b64, x64, s);
+    return;
+  }
+  const GraphKey key{b64, x64, k, int(spec.kind), spec.pre, spec.post, spec.jacobi_weight};
+  auto it = graphs_.find(key);
+  if (it == graphs_.end()) {  // first use: run directly (workspaces, smem limits)
+    cycle_cast(spec, k, b64, x64, s);
+    graphs_.emplace(key, GraphRec{});
+    return;
+  }
+  GraphRec& g = it->second;
+  if (!g.exec) {
+    cudaGraph_t graph = nullptr;
+    HZ_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    set_capturing(true);
+    try {
+      cycle_cast(spec, k, b64, x64, s);
+    } catch (...) {
+      set_capturing(false);
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    set_capturing(false);
+    HZ_CUDA(cudaStreamEndCapture(s, &graph));
+    size_t nn = 0;
+    HZ_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    HZ_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    g.kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      HZ_CUDA(cudaGraphNodeGetType(nd, &ty));
+      if (ty == cudaGraphNodeTypeKernel) ++g.kernels;
+    }
+    const cudaError_t st = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    HZ_CUDA(st);
+  }
+  HZ_CUDA(cudaGraphLaunch(g.exec, s));
+  add_launches(g.kernels);
+}
+
+template <class T>
 Hierarchy<T>::~Hierarchy() {
+  clear_graphs();
   if (hp_fork_) cudaEventDestroy(hp_fork_);
   if (hp_join_) cudaEventDestroy(hp_join_);
   if (hp_) cudaStreamDestroy(hp_);
@@ -799,5 +860,9 @@ template class Hierarchy<double>;
 template class Hierarchy<float>;
 template void Hierarchy<float>::cycle_cast<double2>(const CycleSpec&, int, const double2*, double2*, cudaStream_t);
 template void Hierarchy<float>::cycle_cast<float2>(const CycleSpec&, int, const double2*, float2*, cudaStream_t);
+template void Hierarchy<float>::cycle_cast_graph<double2>(const CycleSpec&, int, const double2*, double2*,
+                                                          cudaStream_t);
+template void Hierarchy<float>::cycle_cast_graph<float2>(const CycleSpec&, int, const double2*, float2*,
+                                                         cudaStream_t);
 
 }  // namespace hz

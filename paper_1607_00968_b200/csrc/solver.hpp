@@ -8,6 +8,8 @@
 #include <array>
 #include <complex>
 #include <functional>
+#include <map>
+#include <tuple>
 #include <memory>
 #include <vector>
 
@@ -106,6 +108,11 @@ class Hierarchy {
   // (XO = double2: widened result; XO = float2: the complex64 result as is)
   template <class XO>
   void cycle_cast(const CycleSpec& spec, int k, const double2* b64, XO* x64, cudaStream_t s);
+  // cycle_cast replayed from a CUDA graph per (b64, x64, k, spec) after its
+  // first direct run (V / W cycles, not in slab mode or while profiling;
+  // HZ_CYCLE_GRAPHS=0 disables): one launch instead of ~50 per cycle
+  template <class XO>
+  void cycle_cast_graph(const CycleSpec& spec, int k, const double2* b64, XO* x64, cudaStream_t s);
   // Galerkin planes / diagonal of level l (host copy, f64) for parity checks
   void download_level(int l, std::vector<cplx>& coef_or_center) const;
   // copy of the level operators (not the coarsest solver) on another GPU
@@ -154,6 +161,21 @@ class Hierarchy {
   int ws_k_ = 0;
   std::vector<DevBuf<V>> wx_, wt_, wb_, wr_;  // per level: solution, ping-pong, rhs, residual
   std::vector<std::unique_ptr<Fgmres<T>>> kfgm_;
+  struct GraphKey {
+    const void* b;
+    const void* x;
+    int k, kind, pre, post;
+    double wj;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(b, x, k, kind, pre, post, wj) < std::tie(o.b, o.x, o.k, o.kind, o.pre, o.post, o.wj);
+    }
+  };
+  struct GraphRec {
+    cudaGraphExec_t exec = nullptr;
+    int64_t kernels = 0;
+  };
+  std::map<GraphKey, GraphRec> graphs_;
+  void clear_graphs();
   // high-priority stream of the coarse part of the cycle (coarse_visit)
   cudaStream_t hp_ = nullptr;
   cudaEvent_t hp_fork_ = nullptr, hp_join_ = nullptr;

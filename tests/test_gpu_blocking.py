@@ -191,3 +191,25 @@ def test_fused_apply_gram_matches_unfused(dim):
             assert r.returncode == 0, r.stderr[-2000:]
             outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("k", [8, 4])
+def test_cycle_graph_replay_matches_direct_launches(k):
+    """The c64 preconditioner replayed from captured CUDA graphs
+    (HZ_CYCLE_GRAPHS, default on) runs the same kernels on the same buffers
+    as the direct launches: the solves are bitwise equal."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    with tempfile.TemporaryDirectory() as d:
+        for flag in ("1", "0"):
+            path = os.path.join(d, f"x{flag}.npy")
+            r = subprocess.run([sys.executable, "-c", ZLO_SOLVE, path, str(k)], cwd=root,
+                               env=dict(os.environ, HZ_CYCLE_GRAPHS=flag), capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])

@@ -30,8 +30,8 @@ CYCLE = (
     "np.save(sys.argv[1], x1)\n")
 
 
-def _run(code, path, flag, *args):
-    env = dict(os.environ, HZ_FUSED_VCYCLE=flag)
+def _run(code, path, flag, *args, **extra_env):
+    env = dict(os.environ, HZ_FUSED_VCYCLE=flag, **extra_env)
     r = subprocess.run([sys.executable, "-c", code, path, *map(str, args)], cwd=ROOT, env=env,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
@@ -61,6 +61,10 @@ def test_fused_vcycle_bitwise_equals_unfused(nx, nz, k, nl, prec, kind):
     assert np.all(np.isfinite(fused))
     if prec == "c64":
         assert np.array_equal(fused, plain), f"max rel diff {rel_err(fused, plain):.3e}"
+        if k % 8 == 0:  # the opt-in two-vector thread units (HZ_FUSED_WIDE=1)
+            with tempfile.TemporaryDirectory() as d:
+                wide = _run(CYCLE, os.path.join(d, "w.npy"), "1", nx, nz, k, nl, prec, kind, HZ_FUSED_WIDE="1")
+            assert np.array_equal(wide, plain)
     else:
         # complex128: same expressions, but nvcc may contract a complex
         # product into FMAs differently in the two kernels (last-bit
