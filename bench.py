@@ -372,8 +372,14 @@ def run_ours(args):
         per = {"kernel": name, "launches": r["count"],
                "algorithmic_bytes_per_launch": r["bytes"] / r["count"],
                "hbm_gbs": round(gbs, 1), "hbm_frac": round(gbs / peak, 4),
-               "traffic": (traffic_tab.get(name) or {}).get("dram_bytes_per_launch"),
-               "traffic_note": (traffic_tab.get(name) or {}).get("note")}
+               "traffic": None, "traffic_note": None}
+        tt = traffic_tab.get(name) or {}
+        if tt.get("dram_over_algorithmic"):
+            # ncu DRAM bytes / algorithmic bytes of the captured launches,
+            # applied to this kernel's mean algorithmic bytes per launch
+            per["traffic"] = round(tt["dram_over_algorithmic"] * r["bytes"] / r["count"])
+            per["traffic_note"] = (f"ncu dram__bytes_read+write = {tt['dram_over_algorithmic']:.3f} x algorithmic "
+                                   f"over {tt.get('launches_captured')} captured launches ({tt.get('note', '')})")
         # the binding roofline: FP64 tensor pipe when the kernel's flops at
         # the DMMA peak take longer than its bytes at the HBM peak (the
         # 32-column Gram / update), else HBM (8-column blocks, stencils)

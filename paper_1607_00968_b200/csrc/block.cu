@@ -715,8 +715,11 @@ int launch_multi_gram(int64_t n, int k, int nb, const BlockTab<T>& X, const cplx
                       cplx_t<T>* partials, int max_slots, cudaStream_t s) {
   if (k > 64) throw HzError(kValidation, "block width k > 64 unsupported");
   if (nb > kMaxBlocks) throw HzError(kValidation, "too many blocks in one Gram");
-  ProfScope prof(sizeof(T) == 8 ? "multi_gram_c128" : "multi_gram_c64",
-                 double(nb + 1) * n * k * sizeof(cplx_t<T>), s, 8.0 * double(n) * k * k * nb);
+  // Y is usually the last X block (the Arnoldi step's [V_0..V_j, W]^H W):
+  // then nb blocks are read, not nb + 1
+  const double blocks = (nb > 0 && X.p[nb - 1] == Y) ? double(nb) : double(nb + 1);
+  ProfScope prof(sizeof(T) == 8 ? "multi_gram_c128" : "multi_gram_c64", blocks * n * k * sizeof(cplx_t<T>), s,
+                 8.0 * double(n) * k * k * nb);
   // ~4 CTAs per SM in total over the nb blocks; at least 32 rows per slot
   // exactly one wave of resident CTAs (3 per SM for the tiled / DMMA Grams)
   // over the nb blocks: a partial last wave would idle up to 2/3 of the GPU

@@ -9,6 +9,29 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 out = sys.argv[2] if len(sys.argv) > 2 else "profiles/ncu_traffic.json"
+# bench workload geometry (config 2, 8-column blocks): fine nodes, coarse
+# (level-1) nodes, block width -- for the per-launch algorithmic bytes
+N, NC, K = 1025 * 513, 513 * 257, 8
+
+
+def algorithmic(k):
+    """Algorithmic bytes of one captured launch (SURVEY 8d formulas, as the
+    library's profiler counts them), or None when the name does not fix them."""
+    m = re.search(r"gram8_kernel<(\d+)>", k)
+    if m:  # Arnoldi Gram: Y = W is the last of the nb X blocks
+        return int(m.group(1)) * N * K * 16
+    m = re.search(r"update8_kernel<(\d+), (double|float)>", k)
+    if m:  # the Arnoldi update writes Q from nb blocks (Yin = null); the
+        # restart update X += Z Y reads nb c64 blocks and X
+        nb = int(m.group(1))
+        return (nb + 1) * N * K * 16 if m.group(2) == "double" else nb * N * K * 8 + 2 * N * K * 16
+    if "fused_pre_kernel<float" in k:
+        return N * (K * (16 + 8) + 16) + NC * K * 8
+    if "fused_post_kernel<float" in k:
+        return N * (K * (8 + 16 + 8) + 16) + NC * K * 8
+    if "apply_lo_kernel" in k:
+        return N * (K * (8 + 16) + 16)
+    return None
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
@@ -42,7 +65,7 @@ def name_of(k):
     return None
 
 
-acc = defaultdict(lambda: {"n": 0, "bytes": 0.0, "us": 0.0})
+acc = defaultdict(lambda: {"n": 0, "bytes": 0.0, "us": 0.0, "alg": 0.0, "nalg": 0, "bytes_alg": 0.0})
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     u = dict(zip(hdr, units))
@@ -52,8 +75,14 @@ for r in rows[2:]:
     b = sum(float(d[m]) * scale[u[m]] for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     acc[nm]["n"] += 1
     acc[nm]["bytes"] += b
+    a = algorithmic(d["Kernel Name"])
+    if a:
+        acc[nm]["alg"] += a
+        acc[nm]["bytes_alg"] += b
+        acc[nm]["nalg"] += 1
     acc[nm]["us"] += float(d["gpu__time_duration.sum"]) * (1e-3 if u["gpu__time_duration.sum"] == "nsecond" else 1)
 res = {k: {"dram_bytes_per_launch": v["bytes"] / v["n"], "launches_captured": v["n"],
+           "dram_over_algorithmic": round(v["bytes_alg"] / v["alg"], 4) if v["nalg"] else None,
            "ncu_us_per_launch": round(v["us"] / v["n"], 2),
            "note": f"mean over {v['n']} consecutive launches of one ncu --set full capture ({rep.split('/')[-1]})"}
        for k, v in acc.items()}
