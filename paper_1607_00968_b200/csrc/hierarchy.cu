@@ -560,17 +560,6 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
     coarse_solve(k, b, x, s);
     return;
   }
-  {  // timing experiments only (wrong preconditioner): HZ_DEBUG_CUT_LEVEL=c
-     // replaces the visits of levels >= c by a zero correction
-    static const int cut = [] {
-      const char* e = std::getenv("HZ_DEBUG_CUT_LEVEL");
-      return e ? std::atoi(e) : 0;
-    }();
-    if (cut > 0 && l >= cut) {
-      HZ_CUDA(cudaMemsetAsync(x, 0, size_t(levels_[l].nodes()) * k * sizeof(V), s));
-      return;
-    }
-  }
   if (l == 0 && x_zero && fused_level0(spec, k)) {
     // fused finest-level visit: pre-smoothing + residual + restriction,
     // coarse visit(s), prolongation + post-smoothing (fused.cu)
