@@ -10,7 +10,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhz_b200.so")
+# HZ_LIB_PATH: an alternative build of the same library (A/B timing of
+# compile-time variants, scripts/build_variant.py); default the in-tree one
+LIB_PATH = os.environ.get("HZ_LIB_PATH") or os.path.join(_HERE, "libhz_b200.so")
 
 # C-ABI symbols (include/hz_b200.h); tests check the library exports each one.
 EXPORTS = (

@@ -644,7 +644,8 @@ void update8_dispatch(int nb, int64_t n, const BlockTab<TT>& X, const double2* H
   if constexpr (NB <= kK8MaxNb) {
     if (nb == NB) {
       const int64_t tiles = (n + 7) / 8;
-      const int grid = int(std::max<int64_t>(1, std::min<int64_t>(2 * kNumSMs, (tiles + 7) / 8)));
+      const int grid =
+          int(std::max<int64_t>(1, std::min<int64_t>(HZ_UPDATE8_MINB * kNumSMs, (tiles + 7) / 8)));
       k8::update8_kernel<NB, TT><<<grid, k8::kThreads, 0, s>>>(n, X, H, Yin, Yout, sign);
       return;
     }

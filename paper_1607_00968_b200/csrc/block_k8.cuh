@@ -103,8 +103,11 @@ __device__ __forceinline__ double2 ld_widen(const XV* p) {
 }
 
 // TT = float: the X_i are complex64 blocks widened on load (exact)
+#ifndef HZ_UPDATE8_MINB
+#define HZ_UPDATE8_MINB 2
+#endif
 template <int NB, class TT = double>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, HZ_UPDATE8_MINB)
 update8_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, const double2* Yin,
                double2* Yout, double sign) {
   __shared__ double2 hs[NB * 64];
