@@ -401,7 +401,7 @@ def run_ours(args):
     dom = max(kern, key=lambda n_: kern[n_]["ms"])
     roofline = roof(dom)
     roofline["share"] = table[dom]["share"]
-    stencil = [n_ for n_ in kern if n_.startswith(("jacobi", "residual", "apply", "restrict", "prolong"))]
+    stencil = [n_ for n_ in kern if n_.startswith(("jacobi", "residual", "apply", "restrict", "prolong", "fused"))]
     roof_st = None
     if stencil:
         dst = max(stencil, key=lambda n_: kern[n_]["ms"])
