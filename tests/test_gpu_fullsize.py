@@ -1,0 +1,83 @@
+"""GPU tier at the BASELINE configs' full sizes. The reference cannot solve
+these in test time on the CPU, so parity is carried by what is cheap for it
+and size independent:
+
+* the operator at full size against the reference's apply_block (1e-12);
+* one multigrid cycle of the bench hierarchy at full size against the
+  reference's MgHierarchy::cycle (1e-12, complex128);
+* the bench solve (32 sources, 4 concurrent 8-column blocks, c64 cycle):
+  every column's residual against the REFERENCE operator, b - A_ref x, within
+  the 1e-6 tolerance; linearity (scaling the sources by 2 scales the
+  solution); the same solve through host buffers and device blocks;
+* configs 3 and 4 (3D): residuals against the reference operator.
+"""
+import numpy as np
+import pytest
+import torch
+
+from hzt_util import rel_err
+from paper_1607_00968_b200 import configs
+
+pytestmark = pytest.mark.gpu
+hz = pytest.importorskip("paper_1607_00968_b200")
+
+
+def _bench_cfg():
+    import bench
+    return bench.build_workload(0, 1, 32)
+
+
+def _ref_residuals(ref, cfg, X, B):
+    R = ref.RefProblem.from_config(cfg)
+    AX = R.apply_block(X)
+    return np.linalg.norm(B - AX, axis=0) / np.linalg.norm(B, axis=0)
+
+
+def test_config2_full_size_apply_matches_reference(ref):
+    cfg = _bench_cfg()
+    P = hz.HelmholtzProblem.from_config(cfg)
+    u = configs.random_block(cfg.num_nodes, 4, seed=21)
+    assert rel_err(P.apply_block(u), ref.RefProblem.from_config(cfg).apply_block(u)) <= 1e-12
+
+
+def test_config2_full_size_cycle_matches_reference(ref):
+    cfg = _bench_cfg()
+    cfg.precond_precision, cfg.krylov_block = "c128", 0
+    S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))
+    b = configs.random_block(cfg.num_nodes, 2, seed=22)
+    x = S.cycle(b)
+    R = ref.RefProblem.from_config(cfg)
+    H = ref.RefHierarchy(R, cfg.nlevels, cfg.shift)
+    xr = H.cycle(b, kind=cfg.cycle, pre=cfg.pre, post=cfg.post, wj=cfg.jacobi_weight)
+    assert rel_err(x, xr) <= 1e-12
+
+
+def test_config2_full_size_bench_solve_properties(ref):
+    cfg = _bench_cfg()
+    S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))
+    B = cfg.rhs_block()
+    X, rep = S.solve_block(B)
+    assert rep.all_converged() and np.all(rep.rel_residual <= cfg.tol)
+    # the solution satisfies the reference's own discrete equation
+    assert np.all(_ref_residuals(ref, cfg, X, B) <= cfg.tol * (1 + 1e-6))
+    # linearity: 2 B -> 2 X (power-of-two scaling is exact through every step)
+    X2, rep2 = S.solve_block(2.0 * B)
+    assert rep2.cycles == rep.cycles
+    assert rel_err(X2, 2.0 * X) <= 1e-14
+    # device blocks give the same solution as host buffers
+    Xd, _ = S.solve_block(torch.from_numpy(B).cuda())
+    assert np.array_equal(Xd.cpu().numpy(), X)
+
+
+@pytest.mark.parametrize("c", [3, 4])
+def test_3d_configs_full_size_residuals_against_reference(ref, c):
+    import sys, os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+    from run_configs import make
+    cfg = make(c)
+    S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))
+    B = cfg.rhs_block()
+    X, rep = S.solve_block(torch.from_numpy(B).cuda())
+    X = X.cpu().numpy()
+    assert rep.all_converged()
+    assert np.all(_ref_residuals(ref, cfg, X, B) <= cfg.tol * (1 + 1e-6))
