@@ -477,7 +477,13 @@ int env_int(const char* name, int dflt) {
 }
 
 // strip shape: NT nodes x 2 threads per node; c64: 4 columns per CTA
-constexpr int kTPN = 2, kPD = 3;
+#ifndef HZ_FUSED_PD
+#define HZ_FUSED_PD 2  // staged rows in flight: 2 measured 3-4 % faster than 3 with 4 concurrent 8-column groups (less shared memory per CTA; profiles/r01_fused_pd_ab.txt)
+#endif
+#ifndef HZ_FUSED_MAXB
+#define HZ_FUSED_MAXB 8
+#endif
+constexpr int kTPN = 2, kPD = HZ_FUSED_PD;
 
 template <class T, class In, int NT, int QU>
 void run_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In* b, cplx_t<T>* x2, cplx_t<T>* rc,
@@ -485,7 +491,7 @@ void run_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In* b,
   using P = PrePlan<T, In, kTPN, NT, kPD, QU>;
   constexpr int TC = (NT - 6) / 2, C = kTPN * QU;
   // resident CTAs per SM: by shared memory (228 KB per SM)
-  constexpr int MINB = int(std::min<size_t>(8, (227 * 1024) / (P::BYTES + 1024)));
+  constexpr int MINB = int(std::min<size_t>(HZ_FUSED_MAXB, (227 * 1024) / (P::BYTES + 1024)));
   const dim3 grid(unsigned((gc.n0 + TC - 1) / TC), unsigned(op.g.k / C), unsigned((gc.n1 + crows - 1) / crows));
   auto kern = fused_pre_kernel<T, In, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB), QU>;
   allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
@@ -497,7 +503,7 @@ void run_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_
                     const In* b, Out* out, int frows, cudaStream_t s) {
   using P = PostPlan<T, In, kTPN, NT, kPD, QU>;
   constexpr int W = NT - 4, C = kTPN * QU;
-  constexpr int MINB = int(std::min<size_t>(8, (227 * 1024) / (P::BYTES + 1024)));
+  constexpr int MINB = int(std::min<size_t>(HZ_FUSED_MAXB, (227 * 1024) / (P::BYTES + 1024)));
   const dim3 grid(unsigned((op.g.n0 + W - 1) / W), unsigned(op.g.k / C), unsigned((op.g.n1 + frows - 1) / frows));
   auto kern = fused_post_kernel<T, In, Out, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB), QU>;
   allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
