@@ -23,9 +23,12 @@ constexpr int kRowsPerStep = 4;  // Gram: rows per DMMA k-step
 
 // row groups in flight per warp and resident CTAs per SM (registers: the
 // Gram keeps 12 NB accumulator registers per lane)
+#ifndef HZ_GRAM8_U12
+#define HZ_GRAM8_U12 2  // row groups in flight per warp for NB <= 2
+#endif
 template <int NB>
 struct Gram8Cfg {
-  static constexpr int U = NB <= 3 ? 2 : 1;
+  static constexpr int U = NB <= 2 ? HZ_GRAM8_U12 : (NB <= 3 ? 2 : 1);
   static constexpr int MINB = NB <= 6 ? 2 : 1;
 };
 

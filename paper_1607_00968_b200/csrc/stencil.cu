@@ -432,8 +432,13 @@ __device__ __forceinline__ void stencil_v4_item(const LevelOp<T>& op, const cplx
   st4(out + e0, o);
 }
 
+// resident CTAs per SM the Galerkin level kernel is compiled for (register
+// cap 65536 / (kBlock * HZ_STENCIL_MINB)); 1 = compiler's choice
+#ifndef HZ_STENCIL_MINB
+#define HZ_STENCIL_MINB 1
+#endif
 template <class T, int NDIM, int MODE, int G>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, HZ_STENCIL_MINB)
 stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
                   cplx_t<T>* __restrict__ out, T wj) {
   stencil_v4_item<T, NDIM, MODE, G>(op, x, b, out, wj, blockIdx.x * kBlock + threadIdx.x);

@@ -179,6 +179,24 @@ def test_zero_is_fixed_point():
     assert not np.any(x)
 
 
+@pytest.mark.parametrize("ndim,n,kind,prec", [(2, (65, 33, 1), "V", "c128"), (3, (17, 17, 9), "W", "c128"),
+                                               (2, (129, 65, 1), "V", "c64")])
+def test_cycle_linearity(ndim, n, kind, prec):
+    """SPEC.md:249-253 cycle linearity: M(a b1 + b2) = a M(b1) + M(b2) for a
+    cycle from x = 0 (a fixed linear map); 1e-12 in complex128, complex64
+    rounding for the mixed-precision preconditioner."""
+    cfg = configs.small_problem(ndim, n, seed=4)
+    o = hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=3, shift_factor=0.5, cycle=hz.CycleSpec(kind))
+    o.precond_precision = prec
+    S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), o)
+    b1 = configs.random_block(cfg.num_nodes, 4, seed=21)
+    b2 = configs.random_block(cfg.num_nodes, 4, seed=22)
+    a = 0.75 - 0.5j
+    lhs = S.cycle(a * b1 + b2)
+    rhs = a * S.cycle(b1) + S.cycle(b2)
+    assert rel_err(lhs, rhs) <= (1e-12 if prec == "c128" else 1e-5)
+
+
 def _check_solve(ref_rep, rep, X, X_ref, tol, sol_tol=1e-5):
     assert rep.all_converged() and ref_rep.all_converged()
     assert np.all(rep.rel_residual <= tol) and np.all(ref_rep.rel_residual <= tol)
