@@ -26,7 +26,8 @@ def make(c):
     elif c == 5:
         cfg = configs.config5(nlevels=4)                   # coarsest 65x65x33
         cfg.shift, cfg.restart = 1.5, 5
-    for key in ("nlevels", "shift", "restart", "max_cycles", "precond_precision", "krylov_block", "jacobi_weight"):
+    for key in ("nlevels", "shift", "restart", "max_cycles", "precond_precision", "krylov_block", "jacobi_weight",
+                "cycle"):
         v = os.environ.get(f"HZ_CFG{c}_{key.upper()}")
         if v is not None:
             setattr(cfg, key, type(getattr(cfg, key))(v))
