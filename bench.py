@@ -9,8 +9,10 @@ are solved as 4 concurrent independent blocks of 8 (hz_options.rhs_block).
 
 One step = one block solve of the rank's k right-hand sides from zero to the
 tolerance (setup excluded). N > 1 runs one process per GPU
-under torchrun; each rank owns its own block of k sources (weak scaling, no
-data-path collective). `value` = all ranks' RHS / max-over-ranks device time.
+under torchrun (started by the driver, or by this script re-executing itself
+through torch.distributed.run when --gpus N > 1 and WORLD_SIZE is unset);
+each rank owns its own block of k sources (weak scaling, no data-path
+collective); the rank count must equal --gpus. `value` = all ranks' RHS / max-over-ranks device time.
 
 The JSON line also carries: `e2e` (same metric through the C ABI with host
 buffers, H2D/D2H inside the timed region), `roofline` (dominant kernel's
@@ -267,9 +269,14 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     import paper_1607_00968_b200 as hz
+    from paper_1607_00968_b200 import parallel
 
     ws, rank, local = dist_env()
+    if ws != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={ws}")
     torch.cuda.set_device(local)
+    if torch.cuda.device_count() < 1:
+        raise SystemExit("bench: no CUDA device")
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = build_workload(rank, ws, WORKLOAD["k"])
@@ -287,13 +294,6 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        if ws == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
     # warm-up (also fixes the cycle count of the workload)
     rep = None
     for _ in range(args.warmup):
@@ -304,30 +304,36 @@ def run_ours(args):
     launches0 = hz.kernel_launch_count()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            _, rep = S.solve_block(Bd, out=Xd)  # library stream; synchronised on return
-            cycles.append(block_cycles(rep, cfg))
-            if not rep.all_converged():
-                raise RuntimeError(f"solve did not converge: {rep.rel_residual}")
+    def step(_i):
+        _, r = S.solve_block(Bd, out=Xd)  # library stream, ordered after `stream`; synchronised on return
+        cycles.append(block_cycles(r, cfg))
+        if not r.all_converged():
+            raise RuntimeError(f"solve did not converge: {r.rel_residual}")
+
+    def ev_stop():
         ev1.record(stream)
-        barrier()
+        ev1.synchronize()
+        return ev0.elapsed_time(ev1)
+
+    with ClockSampler(local) as clk:
+        t_local = parallel.time_steps(step, args.steps, barrier, lambda: ev0.record(stream), ev_stop)
     launches = hz.kernel_launch_count() - launches0
-    t_ms = max_over_ranks(ev0.elapsed_time(ev1))
-    value = ws * k * args.steps / (t_ms / 1e3)
+    value, t_ms = parallel.whole_job_rate(k, args.steps, t_local, device=f"cuda:{local}")
     # ---- e2e: the public C ABI with pinned host buffers (H2D + D2H per step)
     Bp = torch.from_numpy(B_host).pin_memory()
     Xp = torch.empty_like(Bp).pin_memory()
     Bn, Xn = Bp.numpy(), Xp.numpy()
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        _, rep_e = S.solve_block(Bn, out=Xn)
-    torch.cuda.synchronize()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e = ws * k * args.steps / e2e_s
+    wall = {}
+
+    def e2e_step(_i):
+        S.solve_block(Bn, out=Xn)
+
+    def wall_stop():
+        return 1e3 * (time.perf_counter() - wall["t0"])
+
+    e2e_ms_local = parallel.time_steps(e2e_step, args.steps, barrier,
+                                       lambda: wall.__setitem__("t0", time.perf_counter()), wall_stop)
+    e2e, _ = parallel.whole_job_rate(k, args.steps, e2e_ms_local, device=f"cuda:{local}")
     # ---- profiled pass (same steps) for the per-kernel roofline
     # (blocked workload: one block solved alone -- the concurrent blocks run
     # the same kernels at the same shapes, but overlapping kernels would
@@ -446,6 +452,12 @@ def main():
     ap.add_argument("--ref-cycles", type=float, default=None,
                     help="cycle count to extrapolate the reference sample to (default: the sample's own)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched directly with --gpus N: become the torchrun launch the
+        # driver uses (one process per GPU, 127.0.0.1 rendezvous)
+        from paper_1607_00968_b200 import parallel
+        argv = parallel.torchrun_argv(args.gpus, os.path.abspath(__file__), sys.argv[1:])
+        os.execv(argv[0], argv)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

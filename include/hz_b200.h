@@ -154,9 +154,15 @@ HZ_API int hz_solver_slab_info(const hz_solver* s, int* nparts, int* agg_level, 
  * buffers B, X [n][k]; H2D / D2H copies included. Non-convergence is
  * reported in the report (status stays HZ_OK), as in the reference. */
 HZ_API int hz_solve_block(hz_solver* s, int64_t n, int k, const double* B, double* X, hz_report* rep);
-/* device-resident variant (double2*) */
+/* Device-resident variants (double2* on the problem's GPU). The solve runs
+ * on the solver's own stream and is ordered after the caller's pending work
+ * on `stream` (a cudaStream_t; the _stream variant) or on the legacy default
+ * stream (the plain variant): a B written asynchronously on another stream
+ * must use the _stream variant with that stream. X is complete on return. */
 HZ_API int hz_solve_block_device(hz_solver* s, int64_t n, int k, const void* B_dev, void* X_dev,
                           hz_report* rep);
+HZ_API int hz_solve_block_device_stream(hz_solver* s, int64_t n, int k, const void* B_dev, void* X_dev,
+                                        hz_report* rep, void* stream);
 /* Multi-frequency batching (no reference counterpart -- the
    reference solves one (m, omega) at a time): `count` independent block
    solves, one per solver (each solver owns its hierarchy, stream and Krylov
@@ -190,6 +196,8 @@ HZ_API int hz_solve_helmholtz(hz_solver* s, int64_t n, int k, const double* B, d
  * (out := 0; MgHierarchy::cycle(opts.cycle), src/helmholtz_solver.cpp:65-68). */
 HZ_API int hz_cycle(hz_solver* s, int64_t n, int k, const double* b, double* x);
 HZ_API int hz_cycle_device(hz_solver* s, int64_t n, int k, const void* b_dev, void* x_dev);
+/* ordered after the caller's `stream` (cudaStream_t), see hz_solve_block_device_stream */
+HZ_API int hz_cycle_device_stream(hz_solver* s, int64_t n, int k, const void* b_dev, void* x_dev, void* stream);
 
 /* MgHierarchy::coarse_solve (src/multigrid.cpp:114-117) on the coarsest level */
 HZ_API int hz_coarse_solve(hz_solver* s, int64_t nc, int k, const double* b, double* x);

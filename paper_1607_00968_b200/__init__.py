@@ -121,14 +121,14 @@ def solve_blocks_multi(solvers: Sequence["HelmholtzSolver"], Bs, outs=None):
     for i, (S, B) in enumerate(zip(solvers, Bs)):
         n = S.problem.num_nodes
         if dev:
-            B = _dev_block(B, n)
+            B = _dev_block(B, n, S.problem.device)
             import torch
-            X = outs[i] if outs is not None else torch.empty_like(B)
+            X = _check_out(outs[i], B, dev=True) if outs is not None else torch.empty_like(B)
             ptrB.append(B.data_ptr())
             ptrX.append(X.data_ptr())
         else:
             B = _host_block(B, n)
-            X = outs[i] if outs is not None else np.empty_like(B)
+            X = _check_out(outs[i], B, dev=False) if outs is not None else np.empty_like(B)
             ptrB.append(B.ctypes.data)
             ptrX.append(X.ctypes.data)
         r, b = S._report(B.shape[1], S.options.max_cycles + 8)
@@ -264,15 +264,45 @@ def _host_block(a, n: int) -> np.ndarray:
     return a
 
 
-def _dev_block(t, n: int):
+def _dev_block(t, n: int, device: Optional[int] = None):
     import torch
     if t.dtype != torch.complex128 or not t.is_cuda:
         raise ValidationError("device blocks must be complex128 CUDA tensors")
+    if device is not None and t.device.index != device:
+        raise ValidationError(f"block is on cuda:{t.device.index}, the solver on cuda:{device}")
     if t.dim() == 1:
         t = t.reshape(n, 1)
     if t.dim() != 2 or t.shape[0] != n:
         raise ValidationError(f"block must be [n={n}][k], got {tuple(t.shape)}")
     return t.contiguous()
+
+
+def _check_out(out, B, dev: bool):
+    """A caller-supplied solution buffer must be exactly what the C library
+    writes n*k*16 bytes into: complex128, B's [n][k] shape, C-contiguous, on
+    B's side (host / the same device) and not overlapping B (the solve zeroes
+    X before it reads B, src/krylov.cpp:178-200)."""
+    if dev:
+        import torch
+        if not _is_torch(out) or out.dtype != torch.complex128 or not out.is_cuda:
+            raise ValidationError("out must be a complex128 CUDA tensor for a device block")
+        if out.device != B.device:
+            raise ValidationError(f"out is on {out.device}, B on {B.device}")
+        if tuple(out.shape) != tuple(B.shape) or not out.is_contiguous():
+            raise ValidationError(f"out must be a contiguous [n][k] = {tuple(B.shape)} tensor")
+        a0, a1 = out.data_ptr(), out.data_ptr() + out.numel() * 16
+        b0, b1 = B.data_ptr(), B.data_ptr() + B.numel() * 16
+        if a0 < b1 and b0 < a1:
+            raise ValidationError("out must not share memory with B")
+        return out
+    if _is_torch(out) or not isinstance(out, np.ndarray):
+        raise ValidationError("out must be a numpy complex128 array for a host block")
+    if out.dtype != np.complex128 or out.shape != B.shape or not out.flags["C_CONTIGUOUS"] \
+            or not out.flags["WRITEABLE"]:
+        raise ValidationError(f"out must be a writeable C-contiguous complex128 [n][k] = {B.shape} array")
+    if np.shares_memory(out, B):
+        raise ValidationError("out must not share memory with B")
+    return out
 
 
 @dataclasses.dataclass
@@ -548,15 +578,15 @@ class HelmholtzSolver:
         cap = self.options.max_cycles + 8
         if _is_torch(B):
             import torch
-            B = _dev_block(B, n)
-            X = out if out is not None else torch.empty_like(B)
+            B = _dev_block(B, n, self.problem.device)
+            X = _check_out(out, B, dev=True) if out is not None else torch.empty_like(B)
             rep, bufs = self._report(B.shape[1], cap)
-            torch.cuda.current_stream(B.device).synchronize()
-            _check(_native.lib().hz_solve_block_device(self._h, n, B.shape[1], B.data_ptr(), X.data_ptr(),
-                                                       C.byref(rep)))
+            stream = torch.cuda.current_stream(B.device).cuda_stream
+            _check(_native.lib().hz_solve_block_device_stream(self._h, n, B.shape[1], B.data_ptr(), X.data_ptr(),
+                                                              C.byref(rep), stream))
             return X, self._finish(rep, bufs)
         B = _host_block(B, n)
-        X = out if out is not None else np.empty_like(B)
+        X = _check_out(out, B, dev=False) if out is not None else np.empty_like(B)
         rep, bufs = self._report(B.shape[1], cap)
         _check(_native.lib().hz_solve_block(self._h, n, B.shape[1], B.ctypes.data, X.ctypes.data,
                                             C.byref(rep)))
@@ -573,10 +603,10 @@ class HelmholtzSolver:
         n = self.problem.num_nodes
         if _is_torch(b):
             import torch
-            b = _dev_block(b, n)
+            b = _dev_block(b, n, self.problem.device)
             x = torch.empty_like(b)
-            torch.cuda.current_stream(b.device).synchronize()
-            _check(_native.lib().hz_cycle_device(self._h, n, b.shape[1], b.data_ptr(), x.data_ptr()))
+            stream = torch.cuda.current_stream(b.device).cuda_stream
+            _check(_native.lib().hz_cycle_device_stream(self._h, n, b.shape[1], b.data_ptr(), x.data_ptr(), stream))
             return x
         b = _host_block(b, n)
         x = np.empty_like(b)

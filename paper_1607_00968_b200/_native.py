@@ -19,8 +19,8 @@ EXPORTS = (
     "hz_abi_version", "hz_last_error_message", "hz_device_count", "hz_options_default",
     "hz_problem_create", "hz_problem_destroy", "hz_problem_ppw", "hz_problem_num_nodes",
     "hz_apply_block", "hz_apply_block_device", "hz_solver_create", "hz_solver_destroy",
-    "hz_solver_set_tolerance", "hz_solve_block", "hz_solve_block_device", "hz_solve_helmholtz",
-    "hz_cycle", "hz_cycle_device", "hz_coarse_solve", "hz_hierarchy_num_levels",
+    "hz_solver_set_tolerance", "hz_solve_block", "hz_solve_block_device", "hz_solve_block_device_stream",
+    "hz_solve_helmholtz", "hz_cycle", "hz_cycle_device", "hz_cycle_device_stream", "hz_coarse_solve", "hz_hierarchy_num_levels",
     "hz_hierarchy_level_dims", "hz_hierarchy_level_coefficients", "hz_sensitivity_accumulate",
     "hz_sensitivity_accumulate_device", "hz_kernel_launch_count", "hz_profile_begin",
     "hz_profile_end", "hz_profile_report", "hz_measure_fp64_peak", "hz_solve_blocks_multi", "hz_solve_blocks_multi_device", "hz_solver_set_slabs", "hz_solver_slab_info",
@@ -84,6 +84,8 @@ def lib():
         L.hz_block_gram_device.argtypes = [i64, i32, i32, vp, vp, vp]
         L.hz_block_add_scaled_device.argtypes = [i64, i32, i32, vp, vp, vp]
         L.hz_cycle_device.argtypes = [vp, i64, i32, vp, vp]
+        L.hz_cycle_device_stream.argtypes = [vp, i64, i32, vp, vp, vp]
+        L.hz_solve_block_device_stream.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report), vp]
         L.hz_coarse_solve.argtypes = [vp, i64, i32, vp, vp]
         L.hz_hierarchy_num_levels.argtypes = [vp, C.POINTER(i32)]
         L.hz_hierarchy_level_dims.argtypes = [vp, i32, vp]

@@ -202,6 +202,24 @@ void check_block(const Problem& p, int64_t n, int k) {
     throw HzError(kValidation, "helmholtz: n*k too large for one device block");
 }
 
+void require_converged(const Report& r, const char* what) {
+  for (char c : r.converged)
+    if (!c) throw HzError(kConvergence, what);
+}
+
+// The solver runs on its own non-blocking stream. Device entry points order
+// it after the caller's work on `stream` (nullptr: the legacy default
+// stream, which the plain *_device entry points assume), so a block the
+// caller wrote asynchronously is complete before the solve reads it.
+void order_after_caller(hz_solver* s, void* stream) {
+  cudaEvent_t ev = nullptr;
+  HZ_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  const cudaError_t e1 = cudaEventRecord(ev, stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy);
+  const cudaError_t e2 = e1 == cudaSuccess ? cudaStreamWaitEvent(s->stream, ev, 0) : e1;
+  cudaEventDestroy(ev);
+  HZ_CUDA(e2);
+}
+
 void fill_report(const Report& r, int k, hz_report* out) {
   if (!out) return;
   out->cycles = r.cycles;
@@ -798,11 +816,25 @@ int hz_solver_set_tolerance(hz_solver* s, double tol) {
   });
 }
 
+int hz_solve_block_device_stream(hz_solver* s, int64_t n, int k, const void* B, void* X, hz_report* rep,
+                                 void* stream) {
+  return guarded([&] {
+    if (!s || !B || !X) throw HzError(kValidation, "null argument");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    order_after_caller(s, stream);
+    Report r = run_solve(s, k, static_cast<const double2*>(B), static_cast<double2*>(X));
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+    fill_report(r, k, rep);
+  });
+}
+
 int hz_solve_block_device(hz_solver* s, int64_t n, int k, const void* B, void* X, hz_report* rep) {
   return guarded([&] {
     if (!s || !B || !X) throw HzError(kValidation, "null argument");
     check_block(*s->prob, n, k);
     DeviceGuard dg(s->prob->device);
+    order_after_caller(s, nullptr);
     Report r = run_solve(s, k, static_cast<const double2*>(B), static_cast<double2*>(X));
     HZ_CUDA(cudaStreamSynchronize(s->stream));
     fill_report(r, k, rep);
@@ -924,16 +956,35 @@ int hz_block_add_scaled_device(int64_t n, int k, int nb, const void* const* X, c
   });
 }
 
+// solve_helmholtz (src/helmholtz_solver.cpp:81-93): the convergence check runs
+// on the internal Report, so it holds whether or not the caller passes a
+// report (or its converged buffer).
 int hz_solve_helmholtz(hz_solver* s, int64_t n, int k, const double* B, double* X, hz_report* rep) {
-  int st = hz_solve_block(s, n, k, B, X, rep);
-  if (st != HZ_OK) return st;
-  if (rep && rep->converged)
-    for (int j = 0; j < k; ++j)
-      if (!rep->converged[j]) {
-        g_err = "helmholtz solve: tolerance not met within cycle cap";
-        return HZ_CONVERGENCE;
-      }
-  return HZ_OK;
+  return guarded([&] {
+    if (!s || !B || !X) throw HzError(kValidation, "null argument");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    s->ensure_blocks(k);
+    upload_rows(s, k, B, s->dB.get());
+    Report r = run_solve(s, k, s->dB.get(), s->dX.get());
+    download_rows(s, k, s->dX.get(), X);
+    fill_report(r, k, rep);
+    require_converged(r, "helmholtz solve: tolerance not met within cycle cap");
+  });
+}
+
+int hz_cycle_device_stream(hz_solver* s, int64_t n, int k, const void* b, void* x, void* stream) {
+  return guarded([&] {
+    if (!s || !b || !x) throw HzError(kValidation, "null argument");
+    if (s->dense) throw HzError(kState, "dense solver has no multigrid cycle");
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    order_after_caller(s, stream);
+    DevOp<double> op = make_op(s, k);
+    op.prec(static_cast<const double2*>(b), static_cast<double2*>(x), k, s->stream);
+    if (s->slabs) s->slabs->join();
+    HZ_CUDA(cudaStreamSynchronize(s->stream));
+  });
 }
 
 int hz_cycle_device(hz_solver* s, int64_t n, int k, const void* b, void* x) {
@@ -942,6 +993,7 @@ int hz_cycle_device(hz_solver* s, int64_t n, int k, const void* b, void* x) {
     if (s->dense) throw HzError(kState, "dense solver has no multigrid cycle");
     check_block(*s->prob, n, k);
     DeviceGuard dg(s->prob->device);
+    order_after_caller(s, nullptr);
     DevOp<double> op = make_op(s, k);
     op.prec(static_cast<const double2*>(b), static_cast<double2*>(x), k, s->stream);
     if (s->slabs) s->slabs->join();
@@ -1136,10 +1188,6 @@ int hz_fwi_sensitivity_rhs_device(hz_problem* p, int64_t n, int k, const void* U
 }
 
 namespace {
-void require_converged(const Report& r, const char* what) {
-  for (char c : r.converged)
-    if (!c) throw HzError(kConvergence, what);
-}
 // fwi_jacobian_vec (src/helmholtz_solver.cpp:113-125) for k stored fields at
 // once: D = P^T A^{-1} (-w^2 gf U v), one block solve
 void jacobian_vec(hz_solver* s, hz_sampling* smp, int k, const double2* U, const double* v, double2* D,

@@ -48,6 +48,47 @@ def allreduce_max(x: float, device=None) -> float:
     return float(t.item())
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def torchrun_argv(nproc: int, script: str, args: Sequence[str], port: Optional[int] = None) -> list:
+    """The single-node launch the driver uses for N > 1 (one process per GPU,
+    rendezvous on 127.0.0.1): python -m torch.distributed.run ... script args."""
+    import sys
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={int(nproc)}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port or free_port()), script, *args]
+
+
+def time_steps(step: Callable[[int], None], steps: int, barrier: Callable[[], None],
+               start: Callable[[], None], stop: Callable[[], float]) -> float:
+    """Time exactly `steps` calls of step(i), bracketed by barrier() on both
+    sides (barrier = process-group barrier + device synchronize). start() /
+    stop() are the rank-local clock (CUDA events on the launching stream in
+    bench.py); stop() runs after the closing barrier and returns the
+    elapsed milliseconds of this rank."""
+    barrier()
+    start()
+    for i in range(steps):
+        step(i)
+    barrier()
+    return float(stop())
+
+
+def whole_job_rate(units_per_rank_step: float, steps: int, t_ms_local: float, device=None):
+    """Whole-job throughput over all ranks: the max over ranks of the timed
+    region (the slowest rank ends the job) and value = units all ranks
+    processed / that time. Returns (value per second, max ms). Identity
+    reduction without an initialised process group."""
+    import torch.distributed as dist
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    t_ms = allreduce_max(t_ms_local, device=device)
+    return world * units_per_rank_step * steps / (t_ms / 1e3), t_ms
+
+
 @dataclasses.dataclass
 class GradientResult:
     gradient: object        # [n] float64 (torch tensor on the rank's device)

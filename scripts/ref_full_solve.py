@@ -1,0 +1,91 @@
+#!/usr/bin/env python
+"""Run the REFERENCE solver to convergence on the bench workload's first RHS
+block and commit the result as a golden fixture (TEST INFRASTRUCTURE).
+
+The reference's own block_fgmres (oracle/_ref, the unmodified reference
+sources compiled by oracle/Makefile; /root/reference/proj/core/src/krylov.cpp:178-280)
+driven through the SURVEY §3.3 composition -- build_hierarchy +
+MgHierarchy::cycle (V) + block_fgmres -- with exactly bench.py's WORKLOAD
+settings (6 levels, shift 0.9, w_J 0.6, FGMRES(5), tol 1e-6) on block 0
+(columns 0..7) of bench.build_workload(0, 1, 32). The reference has only a
+complex128 preconditioner; our bench runs a complex64 one, so the fixture pins
+(a) the reference's cycle count for the block (bench.py REF_CYCLES) and
+(b) the converged solution, sampled on the receiver (surface) row and on a
+strided node subset, against which tests/test_gpu_fullsize.py checks the GPU
+bench solve (c64 and c128 preconditioner) at 1e-5.
+
+  python scripts/ref_full_solve.py [--threads N] [--out tests/golden/cfg2_bench_block0.npz]
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import platform
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from oracle import ref  # noqa: E402
+
+SAMPLE_STRIDE = 997
+
+
+def sample_nodes(cfg) -> np.ndarray:
+    """Receiver row (the free surface z = 0: nodes 0..nx-1) + every
+    SAMPLE_STRIDE-th node of the grid."""
+    nx = int(cfg.n[0])
+    return np.unique(np.concatenate([np.arange(nx), np.arange(0, cfg.num_nodes, SAMPLE_STRIDE)])).astype(np.int64)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--threads", type=int, default=os.cpu_count())
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "cfg2_bench_block0.npz"))
+    args = ap.parse_args()
+
+    cfg = bench.build_workload(0, 1, bench.WORKLOAD["k"])
+    b = cfg.krylov_block
+    cols = slice(args.block * b, (args.block + 1) * b)
+    B = cfg.rhs_block(cols)
+    ref.set_num_threads(args.threads)
+    t0 = time.perf_counter()
+    R = ref.RefProblem.from_config(cfg)
+    H = ref.RefHierarchy(R, cfg.nlevels, cfg.shift)
+    setup_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    X, rep = ref.krylov_solve(R, H, B, method="fgmres", kind=cfg.cycle, pre=cfg.pre, post=cfg.post,
+                              wj=cfg.jacobi_weight, restart=cfg.restart, tol=cfg.tol,
+                              max_cycles=cfg.max_cycles)
+    solve_s = time.perf_counter() - t0
+    nodes = sample_nodes(cfg)
+    np.savez_compressed(
+        args.out, cycles=rep.cycles, col_cycles=np.asarray(rep.col_cycles), rel_residual=np.asarray(rep.rel_residual),
+        converged=np.asarray(rep.converged), history=np.asarray(rep.history), nodes=nodes, x_sample=X[nodes],
+        x_norm=np.linalg.norm(X, axis=0), source_nodes=np.asarray(cfg.source_nodes[cols]),
+        setup_s=setup_s, solve_s=solve_s, threads=args.threads, cpu=cpu_model(),
+        settings=str(dict(bench.WORKLOAD, block=args.block)))
+    print(f"reference block {args.block}: cycles {rep.cycles}, col_cycles {list(rep.col_cycles)}, "
+          f"max rel residual {np.max(rep.rel_residual):.3e}, converged {rep.all_converged()}, "
+          f"setup {setup_s:.1f} s, solve {solve_s:.1f} s ({solve_s / max(rep.cycles, 1):.3f} s/cycle) "
+          f"on {args.threads} threads ({cpu_model()}) -> {args.out}")
+
+
+if __name__ == "__main__":
+    main()

@@ -101,3 +101,56 @@ def test_allreduce_identity_without_process_group():
     t = torch.arange(4, dtype=torch.float64)
     assert torch.equal(parallel.allreduce_sum(t.clone()), t)
     assert parallel.allreduce_max(3.0) == 3.0
+
+
+def _timing_worker(rank, world, port, out):
+    """Each rank times 3 steps whose length depends on the rank; the job
+    time must be the slowest rank's and the rate count every rank's units."""
+    import time as _t
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    calls = []
+    clock = {}
+
+    def step(i):
+        calls.append(i)
+        _t.sleep(0.02 * (rank + 1))
+
+    def start():
+        clock["t0"] = _t.perf_counter()
+
+    def stop():
+        return 1e3 * (_t.perf_counter() - clock["t0"])
+
+    t_local = parallel.time_steps(step, 3, dist.barrier, start, stop)
+    value, t_max = parallel.whole_job_rate(8, 3, t_local)
+    out[rank] = (calls, t_local, value, t_max)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_bench_timing_world2_max_over_ranks():
+    """bench.py's timed region (parallel.time_steps + whole_job_rate): exactly
+    K steps per rank between barriers, max over ranks, whole-job value."""
+    world = 2
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_timing_worker, args=(world, port, out), nprocs=world, join=True)
+    t_max = max(out[r][1] for r in range(world))
+    for r in range(world):
+        calls, t_local, value, tm = out[r]
+        assert calls == [0, 1, 2]
+        assert tm == t_max  # every rank sees the same reduced time
+        assert value == pytest.approx(world * 8 * 3 / (t_max / 1e3))
+    # the closing barrier makes the fast rank wait for the slow one
+    assert out[0][1] >= 0.9 * 3 * 0.02 * world
+
+
+def test_torchrun_argv_single_node_loopback():
+    argv = parallel.torchrun_argv(4, "bench.py", ["--gpus", "4", "--steps", "2"], port=29555)
+    assert argv[1:4] == ["-m", "torch.distributed.run", "--nnodes=1"]
+    assert "--nproc-per-node=4" in argv
+    assert argv[argv.index("--master-addr") + 1] == "127.0.0.1"
+    assert argv[-5:] == ["bench.py", "--gpus", "4", "--steps", "2"]
