@@ -164,13 +164,36 @@ def config_json(cfg, world, l2_note):
 
 
 # ---------------------------------------------------------------- reference arm
-# Cycles the reference itself needs on this workload to reach 1e-6 (measured
-# with the full oracle solve, scripts/ref_full_solve.py; used to extrapolate
-# the bounded CPU samples when no GPU count is at hand).
-REF_CYCLES = None
+def ref_cycles_measured():
+    """Cycles the REFERENCE solver itself needs to reach 1e-6 on each RHS
+    block of this workload: its own block_fgmres run to convergence
+    (scripts/ref_full_solve.py -> tests/golden/cfg2_bench_block<b>.npz,
+    complex128 preconditioner, the blocking of our arm). Returns
+    ({block: cycles}, cpu model of the run)."""
+    import numpy as np
+    out, cpu = {}, None
+    for b in range(8):
+        f = os.path.join(ROOT, "tests", "golden", f"cfg2_bench_block{b}.npz")
+        if os.path.exists(f):
+            g = np.load(f)
+            out[b] = int(g["cycles"])
+            cpu = str(g["cpu"])
+    return out, cpu
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # GPU cycle count of this workload per 8-column block (mean over the 4
-# blocks; FGMRES(5), 6 levels, shift 0.9, w_J 0.6; scripts/sweep_rhs_block.py,
-# profiles/r01_sweep_rhs_block.jsonl).
+# blocks), the fallback when no reference count was measured for a block
 DEFAULT_CYCLES = 391
 
 
@@ -208,22 +231,39 @@ class ReferenceRunner:
                                        restart=cfg.restart, tol=cfg.tol, max_cycles=sample_cycles)
         return (time.perf_counter() - t0) / max(rep.cycles, 1), rep.cycles
 
-    def rhs_per_s(self, per_cycle, cycles_target):
-        return self.cfg.k / (self.nblocks * per_cycle * cycles_target)
+    def rhs_per_s(self, per_cycle, total_cycles):
+        """total_cycles: preconditioner cycles summed over all blocks"""
+        return self.cfg.k / (per_cycle * total_cycles)
 
-    def describe(self, sample_cycles, cycles_target):
+    def describe(self, sample_cycles, total_cycles, source):
         cfg = self.cfg
         return (f"{sample_cycles} FGMRES({cfg.restart}) iterations (V-cycle + Arnoldi + LS) per step of one "
                 f"{self.block}-column block of the workload ({self.nblocks} blocks) on the reference C++ solver "
-                f"(oracle/_ref, {self.threads} threads, c128 preconditioner), setup excluded; RHS/s = "
-                f"k / (blocks x s_per_cycle x {cycles_target:.0f} cycles to 1e-6)")
+                f"(oracle/_ref, {self.threads} threads of {cpu_model()}, c128 preconditioner -- the reference has "
+                f"no c64 path), setup excluded; RHS/s = k / (s_per_cycle x {total_cycles:.0f} cycles summed over "
+                f"the blocks, {source})")
 
 
-def reference_sample(cfg, cycles_target, sample_cycles, threads=None):
+def ref_total_cycles(nblocks, fallback_per_block):
+    """Cycles of a full reference solve of the workload: the measured
+    per-block counts, the fallback for blocks never measured."""
+    meas, cpu = ref_cycles_measured()
+    total = sum(meas.get(b, fallback_per_block) for b in range(nblocks))
+    n_meas = sum(1 for b in range(nblocks) if b in meas)
+    src = (f"reference-measured cycles for {n_meas}/{nblocks} blocks "
+           f"({', '.join(str(meas[b]) for b in range(nblocks) if b in meas)}; "
+           f"tests/golden/cfg2_bench_block*.npz, scripts/ref_full_solve.py on {cpu})")
+    if n_meas < nblocks:
+        src += f", {fallback_per_block:.0f} (GPU count) for the rest"
+    return total, src
+
+
+def reference_sample(cfg, gpu_cycles_per_block, sample_cycles, threads=None):
     run = ReferenceRunner(cfg, threads)
     per_cycle, _ = run.step(sample_cycles)
-    return run.rhs_per_s(per_cycle, cycles_target), {"cores": run.threads, "s_per_cycle": per_cycle,
-                                                     "sample": run.describe(sample_cycles, cycles_target)}
+    total, src = ref_total_cycles(run.nblocks, gpu_cycles_per_block)
+    return run.rhs_per_s(per_cycle, total), {"cores": run.threads, "s_per_cycle": per_cycle,
+                                             "sample": run.describe(sample_cycles, total, src)}
 
 
 def run_reference(args):
@@ -231,20 +271,29 @@ def run_reference(args):
     if ws > 1 and rank != 0:
         return 0
     cfg = build_workload(0, 1, WORKLOAD["k"])
-    cycles_target = args.ref_cycles or REF_CYCLES or DEFAULT_CYCLES
     run = ReferenceRunner(cfg)
-    vals = []
+    if args.ref_cycles:
+        total, src = args.ref_cycles * run.nblocks, f"{args.ref_cycles:.0f} cycles per block (--ref-cycles)"
+    else:
+        total, src = ref_total_cycles(run.nblocks, DEFAULT_CYCLES)
+    vals, walls = [], []
     for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         per_cycle, _ = run.step(args.ref_sample_cycles)
         if i >= args.warmup:
-            vals.append(run.rhs_per_s(per_cycle, cycles_target))
-    info = {"cores": run.threads, "sample": run.describe(args.ref_sample_cycles, cycles_target)}
+            walls.append(1e3 * (time.perf_counter() - t0))
+            vals.append(run.rhs_per_s(per_cycle, total))
+    info = {"cores": run.threads, "sample": run.describe(args.ref_sample_cycles, total, src)}
     value = statistics.mean(vals)
-    ms = 1e3 * cfg.k / value
+    # a step is the bounded sample (ms_per_step = its measured wall time);
+    # the full-solve time the value extrapolates to is reported beside it
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": statistics.mean(walls),
+            "ms_full_solve_extrapolated": 1e3 * cfg.k / value, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded, SURVEY §8d)",
-            "config": config_json(cfg, 1, "n/a (CPU)"), "impl": "reference",
+            "config": dict(config_json(cfg, 1, "n/a (CPU)"), precision="c128 Krylov / c128 preconditioner",
+                           cpu=cpu_model()),
+            "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": "reference",
                              "sample": info["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -426,6 +475,7 @@ def run_ours(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             v, info = reference_sample(cfg, statistics.mean(cycles), sample_cycles=args.cpu_sample_cycles)
+            info["sample"] += f"; host {cpu_model()}"
             line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": "reference",
                                     "sample": info["sample"]}
         except Exception as e:  # the baseline is reported, never required
@@ -450,7 +500,8 @@ def main():
     ap.add_argument("--cpu-sample-cycles", type=int, default=5,
                     help="FGMRES iterations of the cpu_baseline sample in our arm (one restart)")
     ap.add_argument("--ref-cycles", type=float, default=None,
-                    help="cycle count to extrapolate the reference sample to (default: the sample's own)")
+                    help="per-block cycle count to extrapolate the reference sample to (default: the reference's "
+                         "own measured counts, tests/golden/cfg2_bench_block*.npz)")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launched directly with --gpus N: become the torchrun launch the

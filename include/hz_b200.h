@@ -287,6 +287,54 @@ HZ_API int64_t hz_profile_trace(char* buf, int64_t cap);
    Gram / block-update kernels (MEASURED_PEAKS.json has no FP64 figure). */
 HZ_API int hz_measure_fp64_peak(double* tflops);
 
+
+/* ---- seistomo drop-in surface (include/hz_b200.hpp) ---- */
+
+/* CycleSpec (include/seistomo/multigrid.hpp:17-23) */
+typedef struct hz_cycle_spec {
+  int kind; /* hz_cycle_kind */
+  int pre;
+  int post;
+  double jacobi_weight;
+  int k_inner;
+} hz_cycle_spec;
+
+/* HelmholtzProblem::mass / gamma_factor (include/seistomo/helmholtz.hpp:33-38):
+ * n interleaved complex values, host copy */
+HZ_API int hz_problem_mass(const hz_problem* p, double* out);
+HZ_API int hz_problem_gamma_factor(const hz_problem* p, double* out);
+/* RegularGrid::nearest_node (src/grid.cpp:46-55) of the problem's grid placed
+ * at `origin` (NULL: 0): exact half-spacing ties go to the lower index */
+HZ_API int hz_problem_nearest_node(const hz_problem* p, const double origin[3], const double x[3], int64_t* node);
+/* HelmholtzProblem::point_source (src/helmholtz.cpp:124-132): q[n] (host,
+ * interleaved complex) = amplitude / prod(h) at nearest_node(x), 0 elsewhere;
+ * HZ_VALIDATION if x is outside the grid (RegularGrid::contains, src/grid.cpp:34-44) */
+HZ_API int hz_problem_point_source(const hz_problem* p, const double origin[3], const double x[3], double amp_re,
+                                   double amp_im, double* q);
+/* k point sources as one device block B[n][k] (column j: source at xyz[3j..],
+ * amplitude amp[2j], amp[2j+1]; amp NULL = 1), zero-filled + scattered on `stream` */
+HZ_API int hz_point_sources_device(hz_problem* p, const double origin[3], int k, const double* xyz,
+                                   const double* amp, void* B_dev, void* stream);
+/* HelmholtzProblem::to_csr(shift_factor) (src/helmholtz.cpp:102-122): CSR with
+ * int64 row pointers [n+1], int32 columns (ascending per row) and interleaved
+ * complex values. rp/ci/v NULL: *nnz receives the size only. */
+HZ_API int hz_problem_to_csr(const hz_problem* p, double shift_factor, int64_t* rp, int32_t* ci, double* v,
+                             int64_t cap, int64_t* nnz);
+/* fwi_sensitivity_rhs (src/helmholtz_solver.cpp:95-101) on host buffers */
+HZ_API int hz_fwi_sensitivity_rhs(hz_problem* p, int64_t n, int k, const double* U, const double* v, double* R);
+/* MgHierarchy::cycle(spec, b, x) (include/seistomo/multigrid.hpp:53-55): one
+ * cycle of the solver's c128 hierarchy updating x in place (x_zero != 0:
+ * x := 0 first, the preconditioner case) */
+HZ_API int hz_hierarchy_cycle(hz_solver* s, const hz_cycle_spec* spec, int64_t n, int k, const double* b,
+                              double* x, int x_zero);
+/* block_fgmres(op, B, restart, tol, max_cycles) (method 0, src/krylov.cpp:178-280)
+ * or block_bicgstab(op, B, tol, max_cycles) (method 1, src/krylov.cpp:60-176)
+ * with op = {HelmholtzProblem::apply_block, out := 0; MgHierarchy::cycle(spec)}
+ * (the SURVEY §3.3 composition) on the solver's hierarchy, one block over
+ * all k columns. Non-convergence is reported, not an error. */
+HZ_API int hz_block_krylov(hz_solver* s, int method, const hz_cycle_spec* spec, int restart, double tol,
+                           int max_cycles, int64_t n, int k, const double* B, double* X, hz_report* rep);
+
 #ifdef __cplusplus
 }
 #endif

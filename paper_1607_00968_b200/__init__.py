@@ -336,7 +336,8 @@ class HelmholtzProblem:
     5-point (2D) / 7-point (3D), truncated (Dirichlet) boundary rows."""
 
     def __init__(self, ndim: int, n: Sequence[int], h: Sequence[float], m, omega: float,
-                 gamma: AttenuationField, allow_coarse_ppw: bool = False, device: int = 0):
+                 gamma: AttenuationField, allow_coarse_ppw: bool = False, device: int = 0,
+                 origin: Sequence[float] = (0.0, 0.0, 0.0)):
         n3 = list(n) + [1] * (3 - len(n))
         h3 = list(h) + [1.0] * (3 - len(h))
         self.ndim = int(ndim)
@@ -347,6 +348,7 @@ class HelmholtzProblem:
         self.omega = float(omega)
         self.num_nodes = self.n[0] * self.n[1] * self.n[2]
         self.device = int(device)
+        self.origin = tuple(float(x) for x in (list(origin) + [0.0] * (3 - len(origin)))[:3])
         m = np.ascontiguousarray(m, dtype=np.float64).reshape(-1)
         ramp = np.ascontiguousarray(gamma.ramp, dtype=np.float64).reshape(-1)
         if m.size != self.num_nodes or ramp.size != self.num_nodes:
@@ -382,8 +384,9 @@ class HelmholtzProblem:
 
     def gamma_factor(self) -> np.ndarray:
         """(1 - i gamma/omega) per node (HelmholtzProblem::gamma_factor)."""
-        gam = self.gamma.base + self.omega * self.gamma.ramp
-        return 1.0 - 1j * (gam / self.omega)
+        out = np.empty(self.num_nodes, np.complex128)
+        _check(_native.lib().hz_problem_gamma_factor(self._h, out.ctypes.data))
+        return out
 
     def apply_block(self, u):
         """v = A u (HelmholtzProblem::apply_block, src/helmholtz.cpp:71-100)."""
@@ -401,25 +404,69 @@ class HelmholtzProblem:
                                             out.ctypes.data))
         return out
 
+    def _xyz(self, x) -> np.ndarray:
+        xx = np.zeros(3, np.float64)
+        xx[:len(x)] = np.asarray(x, dtype=np.float64)
+        return xx
+
+    def nearest_node(self, x: Sequence[float]) -> int:
+        """RegularGrid::nearest_node (src/grid.cpp:46-55) on this grid at
+        `origin`: exact half-spacing ties go to the lower index."""
+        node = C.c_int64()
+        o = np.ascontiguousarray(self.origin, np.float64)
+        _check(_native.lib().hz_problem_nearest_node(self._h, o.ctypes.data, self._xyz(x).ctypes.data,
+                                                     C.byref(node)))
+        return int(node.value)
+
     def point_source(self, x: Sequence[float], amplitude: complex = 1.0) -> np.ndarray:
         """FV point source amp/prod(h) at the nearest node, ties to the lower
-        index (HelmholtzProblem::point_source, src/helmholtz.cpp:124-132;
-        RegularGrid::nearest_node, src/grid.cpp:46-55)."""
-        c = [0, 0, 0]
-        cell = 1.0
-        for a in range(self.ndim):
-            f = float(x[a]) / self.h[a]
-            lo, hi = -1e-9, (self.n[a] - 1) + 1e-9
-            if f < lo or f > hi:
-                raise ValidationError("point_source: position outside grid")
-            i = int(np.floor(f + 0.5))
-            if float(i) - f == 0.5:
-                i -= 1
-            c[a] = min(max(i, 0), self.n[a] - 1)
-            cell *= self.h[a]
-        q = np.zeros(self.num_nodes, dtype=np.complex128)
-        q[c[0] + self.n[0] * (c[1] + self.n[1] * c[2])] = amplitude / cell
+        index (HelmholtzProblem::point_source, src/helmholtz.cpp:124-132);
+        ValidationError outside the grid (RegularGrid::contains)."""
+        q = np.empty(self.num_nodes, dtype=np.complex128)
+        o = np.ascontiguousarray(self.origin, np.float64)
+        a = complex(amplitude)
+        _check(_native.lib().hz_problem_point_source(self._h, o.ctypes.data, self._xyz(x).ctypes.data, a.real,
+                                                     a.imag, q.ctypes.data))
         return q
+
+    def point_sources(self, xs, amplitudes=None):
+        """k point sources as one device block [n][k] (complex128 CUDA tensor,
+        column j = point_source(xs[j], amplitudes[j])), zero-filled and
+        scattered on the GPU (hz_point_sources_device)."""
+        import torch
+        xs = np.asarray(xs, dtype=np.float64)
+        k = xs.shape[0]
+        xyz = np.zeros((k, 3), np.float64)
+        xyz[:, :xs.shape[1]] = xs
+        amp = None
+        if amplitudes is not None:
+            amp = np.ascontiguousarray(np.asarray(amplitudes, dtype=np.complex128).reshape(k))
+        B = torch.empty((self.num_nodes, k), dtype=torch.complex128, device=f"cuda:{self.device}")
+        o = np.ascontiguousarray(self.origin, np.float64)
+        stream = torch.cuda.current_stream(B.device).cuda_stream
+        _check(_native.lib().hz_point_sources_device(self._h, o.ctypes.data, k, xyz.ctypes.data,
+                                                     None if amp is None else amp.ctypes.data, B.data_ptr(),
+                                                     stream))
+        return B
+
+    def mass(self) -> np.ndarray:
+        """omega^2 (1 - i gamma/omega) m per node (HelmholtzProblem::mass)."""
+        out = np.empty(self.num_nodes, np.complex128)
+        _check(_native.lib().hz_problem_mass(self._h, out.ctypes.data))
+        return out
+
+    def to_csr(self, shift_factor: float = 0.0):
+        """HelmholtzProblem::to_csr (src/helmholtz.cpp:102-122) as
+        (row_ptr int64, col int32, values complex128)."""
+        nnz = C.c_int64()
+        L = _native.lib()
+        _check(L.hz_problem_to_csr(self._h, float(shift_factor), None, None, None, 0, C.byref(nnz)))
+        rp = np.empty(self.num_nodes + 1, np.int64)
+        ci = np.empty(nnz.value, np.int32)
+        v = np.empty(nnz.value, np.complex128)
+        _check(L.hz_problem_to_csr(self._h, float(shift_factor), rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                   nnz.value, C.byref(nnz)))
+        return rp, ci, v
 
 
 _METHODS = {"MgBicgstab": 0, "MgFgmresW": 1, "MgFgmresK": 2, "DenseLuSmall": 3, "MgFgmres": 4,

@@ -29,7 +29,15 @@ EXPORTS = (
     "hz_fwi_sensitivity_rhs_device", "hz_fwi_jacobian_vec", "hz_fwi_jacobian_vec_device",
     "hz_fwi_jacobian_transpose_vec", "hz_fwi_jacobian_transpose_vec_device", "hz_compact16_device",
     "hz_solve_helmholtz_compact16", "hz_compact16", "hz_block_gram_device", "hz_block_add_scaled_device", "hz_profile_trace",
+    "hz_problem_mass", "hz_problem_gamma_factor", "hz_problem_nearest_node", "hz_problem_point_source",
+    "hz_point_sources_device", "hz_problem_to_csr", "hz_fwi_sensitivity_rhs", "hz_hierarchy_cycle",
+    "hz_block_krylov",
 )
+
+
+class hz_cycle_spec(C.Structure):
+    _fields_ = [("kind", C.c_int), ("pre", C.c_int), ("post", C.c_int), ("jacobi_weight", C.c_double),
+                ("k_inner", C.c_int)]
 
 
 class hz_options(C.Structure):
@@ -85,6 +93,16 @@ def lib():
         L.hz_block_add_scaled_device.argtypes = [i64, i32, i32, vp, vp, vp]
         L.hz_cycle_device.argtypes = [vp, i64, i32, vp, vp]
         L.hz_cycle_device_stream.argtypes = [vp, i64, i32, vp, vp, vp]
+        L.hz_problem_mass.argtypes = [vp, vp]
+        L.hz_problem_gamma_factor.argtypes = [vp, vp]
+        L.hz_problem_nearest_node.argtypes = [vp, vp, vp, C.POINTER(i64)]
+        L.hz_problem_point_source.argtypes = [vp, vp, vp, dbl, dbl, vp]
+        L.hz_point_sources_device.argtypes = [vp, vp, i32, vp, vp, vp, vp]
+        L.hz_problem_to_csr.argtypes = [vp, dbl, vp, vp, vp, i64, C.POINTER(i64)]
+        L.hz_fwi_sensitivity_rhs.argtypes = [vp, i64, i32, vp, vp, vp]
+        L.hz_hierarchy_cycle.argtypes = [vp, C.POINTER(hz_cycle_spec), i64, i32, vp, vp, i32]
+        L.hz_block_krylov.argtypes = [vp, i32, C.POINTER(hz_cycle_spec), i32, dbl, i32, i64, i32, vp, vp,
+                                      C.POINTER(hz_report)]
         L.hz_solve_block_device_stream.argtypes = [vp, i64, i32, vp, vp, C.POINTER(hz_report), vp]
         L.hz_coarse_solve.argtypes = [vp, i64, i32, vp, vp]
         L.hz_hierarchy_num_levels.argtypes = [vp, C.POINTER(i32)]

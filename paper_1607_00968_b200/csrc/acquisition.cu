@@ -258,4 +258,33 @@ Sampling::Sampling(int ndim, const int64_t* n3, const double* h3, const double* 
   upd(d_tw, tw);
 }
 
+namespace {
+constexpr int kMaxPointSources = 64;
+struct PointSources {
+  int64_t node[kMaxPointSources];
+  double2 val[kMaxPointSources];
+};
+// one thread per source column (K15: k nonzeros per block)
+__global__ void point_sources_kernel(int c, int ld, PointSources ps, double2* __restrict__ B) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < c) B[ps.node[j] * ld + j] = ps.val[j];
+}
+}  // namespace
+
+void launch_point_sources(int k, const int64_t* nodes, const double2* vals, double2* B, cudaStream_t st) {
+  for (int j0 = 0; j0 < k; j0 += kMaxPointSources) {
+    // columns [j0, j0 + c) of the [n][k] block: view it as a block whose
+    // column j0 is at B + j0 (same row stride k)
+    const int c = std::min(kMaxPointSources, k - j0);
+    PointSources ps;
+    for (int j = 0; j < c; ++j) {
+      ps.node[j] = nodes[j0 + j];
+      ps.val[j] = vals[j0 + j];
+    }
+    ProfScope prof("point_sources", double(c) * 16, st);
+    point_sources_kernel<<<1, kMaxPointSources, 0, st>>>(c, k, ps, B + j0);
+    HZ_LAUNCH_CHECK();
+  }
+}
+
 }  // namespace hz

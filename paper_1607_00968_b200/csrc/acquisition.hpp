@@ -39,4 +39,7 @@ void launch_colmax(int64_t n, int k, const double2* X, double* part, int nslots,
 // Q[c][i] = packed (half re, half im) of X[i][c] * inv_scale[c]   (Compact16)
 void launch_quantize16(int64_t n, int k, const double2* X, const double* inv_scale, uint32_t* Q, cudaStream_t st);
 
+// B[node_j][j] = val_j for j < k (B already zeroed)      (point_source, batched)
+void launch_point_sources(int k, const int64_t* nodes, const double2* vals, double2* B, cudaStream_t st);
+
 }  // namespace hz

@@ -2,6 +2,7 @@
 // classes to status codes and owns the device-side state behind the opaque
 // hz_problem / hz_solver handles.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <exception>
 #include <cstring>
@@ -1356,6 +1357,235 @@ int hz_solve_helmholtz_compact16(hz_solver* s, int64_t n, int k, const double* B
     s->fQ.ensure(size_t(n) * k);
     compact16(n, k, s->dX.get(), s->fQ.get(), scales, s->fpart, s->fmax, s->stream);
     HZ_CUDA(cudaMemcpy(Q, s->fQ.get(), sizeof(uint32_t) * n * k, cudaMemcpyDeviceToHost));
+  });
+}
+
+
+// ---------------------------------------------------------------- drop-in surface
+// (include/hz_b200.hpp's seistomo-compatible classes; reference file:line
+// next to each)
+
+int hz_problem_mass(const hz_problem* p, double* out) {
+  return guarded([&] {
+    if (!p || !out) throw HzError(kValidation, "null argument");
+    std::memcpy(out, p->p->mass.data(), p->p->mass.size() * sizeof(cplx));
+  });
+}
+
+int hz_problem_gamma_factor(const hz_problem* p, double* out) {
+  return guarded([&] {
+    if (!p || !out) throw HzError(kValidation, "null argument");
+    std::memcpy(out, p->p->gamma_factor.data(), p->p->gamma_factor.size() * sizeof(cplx));
+  });
+}
+
+}  // extern "C"
+
+namespace {
+// RegularGrid::contains / nearest_node (src/grid.cpp:34-55) on the problem's
+// grid placed at `origin`
+bool grid_contains(const Problem& P, const double* origin, const double* x) {
+  const double eps = 1e-9;
+  for (int a = 0; a < P.ndim; ++a) {
+    const double lo = origin[a] - eps * P.h[a];
+    const double hi = origin[a] + double(P.n[a] - 1) * P.h[a] + eps * P.h[a];
+    if (x[a] < lo || x[a] > hi) return false;
+  }
+  return true;
+}
+int64_t grid_nearest(const Problem& P, const double* origin, const double* x) {
+  int64_t c[3] = {0, 0, 0};
+  for (int a = 0; a < P.ndim; ++a) {
+    const double f = (x[a] - origin[a]) / P.h[a];
+    int64_t i = static_cast<int64_t>(std::floor(f + 0.5));
+    if (static_cast<double>(i) - f == 0.5) --i;  // exact tie: toward the lower index
+    c[a] = std::clamp<int64_t>(i, 0, P.n[a] - 1);
+  }
+  return c[0] + P.n[0] * (c[1] + P.n[1] * c[2]);
+}
+// HelmholtzProblem::point_source (src/helmholtz.cpp:124-132): node + amplitude / prod(h)
+std::pair<int64_t, cplx> point_source_entry(const Problem& P, const double* origin, const double* x, cplx amp) {
+  if (!grid_contains(P, origin, x)) throw HzError(kValidation, "point_source: position outside grid");
+  double cell = 1.0;
+  for (int a = 0; a < P.ndim; ++a) cell *= P.h[a];
+  return {grid_nearest(P, origin, x), amp / cell};
+}
+const double kZeroOrigin[3] = {0.0, 0.0, 0.0};
+}  // namespace
+
+extern "C" {
+
+int hz_problem_nearest_node(const hz_problem* p, const double origin[3], const double x[3], int64_t* node) {
+  return guarded([&] {
+    if (!p || !x || !node) throw HzError(kValidation, "null argument");
+    *node = grid_nearest(*p->p, origin ? origin : kZeroOrigin, x);
+  });
+}
+
+int hz_problem_point_source(const hz_problem* p, const double origin[3], const double x[3], double amp_re,
+                            double amp_im, double* q) {
+  return guarded([&] {
+    if (!p || !x || !q) throw HzError(kValidation, "null argument");
+    const auto e = point_source_entry(*p->p, origin ? origin : kZeroOrigin, x, cplx(amp_re, amp_im));
+    std::memset(q, 0, size_t(p->p->num_nodes()) * sizeof(cplx));
+    reinterpret_cast<cplx*>(q)[e.first] = e.second;
+  });
+}
+
+int hz_point_sources_device(hz_problem* p, const double origin[3], int k, const double* xyz, const double* amp,
+                            void* B, void* stream) {
+  return guarded([&] {
+    if (!p || !xyz || !B) throw HzError(kValidation, "null argument");
+    check_block(*p->p, p->p->num_nodes(), k);
+    std::vector<int64_t> nodes(k);
+    std::vector<double2> vals(k);
+    for (int j = 0; j < k; ++j) {
+      const cplx a = amp ? cplx(amp[2 * j], amp[2 * j + 1]) : cplx(1.0, 0.0);
+      const auto e = point_source_entry(*p->p, origin ? origin : kZeroOrigin, xyz + 3 * j, a);
+      nodes[j] = e.first;
+      vals[j] = make_double2(e.second.real(), e.second.imag());
+    }
+    DeviceGuard dg(p->p->device);
+    auto st = static_cast<cudaStream_t>(stream);
+    HZ_CUDA(cudaMemsetAsync(B, 0, size_t(p->p->num_nodes()) * k * sizeof(double2), st));
+    launch_point_sources(k, nodes.data(), vals.data(), static_cast<double2*>(B), st);
+  });
+}
+
+// HelmholtzProblem::to_csr (src/helmholtz.cpp:102-122): rows in node order,
+// columns ascending (CsrBuilder), nnz = 5/7 per interior row
+int hz_problem_to_csr(const hz_problem* p, double shift, int64_t* rp, int32_t* ci, double* v, int64_t cap,
+                      int64_t* nnz) {
+  return guarded([&] {
+    if (!p || !nnz) throw HzError(kValidation, "null argument");
+    const Problem& P = *p->p;
+    const int64_t n0 = P.n[0], n1 = P.n[1], n2 = P.n[2], s1 = n0, s2 = n0 * n1;
+    int64_t cnt = 0;
+    for (int a = 0; a < 3; ++a) cnt += P.n[a] > 1 ? 2 * (P.n[a] - 1) * (P.num_nodes() / P.n[a]) : 0;
+    cnt += P.num_nodes();
+    *nnz = cnt;
+    if (!rp || !ci || !v) return;  // size query
+    if (cap < cnt) throw HzError(kValidation, "to_csr: output capacity below nnz");
+    if (P.num_nodes() > int64_t(INT32_MAX)) throw HzError(kValidation, "to_csr: int32 column indices overflow");
+    const auto c = P.shifted_center(shift);
+    auto* vv = reinterpret_cast<cplx*>(v);
+    int64_t e = 0;
+    rp[0] = 0;
+    for (int64_t kz = 0; kz < n2; ++kz)
+      for (int64_t j = 0; j < n1; ++j)
+        for (int64_t i = 0; i < n0; ++i) {
+          const int64_t idx = i + n0 * (j + n1 * kz);
+          auto put = [&](int64_t col, cplx val) {
+            ci[e] = int32_t(col);
+            vv[e] = val;
+            ++e;
+          };
+          if (kz > 0) put(idx - s2, P.inv_h2[2]);
+          if (j > 0) put(idx - s1, P.inv_h2[1]);
+          if (i > 0) put(idx - 1, P.inv_h2[0]);
+          put(idx, c[idx]);
+          if (i + 1 < n0) put(idx + 1, P.inv_h2[0]);
+          if (j + 1 < n1) put(idx + s1, P.inv_h2[1]);
+          if (kz + 1 < n2) put(idx + s2, P.inv_h2[2]);
+          rp[idx + 1] = e;
+        }
+  });
+}
+
+int hz_fwi_sensitivity_rhs(hz_problem* p, int64_t n, int k, const double* U, const double* v, double* R) {
+  return guarded([&] {
+    if (!p || !U || !v || !R) throw HzError(kValidation, "null argument");
+    check_block(*p->p, n, k);
+    DeviceGuard dg(p->p->device);
+    DevBuf<double2> dU(size_t(n) * k), dR(size_t(n) * k);
+    DevBuf<double> dv{size_t(n)};
+    HZ_CUDA(cudaMemcpy(dU.get(), U, dU.bytes(), cudaMemcpyHostToDevice));
+    HZ_CUDA(cudaMemcpy(dv.get(), v, dv.bytes(), cudaMemcpyHostToDevice));
+    launch_sens_rhs(n, k, p->p->omega * p->p->omega, p->p->d_gf.get(), dU.get(), dv.get(), dR.get(), nullptr);
+    HZ_CUDA(cudaMemcpy(R, dR.get(), dR.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"
+
+namespace {
+CycleSpec spec_from(const hz_cycle_spec* c) {
+  if (!c) throw HzError(kValidation, "null cycle spec");
+  if (c->kind < 0 || c->kind > 2) throw HzError(kValidation, "cycle: unknown kind");
+  if (c->pre < 0 || c->post < 0 || c->k_inner < 1) throw HzError(kValidation, "cycle: bad sweep counts");
+  CycleSpec sp;
+  sp.kind = static_cast<CycleKind>(c->kind);
+  sp.pre = c->pre;
+  sp.post = c->post;
+  sp.jacobi_weight = c->jacobi_weight;
+  sp.k_inner = c->k_inner;
+  return sp;
+}
+// run f with the solver's cycle spec / Krylov settings temporarily replaced
+template <class F>
+void with_settings(hz_solver* s, const CycleSpec& sp, bool bicg, int restart, double tol, int max_cycles, F&& f) {
+  const CycleSpec sp0 = s->spec;
+  const bool b0 = s->bicgstab;
+  const hz_options o0 = s->opts;
+  s->spec = sp;
+  s->bicgstab = bicg;
+  s->opts.fgmres_restart = restart;
+  s->opts.tol = tol;
+  s->opts.max_cycles = max_cycles;
+  s->opts.rhs_block = 0;  // one block over all columns, as block_fgmres
+  try {
+    f();
+  } catch (...) {
+    s->spec = sp0;
+    s->bicgstab = b0;
+    s->opts = o0;
+    throw;
+  }
+  s->spec = sp0;
+  s->bicgstab = b0;
+  s->opts = o0;
+}
+}  // namespace
+
+extern "C" {
+
+int hz_hierarchy_cycle(hz_solver* s, const hz_cycle_spec* spec, int64_t n, int k, const double* b, double* x,
+                       int x_zero) {
+  return guarded([&] {
+    if (!s || !b || !x) throw HzError(kValidation, "null argument");
+    if (s->dense || !s->h64) throw HzError(kState, "solver has no multigrid hierarchy");
+    if (s->slabs) throw HzError(kState, "hz_hierarchy_cycle: not in slab mode");
+    const CycleSpec sp = spec_from(spec);
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    s->ensure_blocks(k);
+    upload_rows(s, k, b, s->dB.get());
+    if (x_zero)
+      HZ_CUDA(cudaMemsetAsync(s->dX.get(), 0, size_t(n) * k * sizeof(double2), s->stream));
+    else
+      upload_rows(s, k, x, s->dX.get());
+    s->h64->cycle(sp, k, s->dB.get(), s->dX.get(), x_zero != 0, s->stream);
+    download_rows(s, k, s->dX.get(), x);
+  });
+}
+
+int hz_block_krylov(hz_solver* s, int method, const hz_cycle_spec* spec, int restart, double tol, int max_cycles,
+                    int64_t n, int k, const double* B, double* X, hz_report* rep) {
+  return guarded([&] {
+    if (!s || !B || !X) throw HzError(kValidation, "null argument");
+    if (s->dense || !s->h64) throw HzError(kState, "solver has no multigrid hierarchy");
+    if (method != 0 && method != 1) throw HzError(kValidation, "block_krylov: method 0 (FGMRES) or 1 (BiCGSTAB)");
+    if (method == 0 && restart < 1) throw HzError(kValidation, "fgmres: restart must be positive");
+    const CycleSpec sp = spec_from(spec);
+    check_block(*s->prob, n, k);
+    DeviceGuard dg(s->prob->device);
+    with_settings(s, sp, method == 1, restart, tol, max_cycles, [&] {
+      s->ensure_blocks(k);
+      upload_rows(s, k, B, s->dB.get());
+      Report r = run_solve(s, k, s->dB.get(), s->dX.get());
+      download_rows(s, k, s->dX.get(), X);
+      fill_report(r, k, rep);
+    });
   });
 }
 

@@ -25,7 +25,7 @@ int main() {
   const std::int64_t n = g.num_nodes();
   SlownessSquaredModel m{g, Field(n, 0.25)};
   const double omega = 2 * M_PI * 2.0 / 10.0 * (1 - 1e-9);
-  AttenuationField a{g, 0.01 * omega, Field(n, 0.0)};
+  AttenuationField a{g, 0.01 * omega, {}, Field(n, 0.0)};
   auto prob = std::make_shared<HelmholtzProblem>(m, omega, a);
   HelmholtzSolveOptions o;  // reference defaults: MgBicgstab, W-cycle, 3 levels, shift 0.2
   HelmholtzSolver solver(prob, o);

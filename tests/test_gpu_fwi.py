@@ -190,7 +190,7 @@ int main(int argc, char** argv) {
   const std::int64_t n = g.num_nodes();
   SlownessSquaredModel m{g, Field(n, 0.25)};
   const double omega = 2 * M_PI * 2.0 / 10.0 * (1 - 1e-9);
-  AttenuationField a{g, 0.01 * omega, Field(n, 0.0)};
+  AttenuationField a{g, 0.01 * omega, {}, Field(n, 0.0)};
   auto prob = std::make_shared<HelmholtzProblem>(m, omega, a);
   HelmholtzSolveOptions o;
   HelmholtzSolver solver(prob, o);
