@@ -33,6 +33,7 @@
 
 #include "kernels.hpp"
 #include "profile.hpp"
+#include "tma.cuh"
 
 namespace hz {
 
@@ -471,6 +472,501 @@ fused_post_kernel(LevelOp<T> op, LevelGeom gc, T wj, const cplx_t<T>* __restrict
   cpa_wait<0>();
 }
 
+
+// ---------------------------------------------------------------------------
+// k = 8 complex64 variants with bulk-copy (TMA) row staging and one barrier
+// per streamed row.
+//
+// A CTA owns a strip of NT fine nodes (halo 4 per side, so every staged row
+// starts 16-byte aligned) and all 8 RHS columns; 4 threads per node, each one
+// 16-byte unit (2 complex64 columns). Thread 0 streams each fine row of the
+// strip (right-hand side b, the node's (centre, D^{-1}) record, and for the
+// post kernel the pre-smoothed iterate and the coarse correction rows) into
+// a PD-deep ring of shared-memory slots with cp.async.bulk, completing on one
+// mbarrier per slot; the copies of the next rows are in flight while the
+// current ones are computed.
+//
+// The stages of the temporal blocking are skewed by two rows so that every
+// stage of step j reads only rows published before the step's single
+// __syncthreads (pre: x1 row j, x2 row j-2, r row j-4, restriction of row
+// j-5; post: x3 row j, x4 row j-2, result row j-4); rings hold 4 rows (2
+// for r). Nodes outside the grid hold exact zeros in every ring, so the
+// stencils need no boundary predicates: a skipped neighbour term of the
+// unfused kernels and an added w * (+0) give the same bits (the running sum
+// starts at +0 and can never be -0), and the fused results stay bitwise
+// equal to the unfused sequence.
+constexpr int kK8 = 8;
+
+template <class In, int NT, int PD>
+struct PreK8Plan {
+  static constexpr int TH = NT * 4, W = NT - 8;
+  static constexpr size_t BROW = size_t(NT) * kK8 * sizeof(In);   // staged b row
+  static constexpr size_t CROW = size_t(NT) * 2 * sizeof(float2);  // staged (centre, D^-1) row
+  static constexpr size_t SLOT = BROW + CROW;
+  static constexpr size_t RROW = size_t(NT) * kK8 * sizeof(float2);  // one ring row
+  static constexpr size_t OFF_SLOTS = 128;  // PD mbarriers first
+  static constexpr size_t OFF_X1 = OFF_SLOTS + PD * SLOT;
+  static constexpr size_t OFF_X2 = OFF_X1 + 4 * RROW;
+  static constexpr size_t OFF_R = OFF_X2 + 4 * RROW;
+  static constexpr size_t BYTES = OFF_R + 2 * RROW + 128;  // + slack: edge threads read one unit past a ring row
+};
+
+__device__ __forceinline__ float4 u2f4(const Unit<float, 2>& u) { return make_float4(u.v[0].x, u.v[0].y, u.v[1].x, u.v[1].y); }
+__device__ __forceinline__ Unit<float, 2> f42u(const float4& a) {
+  Unit<float, 2> u;
+  u.v[0] = make_float2(a.x, a.y);
+  u.v[1] = make_float2(a.z, a.w);
+  return u;
+}
+
+// (A u)[centre] for one 16-byte unit (2 columns): y-neighbours and centre
+// from the thread's registers, x-neighbours from the ring row (units t -+ 4),
+// every neighbour present (zero-padded), Csr::mul_block order
+__device__ __forceinline__ void ax8r(const float4& um, const float4& u0, const float4& up, const float4* r0, int t,
+                                     float2 c, float wx, float wy, float2 (&a)[2]) {
+  const float4 uxm = r0[t - 4], uxp = r0[t + 4];
+  const float2 ums[2] = {make_float2(um.x, um.y), make_float2(um.z, um.w)};
+  const float2 uxms[2] = {make_float2(uxm.x, uxm.y), make_float2(uxm.z, uxm.w)};
+  const float2 u0s[2] = {make_float2(u0.x, u0.y), make_float2(u0.z, u0.w)};
+  const float2 uxps[2] = {make_float2(uxp.x, uxp.y), make_float2(uxp.z, uxp.w)};
+  const float2 ups[2] = {make_float2(up.x, up.y), make_float2(up.z, up.w)};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    float2 acc = czero<float2>();
+    acc = crfma(wy, ums[q], acc);
+    acc = crfma(wx, uxms[q], acc);
+    acc = cfma(c, u0s[q], acc);
+    acc = crfma(wx, uxps[q], acc);
+    acc = crfma(wy, ups[q], acc);
+    a[q] = acc;
+  }
+}
+
+template <int S>
+using Step = std::integral_constant<int, S>;
+
+// restriction of one r row (restrict_kernel order: ey, then ex ascending;
+// zero weights skipped), as in fused_pre_kernel
+__device__ __forceinline__ void restrict_row(int y, int n1, int CY0, int CY1, int64_t rcbase, int64_t rcstride,
+                                             bool rxm, bool rxp, const Unit<float, 2>& rvm,
+                                             const Unit<float, 2>& rv0, const Unit<float, 2>& rvp, float2 (&acc)[2],
+                                             float2* __restrict__ rc) {
+  const float h = 0.5f, one = 1.0f;
+  if (y & 1) {
+    const int J = (y - 1) >> 1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      float2 a = acc[q];
+      if (rxm) a = crfma(h * h, rvm.v[q], a);
+      a = crfma(one * h, rv0.v[q], a);
+      if (rxp) a = crfma(h * h, rvp.v[q], a);
+      acc[q] = a;
+    }
+    if (J >= CY0 && J < CY1) gstore(rc + rcbase + rcstride * J, acc);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      float2 a = czero<float2>();
+      if (rxm) a = crfma(h * h, rvm.v[q], a);
+      a = crfma(one * h, rv0.v[q], a);
+      if (rxp) a = crfma(h * h, rvp.v[q], a);
+      acc[q] = a;
+    }
+  } else {
+    const int J = y >> 1;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      float2 a = acc[q];
+      if (rxm) a = crfma(h * one, rvm.v[q], a);
+      a = crfma(one * one, rv0.v[q], a);
+      if (rxp) a = crfma(h * one, rvp.v[q], a);
+      acc[q] = a;
+    }
+    if (y == n1 - 1 && J >= CY0 && J < CY1) gstore(rc + rcbase + rcstride * J, acc);
+  }
+}
+
+// Steps are unrolled by 4: with rows counted from the first step, every
+// ring row, staging slot and register FIFO entry of a step is a compile-time
+// constant. A thread keeps its own node's rows of every intermediate in
+// registers; the shared-memory rings exist only for the x-neighbours' reads
+// of the centre row (shared-memory wavefronts, not DRAM, bound these kernels:
+// profiles/r02_k8_fused.txt). Stage order D, C, B, A: stage C reads the b /
+// centre FIFO entries of row j-4 before stage A refills them with row j.
+template <class In, int NT, int PD, int MINB>
+__global__ void __launch_bounds__(NT * 4, MINB)
+fused_pre_k8_kernel(LevelOp<float> op, LevelGeom gc, float wj, const In* __restrict__ b, float2* __restrict__ x2out,
+                    float2* __restrict__ rc, int crows) {
+  static_assert(PD == 2 || PD == 4, "staging depth must divide the 4-step unroll");
+  using P = PreK8Plan<In, NT, PD>;
+  constexpr int W = P::W, TC = W / 2, TH = P::TH;
+  constexpr int RU = NT * 4;  // float4 units per ring row
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  float4* x1s = reinterpret_cast<float4*>(sm + P::OFF_X1);
+  float4* x2s = reinterpret_cast<float4*>(sm + P::OFF_X2);
+  float4* rs = reinterpret_cast<float4*>(sm + P::OFF_R);
+  const int n0 = int(op.g.n0), n1 = int(op.g.n1);
+  const int t = threadIdx.x, xs = t >> 2, cg = t & 3;
+  const int CX0 = blockIdx.x * TC, X0 = 2 * CX0, gx0 = X0 - 4, gx = gx0 + xs;
+  const int CY0 = blockIdx.y * crows, CY1 = min(CY0 + crows, int(gc.n1));
+  const int Y0 = 2 * CY0, Y1 = 2 * CY1;
+  const int sa = max(0, -gx0), sb = min(NT, n0 - gx0);  // in-grid strip nodes [sa, sb)
+  const bool inx = xs >= sa && xs < sb;
+  const bool own_x = inx && xs >= 4 && xs < 4 + W;
+  const int64_t x2base = int64_t(gx) * kK8 + cg * 2, x2stride = int64_t(n0) * kK8;
+  const float wx = op.w[0], wy = op.w[1];
+  // restriction units (coarse node ci, column pair rcg): 4 * TC of them,
+  // spread evenly over the warps so that no warp carries the stage alone
+  constexpr int NW = TH / 32, RPW = (4 * TC + NW - 1) / NW;
+  static_assert(RPW <= 32, "one restriction unit per thread");
+  const int lane = t & 31, ru = (t >> 5) * RPW + lane;
+  const int ci = ru >> 2, rcg = ru & 3, I = CX0 + ci;
+  const bool rest = lane < RPW && ru < 4 * TC && I < int(gc.n0);
+  const int rt = (2 * ci + 4) * 4 + rcg;
+  const bool rxm = 2 * I - 1 >= 0, rxp = 2 * I + 1 < n0;
+  const int64_t rcbase = int64_t(I) * kK8 + rcg * 2, rcstride = int64_t(gc.n0) * kK8;
+
+  const int jbeg = Y0 - 3;                                     // first step (x1 row)
+  const int jA0 = max(jbeg, 0), jA1 = min(Y1 + 1, n1 - 1);     // x1 rows loaded
+  const int yB0 = max(Y0 - 2, 0), yB1 = min(Y1, n1 - 1);       // x2 rows
+  const int yC0 = max(Y0 - 1, 0), yC1 = min(Y1 - 1, n1 - 1);   // r rows (and restriction)
+  const int nsteps = ((yC1 + 5 - jbeg + 1) + 3) & ~3;
+
+  // zero the rings and the out-of-grid part of every staging slot, init barriers
+  for (int i = t; i < int((P::BYTES - P::OFF_X1) / 16); i += TH)
+    reinterpret_cast<float4*>(sm + P::OFF_X1)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!inx) {
+#pragma unroll
+    for (int p = 0; p < PD; ++p) {
+      unsigned char* slot = sm + P::OFF_SLOTS + p * P::SLOT;
+      float4* bz = reinterpret_cast<float4*>(slot) + t * (sizeof(In) / 8);
+#pragma unroll
+      for (int v = 0; v < int(sizeof(In) / 8); ++v) bz[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cg == 0) reinterpret_cast<float4*>(slot + P::BROW)[xs] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (t == 0) {
+#pragma unroll
+    for (int p = 0; p < PD; ++p) tma::mbar_init(&bars[p], 1);
+    tma::fence_mbar_init();
+  }
+  tma::fence_proxy_async();
+  __syncthreads();
+  const uint32_t nb = uint32_t(sb - sa);
+  // row r = jbeg + u goes to slot u % PD; rows above the grid only advance
+  // the slot's phase, rows past jA1 are never staged (nor waited for)
+  auto produce = [&](int r) {
+    if (r > jA1) return;
+    const int u = r - jbeg, sl = u % PD;
+    if (r < jA0) {
+      tma::mbar_arrive_expect_tx(&bars[sl], 0);
+      return;
+    }
+    tma::fence_proxy_async();
+    unsigned char* slot = sm + P::OFF_SLOTS + sl * P::SLOT;
+    const int64_t node0 = int64_t(n0) * r + gx0 + sa;
+    tma::mbar_arrive_expect_tx(&bars[sl], nb * uint32_t(kK8 * sizeof(In) + 2 * sizeof(float2)));
+    tma::bulk_g2s(slot + size_t(sa) * kK8 * sizeof(In), b + node0 * kK8, nb * uint32_t(kK8 * sizeof(In)), &bars[sl]);
+    tma::bulk_g2s(slot + P::BROW + size_t(sa) * 16, op.cd + 2 * node0, nb * 16u, &bars[sl]);
+  };
+  if (t == 0)
+#pragma unroll
+    for (int p = 0; p < PD; ++p) produce(jbeg + p);
+
+  // register FIFOs indexed by row mod 4 (relative to jbeg)
+  float2 bq[4][2], cq[4], dq[4];
+  float4 x1q[4], x2q[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    bq[r][0] = bq[r][1] = czero<float2>();
+    cq[r] = dq[r] = czero<float2>();
+    x1q[r] = x2q[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float2 acc[2] = {czero<float2>(), czero<float2>()};
+
+  auto step = [&](auto S_, int j, uint32_t parity) {
+    constexpr int S = decltype(S_)::value;  // (j - jbeg) mod 4
+    constexpr int A = S, B = (S + 2) & 3, C = S, D1 = (S + 3) & 1, SL = S % PD;
+    if (t == 0 && j > jbeg) produce(j - 1 + PD);  // the slot of row j-1 was released by the last barrier
+    // (D) restriction of r row y = j-5
+    {
+      const int y = j - 5;
+      if (rest && y >= yC0 && y <= yC1) {
+        const float4* rr = rs + D1 * RU;
+        const Unit<float, 2> rv0 = f42u(rr[rt]);
+        const Unit<float, 2> rvm = rxm ? f42u(rr[rt - 4]) : rv0, rvp = rxp ? f42u(rr[rt + 4]) : rv0;
+        restrict_row(y, n1, CY0, CY1, rcbase, rcstride, rxm, rxp, rvm, rv0, rvp, acc, rc);
+      }
+    }
+    // (C) r row y = j-4 = b - A x2 (x2 rows j-5, j-4, j-3 in x2q)
+    {
+      const int y = j - 4;
+      if (y >= yC0 && y <= yC1) {
+        float2 a[2];
+        ax8r(x2q[(S + 3) & 3], x2q[S], x2q[(S + 1) & 3], x2s + S * RU, t, cq[C], wx, wy, a);
+        rs[(S & 1) * RU + t] = make_float4(bq[C][0].x - a[0].x, bq[C][0].y - a[0].y, bq[C][1].x - a[1].x,
+                                           bq[C][1].y - a[1].y);
+      }
+    }
+    // (B) x2 row y = j-2 = x1 + wD^-1 (b - A x1) (x1 rows j-3, j-2, j-1 in x1q)
+    {
+      const int y = j - 2;
+      float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (y >= yB0 && y <= yB1) {
+        float2 a[2];
+        ax8r(x1q[(S + 1) & 3], x1q[B], x1q[(S + 3) & 3], x1s + B * RU, t, cq[B], wx, wy, a);
+        const Unit<float, 2> x1 = f42u(x1q[B]);
+        Unit<float, 2> o;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) o.v[q] = cadd(x1.v[q], cmul(dq[B], csub(bq[B][q], a[q])));
+        // out-of-grid nodes: x1 = 0, wD^-1 = 0 and b = 0 give +0 exactly
+        o4 = u2f4(o);
+        if (own_x && y >= Y0 && y < Y1) gstore(x2out + x2base + x2stride * y, o.v);
+      }
+      x2q[B] = o4;
+      x2s[B * RU + t] = o4;
+    }
+    // (A) x1 row j = wD^-1 b (zero for rows / nodes not in the grid)
+    {
+      float4 x1v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j >= jA0 && j <= jA1) {
+        tma::mbar_wait(&bars[SL], parity);
+        const unsigned char* slot = sm + P::OFF_SLOTS + SL * P::SLOT;
+        const In* bs = reinterpret_cast<const In*>(slot) + 2 * t;
+        bq[A][0] = ccast<float2>(bs[0]);
+        bq[A][1] = ccast<float2>(bs[1]);
+        const float4 cdv = reinterpret_cast<const float4*>(slot + P::BROW)[xs];
+        cq[A] = make_float2(cdv.x, cdv.y);
+        dq[A] = make_float2(wj * cdv.z, wj * cdv.w);
+        Unit<float, 2> x1;
+        x1.v[0] = cmul(dq[A], bq[A][0]);
+        x1.v[1] = cmul(dq[A], bq[A][1]);
+        x1v = u2f4(x1);
+      } else {
+        bq[A][0] = bq[A][1] = czero<float2>();
+        cq[A] = dq[A] = czero<float2>();
+      }
+      x1q[A] = x1v;
+      x1s[A * RU + t] = x1v;
+    }
+    __syncthreads();
+  };
+  for (int m = 0; 4 * m < nsteps; ++m) {
+    const int j = jbeg + 4 * m;
+    // fills of a staging slot alternate parity: slot S % PD is filled for the
+    // ((4m + S) / PD)-th time at step 4m + S
+    step(Step<0>{}, j, uint32_t(((4 * m + 0) / PD) & 1));
+    step(Step<1>{}, j + 1, uint32_t(((4 * m + 1) / PD) & 1));
+    step(Step<2>{}, j + 2, uint32_t(((4 * m + 2) / PD) & 1));
+    step(Step<3>{}, j + 3, uint32_t(((4 * m + 3) / PD) & 1));
+  }
+}
+
+template <class In, int NT, int PD>
+struct PostK8Plan {
+  static constexpr int TH = NT * 4, W = NT - 4, NCN = NT / 2 + 1, CS = 4;
+  static constexpr size_t XROW = size_t(NT) * kK8 * sizeof(float2);  // staged x2 row
+  static constexpr size_t BROW = size_t(NT) * kK8 * sizeof(In);
+  static constexpr size_t CROW = size_t(NT) * 2 * sizeof(float2);
+  static constexpr size_t SLOT = XROW + BROW + CROW;
+  static constexpr size_t EROW = size_t(NCN) * kK8 * sizeof(float2);  // staged coarse row
+  static constexpr size_t RROW = size_t(NT) * kK8 * sizeof(float2);
+  static constexpr size_t OFF_SLOTS = 128;  // PD + CS mbarriers first
+  static constexpr size_t OFF_E = OFF_SLOTS + PD * SLOT;
+  static constexpr size_t OFF_X3 = OFF_E + CS * EROW;
+  static constexpr size_t OFF_X4 = OFF_X3 + 4 * RROW;
+  static constexpr size_t BYTES = OFF_X4 + 4 * RROW + 128;  // + slack: edge threads read one unit past a ring row
+};
+
+// Post-smoothing of a zero-start visit, k = 8 complex64: x3 = x2 + P ec,
+// x4 = x3 + wD^-1 (b - A x3), out = (Out)(x4 + wD^-1 (b - A x4)). Same step
+// structure as fused_pre_k8_kernel (stages C, B, A).
+template <class In, class Out, int NT, int PD, int MINB>
+__global__ void __launch_bounds__(NT * 4, MINB)
+fused_post_k8_kernel(LevelOp<float> op, LevelGeom gc, float wj, const float2* __restrict__ x2,
+                     const float2* __restrict__ ec, const In* __restrict__ b, Out* __restrict__ out, int frows) {
+  static_assert(PD == 2 || PD == 4, "staging depth must divide the 4-step unroll");
+  using P = PostK8Plan<In, NT, PD>;
+  constexpr int W = P::W, NCN = P::NCN, CS = P::CS, TH = P::TH;
+  constexpr int RU = NT * 4;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);  // [PD] fine rows, [CS] coarse rows
+  uint64_t* cbars = bars + PD;
+  float4* x3s = reinterpret_cast<float4*>(sm + P::OFF_X3);
+  float4* x4s = reinterpret_cast<float4*>(sm + P::OFF_X4);
+  const int n0 = int(op.g.n0), n1 = int(op.g.n1), c0n = int(gc.n0), c1n = int(gc.n1);
+  const int t = threadIdx.x, xs = t >> 2, cg = t & 3;
+  const int X0 = blockIdx.x * W, gx0 = X0 - 2, gx = gx0 + xs;
+  const int Y0 = blockIdx.y * frows, Y1 = min(Y0 + frows, n1);
+  const int sa = max(0, -gx0), sb = min(NT, n0 - gx0);
+  const bool inx = xs >= sa && xs < sb;
+  const bool own_x = inx && xs >= 2 && xs < 2 + W;
+  const int64_t obase = int64_t(gx) * kK8 + cg * 2, ostride = int64_t(n0) * kK8;
+  const int cxa = (X0 >> 1) - 1;  // coarse nodes of the strip: [cxa, cxa + NCN), in grid [ca, cb)
+  const int ca = max(0, -cxa), cb = min(NCN, c0n - cxa);
+  // prolongation parents along i (prolong_v4_kernel) as strip coarse units
+  const int p0 = ((gx >> 1) - cxa) * 4 + cg, p1 = (((gx + 1) >> 1) - cxa) * 4 + cg;
+  const float wx0 = (gx & 1) ? 0.5f : 1.0f, wx1 = (gx & 1) ? 0.5f : 0.0f;
+  const float wx = op.w[0], wy = op.w[1];
+
+  const int jbeg = Y0 - 2;                                   // first step (x3 row)
+  const int jA0 = max(jbeg, 0), jA1 = min(Y1 + 1, n1 - 1);   // x3 rows (staged fine rows)
+  const int yB0 = max(Y0 - 1, 0), yB1 = min(Y1, n1 - 1);     // x4 rows
+  const int Jc0 = jA0 >> 1, Jc1 = min((jA1 + 1) >> 1, c1n - 1);  // coarse rows
+  const int nsteps = ((Y1 + 3 - jbeg + 1) + 3) & ~3;
+
+  for (int i = t; i < int((P::BYTES - P::OFF_X3) / 16); i += TH)
+    reinterpret_cast<float4*>(sm + P::OFF_X3)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!inx) {
+#pragma unroll
+    for (int p = 0; p < PD; ++p) {
+      unsigned char* slot = sm + P::OFF_SLOTS + p * P::SLOT;
+      reinterpret_cast<float4*>(slot)[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4* bz = reinterpret_cast<float4*>(slot + P::XROW) + t * (sizeof(In) / 8);
+#pragma unroll
+      for (int v = 0; v < int(sizeof(In) / 8); ++v) bz[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (cg == 0) reinterpret_cast<float4*>(slot + P::XROW + P::BROW)[xs] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  for (int i = t; i < CS * NCN * 4; i += TH) {
+    const int cn = (i >> 2) % NCN;
+    if (cn < ca || cn >= cb) reinterpret_cast<float4*>(sm + P::OFF_E)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  if (t == 0) {
+#pragma unroll
+    for (int p = 0; p < PD + CS; ++p) tma::mbar_init(&bars[p], 1);
+    tma::fence_mbar_init();
+  }
+  tma::fence_proxy_async();
+  __syncthreads();
+  const uint32_t nb = uint32_t(sb - sa), ncb = uint32_t(max(cb - ca, 0));
+  int next_c = Jc0;  // next coarse row to stage (thread 0)
+  auto issue_coarse = [&](int J) {
+    const int u = J - Jc0, sl = u & (CS - 1);
+    unsigned char* dst = sm + P::OFF_E + sl * P::EROW + size_t(ca) * kK8 * sizeof(float2);
+    tma::mbar_arrive_expect_tx(&cbars[sl], ncb * uint32_t(kK8 * sizeof(float2)));
+    tma::bulk_g2s(dst, ec + (int64_t(c0n) * J + cxa + ca) * kK8, ncb * uint32_t(kK8 * sizeof(float2)), &cbars[sl]);
+  };
+  auto produce = [&](int r) {
+    if (r > jA1) return;
+    const int u = r - jbeg, sl = u % PD;
+    if (r < jA0) {
+      tma::mbar_arrive_expect_tx(&bars[sl], 0);
+      return;
+    }
+    tma::fence_proxy_async();
+    unsigned char* slot = sm + P::OFF_SLOTS + sl * P::SLOT;
+    const int64_t node0 = int64_t(n0) * r + gx0 + sa;
+    tma::mbar_arrive_expect_tx(&bars[sl], nb * uint32_t(kK8 * (sizeof(float2) + sizeof(In)) + 2 * sizeof(float2)));
+    tma::bulk_g2s(slot + size_t(sa) * kK8 * sizeof(float2), x2 + node0 * kK8, nb * uint32_t(kK8 * sizeof(float2)),
+                  &bars[sl]);
+    tma::bulk_g2s(slot + P::XROW + size_t(sa) * kK8 * sizeof(In), b + node0 * kK8, nb * uint32_t(kK8 * sizeof(In)),
+                  &bars[sl]);
+    tma::bulk_g2s(slot + P::XROW + P::BROW + size_t(sa) * 16, op.cd + 2 * node0, nb * 16u, &bars[sl]);
+    for (; next_c <= min((r + 1) >> 1, Jc1); ++next_c) issue_coarse(next_c);
+  };
+  if (t == 0)
+#pragma unroll
+    for (int p = 0; p < PD; ++p) produce(jbeg + p);
+
+  float2 bq[4][2], cq[4], dq[4];
+  float4 x3q[4], x4q[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    bq[r][0] = bq[r][1] = czero<float2>();
+    cq[r] = dq[r] = czero<float2>();
+    x3q[r] = x4q[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+
+  auto step = [&](auto S_, int j, uint32_t parity) {
+    constexpr int S = decltype(S_)::value;  // (j - jbeg) mod 4
+    constexpr int A = S, B = (S + 2) & 3, C = S, SL = S % PD;
+    if (t == 0 && j > jbeg) produce(j - 1 + PD);
+    // (C) result row y = j-4 (x4 rows j-5, j-4, j-3 in x4q)
+    {
+      const int y = j - 4;
+      if (own_x && y >= Y0 && y < Y1) {
+        float2 a[2];
+        ax8r(x4q[(S + 3) & 3], x4q[S], x4q[(S + 1) & 3], x4s + S * RU, t, cq[C], wx, wy, a);
+        const Unit<float, 2> x4 = f42u(x4q[S]);
+        Out w[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) w[q] = ccast<Out>(cadd(x4.v[q], cmul(dq[C], csub(bq[C][q], a[q]))));
+        gstore(out + obase + ostride * y, w);
+      }
+    }
+    // (B) x4 row y = j-2 (x3 rows j-3, j-2, j-1 in x3q)
+    {
+      const int y = j - 2;
+      float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (y >= yB0 && y <= yB1) {
+        float2 a[2];
+        ax8r(x3q[(S + 1) & 3], x3q[B], x3q[(S + 3) & 3], x3s + B * RU, t, cq[B], wx, wy, a);
+        const Unit<float, 2> x3 = f42u(x3q[B]);
+        Unit<float, 2> o;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) o.v[q] = cadd(x3.v[q], cmul(dq[B], csub(bq[B][q], a[q])));
+        o4 = u2f4(o);
+      }
+      x4q[B] = o4;
+      x4s[B * RU + t] = o4;
+    }
+    // (A) x3 row j = x2 + P ec (zero for rows / nodes not in the grid)
+    {
+      float4 x3v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j >= jA0 && j <= jA1) {
+        tma::mbar_wait(&bars[SL], parity);
+        const int J0 = j >> 1, J1 = (j + 1) >> 1;
+        tma::mbar_wait(&cbars[(J0 - Jc0) & (CS - 1)], uint32_t(((J0 - Jc0) >> 2) & 1));
+        if (J1 != J0) tma::mbar_wait(&cbars[(J1 - Jc0) & (CS - 1)], uint32_t(((J1 - Jc0) >> 2) & 1));
+        const unsigned char* slot = sm + P::OFF_SLOTS + SL * P::SLOT;
+        const In* bs = reinterpret_cast<const In*>(slot + P::XROW) + 2 * t;
+        bq[A][0] = ccast<float2>(bs[0]);
+        bq[A][1] = ccast<float2>(bs[1]);
+        const float4 cdv = reinterpret_cast<const float4*>(slot + P::XROW + P::BROW)[xs];
+        cq[A] = make_float2(cdv.x, cdv.y);
+        dq[A] = make_float2(wj * cdv.z, wj * cdv.w);
+        const float4* er0 = reinterpret_cast<const float4*>(sm + P::OFF_E + ((J0 - Jc0) & (CS - 1)) * P::EROW);
+        const float4* er1 = reinterpret_cast<const float4*>(sm + P::OFF_E + ((J1 - Jc0) & (CS - 1)) * P::EROW);
+        const float wy0 = (j & 1) ? 0.5f : 1.0f, wy1 = (j & 1) ? 0.5f : 0.0f;
+        const float w00 = wx0 * wy0 * 1.0f, w01 = wx1 * wy0 * 1.0f, w10 = wx0 * wy1 * 1.0f, w11 = wx1 * wy1 * 1.0f;
+        const Unit<float, 2> xr = f42u(reinterpret_cast<const float4*>(slot)[t]);
+        const Unit<float, 2> e00 = f42u(er0[p0]), e01 = f42u(er0[p1]);
+        Unit<float, 2> e10 = e00, e11 = e01;
+        if (j & 1) {
+          e10 = f42u(er1[p0]);
+          e11 = f42u(er1[p1]);
+        }
+        Unit<float, 2> x3;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          // parents in (y, x) ascending order, zero weights skipped
+          float2 corr = czero<float2>();
+          corr = crfma(w00, e00.v[q], corr);
+          if (w01 != 0.0f) corr = crfma(w01, e01.v[q], corr);
+          if (w10 != 0.0f) corr = crfma(w10, e10.v[q], corr);
+          if (w11 != 0.0f) corr = crfma(w11, e11.v[q], corr);
+          x3.v[q] = cadd(xr.v[q], corr);
+        }
+        if (inx) x3v = u2f4(x3);
+      } else {
+        bq[A][0] = bq[A][1] = czero<float2>();
+        cq[A] = dq[A] = czero<float2>();
+      }
+      x3q[A] = x3v;
+      x3s[A * RU + t] = x3v;
+    }
+    __syncthreads();
+  };
+  for (int m = 0; 4 * m < nsteps; ++m) {
+    const int j = jbeg + 4 * m;
+    step(Step<0>{}, j, uint32_t(((4 * m + 0) / PD) & 1));
+    step(Step<1>{}, j + 1, uint32_t(((4 * m + 1) / PD) & 1));
+    step(Step<2>{}, j + 2, uint32_t(((4 * m + 2) / PD) & 1));
+    step(Step<3>{}, j + 3, uint32_t(((4 * m + 3) / PD) & 1));
+  }
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -508,6 +1004,68 @@ void run_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_
   auto kern = fused_post_kernel<T, In, Out, kTPN, NT, kPD, (MINB * P::TH > 2048 ? 2048 / P::TH : MINB), QU>;
   allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
   kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, x2, ec, b, out, frows);
+}
+
+// ---- k = 8 complex64 bulk-copy kernels: launch geometry
+#ifndef HZ_K8_NT
+#define HZ_K8_NT 64  // strip width (fine nodes) of the k = 8 kernels: 4 x NT threads per CTA
+#endif
+#ifndef HZ_K8_MINB
+#define HZ_K8_MINB 2  // resident CTAs per SM the register budget is sized for (3 spills)
+#endif
+#ifndef HZ_K8_PD
+#define HZ_K8_PD 4  // staged rows in flight per CTA (2 or 4)
+#endif
+
+template <size_t BYTES, int TH>
+constexpr int k8_blocks_per_sm() {
+  return int(std::min<size_t>(std::min<size_t>((227 * 1024) / (BYTES + 1024), 2048 / TH), 8));
+}
+
+// rows per chunk so that the strips x chunks tiles fill the resident CTA
+// slots of the GPU about once (every tile pays a pipeline fill of a few rows)
+int k8_chunk_rows(int strips, int rows, int per_sm, const char* env) {
+  const int e = env_int(env, 0);
+  if (e > 0) return e;
+  const int slots = std::max(1, kNumSMs * per_sm);
+  const int chunks = std::max(1, slots / std::max(1, strips));
+  return std::max(4, (rows + chunks - 1) / chunks);
+}
+
+template <class In>
+void run_fused_pre_k8(const LevelOp<float>& op, const LevelGeom& gc, float wj, const In* b, float2* x2, float2* rc,
+                      cudaStream_t s) {
+  constexpr int NT = HZ_K8_NT, PD = HZ_K8_PD;
+  using P = PreK8Plan<In, NT, PD>;
+  constexpr int MINB = HZ_K8_MINB;
+  constexpr int TC = P::W / 2;
+  const int strips = int((gc.n0 + TC - 1) / TC);
+  const int crows = k8_chunk_rows(strips, int(gc.n1), std::min(MINB, k8_blocks_per_sm<P::BYTES, P::TH>()),
+                                  "HZ_K8_PRE_ROWS");
+  const dim3 grid(unsigned(strips), unsigned((gc.n1 + crows - 1) / crows));
+  auto kern = fused_pre_k8_kernel<In, NT, PD, MINB>;
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
+  kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, b, x2, rc, crows);
+}
+
+template <class In, class Out>
+void run_fused_post_k8(const LevelOp<float>& op, const LevelGeom& gc, float wj, const float2* x2, const float2* ec,
+                       const In* b, Out* out, cudaStream_t s) {
+  constexpr int NT = HZ_K8_NT, PD = HZ_K8_PD;
+  using P = PostK8Plan<In, NT, PD>;
+  constexpr int MINB = HZ_K8_MINB;
+  const int strips = int((op.g.n0 + P::W - 1) / P::W);
+  const int frows = 2 * k8_chunk_rows(strips, int(gc.n1), std::min(MINB, k8_blocks_per_sm<P::BYTES, P::TH>()),
+                                      "HZ_K8_POST_CROWS");
+  const dim3 grid(unsigned(strips), unsigned((op.g.n1 + frows - 1) / frows));
+  auto kern = fused_post_k8_kernel<In, Out, NT, PD, MINB>;
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
+  kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, x2, ec, b, out, frows);
+}
+
+bool k8_enabled(int k, const void* cd) {
+  static const int env = env_int("HZ_FUSED_K8", 1);
+  return env != 0 && k == kK8 && cd != nullptr;
 }
 
 // strip width in fine nodes: HZ_FUSED_NT = 32, 64 or 128; default 64, and
@@ -552,6 +1110,13 @@ void launch_fused_pre(const LevelOp<T>& op, const LevelGeom& gc, T wj, const In*
   const double n = double(op.g.nodes), nc = double(gc.nodes), k = op.g.k, s_ = sizeof(cplx_t<T>);
   ProfScope prof(sizeof(T) == 8 ? "fused_pre_fine_c128" : "fused_pre_fine_c64",
                  n * (k * (sizeof(In) + s_) + 2.0 * s_) + nc * k * s_, s);
+  if constexpr (std::is_same<T, float>::value) {
+    if (k8_enabled(int(op.g.k), op.cd)) {
+      run_fused_pre_k8<In>(op, gc, wj, b, x2, rc, s);
+      HZ_LAUNCH_CHECK();
+      return;
+    }
+  }
   if (fused_wide<T>(int(op.g.k))) {
     constexpr int QW = 2 * cpt<T>();
     const int nt = fused_nt(int(op.g.k), kTPN * QW);
@@ -578,6 +1143,13 @@ void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cp
   const double n = double(op.g.nodes), nc = double(gc.nodes), k = op.g.k, s_ = sizeof(cplx_t<T>);
   ProfScope prof(sizeof(T) == 8 ? "fused_post_fine_c128" : "fused_post_fine_c64",
                  n * (k * (s_ + sizeof(In) + sizeof(Out)) + 2.0 * s_) + nc * k * s_, s);
+  if constexpr (std::is_same<T, float>::value) {
+    if (k8_enabled(int(op.g.k), op.cd)) {
+      run_fused_post_k8<In, Out>(op, gc, wj, x2, ec, b, out, s);
+      HZ_LAUNCH_CHECK();
+      return;
+    }
+  }
   if (fused_wide<T>(int(op.g.k))) {
     constexpr int QW = 2 * cpt<T>();
     const int nt = fused_nt(int(op.g.k), kTPN * QW);

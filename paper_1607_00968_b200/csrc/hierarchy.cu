@@ -332,6 +332,16 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
     cast(a.center, b.center);
     cast(a.coef, b.coef);
     cast(a.inv_diag, b.inv_diag);
+    if (b.kind == kFine && b.center.size()) {
+      // (centre, D^{-1}) per node in one 16-byte record: a row of the fine
+      // grid is then one 16-byte-aligned bulk copy whatever n0's parity
+      const size_t nn = b.center.size();
+      b.cd.alloc(2 * nn);
+      HZ_CUDA(cudaMemcpy2DAsync(b.cd.get(), 2 * sizeof(float2), b.center.get(), sizeof(float2), sizeof(float2), nn,
+                                cudaMemcpyDeviceToDevice, s));
+      HZ_CUDA(cudaMemcpy2DAsync(b.cd.get() + 1, 2 * sizeof(float2), b.inv_diag.get(), sizeof(float2),
+                                sizeof(float2), nn, cudaMemcpyDeviceToDevice, s));
+    }
   }
   auto cast_all = [&](const DevBuf<double2>& src, DevBuf<float2>& dst) {
     if (!src.size()) return;
@@ -356,6 +366,7 @@ LevelOp<T> Hierarchy<T>::op(int l, int k) const {
   o.center = L.center.get();
   o.coef = L.coef.get();
   o.inv_diag = L.inv_diag.get();
+  o.cd = L.cd.get();
   for (int a = 0; a < 3; ++a) o.w[a] = L.w[a];
   o.level = l;
   return o;
@@ -426,6 +437,7 @@ std::unique_ptr<Hierarchy<T>> Hierarchy<T>::share() const {
     alias(A.center, B.center);
     alias(A.coef, B.coef);
     alias(A.inv_diag, B.inv_diag);
+    alias(A.cd, B.cd);
   }
   alias(ainvT_, H->ainvT_);
   alias(bt_ET_, H->bt_ET_);

@@ -25,6 +25,7 @@ struct LevelOp {
   const V* center = nullptr;   // kFine: diagonal (centre) per node
   const V* coef = nullptr;     // kStencil: [S][nodes]
   const V* inv_diag = nullptr; // Jacobi D^{-1} per node
+  const V* cd = nullptr;       // optional: (centre, D^{-1}) interleaved per node (kFine)
   T w[3] = {0, 0, 0};          // kFine off-diagonal weights (0 on flat axes)
   int level = 0;               // multigrid level (profiling names only)
 };

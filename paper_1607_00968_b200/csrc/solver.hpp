@@ -70,6 +70,7 @@ struct MgLevelDev {
   DevBuf<V> center;    // level 0: shifted centre
   DevBuf<V> coef;      // levels >= 1: [S][n] Galerkin planes
   DevBuf<V> inv_diag;  // D^{-1}
+  DevBuf<V> cd;        // level 0 of the c64 hierarchy: (centre, D^{-1}) interleaved per node (fused k = 8 kernels)
   T w[3] = {0, 0, 0};
   int64_t nodes() const { return dims[0] * dims[1] * dims[2]; }
 };

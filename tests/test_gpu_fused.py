@@ -50,6 +50,11 @@ CASES = [
     (257, 129, 4, 4, "c128", "V"),
     (297, 161, 2, 3, "c128", "W"),
     (65, 41, 6, 3, "c128", "V"),
+    # k = 8 bulk-copy kernels: odd widths / heights against strips of 56 / 60
+    # owned nodes and the row chunks, a grid narrower than one strip
+    (301, 97, 8, 3, "c64", "W"),
+    (65, 49, 8, 3, "c64", "V"),
+    (121, 233, 8, 4, "c64", "V"),
 ]
 
 
@@ -70,6 +75,18 @@ def test_fused_vcycle_bitwise_equals_unfused(nx, nz, k, nl, prec, kind):
         # product into FMAs differently in the two kernels (last-bit
         # differences; the reference parity bar is 1e-12)
         assert rel_err(fused, plain) <= 1e-14
+
+
+@pytest.mark.parametrize("nx,nz,nl,chunk", [(257, 129, 4, "0"), (1025, 513, 5, "0"), (301, 97, 3, "5"), (121, 233, 4, "3")])
+def test_k8_bulk_copy_kernels_equal_streaming_kernels(nx, nz, nl, chunk):
+    """k = 8: the bulk-copy (TMA) fused kernels against the cp.async
+    streaming kernels they replace (HZ_FUSED_K8=0), bitwise, including
+    forced short row chunks (HZ_K8_PRE_ROWS / HZ_K8_POST_CROWS)."""
+    extra = {} if chunk == "0" else {"HZ_K8_PRE_ROWS": chunk, "HZ_K8_POST_CROWS": chunk}
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(CYCLE, os.path.join(d, "n.npy"), "1", nx, nz, 8, nl, "c64", "V", **extra)
+        old = _run(CYCLE, os.path.join(d, "o.npy"), "1", nx, nz, 8, nl, "c64", "V", HZ_FUSED_K8="0")
+    assert np.array_equal(new, old), f"max rel diff {rel_err(new, old):.3e}"
 
 
 def test_fused_c128_cycle_matches_reference():
