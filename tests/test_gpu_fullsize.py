@@ -87,21 +87,22 @@ GOLDEN_BLOCK0 = __import__("os").path.join(__import__("os").path.dirname(__impor
                                            "golden", "cfg2_bench_block0.npz")
 
 
-@pytest.mark.parametrize("precond", ["c64", "c128"])
-def test_config2_bench_block0_matches_reference_full_solve(precond):
-    """Block 0 of the bench workload (8 sources, FGMRES(5) + V(2,2), 6
+@pytest.mark.parametrize("block,precond", [(0, "c64"), (0, "c128"), (1, "c64"), (2, "c64"), (3, "c64")])
+def test_config2_bench_block_matches_reference_full_solve(block, precond):
+    """Blocks of the bench workload (8 sources each, FGMRES(5) + V(2,2), 6
     levels, shift 0.9, w_J 0.6, tol 1e-6) against the REFERENCE's own
     block_fgmres run to convergence on the same block
     (scripts/ref_full_solve.py -> tests/golden/cfg2_bench_block0.npz; the
     reference preconditions in complex128): solution on the receiver row and
     a strided node sample within 1e-5 per column, cycle count within 5 %."""
-    g = np.load(GOLDEN_BLOCK0)
+    g = np.load(GOLDEN_BLOCK0.replace("block0", f"block{block}"))
     cfg = _bench_cfg()
     b = cfg.krylov_block
     cfg.precond_precision, cfg.krylov_block = precond, 0
     S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))
-    B = cfg.rhs_block(slice(0, b))
-    assert np.array_equal(np.asarray(cfg.source_nodes[:b]), g["source_nodes"])
+    cols = slice(block * b, (block + 1) * b)
+    B = cfg.rhs_block(cols)
+    assert np.array_equal(np.asarray(cfg.source_nodes[cols]), g["source_nodes"])
     X, rep = S.solve_block(torch.from_numpy(B).cuda())
     X = X.cpu().numpy()
     assert rep.all_converged() and bool(np.all(g["converged"]))
