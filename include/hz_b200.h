@@ -149,6 +149,10 @@ HZ_API int hz_solver_set_slabs(hz_solver* s, int nparts, const int* devices);
 /* parts, first agglomerated level and planes[l*(nparts+1)+p] = first plane of
  * part p on level l (p = nparts: plane count), up to `cap` entries */
 HZ_API int hz_solver_slab_info(const hz_solver* s, int* nparts, int* agg_level, int64_t* planes, int cap);
+/* number of per-part VMM chunks (cuMemCreate) the slab spanning vectors have
+ * been built from so far in this process; parts on several GPUs always use
+ * them, parts on one GPU only with HZ_SLAB_VMM=1 (diagnostic) */
+HZ_API int64_t hz_slab_vmm_chunks(void);
 
 /* HelmholtzSolver::solve_block (src/helmholtz_solver.cpp:35-72): host
  * buffers B, X [n][k]; H2D / D2H copies included. Non-convergence is

@@ -31,7 +31,7 @@ EXPORTS = (
     "hz_solve_helmholtz_compact16", "hz_compact16", "hz_block_gram_device", "hz_block_add_scaled_device", "hz_profile_trace",
     "hz_problem_mass", "hz_problem_gamma_factor", "hz_problem_nearest_node", "hz_problem_point_source",
     "hz_point_sources_device", "hz_problem_to_csr", "hz_fwi_sensitivity_rhs", "hz_hierarchy_cycle",
-    "hz_block_krylov",
+    "hz_block_krylov", "hz_slab_vmm_chunks",
 )
 
 
@@ -71,6 +71,7 @@ def lib():
         L.hz_last_error_message.restype = C.c_char_p
         L.hz_problem_num_nodes.restype = C.c_int64
         L.hz_kernel_launch_count.restype = C.c_int64
+        L.hz_slab_vmm_chunks.restype = C.c_int64
         L.hz_profile_report.restype = C.c_int64
         L.hz_profile_report.argtypes = [C.c_char_p, C.c_int64]
         L.hz_profile_trace.restype = C.c_int64

@@ -1589,4 +1589,6 @@ int hz_block_krylov(hz_solver* s, int method, const hz_cycle_spec* spec, int res
   });
 }
 
+int64_t hz_slab_vmm_chunks(void) { return vmm_chunks_created(); }
+
 }  // extern "C"

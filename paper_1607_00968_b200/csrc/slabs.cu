@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <string>
 
+#include <atomic>
+#include <cstdlib>
+
 #include "slabs.hpp"
 
 namespace hz {
@@ -162,9 +165,26 @@ void Slabs::fork() const {
   }
 }
 
+// HZ_SLAB_VMM=1 builds the spanning vectors from one cuMemCreate chunk per
+// part mapped into one reservation even when all parts share one GPU, so the
+// multi-GPU allocation path (chunk cuts at the page granularity, mapping,
+// access rights) runs and is tested on a single device.
+static bool force_vmm() {
+  static const bool on = [] {
+    const char* e = std::getenv("HZ_SLAB_VMM");
+    return e && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+bool Slabs::spanning_vmm() const { return multi_device_ || force_vmm(); }
+
+static std::atomic<int64_t> g_vmm_chunks{0};
+int64_t vmm_chunks_created() { return g_vmm_chunks.load(); }
+
 std::shared_ptr<void> Slabs::alloc(int l, size_t row_bytes) const {
   const size_t bytes = size_t(rows(l)) * row_bytes;
-  if (!multi_device_) {
+  if (!spanning_vmm()) {
     const int dev = part_[0].device;
     DeviceGuard g(dev);
     void* p = nullptr;
@@ -221,6 +241,7 @@ std::shared_ptr<void> Slabs::alloc(int l, size_t row_bytes) const {
       prop.location.id = part_[p].device;
       CUmemGenericAllocationHandle h{};
       cu_check(v.create(&h, sz, &prop, 0), "cuMemCreate");
+      g_vmm_chunks.fetch_add(1);
       sp->handles.push_back(h);
       cu_check(v.map(sp->va + b[p], sz, 0, h, 0), "cuMemMap");
       sp->maps.push_back({sp->va + b[p], sz});

@@ -45,6 +45,8 @@ class Slabs {
   const SlabPart& part(int p) const { return part_[p]; }
   cudaStream_t root() const { return part_[0].stream; }
   bool multi_device() const { return multi_device_; }
+  // spanning vectors built from per-part VMM chunks (multi-GPU, or forced by HZ_SLAB_VMM=1)
+  bool spanning_vmm() const;
   int levels() const { return int(cut_.size()); }
   int slow_axis() const { return slow_; }
   // first level handled by part 0 alone (coarse agglomeration): the first
@@ -94,5 +96,8 @@ void alloc_span(DevBuf<E>& b, const Slabs& sl, int l, int k) {
   b.release();  // free first: these blocks are large and HBM may be nearly full
   b.adopt(sl.alloc(l, sizeof(E) * size_t(k)), size_t(sl.rows(l)) * k);
 }
+
+// cuMemCreate chunks made for spanning vectors so far (diagnostic)
+int64_t vmm_chunks_created();
 
 }  // namespace hz
