@@ -119,6 +119,17 @@ HZ_API void hz_options_default(hz_options* opts);
 HZ_API int hz_problem_create(int ndim, const int64_t n[3], const double h[3], const double* m,
                       double omega, double gamma_base, const double* ramp, int allow_coarse_ppw,
                       int device, hz_problem** out);
+/* Same, with the fine-operator stencil: 7 = the reference's 5-point (2D) /
+ * 7-point (3D) operator (hz_problem_create); 27 = the compact 27-point 3D
+ * operator of BASELINE config 4 (uniform spacing; no reference counterpart:
+ * Laplacian as weighted face / edge / corner second differences, mass
+ * distributed over the 27 nodes with symmetric averaging, weights fitted to
+ * the plane-wave phase velocity by scripts/design_27pt.py; boundary rows
+ * truncated like the reference's). The shifted preconditioner operator is the
+ * same discretisation with gamma + shift * omega. */
+HZ_API int hz_problem_create_ex(int ndim, const int64_t n[3], const double h[3], const double* m, double omega,
+                                double gamma_base, const double* ramp, int allow_coarse_ppw, int device,
+                                int stencil, hz_problem** out);
 HZ_API int hz_problem_destroy(hz_problem* p);
 /* HelmholtzProblem::points_per_wavelength (src/helmholtz.cpp:40-43) */
 HZ_API int hz_problem_ppw(const hz_problem* p, double* ppw);

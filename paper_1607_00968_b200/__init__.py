@@ -337,7 +337,7 @@ class HelmholtzProblem:
 
     def __init__(self, ndim: int, n: Sequence[int], h: Sequence[float], m, omega: float,
                  gamma: AttenuationField, allow_coarse_ppw: bool = False, device: int = 0,
-                 origin: Sequence[float] = (0.0, 0.0, 0.0)):
+                 origin: Sequence[float] = (0.0, 0.0, 0.0), stencil: int = 7):
         n3 = list(n) + [1] * (3 - len(n))
         h3 = list(h) + [1.0] * (3 - len(h))
         self.ndim = int(ndim)
@@ -358,15 +358,17 @@ class HelmholtzProblem:
         nn = np.asarray(self.n, dtype=np.int64)
         hh = np.asarray(self.h, dtype=np.float64)
         out = C.c_void_p()
-        _check(_native.lib().hz_problem_create(self.ndim, nn.ctypes.data, hh.ctypes.data, m.ctypes.data,
-                                               self.omega, self.gamma.base, ramp.ctypes.data,
-                                               1 if allow_coarse_ppw else 0, self.device, C.byref(out)))
+        self.stencil = int(stencil)
+        _check(_native.lib().hz_problem_create_ex(self.ndim, nn.ctypes.data, hh.ctypes.data, m.ctypes.data,
+                                                  self.omega, self.gamma.base, ramp.ctypes.data,
+                                                  1 if allow_coarse_ppw else 0, self.device, self.stencil,
+                                                  C.byref(out)))
         self._h = out
 
     @classmethod
     def from_config(cls, cfg, device: int = 0, allow_coarse_ppw: bool = False):
         return cls(cfg.ndim, cfg.n, cfg.h, cfg.m, cfg.omega, AttenuationField(cfg.gamma_base, cfg.ramp),
-                   allow_coarse_ppw=allow_coarse_ppw, device=device)
+                   allow_coarse_ppw=allow_coarse_ppw, device=device, stencil=getattr(cfg, "stencil", 7))
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -31,7 +31,7 @@ EXPORTS = (
     "hz_solve_helmholtz_compact16", "hz_compact16", "hz_block_gram_device", "hz_block_add_scaled_device", "hz_profile_trace",
     "hz_problem_mass", "hz_problem_gamma_factor", "hz_problem_nearest_node", "hz_problem_point_source",
     "hz_point_sources_device", "hz_problem_to_csr", "hz_fwi_sensitivity_rhs", "hz_hierarchy_cycle",
-    "hz_block_krylov", "hz_slab_vmm_chunks",
+    "hz_block_krylov", "hz_slab_vmm_chunks", "hz_problem_create_ex",
 )
 
 
@@ -78,6 +78,7 @@ def lib():
         L.hz_profile_trace.argtypes = [C.c_char_p, C.c_int64]
         vp, i64, dbl, i32 = C.c_void_p, C.c_int64, C.c_double, C.c_int
         L.hz_problem_create.argtypes = [i32, vp, vp, vp, dbl, dbl, vp, i32, i32, C.POINTER(vp)]
+        L.hz_problem_create_ex.argtypes = [i32, vp, vp, vp, dbl, dbl, vp, i32, i32, i32, C.POINTER(vp)]
         L.hz_problem_destroy.argtypes = [vp]
         L.hz_problem_ppw.argtypes = [vp, C.POINTER(dbl)]
         L.hz_problem_num_nodes.argtypes = [vp]

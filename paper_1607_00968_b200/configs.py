@@ -59,6 +59,7 @@ class HelmholtzConfig:
     max_cycles: int = 400
     precond_precision: str = "c128"
     krylov_block: int = 0             # HelmholtzSolveOptions.rhs_block (0 = one block)
+    stencil: int = 7                  # fine operator: 7 (reference 5/7-point) or 27 (compact, config 4)
     note: str = ""
 
     @property

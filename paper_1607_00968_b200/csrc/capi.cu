@@ -291,16 +291,18 @@ DevOp<double> make_op_with(hz_solver* s, Hierarchy<double>* h64, Hierarchy<float
     op.prec = [spec, h32](const double2* in, double2* out, int kk, cudaStream_t st) {
       h32->cycle_cast_graph(*spec, kk, in, out, st);
     };
-    op.prec_lo = [spec, h32](const double2* in, float2* out, int kk, cudaStream_t st) {
-      h32->cycle_cast_graph(*spec, kk, in, out, st);
-    };
-    op.apply_lo = [P](const float2* in, double2* out, int kk, cudaStream_t st) {
-      launch_apply_lo(P->fine_op(kk), in, out, st);
-    };
-    op.apply_lo_gram = [P](const float2* Z, double2* W, const BlockTab<double>& X, int nb, double2* part,
-                           int max_slots, cudaStream_t st) {
-      return launch_gram8_apply(P->fine_op(8), nb, X, Z, W, part, max_slots, st);
-    };
+    if (P->stencil == 7) {  // complex64 Z blocks: the fine apply widens them on load
+      op.prec_lo = [spec, h32](const double2* in, float2* out, int kk, cudaStream_t st) {
+        h32->cycle_cast_graph(*spec, kk, in, out, st);
+      };
+      op.apply_lo = [P](const float2* in, double2* out, int kk, cudaStream_t st) {
+        launch_apply_lo(P->fine_op(kk), in, out, st);
+      };
+      op.apply_lo_gram = [P](const float2* Z, double2* W, const BlockTab<double>& X, int nb, double2* part,
+                             int max_slots, cudaStream_t st) {
+        return launch_gram8_apply(P->fine_op(8), nb, X, Z, W, part, max_slots, st);
+      };
+    }
   }
   else
     op.prec = [spec, h64](const double2* in, double2* out, int kk, cudaStream_t st) {
@@ -596,6 +598,12 @@ void hz_options_default(hz_options* o) {
 int hz_problem_create(int ndim, const int64_t n[3], const double h[3], const double* m,
                       double omega, double gamma_base, const double* ramp, int allow_coarse_ppw,
                       int device, hz_problem** out) {
+  return hz_problem_create_ex(ndim, n, h, m, omega, gamma_base, ramp, allow_coarse_ppw, device, 7, out);
+}
+
+int hz_problem_create_ex(int ndim, const int64_t n[3], const double h[3], const double* m, double omega,
+                         double gamma_base, const double* ramp, int allow_coarse_ppw, int device, int stencil,
+                         hz_problem** out) {
   return guarded([&] {
     if (!out || !n || !h) throw HzError(kValidation, "hz_problem_create: null argument");
     require_device();
@@ -603,7 +611,7 @@ int hz_problem_create(int ndim, const int64_t n[3], const double h[3], const dou
     auto* hp = new hz_problem;
     try {
       hp->p = std::make_shared<Problem>(ndim, n, h, m, omega, gamma_base, ramp, allow_coarse_ppw != 0,
-                                        device);
+                                        device, stencil);
     } catch (...) {
       delete hp;
       throw;
@@ -703,6 +711,7 @@ int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** out) {
     if (o.cycle_kind < 0 || o.cycle_kind > 2) throw HzError(kValidation, "unknown cycle kind");
     const Problem& P = *s->prob;
     if (s->dense) {
+      if (P.stencil == 27) throw HzError(kValidation, "dense_lu_small: 7-point operator only");
       const int64_t n = P.num_nodes();
       if (n > o.dense_threshold)
         throw HzError(kValidation, "dense_lu_small: grid has " + std::to_string(n) +
@@ -720,6 +729,8 @@ int hz_solver_create(hz_problem* p, const hz_options* opts, hz_solver** out) {
 int hz_solver_set_slabs(hz_solver* s, int nparts, const int* devices) {
   return guarded([&] {
     if (!s) throw HzError(kValidation, "null solver");
+    if (s->prob->stencil == 27 && (nparts > 1 || devices))
+      throw HzError(kValidation, "slabs: the 7-point fine operator only");
     DeviceGuard dg(s->prob->device);
     HZ_CUDA(cudaStreamSynchronize(s->stream));
     auto detach = [&] {
@@ -1459,6 +1470,47 @@ int hz_problem_to_csr(const hz_problem* p, double shift, int64_t* rp, int32_t* c
   return guarded([&] {
     if (!p || !nnz) throw HzError(kValidation, "null argument");
     const Problem& P = *p->p;
+    if (P.stencil == 27) {
+      // the compact operator's planes, shifted on the device, in ascending column order
+      const int64_t nn = P.num_nodes();
+      int64_t cnt27 = 0;
+      for (int dz = -1; dz <= 1; ++dz)
+        for (int dy = -1; dy <= 1; ++dy)
+          for (int dx = -1; dx <= 1; ++dx) {
+            int64_t c = 1;
+            const int d[3] = {dx, dy, dz};
+            for (int a = 0; a < 3; ++a) c *= P.n[a] - (d[a] != 0 ? 1 : 0);
+            cnt27 += c;
+          }
+      *nnz = cnt27;
+      if (!rp || !ci || !v) return;
+      if (cap < cnt27) throw HzError(kValidation, "to_csr: output capacity below nnz");
+      DeviceGuard dg(P.device);
+      DevBuf<double2> planes(size_t(27) * nn);
+      P.build_coef27(shift, planes.get(), nullptr);
+      std::vector<cplx> hp(size_t(27) * nn);
+      HZ_CUDA(cudaMemcpy(hp.data(), planes.get(), planes.bytes(), cudaMemcpyDeviceToHost));
+      auto* vv = reinterpret_cast<cplx*>(v);
+      int64_t e = 0;
+      rp[0] = 0;
+      const int64_t n0 = P.n[0], n1 = P.n[1], n2 = P.n[2];
+      for (int64_t kz = 0; kz < n2; ++kz)
+        for (int64_t j = 0; j < n1; ++j)
+          for (int64_t i = 0; i < n0; ++i) {
+            const int64_t idx = i + n0 * (j + n1 * kz);
+            for (int dz = -1; dz <= 1; ++dz)
+              for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                  const int64_t ii = i + dx, jj = j + dy, kk = kz + dz;
+                  if (ii < 0 || ii >= n0 || jj < 0 || jj >= n1 || kk < 0 || kk >= n2) continue;
+                  ci[e] = int32_t(ii + n0 * (jj + n1 * kk));
+                  vv[e] = hp[size_t((dz + 1) * 9 + (dy + 1) * 3 + (dx + 1)) * nn + idx];
+                  ++e;
+                }
+            rp[idx + 1] = e;
+          }
+      return;
+    }
     const int64_t n0 = P.n[0], n1 = P.n[1], n2 = P.n[2], s1 = n0, s2 = n0 * n1;
     int64_t cnt = 0;
     for (int a = 0; a < 3; ++a) cnt += P.n[a] > 1 ? 2 * (P.n[a] - 1) * (P.num_nodes() / P.n[a]) : 0;

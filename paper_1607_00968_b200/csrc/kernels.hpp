@@ -94,6 +94,17 @@ template <class T, class In, class Out>
 void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_t<T>* x2,
                        const cplx_t<T>* ec, const In* b, Out* out, cudaStream_t s);
 
+// Compact 27-point operator (3D, uniform spacing h): planes[s][i],
+// s = (dz+1)*9 + (dy+1)*3 + (dx+1). Laplacian weights lap[q] for neighbour
+// class q = |dx|+|dy|+|dz| (lap[0] is the centre), mass weights mu[q]; the
+// coupling of i and j is lap[q] + mu[q] (M_i + M_j)/2, the centre
+// lap[0] + mu[0] M_i, with M = mass - i shift_w2 m (gamma + shift omega);
+// neighbours outside the grid get 0 (Dirichlet truncation).
+void launch_build27(const LevelGeom& g, const double* lap, const double* mu, const double2* mass, const double* m,
+                    double shift_w2, double2* planes, cudaStream_t s);
+// inv[i] = 1 / planes[centre][i] (Jacobi D^-1 of a stencil level)
+void launch_inv_plane(int64_t n, const double2* centre, double2* inv, cudaStream_t s);
+
 // elementwise casts / copies
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);

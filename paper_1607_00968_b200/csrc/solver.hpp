@@ -35,11 +35,20 @@ struct Problem {
   double inv_h2[3] = {0, 0, 0};
   double center_lap = 0;
   int device = 0;
+  // fine stencil: 7 = the reference's 5-point (2D) / 7-point (3D) operator;
+  // 27 = the compact 27-point operator of config 4 (3D, uniform spacing; no
+  // reference counterpart, weights from scripts/design_27pt.py)
+  int stencil = 7;
   // device: centre of the unshifted operator (center_lap + mass) and (1 - i gamma/omega)
   DevBuf<double2> d_center, d_gf;
+  // stencil 27: unshifted coefficient planes [27][n], the mass and m on the device
+  DevBuf<double2> d_coef27, d_mass;
+  DevBuf<double> d_m;
 
   Problem(int ndim, const int64_t* n, const double* h, const double* m, double omega,
-          double gamma_base, const double* ramp, bool allow_coarse, int device);
+          double gamma_base, const double* ramp, bool allow_coarse, int device, int stencil = 7);
+  // 27 coefficient planes of the operator with gamma shifted by shift * omega
+  void build_coef27(double shift, double2* planes, cudaStream_t s) const;
   int64_t num_nodes() const { return n[0] * n[1] * n[2]; }
   double points_per_wavelength() const;
   double min_h() const;

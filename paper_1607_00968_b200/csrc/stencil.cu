@@ -1012,7 +1012,10 @@ void launch_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* 
 template <class T>
 void launch_apply_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* r,
                            cudaStream_t s) {
-  if (op.kind != kFine) throw HzError(kState, "apply_residual: fine operator only");
+  if (op.kind != kFine) {  // compact 27-point fine operator: the stencil residual
+    dispatch_level<T, 1>(op, x, b, r, T(0), s);
+    return;
+  }
   const int64_t total = op.g.owned_elems();
   ProfScope prof(sizeof(T) == 8 ? "apply_residual_fine_c128" : "apply_residual_fine_c64", level_bytes(op, 1), s);
   if (sizeof(T) == 4 && op.g.k % 4 == 0) {
@@ -1159,5 +1162,61 @@ template void launch_jacobi_zero<float, double2>(const LevelOp<float>&, float, c
 template void launch_cast<float2, double2>(int64_t, const double2*, float2*, cudaStream_t);
 template void launch_cast<double2, float2>(int64_t, const float2*, double2*, cudaStream_t);
 template void launch_cast<double2, double2>(int64_t, const double2*, double2*, cudaStream_t);
+
+namespace {
+struct W27 {
+  double lap[4], mu[4];
+};
+__global__ void __launch_bounds__(128)
+build27_kernel(LevelGeom g, W27 w, const double2* __restrict__ mass, const double* __restrict__ m, double shift_w2,
+               double2* __restrict__ planes) {
+  const int64_t i = int64_t(blockIdx.x) * 128 + threadIdx.x;
+  if (i >= g.nodes) return;
+  uint32_t x, y, z;
+  g.unpack(uint32_t(i), x, y, z);
+  const double2 Mi = make_double2(mass[i].x, mass[i].y - shift_w2 * m[i]);
+  for (int dz = -1; dz <= 1; ++dz)
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int sidx = (dz + 1) * 9 + (dy + 1) * 3 + (dx + 1);
+        const int q = abs(dx) + abs(dy) + abs(dz);
+        const int64_t xx = int64_t(x) + dx, yy = int64_t(y) + dy, zz = int64_t(z) + dz;
+        double2 c = make_double2(0.0, 0.0);
+        if (q == 0) {
+          c = make_double2(w.lap[0] + w.mu[0] * Mi.x, w.mu[0] * Mi.y);
+        } else if (xx >= 0 && xx < g.n0 && yy >= 0 && yy < g.n1 && zz >= 0 && zz < g.n2) {
+          const int64_t j = xx + int64_t(g.n0) * (yy + int64_t(g.n1) * zz);
+          const double2 Mj = make_double2(mass[j].x, mass[j].y - shift_w2 * m[j]);
+          const double avr = 0.5 * (Mi.x + Mj.x), avi = 0.5 * (Mi.y + Mj.y);
+          c = make_double2(w.lap[q] + w.mu[q] * avr, w.mu[q] * avi);
+        }
+        planes[int64_t(sidx) * g.nodes + i] = c;
+      }
+}
+__global__ void inv_plane_kernel(int64_t n, const double2* __restrict__ c, double2* __restrict__ inv) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (i >= n) return;
+  // 1 / (a + ib) = (a - ib) / (a^2 + b^2)
+  const double2 a = c[i];
+  const double d = a.x * a.x + a.y * a.y;
+  inv[i] = make_double2(a.x / d, -a.y / d);
+}
+}  // namespace
+
+void launch_build27(const LevelGeom& g, const double* lap, const double* mu, const double2* mass, const double* m,
+                    double shift_w2, double2* planes, cudaStream_t s) {
+  W27 w;
+  for (int q = 0; q < 4; ++q) {
+    w.lap[q] = lap[q];
+    w.mu[q] = mu[q];
+  }
+  build27_kernel<<<grid_for(g.nodes, 128), 128, 0, s>>>(g, w, mass, m, shift_w2, planes);
+  HZ_LAUNCH_CHECK();
+}
+
+void launch_inv_plane(int64_t n, const double2* centre, double2* inv, cudaStream_t s) {
+  inv_plane_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, centre, inv);
+  HZ_LAUNCH_CHECK();
+}
 
 }  // namespace hz

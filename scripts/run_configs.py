@@ -27,7 +27,7 @@ def make(c):
         cfg = configs.config5(nlevels=4)                   # coarsest 65x65x33
         cfg.shift, cfg.restart = 1.5, 5
     for key in ("nlevels", "shift", "restart", "max_cycles", "precond_precision", "krylov_block", "jacobi_weight",
-                "cycle"):
+                "cycle", "stencil"):
         v = os.environ.get(f"HZ_CFG{c}_{key.upper()}")
         if v is not None:
             setattr(cfg, key, type(getattr(cfg, key))(v))
@@ -55,7 +55,7 @@ if __name__ == "__main__":
             torch.cuda.synchronize(); t = time.time()
             X, rep = S.solve_block(B)
             torch.cuda.synchronize(); dt = time.time() - t
-            out = dict(config=c, name=cfg.name, n=cfg.n, k=cfg.k, nlevels=cfg.nlevels, shift=cfg.shift,
+            out = dict(config=c, name=cfg.name, n=cfg.n, k=cfg.k, stencil=cfg.stencil, nlevels=cfg.nlevels, shift=cfg.shift,
                        restart=cfg.restart, prec=cfg.precond_precision, rhs_block=cfg.krylov_block, slabs=slabs,
                        setup_s=round(setup, 2),
                        solve_s=round(dt, 3), cycles=rep.cycles, converged=rep.all_converged(),
