@@ -50,8 +50,17 @@ UNIT = "RHS/s"
 # grows with it (8k^2 flops per row), so 8-column blocks turn the FP64-bound
 # Gram/update of a 32-column block into HBM-bound ones. At shift 0.5 /
 # w_J 0.8 the V-cycle stalls in the reference oracle and on the GPU alike.
-WORKLOAD = dict(cfg=2, k=32, nlevels=6, shift=0.9, jacobi_weight=0.6, cycle="V", restart=5, tol=1e-6,
-                max_cycles=2000, precond="c64", krylov_block=8)
+WORKLOADS = {
+    "cfg2": dict(cfg=2, k=32, nlevels=6, shift=0.9, jacobi_weight=0.6, cycle="V", restart=5, tol=1e-6,
+                 max_cycles=2000, precond="c64", krylov_block=8, stencil=7),
+    # BASELINE config 4's per-GPU shard (--workload cfg4): 3D 257x257x129 with
+    # the compact 27-point fine operator, 8 of the 64 surface sources per GPU,
+    # c128 FGMRES(10) + c64 V(2,2), 3 levels (4 and 5 levels stall below
+    # 1e-2 in 500 cycles with either stencil: profiles/r02_cfg4_levels.txt)
+    "cfg4": dict(cfg=4, k=8, nlevels=3, shift=0.5, jacobi_weight=0.8, cycle="V", restart=10, tol=1e-6,
+                 max_cycles=600, precond="c64", krylov_block=0, stencil=27),
+}
+WORKLOAD = WORKLOADS["cfg2"]
 
 
 def peaks():
@@ -130,17 +139,25 @@ def dist_env():
 
 
 def rank_sources(cfg, rank, world, k):
-    """Weak scaling: world*k evenly spaced surface sources, rank r owns r, r+world, ..."""
+    """Weak scaling. Config 2: world*k evenly spaced surface sources, rank r
+    owns r, r+world, ... Config 4: the config's 64 sources (8x8 surface grid),
+    8 per GPU: rank r owns sources r, r+8, ... (BASELINE configs[3])."""
     import numpy as np
     from paper_1607_00968_b200 import configs
+    if WORKLOAD["cfg"] == 4:
+        return np.asarray(cfg.source_nodes[rank % 8::8][:k], dtype=np.int64)
     full = configs.config2(nlevels=WORKLOAD["nlevels"], k=k * world)
     return np.asarray(full.source_nodes[rank::world], dtype=np.int64)
 
 
 def build_workload(rank, world, k):
     from paper_1607_00968_b200 import configs
-    cfg = configs.config2(nlevels=WORKLOAD["nlevels"], k=k)
+    if WORKLOAD["cfg"] == 4:
+        cfg = configs.config4(nlevels=WORKLOAD["nlevels"])
+    else:
+        cfg = configs.config2(nlevels=WORKLOAD["nlevels"], k=k)
     cfg.source_nodes = rank_sources(cfg, rank, world, k)
+    cfg.stencil = WORKLOAD["stencil"]
     cfg.shift = WORKLOAD["shift"]
     cfg.jacobi_weight = WORKLOAD["jacobi_weight"]
     cfg.cycle = WORKLOAD["cycle"]
@@ -153,8 +170,14 @@ def build_workload(rank, world, k):
 
 
 def config_json(cfg, world, l2_note):
-    return {"workload": f"BASELINE config 2: 2D {cfg.n[0]}x{cfg.n[1]} layered model, k={cfg.k} RHS/GPU",
-            "grid": list(cfg.n[:2]), "rhs_per_gpu": cfg.k, "global_rhs": cfg.k * world,
+    if WORKLOAD["cfg"] == 4:
+        wl = (f"BASELINE config 4 (per-GPU shard): 3D {cfg.n[0]}x{cfg.n[1]}x{cfg.n[2]} thrust-faulted layered model, "
+              f"compact {cfg.stencil}-point fine stencil, k={cfg.k} RHS/GPU")
+        grid = list(cfg.n)
+    else:
+        wl = f"BASELINE config 2: 2D {cfg.n[0]}x{cfg.n[1]} layered model, k={cfg.k} RHS/GPU"
+        grid = list(cfg.n[:2])
+    return {"workload": wl, "grid": grid, "rhs_per_gpu": cfg.k, "global_rhs": cfg.k * world,
             "solver": f"block FGMRES({cfg.restart}) + {cfg.cycle}({cfg.pre},{cfg.post}) MG, "
                       f"{cfg.nlevels} levels, shift {cfg.shift}, w_J {cfg.jacobi_weight}",
             "rhs_blocking": (f"{-(-cfg.k // cfg.krylov_block)} independent block solves of {cfg.krylov_block} columns"
@@ -269,6 +292,10 @@ def reference_sample(cfg, gpu_cycles_per_block, sample_cycles, threads=None):
 def run_reference(args):
     ws, rank, local = dist_env()
     if ws > 1 and rank != 0:
+        return 0
+    if WORKLOAD["cfg"] != 2:
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no compact 27-point operator "
+                          "(src/helmholtz.cpp:45-100 is 5/7-point only)"}), flush=True)
         return 0
     cfg = build_workload(0, 1, WORKLOAD["k"])
     run = ReferenceRunner(cfg)
@@ -466,13 +493,17 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded, SURVEY §8d; random-free point sources)",
-            "config": config_json(cfg, ws, "inputs larger than L2 (269 MB block, 3.5 GB Krylov bases)"),
+            "config": config_json(cfg, ws, f"inputs larger than L2 ({B_host.nbytes / 1e6:.0f} MB block, Krylov bases "
+                                           f"{(2 * cfg.restart + 1) * B_host.nbytes / 1e9:.1f} GB)"),
             "cycles_per_solve": statistics.mean(cycles), "setup_s": round(setup_s, 3),
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": int(B_host.nbytes),
                     "d2h_bytes_per_step": int(B_host.nbytes)},
             "roofline": roofline, "roofline_stencil": roof_st, "kernels": table, "gpu_launches": int(launches),
             "clocks": clk.summary()}
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and WORKLOAD["cfg"] != 2:
+        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                                "sample": "unavailable: the reference has no compact 27-point operator"}
+    elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             v, info = reference_sample(cfg, statistics.mean(cycles), sample_cycles=args.cpu_sample_cycles)
             info["sample"] += f"; host {cpu_model()}"
@@ -494,6 +525,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg2",
+                    help="cfg2 (default, the BASELINE metric's config) or cfg4 (config 4's per-GPU shard)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-sample-cycles", type=int, default=2,
                     help="FGMRES iterations per reference step (bounded CPU sample)")
@@ -503,6 +536,8 @@ def main():
                     help="per-block cycle count to extrapolate the reference sample to (default: the reference's "
                          "own measured counts, tests/golden/cfg2_bench_block*.npz)")
     args = ap.parse_args()
+    global WORKLOAD
+    WORKLOAD = WORKLOADS[args.workload]
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # launched directly with --gpus N: become the torchrun launch the
         # driver uses (one process per GPU, 127.0.0.1 rendezvous)

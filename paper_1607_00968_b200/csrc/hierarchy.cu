@@ -28,6 +28,7 @@ namespace hz {
 namespace {
 constexpr double k27_a1 = 0.30896924112207297, k27_a2 = 0.5974547869846899;
 constexpr double k27_c1 = 0.49495786061914238, k27_c2 = 0.023557529253244218, k27_c3 = 2.4579791982563098e-08;
+}  // namespace
 void weights27(double h, double* lap, double* mu) {
   const double a3 = 1.0 - k27_a1 - k27_a2, c0 = 1.0 - k27_c1 - k27_c2 - k27_c3, ih2 = 1.0 / (h * h);
   lap[1] = k27_a1 * ih2;
@@ -39,11 +40,12 @@ void weights27(double h, double* lap, double* mu) {
   mu[2] = k27_c2 / 12.0;
   mu[3] = k27_c3 / 8.0;
 }
-}  // namespace
+
+void Problem::weights27(double* w8) const { ::hz::weights27(h[0], w8, w8 + 4); }
 
 void Problem::build_coef27(double shift, double2* planes, cudaStream_t s) const {
   double lap[4], mu[4];
-  weights27(h[0], lap, mu);
+  ::hz::weights27(h[0], lap, mu);
   launch_build27(LevelGeom(n[0], n[1], n[2], 1), lap, mu, d_mass.get(), d_m.get(), shift * omega * omega, planes, s);
 }
 
@@ -109,8 +111,6 @@ Problem::Problem(int ndim_, const int64_t* n_, const double* h_, const double* m
     d_m.alloc(nn);
     HZ_CUDA(cudaMemcpy(d_mass.get(), mass.data(), nn * sizeof(double2), cudaMemcpyHostToDevice));
     HZ_CUDA(cudaMemcpy(d_m.get(), m.data(), nn * sizeof(double), cudaMemcpyHostToDevice));
-    d_coef27.alloc(size_t(27) * nn);
-    build_coef27(0.0, d_coef27.get(), nullptr);
     HZ_CUDA(cudaDeviceSynchronize());
   }
 }
@@ -136,11 +136,11 @@ std::vector<cplx> Problem::shifted_center(double shift) const {
 
 LevelOp<double> Problem::fine_op(int k) const {
   LevelOp<double> op;
-  op.kind = stencil == 27 ? kStencil : kFine;
+  op.kind = stencil == 27 ? kFine27 : kFine;
   op.ndim = ndim;
   op.g = LevelGeom(n[0], n[1], n[2], k);
-  op.coef = d_coef27.get();
-  op.center = d_center.get();
+  op.center = stencil == 27 ? d_mass.get() : d_center.get();
+  if (stencil == 27) weights27(op.w27);
   for (int a = 0; a < 3; ++a) op.w[a] = inv_h2[a];
   return op;
 }
@@ -226,12 +226,13 @@ std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, in
   if (p.stencil == 27) {  // compact 27-point fine operator with gamma + shift * omega
     auto& L0 = H->levels_[0];
     L0.dims = dims[0];
-    L0.kind = kStencil;
+    L0.kind = kFine27;
     const int64_t nn = p.num_nodes();
-    L0.coef.alloc(size_t(27) * nn);
+    p.weights27(L0.w27);
+    L0.center.alloc(nn);
     L0.inv_diag.alloc(nn);
-    p.build_coef27(shift, L0.coef.get(), s);
-    launch_inv_plane(nn, L0.coef.get() + size_t(13) * nn, L0.inv_diag.get(), s);
+    launch_shift_mass(nn, p.d_mass.get(), p.d_m.get(), shift * p.omega * p.omega, L0.center.get(), s);
+    launch_inv_centre27(nn, L0.w27[0], L0.w27[4], L0.center.get(), L0.inv_diag.get(), s);
     HZ_CUDA(cudaStreamSynchronize(s));
   } else {
     auto& L0 = H->levels_[0];
@@ -255,7 +256,19 @@ std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, in
     const int64_t nc = L.nodes();
     L.coef.alloc(size_t(S) * nc);
     LevelGeom gc(dims[l][0], dims[l][1], dims[l][2], 1);
-    launch_galerkin(H->op(l - 1, 1), gc, L.coef.get(), s);
+    if (l == 1 && p.stencil == 27) {
+      // the Galerkin product reads coefficient planes: materialise the
+      // shifted 27-point operator's (identical couplings) for this step only
+      DevBuf<double2> planes(size_t(27) * p.num_nodes());
+      p.build_coef27(shift, planes.get(), s);
+      LevelOp<double> f = H->op(0, 1);
+      f.kind = kStencil;
+      f.coef = planes.get();
+      launch_galerkin(f, gc, L.coef.get(), s);
+      HZ_CUDA(cudaStreamSynchronize(s));
+    } else {
+      launch_galerkin(H->op(l - 1, 1), gc, L.coef.get(), s);
+    }
     std::vector<cplx> diag(nc);
     HZ_CUDA(cudaMemcpyAsync(diag.data(), L.coef.get() + size_t(sc) * nc, nc * sizeof(double2),
                             cudaMemcpyDeviceToHost, s));
@@ -377,6 +390,7 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
     b.dims = a.dims;
     b.kind = a.kind;
     for (int q = 0; q < 3; ++q) b.w[q] = float(a.w[q]);
+    for (int q = 0; q < 8; ++q) b.w27[q] = float(a.w27[q]);
     auto cast = [&](const DevBuf<double2>& src, DevBuf<float2>& dst) {
       if (!src.size()) return;
       dst.alloc(src.size());
@@ -421,6 +435,7 @@ LevelOp<T> Hierarchy<T>::op(int l, int k) const {
   o.inv_diag = L.inv_diag.get();
   o.cd = L.cd.get();
   for (int a = 0; a < 3; ++a) o.w[a] = L.w[a];
+  for (int a = 0; a < 8; ++a) o.w27[a] = L.w27[a];
   o.level = l;
   return o;
 }
@@ -428,7 +443,7 @@ LevelOp<T> Hierarchy<T>::op(int l, int k) const {
 template <class T>
 void Hierarchy<T>::download_level(int l, std::vector<cplx>& out) const {
   const auto& L = levels_[l];
-  const DevBuf<V>& src = L.kind == kFine ? L.center : L.coef;
+  const DevBuf<V>& src = L.kind == kStencil ? L.coef : L.center;
   std::vector<V> tmp(src.size());
   HZ_CUDA(cudaMemcpy(tmp.data(), src.get(), src.bytes(), cudaMemcpyDeviceToHost));
   out.resize(tmp.size());
@@ -487,6 +502,7 @@ std::unique_ptr<Hierarchy<T>> Hierarchy<T>::share() const {
     B.dims = A.dims;
     B.kind = A.kind;
     for (int a = 0; a < 3; ++a) B.w[a] = A.w[a];
+    for (int a = 0; a < 8; ++a) B.w27[a] = A.w27[a];
     alias(A.center, B.center);
     alias(A.coef, B.coef);
     alias(A.inv_diag, B.inv_diag);

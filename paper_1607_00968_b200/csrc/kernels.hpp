@@ -14,7 +14,11 @@ namespace hz {
 //    complex coefficient planes coef[s][node], s = (dz+1)*9 + (dy+1)*3 + (dx+1)
 //    -- ascending s is ascending CSR column, so sums run in the reference's
 //    Csr::mul_block order (inc/csr.hpp:40-54).
-enum OpKind : int { kFine = 0, kStencil = 1 };
+//  * kind == kFine27: the compact 27-point fine operator (config 4) with its
+//    couplings computed on the fly, lap[q] + mu[q] (M_i + M_j)/2 from the
+//    per-node mass M (`center`, gamma already shifted) and the 8 weights
+//    w27 = {lap[0..3], mu[0..3]} -- 1 complex per node instead of 27 planes.
+enum OpKind : int { kFine = 0, kStencil = 1, kFine27 = 2 };
 
 template <class T>
 struct LevelOp {
@@ -27,6 +31,7 @@ struct LevelOp {
   const V* inv_diag = nullptr; // Jacobi D^{-1} per node
   const V* cd = nullptr;       // optional: (centre, D^{-1}) interleaved per node (kFine)
   T w[3] = {0, 0, 0};          // kFine off-diagonal weights (0 on flat axes)
+  T w27[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kFine27: lap[0..3], mu[0..3]
   int level = 0;               // multigrid level (profiling names only)
 };
 
@@ -102,6 +107,10 @@ void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cp
 // neighbours outside the grid get 0 (Dirichlet truncation).
 void launch_build27(const LevelGeom& g, const double* lap, const double* mu, const double2* mass, const double* m,
                     double shift_w2, double2* planes, cudaStream_t s);
+// Ms[i] = mass[i] - i shift_w2 m[i] (the shifted per-node mass of kFine27)
+void launch_shift_mass(int64_t n, const double2* mass, const double* m, double shift_w2, double2* ms, cudaStream_t s);
+// inv[i] = 1 / (lap0 + mu0 Ms[i]) (Jacobi D^-1 of a kFine27 level)
+void launch_inv_centre27(int64_t n, double lap0, double mu0, const double2* ms, double2* inv, cudaStream_t s);
 // inv[i] = 1 / planes[centre][i] (Jacobi D^-1 of a stencil level)
 void launch_inv_plane(int64_t n, const double2* centre, double2* inv, cudaStream_t s);
 

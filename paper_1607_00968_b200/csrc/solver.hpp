@@ -41,14 +41,16 @@ struct Problem {
   int stencil = 7;
   // device: centre of the unshifted operator (center_lap + mass) and (1 - i gamma/omega)
   DevBuf<double2> d_center, d_gf;
-  // stencil 27: unshifted coefficient planes [27][n], the mass and m on the device
-  DevBuf<double2> d_coef27, d_mass;
+  // stencil 27: the mass and m on the device (couplings computed on the fly)
+  DevBuf<double2> d_mass;
   DevBuf<double> d_m;
 
   Problem(int ndim, const int64_t* n, const double* h, const double* m, double omega,
           double gamma_base, const double* ramp, bool allow_coarse, int device, int stencil = 7);
   // 27 coefficient planes of the operator with gamma shifted by shift * omega
   void build_coef27(double shift, double2* planes, cudaStream_t s) const;
+  // kFine27 weights {lap[0..3], mu[0..3]}
+  void weights27(double* w8) const;
   int64_t num_nodes() const { return n[0] * n[1] * n[2]; }
   double points_per_wavelength() const;
   double min_h() const;
@@ -80,6 +82,7 @@ struct MgLevelDev {
   DevBuf<V> coef;      // levels >= 1: [S][n] Galerkin planes
   DevBuf<V> inv_diag;  // D^{-1}
   DevBuf<V> cd;        // level 0 of the c64 hierarchy: (centre, D^{-1}) interleaved per node (fused k = 8 kernels)
+  T w27[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kFine27 weights (center = shifted per-node mass)
   T w[3] = {0, 0, 0};
   int64_t nodes() const { return dims[0] * dims[1] * dims[2]; }
 };

@@ -444,6 +444,93 @@ stencil_v4_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
   stencil_v4_item<T, NDIM, MODE, G>(op, x, b, out, wj, blockIdx.x * kBlock + threadIdx.x);
 }
 
+// Compact 27-point fine level (kFine27): the couplings lap[q] + mu[q] (M_i +
+// M_j)/2 are formed on the fly from the per-node mass (1 complex per node
+// read instead of 27 coefficient planes; each M_j is reused by 27 rows through
+// L1), in the same order and arithmetic as build27_kernel, and summed in
+// ascending plane order like stencil_v4_item. CPT columns per thread
+// (4: 16-byte loads; 1: any k).
+template <class T, int MODE, int CPT>
+__device__ __forceinline__ void fine27_item(const LevelOp<T>& op, const cplx_t<T>* __restrict__ x,
+                                            const cplx_t<T>* __restrict__ b, cplx_t<T>* __restrict__ out, T wj,
+                                            uint32_t t) {
+  using V = cplx_t<T>;
+  const LevelGeom& g = op.g;
+  const uint32_t e0 = g.e_begin() + t * CPT;
+  if (e0 >= g.e_end()) return;
+  uint32_t node, col, i, j, kz;
+  g.div_k.divmod(e0, node, col);
+  g.unpack(node, i, j, kz);
+  const int64_t sx = g.k, sy = int64_t(g.n0) * g.k, sz = int64_t(g.n0) * g.n1 * g.k;
+  const int64_t nx = 1, ny = g.n0, nz = int64_t(g.n0) * g.n1;
+  const V Mi = __ldg(&op.center[node]);
+  const T half = T(0.5);
+  V acc[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) acc[c] = czero<V>();
+  // loads of a group of G neighbours issued before its FMAs: a plane for
+  // complex64, a row for complex128 (register budget)
+  constexpr int G = sizeof(T) == 8 && CPT == 4 ? 3 : 9;
+#pragma unroll
+  for (int s0 = 0; s0 < 27; s0 += G) {
+    V av[G], xv[G][CPT];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      const int s = s0 + q;
+      const int dz = s / 9 - 1, dy = (s / 3) % 3 - 1, dx = s % 3 - 1;
+      const int cls = (dx != 0) + (dy != 0) + (dz != 0);
+      const bool okz = dz < 0 ? kz > 0 : (dz > 0 ? kz + 1 < g.n2 : true);
+      const bool oky = dy < 0 ? j > 0 : (dy > 0 ? j + 1 < g.n1 : true);
+      const bool okx = dx < 0 ? i > 0 : (dx > 0 ? i + 1 < g.n0 : true);
+      const bool ok = okz && oky && okx;
+      const int64_t off = ok ? dz * sz + dy * sy + dx * sx : 0;
+      if (cls == 0) {
+        av[q] = mk(op.w27[0] + op.w27[4] * Mi.x, op.w27[4] * Mi.y);
+      } else {
+        const V Mj = __ldg(&op.center[int64_t(node) + (ok ? dz * nz + dy * ny + dx * nx : 0)]);
+        const T avr = half * (Mi.x + Mj.x), avi = half * (Mi.y + Mj.y);
+        av[q] = ok ? mk(op.w27[cls] + op.w27[4 + cls] * avr, op.w27[4 + cls] * avi) : czero<V>();
+      }
+      if constexpr (CPT == 4) {
+        ld4(x + int64_t(e0) + off, xv[q]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) xv[q][c] = __ldg(x + int64_t(e0) + off + c);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) acc[c] = cfma(av[q], xv[q][c], acc[c]);
+  }
+  V o[CPT];
+  if (MODE == 0) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[c] = acc[c];
+  } else if (MODE == 1) {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[c] = csub(__ldg(b + e0 + c), acc[c]);
+  } else {
+    const V d = __ldg(&op.inv_diag[node]);
+    const V wd = mk(wj * d.x, wj * d.y);
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) o[c] = cadd(__ldg(x + e0 + c), cmul(wd, csub(__ldg(b + e0 + c), acc[c])));
+  }
+  if constexpr (CPT == 4) {
+    st4(out + e0, o);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) out[e0 + c] = o[c];
+  }
+}
+
+template <class T, int MODE, int CPT>
+__global__ void __launch_bounds__(kBlock)
+fine27_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __restrict__ b,
+              cplx_t<T>* __restrict__ out, T wj) {
+  fine27_item<T, MODE, CPT>(op, x, b, out, wj, blockIdx.x * kBlock + threadIdx.x);
+}
+
 // Fine 5/7-point level kernel, 4 columns per thread with 16-byte loads (all
 // loads issued first); same per-column arithmetic and order as fine_ax.
 template <class T, int NDIM, int MODE, class Out = cplx_t<T>>
@@ -888,7 +975,7 @@ constexpr const char* prec_tag() {
 template <class T>
 double level_bytes(const LevelOp<T>& op, int mode) {
   const double s = sizeof(cplx_t<T>), n = double(op.g.owned_nodes()), k = op.g.k;
-  const double coef = op.kind == kFine ? 1.0 : (op.ndim == 3 ? 27.0 : 9.0);
+  const double coef = op.kind != kStencil ? 1.0 : (op.ndim == 3 ? 27.0 : 9.0);
   const double vec = mode == 0 ? 2.0 : 3.0;
   const double diag = mode == 2 ? 1.0 : 0.0;
   return n * (vec * k * s + (coef + diag) * s);
@@ -896,13 +983,15 @@ double level_bytes(const LevelOp<T>& op, int mode) {
 
 template <class T, int MODE>
 const char* level_name(int kind, int level) {
-  static const char* names[2][3][2] = {
+  static const char* names[3][3][2] = {
       {{"apply_fine_c128", "apply_fine_c64"}, {"residual_fine_c128", "residual_fine_c64"},
        {"jacobi_fine_c128", "jacobi_fine_c64"}},
       {{"apply_stencil_c128", "apply_stencil_c64"}, {"residual_stencil_c128", "residual_stencil_c64"},
-       {"jacobi_stencil_c128", "jacobi_stencil_c64"}}};
+       {"jacobi_stencil_c128", "jacobi_stencil_c64"}},
+      {{"apply_fine27_c128", "apply_fine27_c64"}, {"residual_fine27_c128", "residual_fine27_c64"},
+       {"jacobi_fine27_c128", "jacobi_fine27_c64"}}};
   const char* base = names[kind][MODE][sizeof(T) == 8 ? 0 : 1];
-  if (kind == kFine) return base;
+  if (kind != kStencil) return base;
   // Galerkin levels by level index: level 1 streams from HBM, deeper levels
   // are L2-resident and launch/latency bound, so they are reported apart
   return profile_name_level(base, level);
@@ -931,7 +1020,12 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
   }();
   // c64 only: for c128 the 4-column form needs 7 x 64 B per thread in
   // registers and runs slower than one column per thread
-  if (op.kind == kFine && fine_v4 && sizeof(T) == 4 && op.g.k % 4 == 0) {
+  if (op.kind == kFine27) {
+    if (op.g.k % 4 == 0)
+      fine27_kernel<T, MODE, 4><<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op, x, b, out, wj);
+    else
+      fine27_kernel<T, MODE, 1><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+  } else if (op.kind == kFine && fine_v4 && sizeof(T) == 4 && op.g.k % 4 == 0) {
     const int g4 = grid_for(total / 4, kBlock);
     if (op.ndim == 3)
       fine_v4_kernel<T, 3, MODE><<<g4, kBlock, 0, s>>>(op, x, b, out, wj);
@@ -1216,6 +1310,32 @@ void launch_build27(const LevelGeom& g, const double* lap, const double* mu, con
 
 void launch_inv_plane(int64_t n, const double2* centre, double2* inv, cudaStream_t s) {
   inv_plane_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, centre, inv);
+  HZ_LAUNCH_CHECK();
+}
+
+namespace {
+__global__ void shift_mass_kernel(int64_t n, const double2* __restrict__ mass, const double* __restrict__ m,
+                                  double shift_w2, double2* __restrict__ ms) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (i < n) ms[i] = make_double2(mass[i].x, mass[i].y - shift_w2 * m[i]);  // as build27_kernel's M_i
+}
+__global__ void inv_centre27_kernel(int64_t n, double lap0, double mu0, const double2* __restrict__ ms,
+                                    double2* __restrict__ inv) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (i >= n) return;
+  const double2 a = make_double2(lap0 + mu0 * ms[i].x, mu0 * ms[i].y);
+  const double d = a.x * a.x + a.y * a.y;
+  inv[i] = make_double2(a.x / d, -a.y / d);
+}
+}  // namespace
+
+void launch_shift_mass(int64_t n, const double2* mass, const double* m, double shift_w2, double2* ms, cudaStream_t s) {
+  shift_mass_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, mass, m, shift_w2, ms);
+  HZ_LAUNCH_CHECK();
+}
+
+void launch_inv_centre27(int64_t n, double lap0, double mu0, const double2* ms, double2* inv, cudaStream_t s) {
+  inv_centre27_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, lap0, mu0, ms, inv);
   HZ_LAUNCH_CHECK();
 }
 
