@@ -113,8 +113,14 @@ template <int NB, class TT = double>
 __global__ void __launch_bounds__(kThreads, HZ_UPDATE8_MINB)
 update8_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, const double2* Yin,
                double2* Yout, double sign) {
+  // H_i[4s + t][g] staged at hs[i][s][g][t]: the B fragment of lane 4g + t is
+  // hs[i][s][lane], so a warp's fragment load is 512 contiguous bytes
+  // (the [p][q] order put lanes t = 0..3 of a quarter-warp on one bank group)
   __shared__ double2 hs[NB * 64];
-  for (int e = threadIdx.x; e < NB * 64; e += kThreads) hs[e] = H[e];
+  for (int e = threadIdx.x; e < NB * 64; e += kThreads) {
+    const int i = e >> 6, p = (e >> 3) & 7, q = e & 7;
+    hs[i * 64 + (p >> 2) * 32 + q * 4 + (p & 3)] = H[e];
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -138,7 +144,7 @@ update8_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, c
         for (int s = 0; s < 2; ++s)
           if (i0 + c < NB) {
             // B[t][g] = H_i[q0 + t][g], q0 = 4 s
-            const double2 h = hs[(i0 + c) * 64 + (4 * s + t) * 8 + g];
+            const double2 h = hs[(i0 + c) * 64 + s * 32 + lane];
             const double2 x = xa[c][s];
             dmma::mma884(acc[0][0], acc[0][1], x.x, h.x);
             dmma::mma884(acc[1][0], acc[1][1], x.y, h.y);
@@ -240,8 +246,12 @@ template <int NB, class TT = double>
 __global__ void __launch_bounds__(k8::kThreads, 2)
 update16_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, const double2* Yin, double2* Yout,
                 double sign) {
+  // H_i[4 st + t][8 b + g] staged at hs[i][st][b][g][t] (lane-contiguous fragments)
   __shared__ double2 hs[NB * 256];
-  for (int e = threadIdx.x; e < NB * 256; e += k8::kThreads) hs[e] = H[e];
+  for (int e = threadIdx.x; e < NB * 256; e += k8::kThreads) {
+    const int i = e >> 8, p = (e >> 4) & 15, q = e & 15;
+    hs[i * 256 + ((p >> 2) * 2 + (q >> 3)) * 32 + (q & 7) * 4 + (p & 3)] = H[e];
+  }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -263,7 +273,7 @@ update16_kernel(int64_t n, const BlockTab<TT> X, const double2* __restrict__ H, 
       for (int st = 0; st < 4; ++st)
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-          const double2 h = hs[i * 256 + (4 * st + t) * 16 + 8 * b + g];
+          const double2 h = hs[i * 256 + (st * 2 + b) * 32 + lane];
           dmma::mma884(acc[b][0][0], acc[b][0][1], xa[st].x, h.x);
           dmma::mma884(acc[b][1][0], acc[b][1][1], xa[st].y, h.y);
           dmma::mma884(acc[b][2][0], acc[b][2][1], xa[st].x + xa[st].y, h.x + h.y);
