@@ -63,3 +63,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 
 }  // namespace tma
 }  // namespace hz
+
+namespace hz {
+namespace tma {
+// bring [p, p + bytes) into L2 ahead of its loads (bytes % 16 == 0, 16-byte aligned)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+}  // namespace tma
+}  // namespace hz
