@@ -147,6 +147,22 @@ template <class V> __host__ __device__ __forceinline__ typename RealOf<V>::type 
   return a.x * a.x + a.y * a.y;
 }
 
+// damped-Jacobi update x + d (b - a) with every operation rounded as written
+// (no FMA contraction): the Galerkin-level kernels (plain, 4-column,
+// bulk-copy) then produce the same bits whatever nvcc would fuse in each
+__device__ __forceinline__ float2 jacobi_upd(float2 x, float2 d, float2 b, float2 a) {
+  const float sx = __fsub_rn(b.x, a.x), sy = __fsub_rn(b.y, a.y);
+  const float mx = __fsub_rn(__fmul_rn(d.x, sx), __fmul_rn(d.y, sy));
+  const float my = __fadd_rn(__fmul_rn(d.x, sy), __fmul_rn(d.y, sx));
+  return make_float2(__fadd_rn(x.x, mx), __fadd_rn(x.y, my));
+}
+__device__ __forceinline__ double2 jacobi_upd(double2 x, double2 d, double2 b, double2 a) {
+  const double sx = __dsub_rn(b.x, a.x), sy = __dsub_rn(b.y, a.y);
+  const double mx = __dsub_rn(__dmul_rn(d.x, sx), __dmul_rn(d.y, sy));
+  const double my = __dadd_rn(__dmul_rn(d.x, sy), __dmul_rn(d.y, sx));
+  return make_double2(__dadd_rn(x.x, mx), __dadd_rn(x.y, my));
+}
+
 template <class Dst, class Src> __host__ __device__ __forceinline__ Dst ccast(Src s) {
   Dst d;
   d.x = static_cast<decltype(d.x)>(s.x);

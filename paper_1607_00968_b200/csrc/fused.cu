@@ -967,6 +967,162 @@ fused_post_k8_kernel(LevelOp<float> op, LevelGeom gc, float wj, const float2* __
   }
 }
 
+// ---------------------------------------------------------------------------
+// 2D Galerkin level (9-point planes), k = 8 complex64, one stencil per launch
+// (apply / residual / damped Jacobi) with bulk-copy row staging: a CTA owns a
+// strip of NT nodes and streams its rows -- x with a one-node halo, the
+// 80-byte (9 coefficients, D^-1) records, b -- through a PD-deep ring of
+// slots, one mbarrier each; output row j reads the x rows j-1, j, j+1 of three
+// slots. 4 threads per node (2 columns each). Rows outside the grid stage a
+// row inside it (their coefficients are 0, as in the planes), halo nodes
+// outside it hold zeros; sums in ascending plane order, so the results equal
+// the stencil_v4 kernels bitwise.
+template <int MODE, int NT, int PD>
+struct S9Plan {
+  static constexpr int TH = NT * 4;
+  static constexpr size_t XROW = size_t(NT + 2) * kK8 * sizeof(float2);
+  static constexpr size_t CROW = size_t(NT) * 10 * sizeof(float2);
+  static constexpr size_t BROW = MODE == 0 ? 0 : size_t(NT) * kK8 * sizeof(float2);
+  static constexpr size_t SLOT = XROW + CROW + BROW;
+  static constexpr size_t OFF_SLOTS = 128;
+  static constexpr size_t BYTES = OFF_SLOTS + PD * SLOT;
+};
+
+template <int MODE, int NT, int PD, int MINB>
+__global__ void __launch_bounds__(NT * 4, MINB)
+stencil9_k8_kernel(LevelOp<float> op, float wj, const float2* __restrict__ x, const float2* __restrict__ b,
+                   float2* __restrict__ out, int rows) {
+  using P = S9Plan<MODE, NT, PD>;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  const int n0 = int(op.g.n0), n1 = int(op.g.n1);
+  const int t = threadIdx.x, xs = t >> 2, cg = t & 3;
+  const int X0 = blockIdx.x * NT, gx = X0 + xs;
+  const int Y0 = blockIdx.y * rows, Y1 = min(Y0 + rows, n1);
+  const bool inx = gx < n0;
+  // staged x columns [X0 - 1, X0 + NT + 1) clipped to the grid: strip units [xa, xb)
+  const int xa = X0 == 0 ? 1 : 0, xb = min(NT + 2, n0 - X0 + 1);
+  const int nc = min(NT, n0 - X0);  // owned nodes in the grid
+  const int r0 = Y0 - 1, r1 = Y1;   // staged rows (x halo rows included)
+  // zero the x halo units outside the grid in every slot (never overwritten)
+  for (int p = 0; p < PD; ++p) {
+    float4* xr = reinterpret_cast<float4*>(sm + P::OFF_SLOTS + p * P::SLOT);
+    for (int u = t; u < (NT + 2) * 4; u += P::TH) {
+      const int node = u >> 2;
+      if (node < xa || node >= xb) xr[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  if (t == 0) {
+    for (int p = 0; p < PD; ++p) tma::mbar_init(&bars[p], 1);
+    tma::fence_mbar_init();
+  }
+  tma::fence_proxy_async();
+  __syncthreads();
+  auto produce = [&](int r) {
+    if (r > r1) return;
+    tma::fence_proxy_async();
+    const int u = r - r0, sl = u % PD;
+    unsigned char* slot = sm + P::OFF_SLOTS + sl * P::SLOT;
+    const int rr = min(max(r, 0), n1 - 1);  // rows outside the grid: any finite row (coefficients 0)
+    const bool own = r >= Y0 && r < Y1;
+    const uint32_t xbytes = uint32_t(xb - xa) * kK8 * sizeof(float2);
+    uint32_t tx = xbytes;
+    if (own) tx += uint32_t(nc) * (10 * sizeof(float2) + (MODE == 0 ? 0 : kK8 * sizeof(float2)));
+    tma::mbar_arrive_expect_tx(&bars[sl], tx);
+    tma::bulk_g2s(slot + size_t(xa) * kK8 * sizeof(float2), x + (int64_t(n0) * rr + X0 - 1 + xa) * kK8, xbytes,
+                  &bars[sl]);
+    if (own) {
+      tma::bulk_g2s(slot + P::XROW, op.cd + (int64_t(n0) * r + X0) * 10, uint32_t(nc) * 10 * sizeof(float2),
+                    &bars[sl]);
+      if (MODE != 0)
+        tma::bulk_g2s(slot + P::XROW + P::CROW, b + (int64_t(n0) * r + X0) * kK8,
+                      uint32_t(nc) * kK8 * sizeof(float2), &bars[sl]);
+    }
+  };
+  if (t == 0)
+    for (int p = 0; p < PD && r0 + p <= r1; ++p) produce(r0 + p);
+  auto wait_row = [&](int r) {
+    const int u = r - r0;
+    tma::mbar_wait(&bars[u % PD], uint32_t((u / PD) & 1));
+  };
+  wait_row(r0);
+  for (int j = Y0; j < Y1; ++j) {
+    wait_row(j);
+    wait_row(j + 1);
+    const unsigned char* sj = sm + P::OFF_SLOTS + ((j - r0) % PD) * P::SLOT;
+    const float4* xr[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d)
+      xr[d] = reinterpret_cast<const float4*>(sm + P::OFF_SLOTS + ((j - 1 + d - r0) % PD) * P::SLOT);
+    if (inx) {
+      const float2* cf = reinterpret_cast<const float2*>(sj + P::XROW) + xs * 10;
+      float2 av[9];
+      float4 xv[9];
+#pragma unroll
+      for (int sdx = 0; sdx < 9; ++sdx) {
+        const int dy = sdx / 3 - 1, dx = sdx % 3 - 1;
+        av[sdx] = cf[sdx];
+        xv[sdx] = xr[dy + 1][(xs + 1 + dx) * 4 + cg];
+      }
+      float2 acc[2] = {czero<float2>(), czero<float2>()};
+#pragma unroll
+      for (int sdx = 0; sdx < 9; ++sdx) {
+        acc[0] = cfma(av[sdx], make_float2(xv[sdx].x, xv[sdx].y), acc[0]);
+        acc[1] = cfma(av[sdx], make_float2(xv[sdx].z, xv[sdx].w), acc[1]);
+      }
+      float2 o[2];
+      if (MODE == 0) {
+        o[0] = acc[0];
+        o[1] = acc[1];
+      } else {
+        const float4 bv = reinterpret_cast<const float4*>(sj + P::XROW + P::CROW)[t];
+        const float2 bb[2] = {make_float2(bv.x, bv.y), make_float2(bv.z, bv.w)};
+        if (MODE == 1) {
+          o[0] = csub(bb[0], acc[0]);
+          o[1] = csub(bb[1], acc[1]);
+        } else {
+          const float2 d = cf[9];
+          const float2 wd = mk(wj * d.x, wj * d.y);
+          const float4 xc = xv[4];
+          o[0] = jacobi_upd(make_float2(xc.x, xc.y), wd, bb[0], acc[0]);
+          o[1] = jacobi_upd(make_float2(xc.z, xc.w), wd, bb[1], acc[1]);
+        }
+      }
+      gstore(out + (int64_t(n0) * j + gx) * kK8 + cg * 2, o);
+    }
+    __syncthreads();  // row j-1's slot is free: its last reader was this step
+    if (t == 0) produce(j - 1 + PD);
+  }
+}
+
+#ifndef HZ_S9_NT
+#define HZ_S9_NT 64
+#endif
+#ifndef HZ_S9_PD
+#define HZ_S9_PD 4
+#endif
+int env_int(const char* name, int dflt);
+
+template <int MODE>
+void run_stencil9_k8(const LevelOp<float>& op, float wj, const float2* x, const float2* b, float2* out,
+                     cudaStream_t s) {
+  constexpr int NT = HZ_S9_NT, PD = HZ_S9_PD;
+  using P = S9Plan<MODE, NT, PD>;
+  constexpr int MINB = int(std::min<size_t>(std::min<size_t>((227 * 1024) / (P::BYTES + 1024), 2048 / P::TH), 8));
+  const int strips = int((op.g.n0 + NT - 1) / NT);
+  // rows per CTA: enough CTAs for about one resident wave, at least 4 rows
+  // (measured at level 1 of config 2: 4 rows 12.7 us, 8 rows 14.5, 16 rows
+  // 15.4, the plain kernel 13.3; profiles/r02_stencil9_ab.txt)
+  const int slots = kNumSMs * MINB;
+  const int chunks = std::max(1, slots / std::max(1, strips));
+  const int e = env_int("HZ_S9_ROWS", 0);
+  const int rows = e > 0 ? e : std::max(4, int((op.g.n1 + chunks - 1) / chunks));
+  const dim3 grid(unsigned(strips), unsigned((op.g.n1 + rows - 1) / rows));
+  auto kern = stencil9_k8_kernel<MODE, NT, PD, MINB>;
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
+  kern<<<grid, P::TH, P::BYTES, s>>>(op, wj, x, b, out, rows);
+}
+
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
@@ -1091,6 +1247,21 @@ int fused_nt(int k, int cols_per_cta) {
 }
 
 }  // namespace
+
+bool launch_stencil9_k8(const LevelOp<float>& op, int mode, float wj, const float2* x, const float2* b, float2* out,
+                        cudaStream_t s) {
+  static const bool on = env_int("HZ_S9", 1) != 0;
+  if (!on || op.kind != kStencil || op.ndim != 2 || op.g.k != kK8 || !op.cd || op.g.z0 != 0 ||
+      op.g.z1 != op.g.n1)
+    return false;
+  if (mode == 0)
+    run_stencil9_k8<0>(op, wj, x, b, out, s);
+  else if (mode == 1)
+    run_stencil9_k8<1>(op, wj, x, b, out, s);
+  else
+    run_stencil9_k8<2>(op, wj, x, b, out, s);
+  return true;
+}
 
 bool fused_vcycle_enabled() {
   static const bool on = env_int("HZ_FUSED_VCYCLE", 1) != 0;

@@ -399,6 +399,17 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
     cast(a.center, b.center);
     cast(a.coef, b.coef);
     cast(a.inv_diag, b.inv_diag);
+    if (b.kind == kStencil && h64.ndim_ == 2 && b.coef.size()) {
+      // 2D Galerkin level: (9 coefficients, D^{-1}) per node in one 80-byte
+      // record, so a grid row is one 16-byte-aligned bulk copy (stencil9_k8)
+      const size_t nn = b.inv_diag.size();
+      b.cd.alloc(10 * nn);
+      for (int q = 0; q < 10; ++q) {
+        const float2* src = q < 9 ? b.coef.get() + size_t(q) * nn : b.inv_diag.get();
+        HZ_CUDA(cudaMemcpy2DAsync(b.cd.get() + q, 10 * sizeof(float2), src, sizeof(float2), sizeof(float2), nn,
+                                  cudaMemcpyDeviceToDevice, s));
+      }
+    }
     if (b.kind == kFine && b.center.size()) {
       // (centre, D^{-1}) per node in one 16-byte record: a row of the fine
       // grid is then one 16-byte-aligned bulk copy whatever n0's parity

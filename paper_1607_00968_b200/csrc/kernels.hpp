@@ -29,7 +29,7 @@ struct LevelOp {
   const V* center = nullptr;   // kFine: diagonal (centre) per node
   const V* coef = nullptr;     // kStencil: [S][nodes]
   const V* inv_diag = nullptr; // Jacobi D^{-1} per node
-  const V* cd = nullptr;       // optional: (centre, D^{-1}) interleaved per node (kFine)
+  const V* cd = nullptr;       // optional: (centre, D^{-1}) per node (kFine), (9 planes, D^{-1}) per node (2D kStencil)
   T w[3] = {0, 0, 0};          // kFine off-diagonal weights (0 on flat axes)
   T w27[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // kFine27: lap[0..3], mu[0..3]
   int level = 0;               // multigrid level (profiling names only)
@@ -113,6 +113,12 @@ void launch_shift_mass(int64_t n, const double2* mass, const double* m, double s
 void launch_inv_centre27(int64_t n, double lap0, double mu0, const double2* ms, double2* inv, cudaStream_t s);
 // inv[i] = 1 / planes[centre][i] (Jacobi D^-1 of a stencil level)
 void launch_inv_plane(int64_t n, const double2* centre, double2* inv, cudaStream_t s);
+
+// complex64 2D Galerkin level, k = 8, with bulk-copy row staging (fused.cu):
+// MODE 0 apply, 1 residual, 2 damped Jacobi, bitwise equal to the stencil_v4
+// kernels; returns false when it does not apply (then use dispatch_level)
+bool launch_stencil9_k8(const LevelOp<float>& op, int mode, float wj, const float2* x, const float2* b, float2* out,
+                        cudaStream_t s);
 
 // elementwise casts / copies
 template <class Dst, class Src>

@@ -162,7 +162,8 @@ level_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T>* __
   } else {
     const V d = __ldg(&op.inv_diag[el.node]);
     const V wd = mk(wj * d.x, wj * d.y);
-    out[e] = cadd(__ldg(&x[e]), cmul(wd, csub(__ldg(&b[e]), ax)));
+    out[e] = KIND == kFine ? cadd(__ldg(&x[e]), cmul(wd, csub(__ldg(&b[e]), ax)))
+                           : jacobi_upd(__ldg(&x[e]), wd, __ldg(&b[e]), ax);
   }
 }
 
@@ -321,7 +322,7 @@ stencil_mc_kernel(LevelOp<T> op, const cplx_t<T>* __restrict__ x, const cplx_t<T
     const V wd = mk(wj * d.x, wj * d.y);
 #pragma unroll
     for (int c = 0; c < CPT; ++c)
-      out[e0 + c] = cadd(__ldg(&x[e0 + c]), cmul(wd, csub(__ldg(&b[e0 + c]), acc[c])));
+      out[e0 + c] = jacobi_upd(__ldg(&x[e0 + c]), wd, __ldg(&b[e0 + c]), acc[c]);
   }
 }
 
@@ -427,7 +428,7 @@ __device__ __forceinline__ void stencil_v4_item(const LevelOp<T>& op, const cplx
     const V d = __ldg(&op.inv_diag[node]);
     const V wd = mk(wj * d.x, wj * d.y);
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) o[c] = cadd(xc[c], cmul(wd, csub(bv[c], acc[c])));
+    for (int c = 0; c < CPT; ++c) o[c] = jacobi_upd(xc[c], wd, bv[c], acc[c]);
   }
   st4(out + e0, o);
 }
@@ -514,7 +515,7 @@ __device__ __forceinline__ void fine27_item(const LevelOp<T>& op, const cplx_t<T
     const V d = __ldg(&op.inv_diag[node]);
     const V wd = mk(wj * d.x, wj * d.y);
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) o[c] = cadd(__ldg(x + e0 + c), cmul(wd, csub(__ldg(b + e0 + c), acc[c])));
+    for (int c = 0; c < CPT; ++c) o[c] = jacobi_upd(__ldg(x + e0 + c), wd, __ldg(b + e0 + c), acc[c]);
   }
   if constexpr (CPT == 4) {
     st4(out + e0, o);
@@ -1008,6 +1009,23 @@ int64_t stencil_v4_min_elems() {
   return v;
 }
 
+// the bulk-copy 2D Galerkin kernel for levels of at least HZ_S9_MIN_NODES
+// nodes (smaller levels are latency bound: the plain kernel starts faster)
+template <class T, int MODE>
+bool stencil9_bulk(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out, T wj,
+                   cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value) {
+    static const int64_t min_nodes = [] {
+      const char* e = std::getenv("HZ_S9_MIN_NODES");
+      return e ? int64_t(std::atoll(e)) : int64_t(20000);
+    }();
+    if (int64_t(op.g.nodes) < min_nodes) return false;
+    return launch_stencil9_k8(op, MODE, wj, x, b, out, s);
+  } else {
+    return false;
+  }
+}
+
 template <class T, int MODE>
 void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out,
                     T wj, cudaStream_t s) {
@@ -1036,6 +1054,8 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
       level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
     else
       level_kernel<T, 2, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+  } else if (stencil9_bulk<T, MODE>(op, x, b, out, wj, s)) {
+    // complex64 2D Galerkin level, k = 8: bulk-copy row staging (fused.cu)
   } else if (op.g.k % 4 == 0 && total >= stencil_v4_min_elems()) {
     const int g4 = grid_for(total / 4, kBlock);
     static const int variant = [] {

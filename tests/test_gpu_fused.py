@@ -89,6 +89,20 @@ def test_k8_bulk_copy_kernels_equal_streaming_kernels(nx, nz, nl, chunk):
     assert np.array_equal(new, old), f"max rel diff {rel_err(new, old):.3e}"
 
 
+@pytest.mark.parametrize("nx,nz,nl,kind", [(257, 129, 4, "V"), (1025, 513, 5, "V"), (301, 97, 3, "W"),
+                                          (121, 233, 4, "K")])
+def test_bulk_copy_galerkin_level_kernel_equals_plain(nx, nz, nl, kind):
+    """complex64 2D Galerkin levels at k = 8: the bulk-copy row-staged
+    kernel (stencil9_k8, all levels via HZ_S9_MIN_NODES=0) against the plain
+    stencil kernels (HZ_S9=0), bitwise, through whole V / W / K cycles."""
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(CYCLE, os.path.join(d, "n.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9_MIN_NODES="0")
+        old = _run(CYCLE, os.path.join(d, "o.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9="0")
+        odd = _run(CYCLE, os.path.join(d, "r.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9_ROWS="3")
+    assert np.array_equal(new, old), f"max rel diff {rel_err(new, old):.3e}"
+    assert np.array_equal(odd, old)
+
+
 def test_fused_c128_cycle_matches_reference():
     """c128 V(2,2) cycle through the fused fine level vs the compiled
     reference's MgHierarchy::cycle at the 1e-12 parity bar."""
