@@ -1010,14 +1010,16 @@ int64_t stencil_v4_min_elems() {
 }
 
 // the bulk-copy 2D Galerkin kernel for levels of at least HZ_S9_MIN_NODES
-// nodes (smaller levels are latency bound: the plain kernel starts faster)
+// nodes (default 100,000: level 1 of config 2, 131k nodes, 12.7 vs 13.3 us;
+// level 2, 33k nodes, 9.4 vs 8.6 us -- smaller levels are latency bound and the
+// plain kernel starts faster)
 template <class T, int MODE>
 bool stencil9_bulk(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out, T wj,
                    cudaStream_t s) {
   if constexpr (std::is_same<T, float>::value) {
     static const int64_t min_nodes = [] {
       const char* e = std::getenv("HZ_S9_MIN_NODES");
-      return e ? int64_t(std::atoll(e)) : int64_t(20000);
+      return e ? int64_t(std::atoll(e)) : int64_t(100000);
     }();
     if (int64_t(op.g.nodes) < min_nodes) return false;
     return launch_stencil9_k8(op, MODE, wj, x, b, out, s);

@@ -25,6 +25,14 @@ def algorithmic(k):
         # restart update X += Z Y reads nb c64 blocks and X
         nb = int(m.group(1))
         return (nb + 1) * N * K * 16 if m.group(2) == "double" else nb * N * K * 8 + 2 * N * K * 16
+    if "fused_pre_k8_kernel<" in k:
+        return N * (K * (16 + 8) + 16) + NC * K * 8
+    if "fused_post_k8_kernel<" in k:
+        return N * (K * (8 + 16 + 8) + 16) + NC * K * 8
+    m = re.search(r"stencil9_k8_kernel<(\d)", k)
+    if m:  # level-1 Galerkin sweep (2) / residual (1) / apply (0)
+        mode = int(m.group(1))
+        return NC * ((2 if mode == 0 else 3) * K * 8 + (9 + (1 if mode == 2 else 0)) * 8)
     if "fused_pre_kernel<float" in k:
         return N * (K * (16 + 8) + 16) + NC * K * 8
     if "fused_post_kernel<float" in k:
@@ -45,6 +53,13 @@ def name_of(k):
         return "multi_gram_c128"
     if "apply_lo_kernel" in k:
         return "apply_fine_c128"
+    if "fused_pre_k8_kernel<" in k:
+        return "fused_pre_fine_c64"
+    if "fused_post_k8_kernel<" in k:
+        return "fused_post_fine_c64"
+    m = re.search(r"stencil9_k8_kernel<(\d)", k)
+    if m:
+        return {0: "apply_stencil_c64_L1", 1: "residual_stencil_c64_L1", 2: "jacobi_stencil_c64_L1"}[int(m.group(1))]
     if "fused_pre_kernel<float" in k:
         return "fused_pre_fine_c64"
     if "fused_post_kernel<float" in k:
