@@ -274,6 +274,44 @@ void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, co
   HZ_LAUNCH_CHECK();
 }
 
+namespace {
+// B[i][q] = (i == c0 + q) for the chunk's k columns
+__global__ void unit_columns_kernel(int64_t n, int k, int64_t c0, double2* __restrict__ B) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= n * k) return;
+  const int64_t i = e / k;
+  const int q = int(e - i * k);
+  B[e] = make_double2(i == c0 + q ? 1.0 : 0.0, 0.0);
+}
+// ainvT[c0 + q][i] = X[i][q]  (row stride ld)
+__global__ void chunk_transpose_kernel(int64_t n, int k, int64_t c0, const double2* __restrict__ X,
+                                       double2* __restrict__ ainvT, int64_t ld) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= n * k) return;
+  const int64_t i = e / k;
+  const int q = int(e - i * k);
+  if (c0 + q < n) ainvT[(c0 + q) * ld + i] = X[e];
+}
+}  // namespace
+
+DevBuf<double2> bt_explicit_inverse(const LevelGeom& g, const double2* coef, const double2* ET, const double2* FT,
+                                    cudaStream_t s) {
+  const int64_t n = int64_t(g.nodes), m = int64_t(g.n0) * g.n1;
+  constexpr int K = 64;
+  DevBuf<double2> out(size_t(n) * inv_ld(n));
+  DevBuf<double2> B(size_t(n) * K), X(size_t(n) * K), r(size_t(m) * K),
+      part(size_t(std::max(coarse_split(m, K), 1)) * m * K);
+  const LevelGeom gk(g.n0, g.n1, g.n2, K);
+  for (int64_t c0 = 0; c0 < n; c0 += K) {
+    unit_columns_kernel<<<grid_for(n * K, 256), 256, 0, s>>>(n, K, c0, B.get());
+    bt_solve<double>(gk, coef, ET, FT, K, B.get(), X.get(), r.get(), part.get(), s);
+    chunk_transpose_kernel<<<grid_for(n * K, 256), 256, 0, s>>>(n, K, c0, X.get(), out.get(), inv_ld(n));
+  }
+  HZ_LAUNCH_CHECK();
+  HZ_CUDA(cudaStreamSynchronize(s));
+  return out;
+}
+
 template void bt_solve<double>(const LevelGeom&, const double2*, const double2*, const double2*, int,
                                const double2*, double2*, double2*, double2*, cudaStream_t);
 template void bt_solve<float>(const LevelGeom&, const float2*, const float2*, const float2*, int, const float2*,

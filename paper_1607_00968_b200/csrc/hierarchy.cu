@@ -294,6 +294,18 @@ std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, in
       H->bt_ET_.alloc(sz);
       H->bt_FT_.alloc(sz);
       bt_factor(gc, Lc.coef.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
+      // Moderate coarse grids (config 3: 33x33x17): the explicit inverse,
+      // formed once from the plane factors (A X = I in 64-column chunks), makes
+      // every coarse solve one streaming product instead of 2 n2 - 1 dependent
+      // plane steps (HZ_BT_INVERSE_MAX nodes; 0 keeps the plane solve)
+      const char* inv_env = std::getenv("HZ_BT_INVERSE_MAX");
+      const int64_t inv_max = inv_env ? int64_t(std::atoll(inv_env)) : int64_t(0);
+      if (nc <= inv_max) {
+        H->ainvT_ = bt_explicit_inverse(gc, Lc.coef.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
+        H->bt_ = false;
+        H->bt_ET_ = DevBuf<double2>();
+        H->bt_FT_ = DevBuf<double2>();
+      }
       return H;
     }
   }

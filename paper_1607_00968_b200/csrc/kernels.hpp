@@ -149,6 +149,7 @@ void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, co
 // (coarse_bt.cu): ET/FT = [n2][m][inv_ld(m)] transposed plane blocks,
 // m = n0*n1; g.k unused. Solve scratch: r (m*k), part (split partials).
 void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s);
+
 template <class T>
 void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, const cplx_t<T>* FT, int k,
               const cplx_t<T>* b, cplx_t<T>* x, cplx_t<T>* r, cplx_t<T>* part, cudaStream_t s);

@@ -59,6 +59,11 @@ struct Problem {
   LevelOp<double> fine_op(int k) const;  // unshifted, for apply / residual
 };
 
+// explicit inverse of a 3D coarse level (transposed, row stride inv_ld(n))
+// from its block-tridiagonal plane factors (coarse_bt.cu)
+DevBuf<double2> bt_explicit_inverse(const LevelGeom& g, const double2* coef, const double2* ET, const double2* FT,
+                                    cudaStream_t s);
+
 // ------------------------------------------------------------------ cycles
 enum class CycleKind : int { V = 0, W = 1, K = 2 };
 
