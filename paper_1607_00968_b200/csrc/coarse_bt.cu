@@ -11,14 +11,18 @@
 //            S_{j+1} = D_{j+1} - L_{j+1} F_j
 //   forward: y_0 = E_0 b_0;  y_j = E_j (b_j - L_j y_{j-1})
 //   back:    x_{last} = y_{last};  x_j = y_j - F_j x_{j+1}
-// E_j and F_j are dense (stored transposed for the coarse GEMM kernel);
+// E_j and F_j are dense, stored row-major (row = output node of the plane) for
+// planes up to 2 x 148 x 8 nodes and transposed for the coarse GEMM above;
 // L_j, U_j are read straight from the Galerkin stencil planes. Block LU
 // without inter-plane pivoting on the shifted (complex, absorbing) operator;
 // each S_j is inverted by Gauss-Jordan with partial pivoting. Agreement with
 // the reference's banded LU is to cond(A_c) * eps (tested).
 #include <cmath>
+#include <cstdlib>
+#include <type_traits>
 #include <vector>
 
+#include "block_tiled.cuh"
 #include "devbuf.hpp"
 #include "kernels.hpp"
 #include "profile.hpp"
@@ -180,14 +184,6 @@ __global__ void schur_kernel(LevelGeom g, const double2* __restrict__ coef, int 
   S[e] = s;
 }
 
-// dst[c][r] = src[r][c] with row stride ld (transposed copy for the GEMM)
-__global__ void transpose_kernel(int64_t m, const double2* __restrict__ src, double2* __restrict__ dst, int64_t ld) {
-  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
-  if (e >= m * m) return;
-  const int64_t r = e / m, c = e - r * m;
-  dst[c * ld + r] = src[e];
-}
-
 // r = b_j - L_j y_{j-1} for one plane, all k columns
 template <class T>
 __global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, int j, const cplx_t<T>* __restrict__ b,
@@ -211,9 +207,191 @@ __global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, i
   r[e] = s;
 }
 
+// dst[c][r] = src[r][c] with row stride ld (transposed copy for the GEMM)
+__global__ void transpose_kernel(int64_t m, const double2* __restrict__ src, double2* __restrict__ dst, int64_t ld) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= m * m) return;
+  const int64_t r = e / m, c = e - r * m;
+  dst[c * ld + r] = src[e];
+}
+
+// dst[r][c] = src[r][c] with row stride ld
+__global__ void strided_copy_kernel(int64_t m, const double2* __restrict__ src, double2* __restrict__ dst,
+                                    int64_t ld) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= m * m) return;
+  const int64_t r = e / m, c = e - r * m;
+  dst[r * ld + c] = src[e];
+}
+
+template <class V>
+__device__ __forceinline__ void cp_async_elem(V* smem, const V* gmem) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if constexpr (sizeof(V) == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gmem));
+}
+
+// One plane step out = c_in + sign * (P r) with P = E_j or F_j (m x m,
+// row-major, row stride ld) and r an m x k block, for KG of its columns
+// (blockIdx.y = column group); used for small planes (bt_rowmajor), where
+// the split-K GEMM + reduce pair is launch/latency bound. Each warp owns one
+// plane row (two above 2 x 148 x 8 rows) and the whole reduction over l:
+// lanes stride l, the row of P streams from HBM coalesced (next chunk's loads
+// issued before the current chunk's math), the chunk of r (LC nodes x KG
+// columns, column-major in shared memory) is staged once per CTA by cp.async
+// (double-buffered) and read conflict-free by all 8 warps; lane partial sums
+// meet in an xor butterfly, so no split-K partials and no second launch.
+// Deterministic: fixed per-lane order, fixed butterfly.
+template <class T, int RW, int KG, int LC>
+__global__ void __launch_bounds__(256)
+bt_rows_kernel(int64_t m, int k, const cplx_t<T>* __restrict__ P, int64_t ld, const cplx_t<T>* __restrict__ r,
+               cplx_t<T>* out, const cplx_t<T>* c_in, T sign) {
+  using V = cplx_t<T>;
+  constexpr int U = LC / 32;
+  __shared__ __align__(16) V rs[2][KG * LC];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int64_t i0 = int64_t(blockIdx.x) * (8 * RW);
+  const int q0 = blockIdx.y * KG;
+  const int nch = int((m + LC - 1) / LC);
+  int64_t row[RW];
+  bool live[RW];
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    row[t] = i0 + w + 8 * t;
+    live[t] = row[t] < m;
+  }
+  auto stage = [&](int c, V* dst) {
+    const int64_t l0 = int64_t(c) * LC;
+    for (int e = tid; e < LC * KG; e += 256) {
+      const int l = e / KG, q = e - l * KG;
+      if (l0 + l < m)
+        cp_async_elem(dst + q * LC + l, r + (l0 + l) * k + q0 + q);
+      else
+        dst[q * LC + l] = czero<V>();
+    }
+  };
+  auto load_p = [&](int c, V (&pv)[RW][U]) {
+    const int64_t l0 = int64_t(c) * LC;
+#pragma unroll
+    for (int t = 0; t < RW; ++t)
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t l = l0 + lane + 32 * u;
+        pv[t][u] = (live[t] && l < m) ? P[row[t] * ld + l] : czero<V>();
+      }
+  };
+  V acc[RW][KG];
+#pragma unroll
+  for (int t = 0; t < RW; ++t)
+#pragma unroll
+    for (int q = 0; q < KG; ++q) acc[t][q] = czero<V>();
+  V pc[RW][U], pn[RW][U];
+  stage(0, rs[0]);
+  tiled::cp_async_commit();
+  load_p(0, pc);
+  for (int c = 0; c < nch; ++c) {
+    if (c + 1 < nch) {
+      stage(c + 1, rs[(c + 1) & 1]);
+      load_p(c + 1, pn);
+    }
+    tiled::cp_async_commit();
+    tiled::cp_async_wait<1>();
+    __syncthreads();
+    const V* b = rs[c & 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+#pragma unroll
+      for (int q = 0; q < KG; ++q) {
+        const V rv = b[q * LC + lane + 32 * u];
+#pragma unroll
+        for (int t = 0; t < RW; ++t) acc[t][q] = cfma(pc[t][u], rv, acc[t][q]);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < RW; ++t)
+#pragma unroll
+      for (int u = 0; u < U; ++u) pc[t][u] = pn[t][u];
+  }
+  tiled::cp_async_wait<0>();
+#pragma unroll
+  for (int t = 0; t < RW; ++t)
+#pragma unroll
+    for (int q = 0; q < KG; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[t][q].x += __shfl_xor_sync(0xffffffffu, acc[t][q].x, o);
+        acc[t][q].y += __shfl_xor_sync(0xffffffffu, acc[t][q].y, o);
+      }
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    if (!live[t]) continue;
+#pragma unroll
+    for (int q = 0; q < KG; ++q) {
+      if (lane != q) continue;
+      V v = acc[t][q];
+      const int64_t o = row[t] * k + q0 + q;
+      if (c_in) {
+        const V cv = c_in[o];
+        v = mk(cv.x + sign * v.x, cv.y + sign * v.y);
+      }
+      out[o] = v;
+    }
+  }
+}
+
+template <class T, int RW, int KG>
+void bt_rows_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
+                const cplx_t<T>* c_in, T sign, cudaStream_t s) {
+  constexpr int LC = sizeof(T) == 8 ? 128 : 256;  // r chunk: 32 KB of static shared memory, double-buffered
+  const dim3 grid(unsigned((m + 8 * RW - 1) / (8 * RW)), unsigned(k / KG));
+  bt_rows_kernel<T, RW, KG, LC><<<grid, 256, 0, s>>>(m, k, P, ld, r, out, c_in, sign);
+}
+
+template <class T>
+void bt_rows(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
+             const cplx_t<T>* c_in, T sign, cudaStream_t s) {
+  const bool two = m > int64_t(kNumSMs) * 8;
+  auto go = [&](auto kg) {
+    constexpr int KG = decltype(kg)::value;
+    if (two)
+      bt_rows_go<T, 2, KG>(m, k, P, ld, r, out, c_in, sign, s);
+    else
+      bt_rows_go<T, 1, KG>(m, k, P, ld, r, out, c_in, sign, s);
+  };
+  if (k % 8 == 0)
+    go(std::integral_constant<int, 8>());
+  else if (k % 4 == 0)
+    go(std::integral_constant<int, 4>());
+  else if (k % 2 == 0)
+    go(std::integral_constant<int, 2>());
+  else
+    go(std::integral_constant<int, 1>());
+}
+
+// out = c_in + sign * P r for one plane block: row-major P and the row-owner
+// kernel for small planes, P^T (stored transposed) and the split-K coarse
+// GEMM above that size, where the GEMM's register tile is the better
+// FP32-issue/HBM balance (profiles/r02_bt_rows_ab.txt)
+template <class T>
+void bt_step(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
+             const cplx_t<T>* c_in, T sign, cplx_t<T>* part, cudaStream_t s) {
+  if (bt_rowmajor(m))
+    bt_rows<T>(m, k, P, ld, r, out, c_in, sign, s);
+  else
+    launch_coarse_gemm<T>(m, k, P, ld, r, out, c_in, sign, part, s);
+}
+
 }  // namespace
 
-// ---- setup: E_j^T and F_j^T (f64), row stride inv_ld(m)
+bool bt_rowmajor(int64_t m) {
+  const char* e = std::getenv("HZ_BT_ROWS_MAX");
+  return m <= (e ? int64_t(std::atoll(e)) : int64_t(2) * kNumSMs * 8);
+}
+
+// ---- setup: E_j and F_j (f64, row-major), row stride inv_ld(m)
 void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s) {
   const int64_t m = int64_t(g.n0) * g.n1;
   const int np = int(g.n2);
@@ -237,10 +415,16 @@ void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT
     for (int64_t p = 0; p < m; ++p)
       if (hpiv[p] < 0) throw HzError(kFactorization, "block-tridiagonal coarse solve: singular plane block");
     // S now holds E_j
-    transpose_kernel<<<gmm, 256, 0, s>>>(m, S.get(), ET + int64_t(j) * m * ld, ld);
+    if (bt_rowmajor(m))
+      strided_copy_kernel<<<gmm, 256, 0, s>>>(m, S.get(), ET + int64_t(j) * m * ld, ld);
+    else
+      transpose_kernel<<<gmm, 256, 0, s>>>(m, S.get(), ET + int64_t(j) * m * ld, ld);
     if (j + 1 < np) {
       mul_eu_kernel<<<gmm, 256, 0, s>>>(g, coef, j, S.get(), F.get());
-      transpose_kernel<<<gmm, 256, 0, s>>>(m, F.get(), FT + int64_t(j) * m * ld, ld);
+      if (bt_rowmajor(m))
+        strided_copy_kernel<<<gmm, 256, 0, s>>>(m, F.get(), FT + int64_t(j) * m * ld, ld);
+      else
+        transpose_kernel<<<gmm, 256, 0, s>>>(m, F.get(), FT + int64_t(j) * m * ld, ld);
       build_block_kernel<<<gmm, 256, 0, s>>>(g, coef, j + 1, 0, S.get());
       schur_kernel<<<gmm, 256, 0, s>>>(g, coef, j + 1, F.get(), S.get());
     }
@@ -262,15 +446,14 @@ void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, co
   ProfScope prof(sizeof(T) == 8 ? "coarse_bt_c128" : "coarse_bt_c64",
                  (2.0 * np - 1.0) * double(m) * m * sizeof(V), s, 8.0 * (2.0 * np - 1.0) * double(m) * m * k);
   // forward: x holds y
-  launch_coarse_gemm<T>(m, k, ET, ld, b, x, nullptr, T(1), part, s);
+  bt_step<T>(m, k, ET, ld, b, x, nullptr, T(1), part, s);
   for (int j = 1; j < np; ++j) {
     couple_kernel<T><<<grid_for(pk, 256), 256, 0, s>>>(gk, coef, j, b + j * pk, x + (j - 1) * pk, r, k);
-    launch_coarse_gemm<T>(m, k, ET + int64_t(j) * m * ld, ld, r, x + j * pk, nullptr, T(1), part, s);
+    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, r, x + j * pk, nullptr, T(1), part, s);
   }
   // backward: x_j = y_j - F_j x_{j+1}
   for (int j = np - 2; j >= 0; --j)
-    launch_coarse_gemm<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j + 1) * pk, x + j * pk, x + j * pk, T(-1),
-                          part, s);
+    bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j + 1) * pk, x + j * pk, x + j * pk, T(-1), part, s);
   HZ_LAUNCH_CHECK();
 }
 

@@ -146,8 +146,12 @@ void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, co
                         const cplx_t<T>* c_in, T sign, cplx_t<T>* part, cudaStream_t s);
 
 // Block-tridiagonal (plane) direct solver of a 3D coarsest Galerkin operator
-// (coarse_bt.cu): ET/FT = [n2][m][inv_ld(m)] transposed plane blocks,
+// (coarse_bt.cu): ET/FT = [n2][m][inv_ld(m)] plane blocks E_j, F_j: row-major
+// when bt_rowmajor(m) (the row-owner kernel), else transposed (coarse GEMM);
 // m = n0*n1; g.k unused. Solve scratch: r (m*k), part (split partials).
+// planes up to 2 x 148 x 8 nodes (HZ_BT_ROWS_MAX overrides) use the row-major
+// layout; read when the factor is built and at every solve
+bool bt_rowmajor(int64_t m);
 void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s);
 
 template <class T>

@@ -181,14 +181,18 @@ def test_rank_deficient_block_matches_reference(ref):
     assert rel_err(X[:, 2], X[:, 0]) <= 1e-12  # coincident sources, identical columns
 
 
-@pytest.mark.parametrize("inverse", ["0", "40000"])
+@pytest.mark.parametrize("inverse,rows", [("0", None), ("0", "0"), ("40000", None)])
 @pytest.mark.parametrize("n,nl", [((17, 17, 9), 2), ((33, 33, 17), 3), ((33, 17, 17), 2)])
-def test_block_tridiagonal_coarse_solve_matches_reference(ref, n, nl, inverse, monkeypatch):
+def test_block_tridiagonal_coarse_solve_matches_reference(ref, n, nl, inverse, rows, monkeypatch):
     """The plane block-tridiagonal coarsest solver (coarse_bt.cu) against the
     reference's banded LU (MgHierarchy::coarse_solve, src/multigrid.cpp:114-117);
-    inverse = 40000: the explicit inverse formed from the plane factors."""
+    rows = "0": transposed planes + split-K GEMM (the large-plane layout) instead
+    of the row-owner kernel; inverse = 40000: the explicit inverse formed from
+    the plane factors."""
     monkeypatch.setenv("HZ_COARSE", "bt")
     monkeypatch.setenv("HZ_BT_INVERSE_MAX", inverse)
+    if rows is not None:
+        monkeypatch.setenv("HZ_BT_ROWS_MAX", rows)
     cfg = configs.small_problem(3, n, seed=3)
     P = hz.HelmholtzProblem.from_config(cfg)
     S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
