@@ -291,17 +291,19 @@ DevOp<double> make_op_with(hz_solver* s, Hierarchy<double>* h64, Hierarchy<float
     op.prec = [spec, h32](const double2* in, double2* out, int kk, cudaStream_t st) {
       h32->cycle_cast_graph(*spec, kk, in, out, st);
     };
-    if (P->stencil == 7) {  // complex64 Z blocks: the fine apply widens them on load
+    {  // complex64 Z blocks: the fine apply widens them on load
+      if (P->stencil != 7) op.lo_ok = [P](int kk) { return stream3d_ok(P->fine_op(kk)); };
       op.prec_lo = [spec, h32](const double2* in, float2* out, int kk, cudaStream_t st) {
         h32->cycle_cast_graph(*spec, kk, in, out, st);
       };
       op.apply_lo = [P](const float2* in, double2* out, int kk, cudaStream_t st) {
         launch_apply_lo(P->fine_op(kk), in, out, st);
       };
-      op.apply_lo_gram = [P](const float2* Z, double2* W, const BlockTab<double>& X, int nb, double2* part,
-                             int max_slots, cudaStream_t st) {
-        return launch_gram8_apply(P->fine_op(8), nb, X, Z, W, part, max_slots, st);
-      };
+      if (P->stencil == 7)
+        op.apply_lo_gram = [P](const float2* Z, double2* W, const BlockTab<double>& X, int nb, double2* part,
+                               int max_slots, cudaStream_t st) {
+          return launch_gram8_apply(P->fine_op(8), nb, X, Z, W, part, max_slots, st);
+        };
     }
   }
   else

@@ -391,6 +391,101 @@ bool bt_rowmajor(int64_t m) {
   return m <= (e ? int64_t(std::atoll(e)) : int64_t(2) * kNumSMs * 8);
 }
 
+// ---- sweep-axis permutation
+// The factors hold 2 n_planes m^2 complex values with m the nodes per plane, so
+// the solve streams N * m values: it pays to sweep along the LONGEST axis
+// (planes of the two shortest). A 65 x 65 x 33 coarsest grid swept along y has
+// planes of 65 x 33 = 2,145 nodes instead of 4,225: half the factor bytes
+// per solve and a quarter of the Gauss-Jordan setup flops. The operator and
+// the vectors are re-indexed onto the permuted grid (new axis a = old axis
+// perm[a]); the solve itself is unchanged.
+namespace {
+struct Perm3 {
+  int p[3];
+  uint32_t n[3];  // old dims
+};
+__device__ __forceinline__ int64_t old_node(const Perm3& pm, const LevelGeom& gT, uint32_t nodeT) {
+  uint32_t cT[3];
+  gT.unpack(nodeT, cT[0], cT[1], cT[2]);
+  uint32_t c[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) c[pm.p[a]] = cT[a];
+  return int64_t(c[0]) + int64_t(pm.n[0]) * (int64_t(c[1]) + int64_t(pm.n[1]) * c[2]);
+}
+__global__ void permute_coef_kernel(LevelGeom gT, Perm3 pm, const double2* __restrict__ coef,
+                                    double2* __restrict__ coefT) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= int64_t(27) * gT.nodes) return;
+  const int sT = int(e / gT.nodes);
+  const uint32_t nodeT = uint32_t(e - int64_t(sT) * gT.nodes);
+  const int dT[3] = {sT % 3 - 1, (sT / 3) % 3 - 1, sT / 9 - 1};
+  int d[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < 3; ++a) d[pm.p[a]] = dT[a];
+  coefT[e] = coef[int64_t(plane_s(d[0], d[1], d[2])) * gT.nodes + old_node(pm, gT, nodeT)];
+}
+// INV = false: dst[nodeT] = src[node]; true: dst[node] = src[nodeT] (k columns each)
+template <class V, bool INV>
+__global__ void permute_vec_kernel(LevelGeom gT, Perm3 pm, int k, const V* __restrict__ src, V* __restrict__ dst) {
+  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (e >= int64_t(gT.nodes) * k) return;
+  const uint32_t nodeT = uint32_t(e / k);
+  const int q = int(e - int64_t(nodeT) * k);
+  const int64_t o = old_node(pm, gT, nodeT) * k + q;
+  if (INV)
+    dst[o] = src[e];
+  else
+    dst[e] = src[o];
+}
+Perm3 make_perm(const LevelGeom& g, const int* perm) {
+  Perm3 pm;
+  for (int a = 0; a < 3; ++a) pm.p[a] = perm[a];
+  pm.n[0] = g.n0;
+  pm.n[1] = g.n1;
+  pm.n[2] = g.n2;
+  return pm;
+}
+}  // namespace
+
+void bt_sweep_perm(const int64_t* dims, int* perm) {
+  // sweep along the longest axis (ties: the slowest), the others in order
+  int sweep = 2;
+  for (int a = 1; a >= 0; --a)
+    if (dims[a] > dims[sweep]) sweep = a;
+  int q = 0;
+  for (int a = 0; a < 3; ++a)
+    if (a != sweep) perm[q++] = a;
+  perm[2] = sweep;
+  const char* e = std::getenv("HZ_BT_PERMUTE");
+  if (e && e[0] == '0') perm[0] = 0, perm[1] = 1, perm[2] = 2;
+}
+
+LevelGeom bt_permuted_geom(const LevelGeom& g, const int* perm) {
+  const int64_t n[3] = {g.n0, g.n1, g.n2};
+  return LevelGeom(n[perm[0]], n[perm[1]], n[perm[2]], int(g.k));
+}
+
+void bt_permute_coef(const LevelGeom& g, const int* perm, const double2* coef, double2* coefT, cudaStream_t s) {
+  const LevelGeom gT = bt_permuted_geom(g, perm);
+  permute_coef_kernel<<<grid_for(int64_t(27) * g.nodes, 256), 256, 0, s>>>(gT, make_perm(g, perm), coef, coefT);
+  HZ_LAUNCH_CHECK();
+}
+
+template <class T>
+void bt_permute_vec(const LevelGeom& g, const int* perm, int k, bool inverse, const cplx_t<T>* src, cplx_t<T>* dst,
+                    cudaStream_t s) {
+  using V = cplx_t<T>;
+  const LevelGeom gT = bt_permuted_geom(g, perm);
+  const int grid = grid_for(int64_t(g.nodes) * k, 256);
+  if (inverse)
+    permute_vec_kernel<V, true><<<grid, 256, 0, s>>>(gT, make_perm(g, perm), k, src, dst);
+  else
+    permute_vec_kernel<V, false><<<grid, 256, 0, s>>>(gT, make_perm(g, perm), k, src, dst);
+  HZ_LAUNCH_CHECK();
+}
+template void bt_permute_vec<double>(const LevelGeom&, const int*, int, bool, const double2*, double2*, cudaStream_t);
+template void bt_permute_vec<float>(const LevelGeom&, const int*, int, bool, const float2*, float2*, cudaStream_t);
+
 // ---- setup: E_j and F_j (f64, row-major), row stride inv_ld(m)
 void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s) {
   const int64_t m = int64_t(g.n0) * g.n1;

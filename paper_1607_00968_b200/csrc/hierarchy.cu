@@ -288,18 +288,31 @@ std::unique_ptr<Hierarchy<double>> Hierarchy<double>::build(const Problem& p, in
     if (mode && std::string(mode) == "dense") bt = false;
     if (bt) {
       const LevelGeom gc(Lc.dims[0], Lc.dims[1], Lc.dims[2], 1);
-      const int64_t m = Lc.dims[0] * Lc.dims[1];
-      const size_t sz = size_t(Lc.dims[2]) * m * inv_ld(m);
-      H->bt_ = true;
-      H->bt_ET_.alloc(sz);
-      H->bt_FT_.alloc(sz);
-      bt_factor(gc, Lc.coef.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
       // Moderate coarse grids (config 3: 33x33x17): the explicit inverse,
       // formed once from the plane factors (A X = I in 64-column chunks), makes
       // every coarse solve one streaming product instead of 2 n2 - 1 dependent
       // plane steps (HZ_BT_INVERSE_MAX nodes; 0 keeps the plane solve)
       const char* inv_env = std::getenv("HZ_BT_INVERSE_MAX");
       const int64_t inv_max = inv_env ? int64_t(std::atoll(inv_env)) : int64_t(0);
+      // the plane solve sweeps along the longest axis (coarse_bt.cu)
+      if (nc > inv_max) bt_sweep_perm(Lc.dims.data(), H->bt_perm_);
+      H->bt_ = true;
+      if (H->bt_permuted()) {
+        const LevelGeom gT = bt_permuted_geom(gc, H->bt_perm_);
+        const int64_t m = int64_t(gT.n0) * gT.n1;
+        const size_t sz = size_t(gT.n2) * m * inv_ld(m);
+        H->bt_coef_.alloc(size_t(27) * nc);
+        bt_permute_coef(gc, H->bt_perm_, Lc.coef.get(), H->bt_coef_.get(), s);
+        H->bt_ET_.alloc(sz);
+        H->bt_FT_.alloc(sz);
+        bt_factor(gT, H->bt_coef_.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
+        return H;
+      }
+      const int64_t m = Lc.dims[0] * Lc.dims[1];
+      const size_t sz = size_t(Lc.dims[2]) * m * inv_ld(m);
+      H->bt_ET_.alloc(sz);
+      H->bt_FT_.alloc(sz);
+      bt_factor(gc, Lc.coef.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
       if (nc <= inv_max) {
         H->ainvT_ = bt_explicit_inverse(gc, Lc.coef.get(), H->bt_ET_.get(), H->bt_FT_.get(), s);
         H->bt_ = false;
@@ -422,7 +435,7 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
                                   cudaMemcpyDeviceToDevice, s));
       }
     }
-    if (b.kind == kFine && b.center.size()) {
+    if ((b.kind == kFine || b.kind == kFine27) && b.center.size()) {
       // (centre, D^{-1}) per node in one 16-byte record: a row of the fine
       // grid is then one 16-byte-aligned bulk copy whatever n0's parity
       const size_t nn = b.center.size();
@@ -440,6 +453,8 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
   };
   cast_all(h64.ainvT_, H->ainvT_);
   H->bt_ = h64.bt_;
+  for (int a = 0; a < 3; ++a) H->bt_perm_[a] = h64.bt_perm_[a];
+  cast_all(h64.bt_coef_, H->bt_coef_);
   cast_all(h64.bt_ET_, H->bt_ET_);
   cast_all(h64.bt_FT_, H->bt_FT_);
   HZ_CUDA(cudaStreamSynchronize(s));
@@ -532,6 +547,8 @@ std::unique_ptr<Hierarchy<T>> Hierarchy<T>::share() const {
     alias(A.cd, B.cd);
   }
   alias(ainvT_, H->ainvT_);
+  for (int a = 0; a < 3; ++a) H->bt_perm_[a] = bt_perm_[a];
+  alias(bt_coef_, H->bt_coef_);
   alias(bt_ET_, H->bt_ET_);
   alias(bt_FT_, H->bt_FT_);
   return H;
@@ -602,9 +619,14 @@ void Hierarchy<T>::ensure_ws(int k) {
   const int64_t nc = coarse_n();
   if (bt_) {
     const auto& Lc = levels_.back();
-    const int64_t m = Lc.dims[0] * Lc.dims[1];
+    const LevelGeom gT = bt_permuted_geom(LevelGeom(Lc.dims[0], Lc.dims[1], Lc.dims[2], k), bt_perm_);
+    const int64_t m = int64_t(gT.n0) * gT.n1;
     cpart_.alloc(size_t(std::max(coarse_split(m, k), 1)) * m * k);
     bt_r_.alloc(size_t(m) * k);
+    if (bt_permuted()) {
+      bt_b_.alloc(size_t(nc) * k);
+      bt_x_.alloc(size_t(nc) * k);
+    }
   } else {
     cpart_.alloc(size_t(std::max(coarse_split(nc, k), 1)) * nc * k);
   }
@@ -617,6 +639,14 @@ void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
   if (bt_) {
     const auto& Lc = levels_.back();
     const LevelGeom gc(Lc.dims[0], Lc.dims[1], Lc.dims[2], k);
+    if (bt_permuted()) {
+      const LevelGeom gT = bt_permuted_geom(gc, bt_perm_);
+      bt_permute_vec<T>(gc, bt_perm_, k, false, b, bt_b_.get(), s);
+      bt_solve<T>(gT, bt_coef_.get(), bt_ET_.get(), bt_FT_.get(), k, bt_b_.get(), bt_x_.get(), bt_r_.get(),
+                  cpart_.get(), s);
+      bt_permute_vec<T>(gc, bt_perm_, k, true, bt_x_.get(), x, s);
+      return;
+    }
     bt_solve<T>(gc, Lc.coef.get(), bt_ET_.get(), bt_FT_.get(), k, b, x, bt_r_.get(), cpart_.get(), s);
     return;
   }

@@ -99,6 +99,20 @@ template <class T, class In, class Out>
 void launch_fused_post(const LevelOp<T>& op, const LevelGeom& gc, T wj, const cplx_t<T>* x2,
                        const cplx_t<T>* ec, const In* b, Out* out, cudaStream_t s);
 
+// Plane-streaming 3D fine-level kernels for 8-column blocks (stream3d.cu):
+// 7-point (bitwise equal to the element kernels) and compact 27-point
+// (separable class sums), bulk-copy tile staging with an mbarrier ring.
+// mode 0 apply, 1 residual, 2 damped Jacobi (Out may be double2 for the
+// complex64 level: the cycle's last sweep), 3 residual in apply_block order.
+// Return false when they do not apply (HZ_STREAM3D=0, other k, slab ranges).
+template <class T>
+bool stream3d_ok(const LevelOp<T>& op);
+template <class T, class Out>
+bool launch_stream3d(const LevelOp<T>& op, int mode, T wj, const cplx_t<T>* x, const cplx_t<T>* b, Out* out,
+                     cudaStream_t s);
+// complex128 fine operator applied to a complex64 block (widened on load)
+bool launch_stream3d_lo(const LevelOp<double>& op, const float2* x, double2* out, cudaStream_t s);
+
 // Compact 27-point operator (3D, uniform spacing h): planes[s][i],
 // s = (dz+1)*9 + (dy+1)*3 + (dx+1). Laplacian weights lap[q] for neighbour
 // class q = |dx|+|dy|+|dz| (lap[0] is the centre), mass weights mu[q]; the
@@ -153,6 +167,16 @@ void launch_coarse_gemm(int64_t n, int k, const cplx_t<T>* ainvT, int64_t ld, co
 // layout; read when the factor is built and at every solve
 bool bt_rowmajor(int64_t m);
 void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s);
+
+// sweep-axis permutation of the plane solver: perm[a] = old axis of new axis
+// a, the longest axis last (HZ_BT_PERMUTE=0: identity); the operator planes
+// and the right-hand side / solution blocks are re-indexed onto that grid
+void bt_sweep_perm(const int64_t* dims, int* perm);
+LevelGeom bt_permuted_geom(const LevelGeom& g, const int* perm);
+void bt_permute_coef(const LevelGeom& g, const int* perm, const double2* coef, double2* coefT, cudaStream_t s);
+template <class T>
+void bt_permute_vec(const LevelGeom& g, const int* perm, int k, bool inverse, const cplx_t<T>* src, cplx_t<T>* dst,
+                    cudaStream_t s);
 
 template <class T>
 void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, const cplx_t<T>* FT, int k,

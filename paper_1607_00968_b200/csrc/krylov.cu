@@ -490,7 +490,7 @@ Report Fgmres<T>::solve(const DevOp<T>& op, int k, const V* B, V* X, int restart
     const char* e = std::getenv("HZ_ZLO");
     return !(e && e[0] == '0');
   }();
-  const bool lo = zlo_env && !sl_ && op.prec_lo && op.apply_lo &&
+  const bool lo = zlo_env && !sl_ && op.prec_lo && op.apply_lo && (!op.lo_ok || op.lo_ok(k)) &&
                   size_t(restart) * k * k * sizeof(V) <= 192 * 1024;
   ensure(n, k, restart, lo);
   // off by default (HZ_GRAM_APPLY=1 enables): the fused kernel took 90 us

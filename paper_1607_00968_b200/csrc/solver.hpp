@@ -152,6 +152,12 @@ class Hierarchy {
   // block-tridiagonal plane solver of a large 3D coarsest level
   bool bt_ = false;
   DevBuf<V> bt_ET_, bt_FT_, bt_r_;
+  // sweep-axis permutation of the plane solver (identity: planes of axis 2);
+  // bt_coef_ = the coarsest operator's planes on the permuted grid, bt_b_ /
+  // bt_x_ = the re-indexed right-hand side / solution of a solve
+  int bt_perm_[3] = {0, 1, 2};
+  DevBuf<V> bt_coef_, bt_b_, bt_x_;
+  bool bt_permuted() const { return bt_perm_[0] != 0 || bt_perm_[1] != 1 || bt_perm_[2] != 2; }
   int ndim_ = 2;
   int64_t band_ = 0;
 
@@ -233,6 +239,8 @@ struct DevOp {
   // keeps its Z blocks in complex64 -- the same values at half the bytes
   std::function<void(const V* in, float2* out, int k, cudaStream_t)> prec_lo;
   std::function<void(const float2* in, V* out, int k, cudaStream_t)> apply_lo;
+  // optional: block widths apply_lo supports (unset: all)
+  std::function<bool(int k)> lo_ok;
   // optional apply_lo fused with the Arnoldi Gram: W = A Z and the partial
   // Grams of [X_0..X_{nb-2}, W]^H W (k = 8); returns the slots written
   std::function<int(const float2* Z, V* W, const BlockTab<T>& X, int nb, V* partials, int max_slots, cudaStream_t)>

@@ -1040,7 +1040,9 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
   }();
   // c64 only: for c128 the 4-column form needs 7 x 64 B per thread in
   // registers and runs slower than one column per thread
-  if (op.kind == kFine27) {
+  if (launch_stream3d<T, cplx_t<T>>(op, MODE, wj, x, b, out, s)) {
+    return;  // 3D fine level, k = 8: plane-streaming kernels (stream3d.cu)
+  } else if (op.kind == kFine27) {
     if (op.g.k % 4 == 0)
       fine27_kernel<T, MODE, 4><<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op, x, b, out, wj);
     else
@@ -1096,9 +1098,10 @@ void launch_apply(const LevelOp<T>& op, const cplx_t<T>* u, cplx_t<T>* out, cuda
   dispatch_level<T, 0>(op, u, nullptr, out, T(0), s);
 }
 void launch_apply_lo(const LevelOp<double>& op, const float2* u, double2* out, cudaStream_t s) {
-  if (op.kind != kFine) throw HzError(kState, "apply_lo: fine operator only");
   const double n = double(op.g.owned_nodes()), k = op.g.k;
-  ProfScope prof("apply_fine_c128", n * (k * (8.0 + 16.0) + 16.0), s);
+  ProfScope prof(op.kind == kFine27 ? "apply_fine27_c128" : "apply_fine_c128", n * (k * (8.0 + 16.0) + 16.0), s);
+  if (launch_stream3d_lo(op, u, out, s)) return;
+  if (op.kind != kFine) throw HzError(kState, "apply_lo: 5/7-point operator, or 8-column blocks of the 27-point one");
   const int grid = grid_for(op.g.owned_elems(), kBlock);
   if (op.ndim == 3)
     apply_lo_kernel<3><<<grid, kBlock, 0, s>>>(op, u, out);
@@ -1134,6 +1137,7 @@ void launch_apply_residual(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_
   }
   const int64_t total = op.g.owned_elems();
   ProfScope prof(sizeof(T) == 8 ? "apply_residual_fine_c128" : "apply_residual_fine_c64", level_bytes(op, 1), s);
+  if (launch_stream3d<T, cplx_t<T>>(op, 3, T(0), x, b, r, s)) return;
   if (sizeof(T) == 4 && op.g.k % 4 == 0) {
     const int g4 = grid_for(total / 4, kBlock);
     if (op.ndim == 3)
@@ -1206,7 +1210,9 @@ void launch_prolong_correct(const LevelGeom& gf, const LevelGeom& gc, int ndim,
   HZ_LAUNCH_CHECK();
 }
 
-bool fused_fine_ok(const LevelOp<float>& op) { return op.kind == kFine && op.g.k % 4 == 0; }
+bool fused_fine_ok(const LevelOp<float>& op) {
+  return (op.kind == kFine && op.g.k % 4 == 0) || (op.kind == kFine27 && stream3d_ok(op));
+}
 bool cast_zero_ok(const LevelOp<float>& op) { return op.g.k % 4 == 0; }
 
 void launch_jacobi_zero_cast(const LevelOp<float>& op, float wj, const double2* b64, float2* b32, float2* x1,
@@ -1223,6 +1229,8 @@ void launch_jacobi_out64(const LevelOp<float>& op, float wj, const float2* x, co
   const int64_t total = op.g.owned_elems();
   const double n = double(op.g.owned_nodes()), k = op.g.k;
   ProfScope prof("jacobi_out64_fine_c64", n * (k * (8.0 + 8.0 + 16.0) + 8.0 + 8.0), s);
+  if (launch_stream3d<float, double2>(op, 2, wj, x, b, out, s)) return;
+  if (op.kind != kFine) throw HzError(kState, "jacobi_out64: 5/7-point operator, or 8-column blocks of the 27-point one");
   if (op.ndim == 3)
     fine_v4_kernel<float, 3, 2, double2><<<grid_for(total / 4, kBlock), kBlock, 0, s>>>(op, x, b, out, wj);
   else

@@ -1,0 +1,125 @@
+"""GPU tier: the plane-streaming 3D fine-level kernels for 8-column blocks
+(csrc/stream3d.cu) against the element kernels they replace (HZ_STREAM3D=0),
+the numpy specification of the 27-point operator, and the reference oracle.
+
+7-point (apply_block, src/helmholtz.cpp:71-100; relax / residual,
+src/multigrid.cpp:119-136,173-175): the same per-column operations in the same
+order, so complex64 cycles are bitwise equal and complex128 ones equal to the
+last bit or two (FMA contraction). 27-point: separable class sums, a different
+summation order, so equal to rounding only."""
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+import pytest
+
+from hzt_util import rel_err
+from paper_1607_00968_b200 import configs
+
+pytestmark = pytest.mark.gpu
+hz = pytest.importorskip("paper_1607_00968_b200")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CODE = (
+    "import sys; sys.path.insert(0, '.'); import numpy as np\n"
+    "import paper_1607_00968_b200 as hz; from paper_1607_00968_b200 import configs\n"
+    "n = tuple(int(v) for v in sys.argv[2].split('x')); nl, prec, stencil, kind = int(sys.argv[3]), sys.argv[4], int(sys.argv[5]), sys.argv[6]\n"
+    "cfg = configs.small_problem(3, n, seed=7, layer=3); cfg.stencil = stencil\n"
+    "P = hz.HelmholtzProblem.from_config(cfg)\n"
+    "S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method='MgFgmres', nlevels=nl, shift_factor=0.5,\n"
+    "                       cycle=hz.CycleSpec(kind), precond_precision=prec))\n"
+    "b = configs.random_block(cfg.num_nodes, 8, seed=11)\n"
+    "x1 = S.cycle(b); x2 = S.cycle(b)\n"
+    "assert np.array_equal(x1, x2), 'cycle not deterministic'\n"
+    "u = configs.random_block(cfg.num_nodes, 8, seed=12)\n"
+    "np.savez(sys.argv[1], cycle=x1, apply=P.apply_block(u))\n")
+
+
+def _run(path, flag, n, nl, prec, stencil, kind, **extra):
+    env = dict(os.environ, HZ_STREAM3D=flag, **extra)
+    r = subprocess.run([sys.executable, "-c", CODE, path, "x".join(map(str, n)), str(nl), prec, str(stencil), kind],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return np.load(path)
+
+
+# grids narrower / wider than one tile (32 x 8 complex64, 16 x 8 complex128),
+# tile edges one node past a multiple of the tile, several z chunks
+GRIDS = [((33, 17, 9), 2), ((49, 37, 21), 2), ((17, 41, 13), 2), ((97, 33, 65), 3), ((65, 65, 33), 3)]
+
+
+@pytest.mark.parametrize("prec", ["c64", "c128"])
+@pytest.mark.parametrize("n,nl", GRIDS)
+def test_seven_point_streaming_equals_element_kernels(n, nl, prec):
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(os.path.join(d, "a.npz"), "1", n, nl, prec, 7, "V")
+        old = _run(os.path.join(d, "b.npz"), "0", n, nl, prec, 7, "V")
+    assert np.all(np.isfinite(new["cycle"]))
+    if prec == "c64":
+        assert np.array_equal(new["cycle"], old["cycle"]), rel_err(new["cycle"], old["cycle"])
+    else:
+        assert rel_err(new["cycle"], old["cycle"]) <= 1e-14
+    assert rel_err(new["apply"], old["apply"]) <= 1e-15
+
+
+@pytest.mark.parametrize("zlen", ["4", "7"])
+def test_seven_point_streaming_is_independent_of_the_z_chunking(zlen):
+    n, nl = (49, 37, 21), 2
+    with tempfile.TemporaryDirectory() as d:
+        a = _run(os.path.join(d, "a.npz"), "1", n, nl, "c64", 7, "W")
+        b = _run(os.path.join(d, "b.npz"), "1", n, nl, "c64", 7, "W", HZ_STREAM3D_ZLEN=zlen)
+        c = _run(os.path.join(d, "c.npz"), "1", n, nl, "c64", 27, "V")
+        e = _run(os.path.join(d, "e.npz"), "1", n, nl, "c64", 27, "V", HZ_STREAM3D_ZLEN=zlen)
+    assert np.array_equal(a["cycle"], b["cycle"]) and np.array_equal(a["apply"], b["apply"])
+    assert np.array_equal(c["cycle"], e["cycle"]) and np.array_equal(c["apply"], e["apply"])
+
+
+@pytest.mark.parametrize("prec,tol", [("c64", 2e-5), ("c128", 1e-12)])
+@pytest.mark.parametrize("n,nl", GRIDS[:4])
+def test_27_point_streaming_matches_element_kernels(n, nl, prec, tol):
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(os.path.join(d, "a.npz"), "1", n, nl, prec, 27, "V")
+        old = _run(os.path.join(d, "b.npz"), "0", n, nl, prec, 27, "V")
+    assert np.all(np.isfinite(new["cycle"]))
+    assert rel_err(new["cycle"], old["cycle"]) <= tol
+    assert rel_err(new["apply"], old["apply"]) <= 1e-13
+
+
+def test_27_point_streaming_apply_matches_specification():
+    """k = 8 takes the streaming kernel: against the numpy / scipy statement of
+    the operator (tests/hzt_util.csr27), complex128."""
+    from hzt_util import csr27
+    for n in [(17, 15, 13), (35, 19, 9), (33, 9, 21)]:
+        cfg = configs.small_problem(3, n, seed=4, layer=3)
+        cfg.stencil = 27
+        P = hz.HelmholtzProblem.from_config(cfg)
+        u = configs.random_block(cfg.num_nodes, 8, seed=2)
+        assert rel_err(P.apply_block(u), csr27(cfg) @ u) <= 1e-13
+
+
+def test_seven_point_streaming_apply_matches_reference(ref):
+    for n in [(33, 17, 9), (19, 35, 11)]:
+        cfg = configs.small_problem(3, n, seed=5, layer=3)
+        P = hz.HelmholtzProblem.from_config(cfg)
+        R = ref.RefProblem.from_config(cfg)
+        u = configs.random_block(cfg.num_nodes, 8, seed=3)
+        assert rel_err(P.apply_block(u), R.apply_block(u)) <= 1e-12
+
+
+def test_27_point_complex64_z_blocks_solve():
+    """27-point solve with the complex64 preconditioner: the Z blocks stay
+    complex64 and W = A Z widens them on load (launch_stream3d_lo); the
+    residual is checked against the operator's numpy statement."""
+    from hzt_util import csr27
+    cfg = configs.config3(nlevels=3, n=(65, 65, 33), sgrid=3, layer=8)
+    cfg.stencil, cfg.precond_precision = 27, "c64"
+    cfg.source_nodes = cfg.source_nodes[:8]
+    cfg.restart, cfg.max_cycles = 10, 400
+    S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))
+    B = cfg.rhs_block()
+    X, rep = S.solve_block(B)
+    assert rep.all_converged()
+    res = np.linalg.norm(B - csr27(cfg) @ X, axis=0) / np.linalg.norm(B, axis=0)
+    assert np.all(res <= cfg.tol * (1 + 1e-6)), res
