@@ -144,9 +144,9 @@ __global__ void gj_unswap_kernel(int64_t m, double2* __restrict__ S, int p, cons
   S[r * m + q] = a;
 }
 
-// F[r][c] = sum_l E[r][l] U[l][c], U = plane j -> j+1 coupling (9 per column)
-__global__ void mul_eu_kernel(LevelGeom g, const double2* __restrict__ coef, int j, const double2* __restrict__ E,
-                              double2* __restrict__ F) {
+// F[r][c] = sum_l E[r][l] U[l][c], U = plane j -> j+dir coupling (9 per column)
+__global__ void mul_eu_kernel(LevelGeom g, const double2* __restrict__ coef, int j, int dir,
+                              const double2* __restrict__ E, double2* __restrict__ F) {
   const int64_t m = int64_t(g.n0) * g.n1;
   const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
   if (e >= m * m) return;
@@ -155,18 +155,18 @@ __global__ void mul_eu_kernel(LevelGeom g, const double2* __restrict__ coef, int
   double2 s = make_double2(0.0, 0.0);
   for (int dy = -1; dy <= 1; ++dy)
     for (int dx = -1; dx <= 1; ++dx) {
-      const int li = ci - dx, lj = cj - dy;  // l + (dx, dy, +1) = c
+      const int li = ci - dx, lj = cj - dy;  // l + (dx, dy, dir) = c
       if (li < 0 || li >= int(g.n0) || lj < 0 || lj >= int(g.n1)) continue;
       const int64_t l = li + int64_t(g.n0) * lj;
-      const double2 u = coef[int64_t(plane_s(dx, dy, 1)) * g.nodes + int64_t(j) * m + l];
+      const double2 u = coef[int64_t(plane_s(dx, dy, dir)) * g.nodes + int64_t(j) * m + l];
       s = cfma(E[r * m + l], u, s);
     }
   F[e] = s;
 }
 
-// S[r][c] = D[r][c] - sum_l L[r][l] F[l][c], L = plane j+1 -> j coupling
-__global__ void schur_kernel(LevelGeom g, const double2* __restrict__ coef, int j1, const double2* __restrict__ F,
-                             double2* __restrict__ S) {
+// S[r][c] -= sum_l L[r][l] F[l][c], L = plane j1 -> j1-dir coupling (F of plane j1-dir)
+__global__ void schur_kernel(LevelGeom g, const double2* __restrict__ coef, int j1, int dir,
+                             const double2* __restrict__ F, double2* __restrict__ S) {
   const int64_t m = int64_t(g.n0) * g.n1;
   const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
   if (e >= m * m) return;
@@ -178,16 +178,18 @@ __global__ void schur_kernel(LevelGeom g, const double2* __restrict__ coef, int 
       const int li = ri + dx, lj = rj + dy;
       if (li < 0 || li >= int(g.n0) || lj < 0 || lj >= int(g.n1)) continue;
       const int64_t l = li + int64_t(g.n0) * lj;
-      const double2 a = coef[int64_t(plane_s(dx, dy, -1)) * g.nodes + int64_t(j1) * m + r];
+      const double2 a = coef[int64_t(plane_s(dx, dy, -dir)) * g.nodes + int64_t(j1) * m + r];
       s = csub(s, cmul(a, F[l * m + c]));
     }
   S[e] = s;
 }
 
-// r = b_j - L_j y_{j-1} for one plane, all k columns
+// r = b_j - L_j y_{j-dir} for one plane, all k columns (L = plane j -> j-dir
+// coupling; b may be r itself: the middle plane of the twisted sweep
+// subtracts both neighbours in two passes)
 template <class T>
-__global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, int j, const cplx_t<T>* __restrict__ b,
-                              const cplx_t<T>* __restrict__ yprev, cplx_t<T>* __restrict__ r, int k) {
+__global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, int j, int dir, const cplx_t<T>* b,
+                              const cplx_t<T>* __restrict__ yprev, cplx_t<T>* r, int k) {
   using V = cplx_t<T>;
   const int64_t m = int64_t(g.n0) * g.n1;
   const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
@@ -201,7 +203,7 @@ __global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, i
       const int li = ri + dx, lj = rj + dy;
       if (li < 0 || li >= int(g.n0) || lj < 0 || lj >= int(g.n1)) continue;
       const int64_t l = li + int64_t(g.n0) * lj;
-      const V a = coef[int64_t(plane_s(dx, dy, -1)) * g.nodes + int64_t(j) * m + row];
+      const V a = coef[int64_t(plane_s(dx, dy, -dir)) * g.nodes + int64_t(j) * m + row];
       s = csub(s, cmul(a, yprev[l * k + q]));
     }
   r[e] = s;
@@ -486,17 +488,37 @@ void bt_permute_vec(const LevelGeom& g, const int* perm, int k, bool inverse, co
 template void bt_permute_vec<double>(const LevelGeom&, const int*, int, bool, const double2*, double2*, cudaStream_t);
 template void bt_permute_vec<float>(const LevelGeom&, const int*, int, bool, const float2*, float2*, cudaStream_t);
 
-// ---- setup: E_j and F_j (f64, row-major), row stride inv_ld(m)
+// ---- twisted (two-sided) elimination
+// The sweep is a chain of dependent plane steps, each too small to fill the
+// GPU (latency bound), so the chain is cut in two: planes 0 .. mid-1 are
+// eliminated top-down and planes np-1 .. mid+1 bottom-up, concurrently on two
+// streams; the middle plane takes both Schur contributions, and the two back
+// substitutions run outward concurrently again. Half the dependent steps,
+// the same factor bytes. HZ_BT_TWISTED=0: mid = np-1, the one-sided sweep.
+int bt_mid(int np) {
+  const char* e = std::getenv("HZ_BT_TWISTED");
+  if (e && e[0] == '0') return np - 1;
+  return np / 2;
+}
+
+// ---- setup: E_j (every plane) and F_j (coupling factor towards the middle),
+// f64, row stride inv_ld(m); row-major or transposed per bt_rowmajor(m)
 void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT, cudaStream_t s) {
   const int64_t m = int64_t(g.n0) * g.n1;
   const int np = int(g.n2);
+  const int mid = bt_mid(np);
   const int64_t ld = inv_ld(m);
-  DevBuf<double2> S(size_t(m) * m), F(size_t(m) * m), col(m), row(m);
+  DevBuf<double2> S(size_t(m) * m), F1(size_t(m) * m), F2(size_t(m) * m), col(m), row(m);
   DevBuf<int> piv(m);
   const int gmm = grid_for(m * m, 256), gm = grid_for(m, 256);
   ProfScope prof("bt_factor", 0.0, s);
-  build_block_kernel<<<gmm, 256, 0, s>>>(g, coef, 0, 0, S.get());
-  for (int j = 0; j < np; ++j) {
+  auto store = [&](const double2* src, double2* dst) {
+    if (bt_rowmajor(m))
+      strided_copy_kernel<<<gmm, 256, 0, s>>>(m, src, dst, ld);
+    else
+      transpose_kernel<<<gmm, 256, 0, s>>>(m, src, dst, ld);
+  };
+  auto invert = [&](int j) {  // S <- S^{-1} (Gauss-Jordan, partial pivoting), stored as E_j
     for (int p = 0; p < m; ++p) {
       gj_pivot_kernel<<<1, 1024, 0, s>>>(m, S.get(), p, piv.get());
       gj_prepare_kernel<<<gm, 256, 0, s>>>(m, S.get(), p, piv.get(), col.get(), row.get());
@@ -509,46 +531,94 @@ void bt_factor(const LevelGeom& g, const double2* coef, double2* ET, double2* FT
     HZ_CUDA(cudaStreamSynchronize(s));
     for (int64_t p = 0; p < m; ++p)
       if (hpiv[p] < 0) throw HzError(kFactorization, "block-tridiagonal coarse solve: singular plane block");
-    // S now holds E_j
-    if (bt_rowmajor(m))
-      strided_copy_kernel<<<gmm, 256, 0, s>>>(m, S.get(), ET + int64_t(j) * m * ld, ld);
-    else
-      transpose_kernel<<<gmm, 256, 0, s>>>(m, S.get(), ET + int64_t(j) * m * ld, ld);
-    if (j + 1 < np) {
-      mul_eu_kernel<<<gmm, 256, 0, s>>>(g, coef, j, S.get(), F.get());
-      if (bt_rowmajor(m))
-        strided_copy_kernel<<<gmm, 256, 0, s>>>(m, F.get(), FT + int64_t(j) * m * ld, ld);
-      else
-        transpose_kernel<<<gmm, 256, 0, s>>>(m, F.get(), FT + int64_t(j) * m * ld, ld);
-      build_block_kernel<<<gmm, 256, 0, s>>>(g, coef, j + 1, 0, S.get());
-      schur_kernel<<<gmm, 256, 0, s>>>(g, coef, j + 1, F.get(), S.get());
+    store(S.get(), ET + int64_t(j) * m * ld);
+  };
+  // one chain: planes j0, j0+dir, ... up to (not including) mid
+  auto chain = [&](int j0, int dir, double2* F) {
+    for (int j = j0; j != mid; j += dir) {
+      build_block_kernel<<<gmm, 256, 0, s>>>(g, coef, j, 0, S.get());
+      if (j != j0) schur_kernel<<<gmm, 256, 0, s>>>(g, coef, j, dir, F, S.get());
+      invert(j);
+      mul_eu_kernel<<<gmm, 256, 0, s>>>(g, coef, j, dir, S.get(), F);
+      store(F, FT + int64_t(j) * m * ld);
     }
-  }
+  };
+  chain(0, 1, F1.get());
+  chain(np - 1, -1, F2.get());
+  build_block_kernel<<<gmm, 256, 0, s>>>(g, coef, mid, 0, S.get());
+  if (mid > 0) schur_kernel<<<gmm, 256, 0, s>>>(g, coef, mid, 1, F1.get(), S.get());
+  if (mid < np - 1) schur_kernel<<<gmm, 256, 0, s>>>(g, coef, mid, -1, F2.get(), S.get());
+  invert(mid);
   HZ_LAUNCH_CHECK();
   HZ_CUDA(cudaStreamSynchronize(s));
 }
 
-// ---- solve: x = A_c^{-1} b (k columns), y/r scratch (n_c k and m k)
+// ---- solve: x = A_c^{-1} b (k columns); scratch r (2 m k) and part (two
+// split-K partial sets); aux = second stream + fork / join events
 template <class T>
 void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, const cplx_t<T>* FT, int k,
-              const cplx_t<T>* b, cplx_t<T>* x, cplx_t<T>* r, cplx_t<T>* part, cudaStream_t s) {
+              const cplx_t<T>* b, cplx_t<T>* x, cplx_t<T>* r, cplx_t<T>* part, const BtAux& aux, cudaStream_t s) {
   using V = cplx_t<T>;
   const int64_t m = int64_t(g.n0) * g.n1;
   const int np = int(g.n2);
+  const int mid = bt_mid(np);
   const int64_t ld = inv_ld(m);
   const int64_t pk = m * k;
-  LevelGeom gk = g;
+  const int gk = grid_for(pk, 256);
   ProfScope prof(sizeof(T) == 8 ? "coarse_bt_c128" : "coarse_bt_c64",
                  (2.0 * np - 1.0) * double(m) * m * sizeof(V), s, 8.0 * (2.0 * np - 1.0) * double(m) * m * k);
-  // forward: x holds y
-  bt_step<T>(m, k, ET, ld, b, x, nullptr, T(1), part, s);
-  for (int j = 1; j < np; ++j) {
-    couple_kernel<T><<<grid_for(pk, 256), 256, 0, s>>>(gk, coef, j, b + j * pk, x + (j - 1) * pk, r, k);
-    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, r, x + j * pk, nullptr, T(1), part, s);
+  const bool two = mid < np - 1;  // a bottom-up chain exists
+  cudaStream_t s2 = two ? aux.s2 : s;
+  V* r2 = r + pk;
+  V* part2 = part + int64_t(std::max(coarse_split(m, k), 1)) * pk;
+  auto fork = [&] {
+    if (!two) return;
+    HZ_CUDA(cudaEventRecord(aux.fork, s));
+    HZ_CUDA(cudaStreamWaitEvent(s2, aux.fork, 0));
+  };
+  auto join = [&] {
+    if (!two) return;
+    HZ_CUDA(cudaEventRecord(aux.join, s2));
+    HZ_CUDA(cudaStreamWaitEvent(s, aux.join, 0));
+  };
+  // forward elimination from both ends (x holds y)
+  fork();
+  for (int j = 0; j < mid; ++j) {
+    const V* rhs = b + j * pk;
+    if (j > 0) {
+      couple_kernel<T><<<gk, 256, 0, s>>>(g, coef, j, 1, rhs, x + (j - 1) * pk, r, k);
+      rhs = r;
+    }
+    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, rhs, x + j * pk, nullptr, T(1), part, s);
   }
-  // backward: x_j = y_j - F_j x_{j+1}
-  for (int j = np - 2; j >= 0; --j)
+  for (int j = np - 1; j > mid; --j) {
+    const V* rhs = b + j * pk;
+    if (j < np - 1) {
+      couple_kernel<T><<<gk, 256, 0, s2>>>(g, coef, j, -1, rhs, x + (j + 1) * pk, r2, k);
+      rhs = r2;
+    }
+    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, rhs, x + j * pk, nullptr, T(1), part2, s2);
+  }
+  join();
+  {  // middle plane: both neighbours' contributions
+    const V* rhs = b + mid * pk;
+    if (mid > 0) {
+      couple_kernel<T><<<gk, 256, 0, s>>>(g, coef, mid, 1, rhs, x + (mid - 1) * pk, r, k);
+      rhs = r;
+    }
+    if (mid < np - 1) {
+      couple_kernel<T><<<gk, 256, 0, s>>>(g, coef, mid, -1, rhs, x + (mid + 1) * pk, r, k);
+      rhs = r;
+    }
+    bt_step<T>(m, k, ET + int64_t(mid) * m * ld, ld, rhs, x + mid * pk, nullptr, T(1), part, s);
+  }
+  // back substitution outward: x_j = y_j - F_j x_{j +- 1}
+  fork();
+  for (int j = mid - 1; j >= 0; --j)
     bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j + 1) * pk, x + j * pk, x + j * pk, T(-1), part, s);
+  for (int j = mid + 1; j < np; ++j)
+    bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j - 1) * pk, x + j * pk, x + j * pk, T(-1), part2, s2);
+  join();
   HZ_LAUNCH_CHECK();
 }
 
@@ -577,12 +647,14 @@ DevBuf<double2> bt_explicit_inverse(const LevelGeom& g, const double2* coef, con
   const int64_t n = int64_t(g.nodes), m = int64_t(g.n0) * g.n1;
   constexpr int K = 64;
   DevBuf<double2> out(size_t(n) * inv_ld(n));
-  DevBuf<double2> B(size_t(n) * K), X(size_t(n) * K), r(size_t(m) * K),
-      part(size_t(std::max(coarse_split(m, K), 1)) * m * K);
+  DevBuf<double2> B(size_t(n) * K), X(size_t(n) * K), r(size_t(2) * m * K),
+      part(size_t(2) * std::max(coarse_split(m, K), 1) * m * K);
   const LevelGeom gk(g.n0, g.n1, g.n2, K);
+  BtAux aux;
+  aux.ensure();
   for (int64_t c0 = 0; c0 < n; c0 += K) {
     unit_columns_kernel<<<grid_for(n * K, 256), 256, 0, s>>>(n, K, c0, B.get());
-    bt_solve<double>(gk, coef, ET, FT, K, B.get(), X.get(), r.get(), part.get(), s);
+    bt_solve<double>(gk, coef, ET, FT, K, B.get(), X.get(), r.get(), part.get(), aux, s);
     chunk_transpose_kernel<<<grid_for(n * K, 256), 256, 0, s>>>(n, K, c0, X.get(), out.get(), inv_ld(n));
   }
   HZ_LAUNCH_CHECK();
@@ -591,8 +663,20 @@ DevBuf<double2> bt_explicit_inverse(const LevelGeom& g, const double2* coef, con
 }
 
 template void bt_solve<double>(const LevelGeom&, const double2*, const double2*, const double2*, int,
-                               const double2*, double2*, double2*, double2*, cudaStream_t);
+                               const double2*, double2*, double2*, double2*, const BtAux&, cudaStream_t);
 template void bt_solve<float>(const LevelGeom&, const float2*, const float2*, const float2*, int, const float2*,
-                              float2*, float2*, float2*, cudaStream_t);
+                              float2*, float2*, float2*, const BtAux&, cudaStream_t);
+
+void BtAux::ensure() {
+  if (s2) return;
+  HZ_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  HZ_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+  HZ_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+}
+BtAux::~BtAux() {
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
+  if (s2) cudaStreamDestroy(s2);
+}
 
 }  // namespace hz

@@ -621,8 +621,9 @@ void Hierarchy<T>::ensure_ws(int k) {
     const auto& Lc = levels_.back();
     const LevelGeom gT = bt_permuted_geom(LevelGeom(Lc.dims[0], Lc.dims[1], Lc.dims[2], k), bt_perm_);
     const int64_t m = int64_t(gT.n0) * gT.n1;
-    cpart_.alloc(size_t(std::max(coarse_split(m, k), 1)) * m * k);
-    bt_r_.alloc(size_t(m) * k);
+    cpart_.alloc(size_t(2) * std::max(coarse_split(m, k), 1) * m * k);
+    bt_r_.alloc(size_t(2) * m * k);
+    bt_aux_.ensure();
     if (bt_permuted()) {
       bt_b_.alloc(size_t(nc) * k);
       bt_x_.alloc(size_t(nc) * k);
@@ -643,11 +644,11 @@ void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
       const LevelGeom gT = bt_permuted_geom(gc, bt_perm_);
       bt_permute_vec<T>(gc, bt_perm_, k, false, b, bt_b_.get(), s);
       bt_solve<T>(gT, bt_coef_.get(), bt_ET_.get(), bt_FT_.get(), k, bt_b_.get(), bt_x_.get(), bt_r_.get(),
-                  cpart_.get(), s);
+                  cpart_.get(), bt_aux_, s);
       bt_permute_vec<T>(gc, bt_perm_, k, true, bt_x_.get(), x, s);
       return;
     }
-    bt_solve<T>(gc, Lc.coef.get(), bt_ET_.get(), bt_FT_.get(), k, b, x, bt_r_.get(), cpart_.get(), s);
+    bt_solve<T>(gc, Lc.coef.get(), bt_ET_.get(), bt_FT_.get(), k, b, x, bt_r_.get(), cpart_.get(), bt_aux_, s);
     return;
   }
   launch_coarse_solve<T>(coarse_n(), k, ainvT_.get(), b, x, cpart_.get(), s);

@@ -178,9 +178,23 @@ template <class T>
 void bt_permute_vec(const LevelGeom& g, const int* perm, int k, bool inverse, const cplx_t<T>* src, cplx_t<T>* dst,
                     cudaStream_t s);
 
+// second stream + fork / join events of the two-sided (twisted) sweep; one
+// per concurrently solving hierarchy view
+struct BtAux {
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  BtAux() = default;
+  BtAux(const BtAux&) = delete;
+  BtAux& operator=(const BtAux&) = delete;
+  ~BtAux();
+  void ensure();
+};
+// planes [0, mid) are eliminated top-down, (mid, n2) bottom-up (HZ_BT_TWISTED=0: mid = n2 - 1)
+int bt_mid(int np);
+// scratch: r = 2 m k entries, part = 2 coarse_split(m, k) m k entries
 template <class T>
 void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, const cplx_t<T>* FT, int k,
-              const cplx_t<T>* b, cplx_t<T>* x, cplx_t<T>* r, cplx_t<T>* part, cudaStream_t s);
+              const cplx_t<T>* b, cplx_t<T>* x, cplx_t<T>* r, cplx_t<T>* part, const BtAux& aux, cudaStream_t s);
 
 // ---- block (tall-skinny) kernels, node-major [n][k] blocks (inc/block.hpp)
 // Tables of block pointers travel by value in the kernel parameters (no

@@ -155,6 +155,7 @@ class Hierarchy {
   // sweep-axis permutation of the plane solver (identity: planes of axis 2);
   // bt_coef_ = the coarsest operator's planes on the permuted grid, bt_b_ /
   // bt_x_ = the re-indexed right-hand side / solution of a solve
+  BtAux bt_aux_;
   int bt_perm_[3] = {0, 1, 2};
   DevBuf<V> bt_coef_, bt_b_, bt_x_;
   bool bt_permuted() const { return bt_perm_[0] != 0 || bt_perm_[1] != 1 || bt_perm_[2] != 2; }
