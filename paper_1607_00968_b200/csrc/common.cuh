@@ -143,6 +143,22 @@ template <class V, class T> __host__ __device__ __forceinline__ V cscale(T s, V 
   r.y = s * b.y;
   return r;
 }
+// complex64 on the device: packed FP32 pairs (FFMA2 / FADD2 / FMUL2 on sm_100),
+// one issue slot per complex value instead of two. Per component these are the
+// IEEE operations of the generic forms above in the same order, so the bits
+// are the same. HZ_NO_PACKED_F32 (compile time) keeps the scalar forms.
+#if defined(__CUDA_ARCH__) && !defined(HZ_NO_PACKED_F32)
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 crfma(float s, float2 b, float2 acc) {
+  return __ffma2_rn(make_float2(s, s), b, acc);
+}
+__device__ __forceinline__ float2 cscale(float s, float2 b) { return __fmul2_rn(make_float2(s, s), b); }
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
+  const float2 t = __ffma2_rn(make_float2(a.x, a.x), b, acc);
+  return __ffma2_rn(make_float2(-a.y, a.y), make_float2(b.y, b.x), t);
+}
+#endif
+
 template <class V> __host__ __device__ __forceinline__ typename RealOf<V>::type cabs2(V a) {
   return a.x * a.x + a.y * a.y;
 }

@@ -181,18 +181,19 @@ def test_rank_deficient_block_matches_reference(ref):
     assert rel_err(X[:, 2], X[:, 0]) <= 1e-12  # coincident sources, identical columns
 
 
-@pytest.mark.parametrize("inverse,rows,permute,twisted", [("0", None, "1", "1"), ("0", "0", "1", "1"),
+@pytest.mark.parametrize("inverse,rows,permute,twisted", [("0", None, "2", "1"), ("0", "0", "1", "1"),
                                                           ("40000", None, "1", "1"), ("0", None, "0", "1"),
-                                                          ("0", None, "1", "0"), ("0", "0", "0", "0")])
+                                                          ("0", None, "2", "0"), ("0", "0", "0", "0")])
 @pytest.mark.parametrize("n,nl", [((17, 17, 9), 2), ((33, 33, 17), 3), ((33, 17, 17), 2), ((17, 33, 25), 2)])
 def test_block_tridiagonal_coarse_solve_matches_reference(ref, n, nl, inverse, rows, permute, twisted, monkeypatch):
     """The plane block-tridiagonal coarsest solver (coarse_bt.cu) against the
     reference's banded LU (MgHierarchy::coarse_solve, src/multigrid.cpp:114-117);
     rows = "0": transposed planes + split-K GEMM (the large-plane layout) instead
     of the row-owner kernel; inverse = 40000: the explicit inverse formed from
-    the plane factors; permute = "1" (default): the sweep runs along the longest
-    axis of the coarsest grid (y for 9x9x5, x for 17x9x9, y for 9x17x13) on
-    re-indexed planes, "0": along z; twisted = "1" (default): two-sided
+    the plane factors; permute = "2": the sweep runs along the longest axis of
+    the coarsest grid (y for 9x9x5, x for 17x9x9, y for 9x17x13) on re-indexed
+    planes, "1" (default): the same for planes above the row-owner limit
+    (with rows = "0": all), "0": along z; twisted = "1" (default): two-sided
     elimination meeting at the middle plane on two streams, "0": one-sided."""
     monkeypatch.setenv("HZ_COARSE", "bt")
     monkeypatch.setenv("HZ_BT_TWISTED", twisted)
