@@ -191,21 +191,31 @@ template <class T>
 __global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, int j, int dir, const cplx_t<T>* b,
                               const cplx_t<T>* __restrict__ yprev, cplx_t<T>* r, int k) {
   using V = cplx_t<T>;
-  const int64_t m = int64_t(g.n0) * g.n1;
-  const int64_t e = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  const int n0 = int(g.n0), n1 = int(g.n1);
+  const int m = n0 * n1;
+  const int e = int(blockIdx.x) * 256 + threadIdx.x;
   if (e >= m * k) return;
-  const int64_t row = e / k;
-  const int q = int(e - row * k);
-  const int ri = int(row % g.n0), rj = int(row / g.n0);
-  V s = b[e];
+  const int row = e / k;
+  const int q = e - row * k;
+  const int rj = row / n0, ri = row - rj * n0;
+  // the 9 couplings and neighbours are loaded first (masked), then summed in
+  // the fixed (dy, dx) order
+  V av[9], yv[9];
+  bool ok[9];
+#pragma unroll
   for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
     for (int dx = -1; dx <= 1; ++dx) {
+      const int s9 = (dy + 1) * 3 + dx + 1;
       const int li = ri + dx, lj = rj + dy;
-      if (li < 0 || li >= int(g.n0) || lj < 0 || lj >= int(g.n1)) continue;
-      const int64_t l = li + int64_t(g.n0) * lj;
-      const V a = coef[int64_t(plane_s(dx, dy, -dir)) * g.nodes + int64_t(j) * m + row];
-      s = csub(s, cmul(a, yprev[l * k + q]));
+      ok[s9] = li >= 0 && li < n0 && lj >= 0 && lj < n1;
+      av[s9] = __ldg(&coef[int64_t(plane_s(dx, dy, -dir)) * g.nodes + int64_t(j) * m + row]);
+      yv[s9] = __ldg(&yprev[ok[s9] ? (li + n0 * lj) * k + q : e]);
     }
+  V s = b[e];
+#pragma unroll
+  for (int s9 = 0; s9 < 9; ++s9)
+    if (ok[s9]) s = csub(s, cmul(av[s9], yv[s9]));
   r[e] = s;
 }
 
@@ -246,76 +256,91 @@ __device__ __forceinline__ void cp_async_elem(V* smem, const V* gmem) {
 // (double-buffered) and read conflict-free by all 8 warps; lane partial sums
 // meet in an xor butterfly, so no split-K partials and no second launch.
 // Deterministic: fixed per-lane order, fixed butterfly.
-template <class T, int RW, int KG, int LC>
+template <class T, int RW, int KG, int LC, int PF>
 __global__ void __launch_bounds__(256)
-bt_rows_kernel(int64_t m, int k, const cplx_t<T>* __restrict__ P, int64_t ld, const cplx_t<T>* __restrict__ r,
+bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx_t<T>* __restrict__ r,
                cplx_t<T>* out, const cplx_t<T>* c_in, T sign) {
   using V = cplx_t<T>;
   constexpr int U = LC / 32;
-  __shared__ __align__(16) V rs[2][KG * LC];
+  // chunk of r in its natural [l][q] order, rows padded to KG + 1 values: the
+  // staging writes and the per-lane reads (lane = l) are both conflict free
+  constexpr int RS = KG + 1;
+  __shared__ __align__(16) V rs[2][LC * RS];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int64_t i0 = int64_t(blockIdx.x) * (8 * RW);
+  const int i0 = int(blockIdx.x) * (8 * RW);
   const int q0 = blockIdx.y * KG;
-  const int nch = int((m + LC - 1) / LC);
-  int64_t row[RW];
+  const int nch = (m + LC - 1) / LC;
+  // rows past the end are clamped (computed, not stored): no predicates in the loop
+  const V* prow[RW];
   bool live[RW];
 #pragma unroll
   for (int t = 0; t < RW; ++t) {
-    row[t] = i0 + w + 8 * t;
-    live[t] = row[t] < m;
+    const int row = i0 + w + 8 * t;
+    live[t] = row < m;
+    prow[t] = P + int64_t(min(row, m - 1)) * ld + lane;
   }
+  const V* rq = r + q0;
   auto stage = [&](int c, V* dst) {
-    const int64_t l0 = int64_t(c) * LC;
+    const int l0 = c * LC;
+#pragma unroll
     for (int e = tid; e < LC * KG; e += 256) {
-      const int l = e / KG, q = e - l * KG;
+      const int l = e / KG, q = e % KG;
       if (l0 + l < m)
-        cp_async_elem(dst + q * LC + l, r + (l0 + l) * k + q0 + q);
+        cp_async_elem(dst + l * RS + q, rq + (l0 + l) * k + q);
       else
-        dst[q * LC + l] = czero<V>();
+        dst[l * RS + q] = czero<V>();
     }
   };
   auto load_p = [&](int c, V (&pv)[RW][U]) {
-    const int64_t l0 = int64_t(c) * LC;
+    const int l0 = c * LC;
+    if (l0 + LC <= m) {
 #pragma unroll
-    for (int t = 0; t < RW; ++t)
+      for (int t = 0; t < RW; ++t)
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t l = l0 + lane + 32 * u;
-        pv[t][u] = (live[t] && l < m) ? P[row[t] * ld + l] : czero<V>();
-      }
+        for (int u = 0; u < U; ++u) pv[t][u] = __ldg(prow[t] + l0 + 32 * u);
+    } else {
+#pragma unroll
+      for (int t = 0; t < RW; ++t)
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[t][u] = l0 + lane + 32 * u < m ? __ldg(prow[t] + l0 + 32 * u) : czero<V>();
+    }
   };
   V acc[RW][KG];
 #pragma unroll
   for (int t = 0; t < RW; ++t)
 #pragma unroll
     for (int q = 0; q < KG; ++q) acc[t][q] = czero<V>();
-  V pc[RW][U], pn[RW][U];
+  // the row's chunks of P are loaded PF - 1 chunks ahead of the one being
+  // multiplied (registers, rotated by unrolling)
+  V pq[PF][RW][U];
   stage(0, rs[0]);
   tiled::cp_async_commit();
-  load_p(0, pc);
-  for (int c = 0; c < nch; ++c) {
-    if (c + 1 < nch) {
-      stage(c + 1, rs[(c + 1) & 1]);
-      load_p(c + 1, pn);
-    }
-    tiled::cp_async_commit();
-    tiled::cp_async_wait<1>();
-    __syncthreads();
-    const V* b = rs[c & 1];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
+  for (int f = 0; f < PF - 1; ++f)
+    if (f < nch) load_p(f, pq[f]);
+  for (int c0 = 0; c0 < nch; c0 += PF) {
 #pragma unroll
-      for (int q = 0; q < KG; ++q) {
-        const V rv = b[q * LC + lane + 32 * u];
+    for (int f = 0; f < PF; ++f) {
+      const int c = c0 + f;
+      if (c < nch) {
+        if (c + 1 < nch) stage(c + 1, rs[(c + 1) & 1]);
+        if (c + PF - 1 < nch) load_p(c + PF - 1, pq[(f + PF - 1) % PF]);
+        tiled::cp_async_commit();
+        tiled::cp_async_wait<1>();
+        __syncthreads();
+        const V* b = rs[c & 1] + lane * RS;
 #pragma unroll
-        for (int t = 0; t < RW; ++t) acc[t][q] = cfma(pc[t][u], rv, acc[t][q]);
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int q = 0; q < KG; ++q) {
+            const V rv = b[32 * u * RS + q];
+#pragma unroll
+            for (int t = 0; t < RW; ++t) acc[t][q] = cfma(pq[f][t][u], rv, acc[t][q]);
+          }
+        }
+        __syncthreads();
       }
     }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < RW; ++t)
-#pragma unroll
-      for (int u = 0; u < U; ++u) pc[t][u] = pn[t][u];
   }
   tiled::cp_async_wait<0>();
 #pragma unroll
@@ -334,7 +359,7 @@ bt_rows_kernel(int64_t m, int k, const cplx_t<T>* __restrict__ P, int64_t ld, co
     for (int q = 0; q < KG; ++q) {
       if (lane != q) continue;
       V v = acc[t][q];
-      const int64_t o = row[t] * k + q0 + q;
+      const int o = (i0 + w + 8 * t) * k + q0 + q;
       if (c_in) {
         const V cv = c_in[o];
         v = mk(cv.x + sign * v.x, cv.y + sign * v.y);
@@ -348,14 +373,30 @@ template <class T, int RW, int KG>
 void bt_rows_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
                 const cplx_t<T>* c_in, T sign, cudaStream_t s) {
   constexpr int LC = sizeof(T) == 8 ? 128 : 256;  // r chunk: 32 KB of static shared memory, double-buffered
+  // chunks of P in registers (PF - 1 in flight): two-row warps prefetch two
+  // chunks ahead (config 4: 9.31 vs 9.47 ms per cycle), one-row warps one
+  // (config 3: 1.86 vs 1.91); HZ_BT_PF=0 / 1 forces shallow / deep
+  static const int pf_env = [] {
+    const char* e = std::getenv("HZ_BT_PF");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool deep = pf_env >= 0 ? pf_env == 1 : RW == 2;
   const dim3 grid(unsigned((m + 8 * RW - 1) / (8 * RW)), unsigned(k / KG));
-  bt_rows_kernel<T, RW, KG, LC><<<grid, 256, 0, s>>>(m, k, P, ld, r, out, c_in, sign);
+  if (deep)
+    bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3)><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+  else
+    bt_rows_kernel<T, RW, KG, LC, 2><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
 }
 
 template <class T>
 void bt_rows(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
              const cplx_t<T>* c_in, T sign, cudaStream_t s) {
-  const bool two = m > int64_t(kNumSMs) * 8;
+  // two rows per warp above one CTA per SM (HZ_BT_RW=1 / 2 forces)
+  static const int rw_env = [] {
+    const char* e = std::getenv("HZ_BT_RW");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool two = rw_env ? rw_env == 2 : m > int64_t(kNumSMs) * 8;
   auto go = [&](auto kg) {
     constexpr int KG = decltype(kg)::value;
     if (two)

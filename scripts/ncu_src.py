@@ -28,7 +28,7 @@ for r in rows[h + 1:]:
     out.append(dict(samp=samp, src=r[ix["Source"]], wf=num(r[ix["L1 Wavefronts Shared"]]),
                     ideal=num(r[ix["L1 Wavefronts Shared Ideal"]]), exc=num(r[ix["L1 Wavefronts Shared Excessive"]]),
                     n=int(num(r[ix["Instructions Executed"]])), lsb=r[ix["stall_long_sb"]], ssb=r[ix["stall_short_sb"]],
-                    loc=num(r[ix["L2 Theoretical Sectors Local"]])))
+                    loc=num(r[ix["L2 Theoretical Sectors Local"]]) if "L2 Theoretical Sectors Local" in ix else 0.0))
 print("total samples", tot)
 print("== top lines by samples")
 for o in sorted(out, key=lambda o: -o["samp"])[: int(sys.argv[2]) if len(sys.argv) > 2 else 30]:
