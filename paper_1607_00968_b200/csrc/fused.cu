@@ -1263,6 +1263,196 @@ bool launch_stencil9_k8(const LevelOp<float>& op, int mode, float wj, const floa
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Two damped-Jacobi sweeps of a 2D Galerkin level in one launch (k = 8,
+// complex64): relax(..., 2 sweeps) of src/multigrid.cpp:119-136 with the
+// intermediate iterate kept in shared memory. ZERO: the visit starts from
+// x = 0, so the first sweep is x1 = wD^-1 b (jacobi_zero) and no iterate is
+// read at all.
+//
+// A CTA owns NT - 2 nodes of a strip of NT (one halo node per side for the
+// first sweep) and a chunk of rows; rows stream through a PD-deep ring of
+// slots (x with a one-node halo, the 80-byte (9 coefficients, D^-1) records,
+// b), one mbarrier each, as in stencil9_k8_kernel. Step j computes the first
+// sweep's row j into a 4-row ring and the second sweep's row j - 2 from the
+// ring rows j - 3 .. j - 1 published by earlier barriers: one __syncthreads
+// per step. Same per-column operations in the same order as two
+// stencil9_k8 / stencil_v4 launches (ascending plane order, jacobi_upd), and
+// couplings that leave the grid are exact zeros in the records, so the
+// results are bitwise equal.
+template <bool ZERO, int NT, int PD>
+struct S9PairPlan {
+  static constexpr int TH = NT * 4;
+  static constexpr size_t XROW = ZERO ? 0 : size_t(NT + 2) * kK8 * sizeof(float2);
+  static constexpr size_t CROW = size_t(NT) * 10 * sizeof(float2);
+  static constexpr size_t BROW = size_t(NT) * kK8 * sizeof(float2);
+  static constexpr size_t SLOT = XROW + CROW + BROW;
+  static constexpr size_t RROW = size_t(NT) * kK8 * sizeof(float2);
+  static constexpr size_t OFF_SLOTS = 128;
+  static constexpr size_t OFF_RING = OFF_SLOTS + PD * SLOT;
+  static constexpr size_t BYTES = OFF_RING + 4 * RROW;
+};
+
+template <bool ZERO, int NT, int PD, int MINB>
+__global__ void __launch_bounds__(NT * 4, MINB)
+stencil9_pair_k8_kernel(LevelOp<float> op, float wj, const float2* __restrict__ x, const float2* __restrict__ b,
+                        float2* __restrict__ out, int rows) {
+  using P = S9PairPlan<ZERO, NT, PD>;
+  static_assert(PD >= 5, "rows j-2 .. j+1 are live in a step");
+  constexpr int RU = NT * 4;  // float4 units per ring row
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  float4* ring = reinterpret_cast<float4*>(sm + P::OFF_RING);
+  const int n0 = int(op.g.n0), n1 = int(op.g.n1);
+  const int t = threadIdx.x, xs = t >> 2, cg = t & 3;
+  const int X0 = blockIdx.x * (NT - 2), gx = X0 - 1 + xs;  // strip nodes [X0 - 1, X0 + NT - 1)
+  const int Y0 = blockIdx.y * rows, Y1 = min(Y0 + rows, n1);
+  const bool inx = gx >= 0 && gx < n0;
+  const bool own_x = inx && xs >= 1 && xs < NT - 1;
+  const int rA0 = max(Y0 - 1, 0), rA1 = min(Y1, n1 - 1);  // first-sweep rows (inclusive)
+  const int r0 = Y0 - 2, r1 = Y1 + 1;                     // streamed rows
+  // in-grid parts of a staged row: records / b over strip nodes [sa, sb), x over units [xa, xb) of
+  // nodes [X0 - 2, X0 + NT)
+  const int sa = max(0, 1 - X0), sb = min(NT, n0 - X0 + 1);
+  const int xa = max(0, 2 - X0), xb = min(NT + 2, n0 - X0 + 2);
+  for (int i = t; i < int((P::BYTES - P::OFF_SLOTS) / 16); i += P::TH)
+    reinterpret_cast<float4*>(sm + P::OFF_SLOTS)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t == 0) {
+    for (int p = 0; p < PD; ++p) tma::mbar_init(&bars[p], 1);
+    tma::fence_mbar_init();
+  }
+  tma::fence_proxy_async();
+  __syncthreads();
+  auto produce = [&](int r) {
+    if (r > r1) return;
+    tma::fence_proxy_async();
+    const int sl = (r - r0) % PD;
+    unsigned char* slot = sm + P::OFF_SLOTS + sl * P::SLOT;
+    const bool recs = r >= rA0 && r <= rA1;
+    const int rr = min(max(r, 0), n1 - 1);  // x rows outside the grid: any finite row (their couplings are 0)
+    const uint32_t xbytes = ZERO ? 0u : uint32_t(xb - xa) * kK8 * sizeof(float2);
+    const uint32_t nrec = uint32_t(sb - sa);
+    tma::mbar_arrive_expect_tx(&bars[sl], xbytes + (recs ? nrec * uint32_t((10 + kK8) * sizeof(float2)) : 0u));
+    if (!ZERO)
+      tma::bulk_g2s(slot + size_t(xa) * kK8 * sizeof(float2), x + (int64_t(n0) * rr + X0 - 2 + xa) * kK8, xbytes,
+                    &bars[sl]);
+    if (recs) {
+      const int64_t node0 = int64_t(n0) * r + X0 - 1 + sa;
+      tma::bulk_g2s(slot + P::XROW + size_t(sa) * 10 * sizeof(float2), op.cd + node0 * 10,
+                    nrec * uint32_t(10 * sizeof(float2)), &bars[sl]);
+      tma::bulk_g2s(slot + P::XROW + P::CROW + size_t(sa) * kK8 * sizeof(float2), b + node0 * kK8,
+                    nrec * uint32_t(kK8 * sizeof(float2)), &bars[sl]);
+    }
+  };
+  if (t == 0)
+    for (int p = 0; p < PD; ++p) produce(r0 + p);
+  auto wait_row = [&](int r) {
+    const int u = r - r0;
+    tma::mbar_wait(&bars[u % PD], uint32_t((u / PD) & 1));
+  };
+  auto slot_of = [&](int r) { return sm + P::OFF_SLOTS + ((r - r0) % PD) * P::SLOT; };
+  // one sweep's output for this thread's 2 columns of row r: xr = the three x rows (units of 4 per
+  // node, unit 0 = node `base` - 1), own value xc
+  auto sweep = [&](const unsigned char* srow, const float4* xm1, const float4* x00, const float4* xp1, int base,
+                   float2 (&o)[2]) {
+    const float2* cf = reinterpret_cast<const float2*>(srow + P::XROW) + xs * 10;
+    const float4* xr[3] = {xm1, x00, xp1};
+    float2 av[9];
+    float4 xv[9];
+#pragma unroll
+    for (int sdx = 0; sdx < 9; ++sdx) {
+      const int dy = sdx / 3 - 1, dx = sdx % 3 - 1;
+      av[sdx] = cf[sdx];
+      xv[sdx] = xr[dy + 1][(base + dx) * 4 + cg];
+    }
+    float2 acc[2] = {czero<float2>(), czero<float2>()};
+#pragma unroll
+    for (int sdx = 0; sdx < 9; ++sdx) {
+      acc[0] = cfma(av[sdx], make_float2(xv[sdx].x, xv[sdx].y), acc[0]);
+      acc[1] = cfma(av[sdx], make_float2(xv[sdx].z, xv[sdx].w), acc[1]);
+    }
+    const float4 bv = reinterpret_cast<const float4*>(srow + P::XROW + P::CROW)[t];
+    const float2 d = cf[9];
+    const float2 wd = mk(wj * d.x, wj * d.y);
+    const float4 xc = xv[4];
+    o[0] = jacobi_upd(make_float2(xc.x, xc.y), wd, make_float2(bv.x, bv.y), acc[0]);
+    o[1] = jacobi_upd(make_float2(xc.z, xc.w), wd, make_float2(bv.z, bv.w), acc[1]);
+  };
+  for (int j = Y0 - 1; j <= Y1 + 1; ++j) {
+    // (2) second sweep, row y = j - 2, from the ring rows y - 1, y, y + 1
+    const int y = j - 2;
+    if (own_x && y >= Y0 && y < Y1) {
+      float2 o[2];
+      sweep(slot_of(y), ring + ((y + 3) & 3) * RU, ring + (y & 3) * RU, ring + ((y + 1) & 3) * RU, xs, o);
+      gstore(out + (int64_t(n0) * y + gx) * kK8 + cg * 2, o);
+    }
+    // (1) first sweep, row j, into the ring
+    float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (j >= rA0 && j <= rA1) {
+      if (ZERO) {
+        wait_row(j);
+        if (inx) {
+          const unsigned char* srow = slot_of(j);
+          const float2 d = (reinterpret_cast<const float2*>(srow + P::XROW) + xs * 10)[9];
+          const float2 wd = mk(wj * d.x, wj * d.y);
+          const float4 bv = reinterpret_cast<const float4*>(srow + P::XROW + P::CROW)[t];
+          const float2 a = cmul(wd, make_float2(bv.x, bv.y)), c = cmul(wd, make_float2(bv.z, bv.w));
+          x1 = make_float4(a.x, a.y, c.x, c.y);
+        }
+      } else {
+        wait_row(j - 1);
+        wait_row(j);
+        wait_row(j + 1);
+        if (inx) {
+          float2 o[2];
+          sweep(slot_of(j), reinterpret_cast<const float4*>(slot_of(j - 1)), reinterpret_cast<const float4*>(slot_of(j)),
+                reinterpret_cast<const float4*>(slot_of(j + 1)), xs + 1, o);
+          x1 = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+        }
+      }
+    }
+    ring[(j & 3) * RU + t] = x1;
+    __syncthreads();  // row j - 2's slot is free: its last readers were this step's sweeps
+    if (t == 0 && j - 2 >= r0) produce(j - 2 + PD);
+  }
+}
+
+template <bool ZERO>
+void run_stencil9_pair_k8(const LevelOp<float>& op, float wj, const float2* x, const float2* b, float2* out,
+                          cudaStream_t s) {
+  constexpr int NT = 64, PD = 6;
+  using P = S9PairPlan<ZERO, NT, PD>;
+  constexpr int MINB = int(std::min<size_t>(std::min<size_t>((227 * 1024) / (P::BYTES + 1024), 2048 / P::TH), 8));
+  const int strips = int((op.g.n0 + NT - 3) / (NT - 2));
+  // rows per CTA: about one resident wave of CTAs, at least 8 rows (3 extra rows are staged and 2 extra
+  // first-sweep rows computed per chunk); HZ_S9P_ROWS forces
+  const int chunks = std::max(1, kNumSMs * MINB / std::max(1, strips));
+  const int e = env_int("HZ_S9P_ROWS", 0);
+  const int rows = e > 0 ? e : std::max(8, int((op.g.n1 + chunks - 1) / chunks));
+  const dim3 grid(unsigned(strips), unsigned((op.g.n1 + rows - 1) / rows));
+  auto kern = stencil9_pair_k8_kernel<ZERO, NT, PD, MINB>;
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
+  kern<<<grid, P::TH, P::BYTES, s>>>(op, wj, x, b, out, rows);
+}
+
+bool launch_stencil9_pair_k8(const LevelOp<float>& op, float wj, const float2* x, const float2* b, float2* out,
+                             cudaStream_t s) {
+  static const bool on = env_int("HZ_S9_PAIR", 1) != 0;
+  static const int64_t min_nodes = env_int("HZ_S9_PAIR_MIN_NODES", 100000);
+  if (!on || op.kind != kStencil || op.ndim != 2 || op.g.k != kK8 || !op.cd || op.g.z0 != 0 ||
+      op.g.z1 != op.g.n1 || int64_t(op.g.nodes) < min_nodes || op.g.n1 < 4)
+    return false;
+  const double n = double(op.g.nodes);
+  ProfScope prof(x ? "jacobi2_stencil_c64_L1" : "jacobi2_zero_stencil_c64_L1",
+                 n * (kK8 * 8.0 * (x ? 3.0 : 2.0) + 80.0), s);
+  if (x)
+    run_stencil9_pair_k8<false>(op, wj, x, b, out, s);
+  else
+    run_stencil9_pair_k8<true>(op, wj, x, b, out, s);
+  HZ_LAUNCH_CHECK();
+  return true;
+}
+
 bool fused_vcycle_enabled() {
   static const bool on = env_int("HZ_FUSED_VCYCLE", 1) != 0;
   return on;

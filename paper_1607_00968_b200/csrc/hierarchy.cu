@@ -668,6 +668,16 @@ void Hierarchy<T>::relax(int l, const CycleSpec& spec, int sweeps, int k, const 
                          V*& other, bool& cur_zero, cudaStream_t s) {
   const T wj = T(spec.jacobi_weight);
   const bool sl = slab_level(l);
+  if constexpr (std::is_same<T, float>::value) {
+    // both sweeps of a V(2,2) visit of a large 2D Galerkin level in one launch
+    // (fused.cu); the result lands in `other`, which becomes the iterate
+    if (sweeps == 2 && !sl && l > 0 &&
+        launch_stencil9_pair_k8(op(l, k), wj, cur_zero ? nullptr : cur, b, other, s)) {
+      std::swap(cur, other);
+      cur_zero = false;
+      return;
+    }
+  }
   for (int sw = 0; sw < sweeps; ++sw) {
     // one exchange step per sweep: a part's sweep reads its neighbours'
     // faces of cur (and must not overwrite `other` while they still read it)

@@ -134,6 +134,14 @@ void launch_inv_plane(int64_t n, const double2* centre, double2* inv, cudaStream
 bool launch_stencil9_k8(const LevelOp<float>& op, int mode, float wj, const float2* x, const float2* b, float2* out,
                         cudaStream_t s);
 
+// two damped-Jacobi sweeps of a complex64 2D Galerkin level (k = 8) in one
+// launch, the intermediate iterate in shared memory (fused.cu); x == nullptr:
+// the sweeps start from x = 0. out must not alias x. Bitwise equal to two
+// launch_jacobi calls (or launch_jacobi_zero + launch_jacobi); false when it
+// does not apply (small levels, other k / layouts, HZ_S9_PAIR=0)
+bool launch_stencil9_pair_k8(const LevelOp<float>& op, float wj, const float2* x, const float2* b, float2* out,
+                             cudaStream_t s);
+
 // elementwise casts / copies
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);

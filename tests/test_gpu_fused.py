@@ -103,6 +103,23 @@ def test_bulk_copy_galerkin_level_kernel_equals_plain(nx, nz, nl, kind):
     assert np.array_equal(odd, old)
 
 
+@pytest.mark.parametrize("nx,nz,nl,kind,rows", [(257, 129, 4, "V", "0"), (1025, 513, 5, "V", "0"), (301, 97, 3, "W", "5"),
+                                               (121, 233, 4, "K", "9"), (65, 49, 3, "V", "4"), (1025, 513, 6, "W", "13")])
+def test_two_sweep_galerkin_level_kernel_equals_single_sweeps(nx, nz, nl, kind, rows):
+    """complex64 2D Galerkin levels at k = 8: both Jacobi sweeps of a visit in
+    one launch (stencil9_pair_k8, zero-start and general; every level via
+    HZ_S9_PAIR_MIN_NODES=0, odd row chunks via HZ_S9P_ROWS) against one launch
+    per sweep (HZ_S9_PAIR=0), bitwise, through whole V / W / K cycles; the
+    default (levels of >= 100k nodes only) likewise."""
+    extra = {} if rows == "0" else {"HZ_S9P_ROWS": rows}
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(CYCLE, os.path.join(d, "n.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9_PAIR_MIN_NODES="0", **extra)
+        old = _run(CYCLE, os.path.join(d, "o.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9_PAIR="0")
+        dfl = _run(CYCLE, os.path.join(d, "d.npy"), "1", nx, nz, 8, nl, "c64", kind)
+    assert np.array_equal(new, old), f"max rel diff {rel_err(new, old):.3e}"
+    assert np.array_equal(dfl, old)
+
+
 def test_fused_c128_cycle_matches_reference():
     """c128 V(2,2) cycle through the fused fine level vs the compiled
     reference's MgHierarchy::cycle at the 1e-12 parity bar."""
