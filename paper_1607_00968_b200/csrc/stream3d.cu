@@ -50,9 +50,13 @@ namespace {
 
 namespace s3 {
 
+#ifndef HZ_S3_LATE
+#define HZ_S3_LATE 1
+#endif
+
 constexpr int kSlots = 5;   // ring of plane slots
 constexpr int kAhead = 3;   // planes in flight ahead of the one being computed
-constexpr int kBarBytes = 128;
+constexpr int kBarBytes = 256;  // mbarriers (128 B), then the 27-point weights
 
 template <class T, class XV>
 struct Tile;
@@ -207,7 +211,7 @@ stream3d_kernel(const Args<T, XV, Out> a) {
   // 27-point Jacobi: the pending row's own x and D^-1 are read back from the
   // previous plane's slot when it is finished (held one step longer, one
   // plane less in flight) instead of being carried in registers
-  constexpr bool LATE = KIND == kFine27 && MODE == 2;
+  constexpr bool LATE = KIND == kFine27 && MODE == 2 && HZ_S3_LATE;
   constexpr int AHEAD = LATE ? kAhead - 1 : kAhead;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -218,6 +222,7 @@ stream3d_kernel(const Args<T, XV, Out> a) {
   const int n0 = int(g.n0), n1 = int(g.n1), n2 = int(g.n2);
   const int tid = int(threadIdx.x), lane = tid & 31;
 
+  if (tid < 8) reinterpret_cast<T*>(smem + 128)[tid] = (tid < 5 ? T(1) : T(0.5)) * a.op.w27[tid];
   if (tid == 0) {
     for (int q = 0; q < kSlots; ++q) {
       tma::mbar_init(&full[q], 1);
@@ -337,8 +342,10 @@ stream3d_kernel(const Args<T, XV, Out> a) {
   int ci = 0;  // planes consumed so far
   bool held = false;  // LATE: the last consumed plane's slot is still held
   const T wx = a.op.w[0], wy = a.op.w[1], wz = a.op.w[2];
-  const T l0 = a.op.w27[0], l1 = a.op.w27[1], l2 = a.op.w27[2], l3 = a.op.w27[3];
-  const T m0 = a.op.w27[4], h1 = T(0.5) * a.op.w27[5], h2 = T(0.5) * a.op.w27[6], h3 = T(0.5) * a.op.w27[7];
+  // the 27-point weights {lap0..3, mu0, mu1/2, mu2/2, mu3/2} are read from shared memory where they are used
+  // (volatile: not hoisted back into eight live registers of a kernel that is short of them)
+  const volatile T* wsm = reinterpret_cast<const volatile T*>(smem + 128);
+  constexpr int kL0 = 0, kL1 = 1, kL2 = 2, kL3 = 3, kM0 = 4, kH1 = 5, kH2 = 6, kH3 = 7;
 
   using St = Carry<V, CPT>;
   auto finish = [&](int p, const St& in, const V* ax) {  // output of plane p from A x
@@ -358,9 +365,13 @@ stream3d_kernel(const Args<T, XV, Out> a) {
   };
   // 27-point, MODE != 0: b is folded into the pending sum when the plane is
   // started (s1 carries A x - b), so it is not held until the plane finishes
-  auto finish_nr = [&](int p, const V* nr) {
+  auto finish_nr = [&](int p, const St& in, const V* nr) {
     V o[CPT];
-    if constexpr (MODE == 2) {
+    if constexpr (MODE == 2 && !LATE) {
+      const V nwd = mk(-in.wd.x, -in.wd.y);
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) o[q] = p_cfma(nwd, nr[q], in.u[q]);
+    } else if constexpr (MODE == 2) {
       const unsigned char* sl = slots + ((ci + kSlots - 1) % kSlots) * C::SLOT;  // plane p's slot
       V xo[CPT], Mx, d;
       lds_cols<V, XV, NU>(sl + C::U_OFF + cnode * C::NBX, uo, xo);
@@ -451,9 +462,10 @@ stream3d_kernel(const Args<T, XV, Out> a) {
 #pragma unroll
           for (int q = 0; q < CPT; ++q) {
             const V v0 = cmul(Mn, out.u[q]);
-            out.s1[q] = p_rfma(m0, v0, p_rfma(l0, out.u[q], in.p1[q]));
+            out.s1[q] = p_rfma(T(wsm[kM0]), v0, p_rfma(T(wsm[kL0]), out.u[q], in.p1[q]));
             out.s2[q] = in.p2[q];
-            out.p1[q] = p_rfma(h1, v0, p_scale(l1, out.u[q]));
+            const T h1 = wsm[kH1];
+            out.p1[q] = p_rfma(h1, v0, p_scale(T(wsm[kL1]), out.u[q]));
             out.p2[q] = p_scale(h1, out.u[q]);
           }
           // in-plane faces, then corners: Q(u) and Q(M u) folded into the channels
@@ -481,8 +493,8 @@ stream3d_kernel(const Args<T, XV, Out> a) {
                 }
               }
             }
-            const T la = cls == 1 ? l1 : l2, ha = cls == 1 ? h1 : h2;  // same plane
-            const T lb = cls == 1 ? l2 : l3, hb = cls == 1 ? h2 : h3;  // adjacent planes
+            const T la = wsm[cls == 1 ? kL1 : kL2], ha = wsm[cls == 1 ? kH1 : kH2];  // same plane
+            const T lb = wsm[cls == 1 ? kL2 : kL3], hb = wsm[cls == 1 ? kH2 : kH3];  // adjacent planes
 #pragma unroll
             for (int q = 0; q < CPT; ++q) {
               const V qv = mk(qa[q].x - qb[q].y, qa[q].y + qb[q].x);
@@ -504,7 +516,7 @@ stream3d_kernel(const Args<T, XV, Out> a) {
           if constexpr (MODE == 0)
             finish(p - 1, in, ax);
           else
-            finish_nr(p - 1, ax);
+            finish_nr(p - 1, in, ax);
         }
         if (p >= zs && p < ze) {
           out.M = Mn;
@@ -513,6 +525,11 @@ stream3d_kernel(const Args<T, XV, Out> a) {
             lds_cols<V, V, NU>(sl + C::B_OFF + inode * C::NBV, uo, bv);
 #pragma unroll
             for (int q = 0; q < CPT; ++q) out.s1[q] = csub(out.s1[q], bv[q]);
+          }
+          if constexpr (MODE == 2 && !LATE) {
+            V d = dn;
+            if constexpr (C::HAS_D) d = *reinterpret_cast<const V*>(sl + C::D_OFF + inode * 16);
+            out.wd = mk(a.wj * d.x, a.wj * d.y);
           }
         }
       }
