@@ -1453,6 +1453,218 @@ bool launch_stencil9_pair_k8(const LevelOp<float>& op, float wj, const float2* x
   return true;
 }
 
+// ---------------------------------------------------------------------------
+// Zero-start pre-smoothing visit of a 2D Galerkin level in one launch (k = 8,
+// complex64): x1 = wD^-1 b, x2 = x1 + wD^-1 (b - A x1), r = b - A x2 and the
+// restriction rc = P^T r (cycle_rec, src/multigrid.cpp:162-178), with x1 and r
+// never written to memory. The geometry is fused_pre_k8_kernel's (strip of NT
+// nodes = 2 * TC + 8, halo 4 per side, chunks of coarse rows, restriction
+// units spread over the warps, restrict_row); the operator is the 9-point
+// stencil read from the level's 80-byte records, so all three rows of every
+// stage come from shared-memory rings (4 rows of x1, 4 of x2, 2 of r), and the
+// record / b rows stay in their slots until the stage that needs them last
+// (row j - 4) has run. Stages of step j: restriction of r row j - 5, r row
+// j - 4, x2 row j - 2, x1 row j; each reads only ring rows published by an
+// earlier step's barrier. Same operations in the same order as the unfused
+// kernels: bitwise equal.
+template <int NT, int PD>
+struct S9PrePlan {
+  static constexpr int TH = NT * 4, W = NT - 8, TC = W / 2;
+  static constexpr size_t CROW = size_t(NT) * 10 * sizeof(float2);
+  static constexpr size_t BROW = size_t(NT) * kK8 * sizeof(float2);
+  static constexpr size_t SLOT = CROW + BROW;
+  static constexpr size_t RROW = size_t(NT) * kK8 * sizeof(float2);
+  static constexpr size_t OFF_SLOTS = 128;
+  static constexpr size_t OFF_X1 = OFF_SLOTS + PD * SLOT;
+  static constexpr size_t OFF_X2 = OFF_X1 + 4 * RROW;
+  static constexpr size_t OFF_R = OFF_X2 + 4 * RROW;
+  static constexpr size_t BYTES = OFF_R + 2 * RROW;
+};
+
+template <int NT, int PD, int MINB>
+__global__ void __launch_bounds__(NT * 4, MINB)
+stencil9_pre_k8_kernel(LevelOp<float> op, LevelGeom gc, float wj, const float2* __restrict__ b,
+                       float2* __restrict__ x2out, float2* __restrict__ rc, int crows) {
+  using P = S9PrePlan<NT, PD>;
+  static_assert(PD >= 6, "rows j-4 .. j are live in a step");
+  constexpr int W = P::W, TC = P::TC, TH = P::TH, RU = NT * 4;
+  extern __shared__ __align__(128) unsigned char sm[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+  float4* x1s = reinterpret_cast<float4*>(sm + P::OFF_X1);
+  float4* x2s = reinterpret_cast<float4*>(sm + P::OFF_X2);
+  float4* rs = reinterpret_cast<float4*>(sm + P::OFF_R);
+  const int n0 = int(op.g.n0), n1 = int(op.g.n1);
+  const int t = threadIdx.x, xs = t >> 2, cg = t & 3;
+  const int CX0 = blockIdx.x * TC, X0 = 2 * CX0, gx0 = X0 - 4, gx = gx0 + xs;
+  const int CY0 = blockIdx.y * crows, CY1 = min(CY0 + crows, int(gc.n1));
+  const int Y0 = 2 * CY0, Y1 = 2 * CY1;
+  const int sa = max(0, -gx0), sb = min(NT, n0 - gx0);  // in-grid strip nodes [sa, sb)
+  const bool inx = xs >= sa && xs < sb;
+  const bool own_x = inx && xs >= 4 && xs < 4 + W;
+  // restriction units (coarse node ci, column pair rcg), spread evenly over the warps
+  constexpr int NW = TH / 32, RPW = (4 * TC + NW - 1) / NW;
+  static_assert(RPW <= 32, "one restriction unit per thread");
+  const int lane = t & 31, ru = (t >> 5) * RPW + lane;
+  const int ci = ru >> 2, rcg = ru & 3, I = CX0 + ci;
+  const bool rest = lane < RPW && ru < 4 * TC && I < int(gc.n0);
+  const int rt = (2 * ci + 4) * 4 + rcg;
+  const bool rxm = 2 * I - 1 >= 0, rxp = 2 * I + 1 < n0;
+  const int64_t rcbase = int64_t(I) * kK8 + rcg * 2, rcstride = int64_t(gc.n0) * kK8;
+
+  const int jbeg = Y0 - 3;                                    // first step (x1 row)
+  const int jA0 = max(jbeg, 0), jA1 = min(Y1 + 1, n1 - 1);    // x1 rows = staged rows
+  const int yB0 = max(Y0 - 2, 0), yB1 = min(Y1, n1 - 1);      // x2 rows
+  const int yC0 = max(Y0 - 1, 0), yC1 = min(Y1 - 1, n1 - 1);  // r rows (and restriction)
+  const int jend = yC1 + 5;                                   // last step (restriction of row yC1)
+
+  for (int i = t; i < int((P::BYTES - P::OFF_SLOTS) / 16); i += TH)
+    reinterpret_cast<float4*>(sm + P::OFF_SLOTS)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t == 0) {
+    for (int p = 0; p < PD; ++p) tma::mbar_init(&bars[p], 1);
+    tma::fence_mbar_init();
+  }
+  tma::fence_proxy_async();
+  __syncthreads();
+  const uint32_t nb = uint32_t(sb - sa);
+  // staged row r (in [jA0, jA1]) goes to slot (r - jA0) % PD
+  auto produce = [&](int r) {
+    if (r < jA0 || r > jA1) return;
+    tma::fence_proxy_async();
+    const int sl = (r - jA0) % PD;
+    unsigned char* slot = sm + P::OFF_SLOTS + sl * P::SLOT;
+    const int64_t node0 = int64_t(n0) * r + gx0 + sa;
+    tma::mbar_arrive_expect_tx(&bars[sl], nb * uint32_t((10 + kK8) * sizeof(float2)));
+    tma::bulk_g2s(slot + size_t(sa) * 10 * sizeof(float2), op.cd + node0 * 10, nb * uint32_t(10 * sizeof(float2)),
+                  &bars[sl]);
+    tma::bulk_g2s(slot + P::CROW + size_t(sa) * kK8 * sizeof(float2), b + node0 * kK8,
+                  nb * uint32_t(kK8 * sizeof(float2)), &bars[sl]);
+  };
+  if (t == 0)
+    for (int p = 0; p < PD; ++p) produce(jA0 + p);
+  auto slot_of = [&](int r) { return sm + P::OFF_SLOTS + ((r - jA0) % PD) * P::SLOT; };
+  // (A u)[this thread's 2 columns] of row y from three ring rows, coefficients from the row's records
+  auto ax9 = [&](const unsigned char* srow, const float4* rm, const float4* r0, const float4* rp, float2 (&acc)[2],
+                 float4& centre) {
+    const float2* cf = reinterpret_cast<const float2*>(srow) + xs * 10;
+    const float4* xr[3] = {rm, r0, rp};
+    float2 av[9];
+    float4 xv[9];
+#pragma unroll
+    for (int sdx = 0; sdx < 9; ++sdx) {
+      const int dy = sdx / 3 - 1, dx = sdx % 3 - 1;
+      av[sdx] = cf[sdx];
+      xv[sdx] = xr[dy + 1][(xs + dx) * 4 + cg];
+    }
+    acc[0] = acc[1] = czero<float2>();
+#pragma unroll
+    for (int sdx = 0; sdx < 9; ++sdx) {
+      acc[0] = cfma(av[sdx], make_float2(xv[sdx].x, xv[sdx].y), acc[0]);
+      acc[1] = cfma(av[sdx], make_float2(xv[sdx].z, xv[sdx].w), acc[1]);
+    }
+    centre = xv[4];
+  };
+  float2 racc[2] = {czero<float2>(), czero<float2>()};
+  for (int j = jbeg; j <= jend; ++j) {
+    // (D) restriction of r row y = j - 5
+    {
+      const int y = j - 5;
+      if (rest && y >= yC0 && y <= yC1) {
+        const float4* rr = rs + (y & 1) * RU;
+        const Unit<float, 2> rv0 = f42u(rr[rt]);
+        const Unit<float, 2> rvm = rxm ? f42u(rr[rt - 4]) : rv0, rvp = rxp ? f42u(rr[rt + 4]) : rv0;
+        restrict_row(y, n1, CY0, CY1, rcbase, rcstride, rxm, rxp, rvm, rv0, rvp, racc, rc);
+      }
+    }
+    // (C) r row y = j - 4 = b - A x2
+    {
+      const int y = j - 4;
+      float4 rv = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (inx && xs >= 2 && xs < NT - 2 && y >= yC0 && y <= yC1) {
+        const unsigned char* srow = slot_of(y);
+        float2 a[2];
+        float4 c4;
+        ax9(srow, x2s + ((y + 3) & 3) * RU, x2s + (y & 3) * RU, x2s + ((y + 1) & 3) * RU, a, c4);
+        const float4 bv = reinterpret_cast<const float4*>(srow + P::CROW)[t];
+        const float2 r0 = csub(make_float2(bv.x, bv.y), a[0]), r1 = csub(make_float2(bv.z, bv.w), a[1]);
+        rv = make_float4(r0.x, r0.y, r1.x, r1.y);
+      }
+      rs[(y & 1) * RU + t] = rv;
+    }
+    // (B) x2 row y = j - 2 = x1 + wD^-1 (b - A x1)
+    {
+      const int y = j - 2;
+      float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (inx && xs >= 1 && xs < NT - 1 && y >= yB0 && y <= yB1) {
+        const unsigned char* srow = slot_of(y);
+        float2 a[2];
+        float4 c4;
+        ax9(srow, x1s + ((y + 3) & 3) * RU, x1s + (y & 3) * RU, x1s + ((y + 1) & 3) * RU, a, c4);
+        const float4 bv = reinterpret_cast<const float4*>(srow + P::CROW)[t];
+        const float2 d = (reinterpret_cast<const float2*>(srow) + xs * 10)[9];
+        const float2 wd = mk(wj * d.x, wj * d.y);
+        float2 o[2];
+        o[0] = jacobi_upd(make_float2(c4.x, c4.y), wd, make_float2(bv.x, bv.y), a[0]);
+        o[1] = jacobi_upd(make_float2(c4.z, c4.w), wd, make_float2(bv.z, bv.w), a[1]);
+        o4 = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+        if (own_x && y >= Y0 && y < Y1) gstore(x2out + (int64_t(n0) * y + gx) * kK8 + cg * 2, o);
+      }
+      x2s[(y & 3) * RU + t] = o4;
+    }
+    // (A) x1 row j = wD^-1 b
+    {
+      float4 x1 = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j >= jA0 && j <= jA1) {
+        const int u = j - jA0;
+        tma::mbar_wait(&bars[u % PD], uint32_t((u / PD) & 1));
+        if (inx) {
+          const unsigned char* srow = slot_of(j);
+          const float2 d = (reinterpret_cast<const float2*>(srow) + xs * 10)[9];
+          const float2 wd = mk(wj * d.x, wj * d.y);
+          const float4 bv = reinterpret_cast<const float4*>(srow + P::CROW)[t];
+          const float2 a = cmul(wd, make_float2(bv.x, bv.y)), c = cmul(wd, make_float2(bv.z, bv.w));
+          x1 = make_float4(a.x, a.y, c.x, c.y);
+        }
+      }
+      x1s[(j & 3) * RU + t] = x1;
+    }
+    __syncthreads();  // row j - 4's slot is free: the r stage was its last reader
+    if (t == 0 && j - 4 >= jA0) produce(j - 4 + PD);
+  }
+}
+
+void run_stencil9_pre_k8(const LevelOp<float>& op, const LevelGeom& gc, float wj, const float2* b, float2* x2,
+                         float2* rc, cudaStream_t s) {
+  constexpr int NT = 64, PD = 7;
+  using P = S9PrePlan<NT, PD>;
+  constexpr int MINB = int(std::min<size_t>(std::min<size_t>((227 * 1024) / (P::BYTES + 1024), 2048 / P::TH), 8));
+  const int strips = int((gc.n0 + P::TC - 1) / P::TC);
+  // coarse rows per CTA: about one resident wave, at least 4 (5 extra fine rows are staged per chunk)
+  const int chunks = std::max(1, kNumSMs * MINB / std::max(1, strips));
+  const int e = env_int("HZ_S9PRE_ROWS", 0);
+  const int crows = e > 0 ? e : std::max(4, int((gc.n1 + chunks - 1) / chunks));
+  const dim3 grid(unsigned(strips), unsigned((gc.n1 + crows - 1) / crows));
+  auto kern = stencil9_pre_k8_kernel<NT, PD, MINB>;
+  allow_dyn_smem(reinterpret_cast<const void*>(kern), int(P::BYTES));
+  kern<<<grid, P::TH, P::BYTES, s>>>(op, gc, wj, b, x2, rc, crows);
+}
+
+bool launch_stencil9_pre_k8(const LevelOp<float>& op, const LevelGeom& gc, float wj, const float2* b, float2* x2,
+                            float2* rc, cudaStream_t s) {
+  // opt-in (HZ_S9_PRE=1): measured neutral to slightly slower on the bench (73.0 vs 73.6 RHS/s in interleaved
+  // repetitions, profiles/r02_s9_pre_ab.txt) although it replaces 37.5 us of kernels by 26.7 us -- with four
+  // groups in flight its 104 KB of shared memory per CTA displaces the other groups' kernels
+  static const bool on = env_int("HZ_S9_PRE", 0) != 0;
+  static const int64_t min_nodes = env_int("HZ_S9_PRE_MIN_NODES", 100000);
+  if (!on || op.kind != kStencil || op.ndim != 2 || op.g.k != kK8 || !op.cd || op.g.z0 != 0 ||
+      op.g.z1 != op.g.n1 || int64_t(op.g.nodes) < min_nodes || op.g.n1 < 5)
+    return false;
+  const double n = double(op.g.nodes), nc = double(gc.nodes);
+  ProfScope prof("fused_pre_stencil_c64_L1", n * (kK8 * 8.0 * 2.0 + 80.0) + nc * kK8 * 8.0, s);
+  run_stencil9_pre_k8(op, gc, wj, b, x2, rc, s);
+  HZ_LAUNCH_CHECK();
+  return true;
+}
+
 bool fused_vcycle_enabled() {
   static const bool on = env_int("HZ_FUSED_VCYCLE", 1) != 0;
   return on;

@@ -719,6 +719,24 @@ void Hierarchy<T>::cycle_rec(int l, const CycleSpec& spec, int k, const V* b, V*
   V* cur = x;
   V* other = wt_[l].get();
   bool cur_zero = x_zero;
+  if constexpr (std::is_same<T, float>::value) {
+    // large 2D Galerkin level visited from x = 0: both pre-sweeps, the
+    // residual and its restriction in one launch (fused.cu); the iterate
+    // lands in `other`, the correction and the post-sweeps follow as usual
+    if (l > 0 && x_zero && !sl_ && spec.pre == 2) {
+      const LevelGeom gcl(levels_[l + 1].dims[0], levels_[l + 1].dims[1], levels_[l + 1].dims[2], k);
+      if (launch_stencil9_pre_k8(op(l, k), gcl, T(spec.jacobi_weight), b, other, wb_[l + 1].get(), s)) {
+        std::swap(cur, other);
+        coarse_visit(l, spec, k, s);
+        launch_prolong_correct<T>(op(l, k).g, gcl, ndim_, wx_[l + 1].get(), cur, s);
+        cur_zero = false;
+        relax(l, spec, spec.post, k, b, cur, other, cur_zero, s);
+        if (cur != x)
+          HZ_CUDA(cudaMemcpyAsync(x, cur, size_t(levels_[l].nodes()) * k * sizeof(V), cudaMemcpyDeviceToDevice, s));
+        return;
+      }
+    }
+  }
   relax(l, spec, spec.pre, k, b, cur, other, cur_zero, s);
   const size_t rowb = size_t(k) * sizeof(V);
   coarse_correction(l, spec, k, b, cur, cur_zero, s);

@@ -142,6 +142,13 @@ bool launch_stencil9_k8(const LevelOp<float>& op, int mode, float wj, const floa
 bool launch_stencil9_pair_k8(const LevelOp<float>& op, float wj, const float2* x, const float2* b, float2* out,
                              cudaStream_t s);
 
+// zero-start pre-smoothing visit of a complex64 2D Galerkin level (k = 8) in
+// one launch: both sweeps from x = 0, the residual and its restriction
+// (x2 = the pre-smoothed iterate, rc = P^T (b - A x2)); bitwise equal to
+// jacobi_zero + jacobi + residual + restrict. False when it does not apply.
+bool launch_stencil9_pre_k8(const LevelOp<float>& op, const LevelGeom& gc, float wj, const float2* b, float2* x2,
+                            float2* rc, cudaStream_t s);
+
 // elementwise casts / copies
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);

@@ -120,6 +120,25 @@ def test_two_sweep_galerkin_level_kernel_equals_single_sweeps(nx, nz, nl, kind, 
     assert np.array_equal(dfl, old)
 
 
+@pytest.mark.parametrize("nx,nz,nl,kind,rows", [(257, 129, 4, "V", "0"), (1025, 513, 5, "V", "0"), (301, 97, 3, "W", "5"),
+                                               (121, 233, 4, "K", "3"), (65, 49, 3, "V", "2"), (1025, 513, 6, "W", "7")])
+def test_fused_galerkin_level_pre_visit_equals_unfused(nx, nz, nl, kind, rows):
+    """complex64 2D Galerkin levels at k = 8 visited from x = 0: both
+    pre-sweeps, the residual and its restriction in one launch
+    (stencil9_pre_k8, opt-in with HZ_S9_PRE=1; every level via
+    HZ_S9_PRE_MIN_NODES=0, odd coarse-row chunks via HZ_S9PRE_ROWS) against the
+    unfused kernels (HZ_S9_PRE=0 and HZ_S9_PAIR=0), bitwise, through whole
+    V / W / K cycles."""
+    extra = {} if rows == "0" else {"HZ_S9PRE_ROWS": rows}
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(CYCLE, os.path.join(d, "n.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9_PRE="1",
+                   HZ_S9_PRE_MIN_NODES="0", HZ_S9_PAIR_MIN_NODES="0", **extra)
+        old = _run(CYCLE, os.path.join(d, "o.npy"), "1", nx, nz, 8, nl, "c64", kind, HZ_S9_PRE="0", HZ_S9_PAIR="0")
+        dfl = _run(CYCLE, os.path.join(d, "d.npy"), "1", nx, nz, 8, nl, "c64", kind)
+    assert np.array_equal(new, old), f"max rel diff {rel_err(new, old):.3e}"
+    assert np.array_equal(dfl, old)
+
+
 def test_fused_c128_cycle_matches_reference():
     """c128 V(2,2) cycle through the fused fine level vs the compiled
     reference's MgHierarchy::cycle at the 1e-12 parity bar."""
