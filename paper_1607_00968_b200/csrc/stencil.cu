@@ -179,6 +179,45 @@ apply_lo_kernel(LevelOp<double> op, const float2* __restrict__ x, double2* __res
   out[e] = fine_ax<double, NDIM, false, float2>(op, x, e, el);
 }
 
+// the same for two consecutive columns per thread (k even): 16-byte loads of
+// the complex64 block, 32 bytes stored; per column the operations of fine_ax
+// in the same order (apply_block: centre, x-, x+, y-, y+, z-, z+)
+template <int NDIM>
+__global__ void __launch_bounds__(kBlock)
+apply_lo2_kernel(LevelOp<double> op, const float2* __restrict__ x, double2* __restrict__ out) {
+  const LevelGeom& g = op.g;
+  const uint32_t e = g.e_begin() + (blockIdx.x * kBlock + threadIdx.x) * 2;
+  if (e >= g.e_end()) return;
+  uint32_t node, col, i, j, kz;
+  g.div_k.divmod(e, node, col);
+  g.unpack(node, i, j, kz);
+  const uint32_t sx = g.k, sy = g.n0 * g.k, sz = g.n0 * g.n1 * g.k;
+  const bool xm = i > 0, xp = i + 1 < g.n0, ym = j > 0, yp = j + 1 < g.n1;
+  const bool zm = NDIM == 3 && kz > 0, zp = NDIM == 3 && kz + 1 < g.n2;
+  auto ld = [&](uint32_t at) { return __ldg(reinterpret_cast<const float4*>(x + at)); };
+  const double2 c = __ldg(&op.center[node]);
+  const float4 u0 = ld(e), uxm = ld(xm ? e - sx : e), uxp = ld(xp ? e + sx : e), uym = ld(ym ? e - sy : e),
+               uyp = ld(yp ? e + sy : e);
+  float4 uzm = u0, uzp = u0;
+  if (NDIM == 3) {
+    uzm = ld(zm ? e - sz : e);
+    uzp = ld(zp ? e + sz : e);
+  }
+  const double wx = op.w[0], wy = op.w[1], wz = op.w[2];
+  auto col_of = [](const float4& v, int q) { return q == 0 ? mk(double(v.x), double(v.y)) : mk(double(v.z), double(v.w)); };
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    double2 acc = cmul(c, col_of(u0, q));
+    if (xm) acc = crfma(wx, col_of(uxm, q), acc);
+    if (xp) acc = crfma(wx, col_of(uxp, q), acc);
+    if (ym) acc = crfma(wy, col_of(uym, q), acc);
+    if (yp) acc = crfma(wy, col_of(uyp, q), acc);
+    if (zm) acc = crfma(wz, col_of(uzm, q), acc);
+    if (zp) acc = crfma(wz, col_of(uzp, q), acc);
+    out[e + q] = acc;
+  }
+}
+
 // W = A Z (complex128 fine operator, Z complex64 widened on load, K = 8)
 // fused with the Gram [X_0..X_{NB-2}, W]^H W of the Arnoldi step: the
 // register-direct k8::gram8_kernel with its Y = X_{NB-1} operand computed in
@@ -1102,6 +1141,19 @@ void launch_apply_lo(const LevelOp<double>& op, const float2* u, double2* out, c
   ProfScope prof(op.kind == kFine27 ? "apply_fine27_c128" : "apply_fine_c128", n * (k * (8.0 + 16.0) + 16.0), s);
   if (launch_stream3d_lo(op, u, out, s)) return;
   if (op.kind != kFine) throw HzError(kState, "apply_lo: 5/7-point operator, or 8-column blocks of the 27-point one");
+  static const bool two = [] {  // HZ_APPLY_LO2=0: one column per thread
+    const char* e = std::getenv("HZ_APPLY_LO2");
+    return !(e && e[0] == '0');
+  }();
+  if (two && op.g.k % 2 == 0) {
+    const int grid2 = grid_for(op.g.owned_elems() / 2, kBlock);
+    if (op.ndim == 3)
+      apply_lo2_kernel<3><<<grid2, kBlock, 0, s>>>(op, u, out);
+    else
+      apply_lo2_kernel<2><<<grid2, kBlock, 0, s>>>(op, u, out);
+    HZ_LAUNCH_CHECK();
+    return;
+  }
   const int grid = grid_for(op.g.owned_elems(), kBlock);
   if (op.ndim == 3)
     apply_lo_kernel<3><<<grid, kBlock, 0, s>>>(op, u, out);

@@ -193,6 +193,28 @@ def test_fused_apply_gram_matches_unfused(dim):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("dim", ["2d", "3d"])
+def test_two_column_apply_of_complex64_blocks_matches_one_column(dim):
+    """W = A Z on complex64 Z blocks with two columns per thread
+    (apply_lo2_kernel, default) against one column per thread
+    (HZ_APPLY_LO2=0): the same per-column operations, bitwise equal solves."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    with tempfile.TemporaryDirectory() as d:
+        for flag in ("1", "0"):
+            path = os.path.join(d, f"x{flag}.npy")
+            r = subprocess.run([sys.executable, "-c", GA_SOLVE, path, dim], cwd=root,
+                               env=dict(os.environ, HZ_APPLY_LO2=flag), capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("k", [8, 4])
 def test_cycle_graph_replay_matches_direct_launches(k):
     """The c64 preconditioner replayed from captured CUDA graphs
