@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libhz_b200.so")
 OBJ = os.path.join(HERE, "build")
-SOURCES = ["stencil.cu", "stream3d.cu", "fused.cu", "block.cu", "coarse.cu", "coarse_bt.cu", "hierarchy.cu", "krylov.cu", "slabs.cu", "acquisition.cu", "capi.cu"]
+SOURCES = ["stencil.cu", "stream3d.cu", "galerkin3d.cu", "fused.cu", "block.cu", "coarse.cu", "coarse_bt.cu", "hierarchy.cu", "krylov.cu", "slabs.cu", "acquisition.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",

@@ -435,6 +435,12 @@ std::unique_ptr<Hierarchy<float>> Hierarchy<float>::rounded(const Hierarchy<doub
                                   cudaMemcpyDeviceToDevice, s));
       }
     }
+    if (b.kind == kStencil && h64.ndim_ == 3 && b.coef.size() && b.nodes() >= galerkin3d_min_nodes()) {
+      // large 3D Galerkin level: the 27 coefficients (and D^{-1}) per node as
+      // three 80-byte record groups for the plane-streaming kernel (galerkin3d.cu)
+      b.cd.alloc(size_t(30) * b.nodes());
+      launch_galerkin3d_records(b.nodes(), b.coef.get(), b.inv_diag.get(), b.cd.get(), s);
+    }
     if ((b.kind == kFine || b.kind == kFine27) && b.center.size()) {
       // (centre, D^{-1}) per node in one 16-byte record: a row of the fine
       // grid is then one 16-byte-aligned bulk copy whatever n0's parity

@@ -149,6 +149,17 @@ bool launch_stencil9_pair_k8(const LevelOp<float>& op, float wj, const float2* x
 bool launch_stencil9_pre_k8(const LevelOp<float>& op, const LevelGeom& gc, float wj, const float2* b, float2* x2,
                             float2* rc, cudaStream_t s);
 
+// plane-streaming kernel of a complex64 3D Galerkin level, k = 8
+// (galerkin3d.cu): mode 0 apply, 1 residual, 2 damped Jacobi, bitwise equal
+// to the stencil_v4 kernels. op.cd = the level's three record groups
+// [3][nodes][10] (launch_galerkin3d_records), kept for levels of at least
+// galerkin3d_min_nodes() nodes. False when it does not apply (HZ_G3=0, ...).
+int64_t galerkin3d_min_nodes();
+void launch_galerkin3d_records(int64_t nodes, const float2* coef, const float2* inv_diag, float2* rec,
+                               cudaStream_t s);
+bool launch_galerkin3d(const LevelOp<float>& op, int mode, float wj, const float2* x, const float2* b, float2* out,
+                       cudaStream_t s);
+
 // elementwise casts / copies
 template <class Dst, class Src>
 void launch_cast(int64_t count, const Src* in, Dst* out, cudaStream_t s);

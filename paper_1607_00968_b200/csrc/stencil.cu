@@ -1068,6 +1068,17 @@ bool stencil9_bulk(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b,
 }
 
 template <class T, int MODE>
+bool galerkin3d_stream(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out, T wj,
+                       cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value) {
+    if (op.ndim != 3 || !op.cd) return false;
+    return launch_galerkin3d(op, MODE, wj, x, b, out, s);
+  } else {
+    return false;
+  }
+}
+
+template <class T, int MODE>
 void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b, cplx_t<T>* out,
                     T wj, cudaStream_t s) {
   const int64_t total = op.g.owned_elems();
@@ -1097,6 +1108,8 @@ void dispatch_level(const LevelOp<T>& op, const cplx_t<T>* x, const cplx_t<T>* b
       level_kernel<T, 3, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
     else
       level_kernel<T, 2, kFine, MODE><<<grid, kBlock, 0, s>>>(op, x, b, out, wj);
+  } else if (galerkin3d_stream<T, MODE>(op, x, b, out, wj, s)) {
+    // complex64 3D Galerkin level, k = 8: plane streaming (galerkin3d.cu)
   } else if (stencil9_bulk<T, MODE>(op, x, b, out, wj, s)) {
     // complex64 2D Galerkin level, k = 8: bulk-copy row staging (fused.cu)
   } else if (op.g.k % 4 == 0 && total >= stencil_v4_min_elems()) {

@@ -92,6 +92,24 @@ def test_27_point_streaming_matches_element_kernels(n, nl, prec, tol):
     assert rel_err(new["apply"], old["apply"]) <= 1e-13
 
 
+@pytest.mark.parametrize("stencil", [7, 27])
+@pytest.mark.parametrize("n,nl,kind,ctas", [((33, 17, 9), 2, "V", "0"), ((49, 37, 21), 3, "W", "5"),
+                                            ((97, 33, 65), 3, "V", "0"), ((65, 65, 33), 3, "K", "148"),
+                                            ((35, 67, 41), 2, "V", "1")])
+def test_galerkin_level_streaming_equals_element_kernels(n, nl, kind, ctas, stencil):
+    """complex64 3D Galerkin levels at k = 8: the plane-streaming kernel
+    (galerkin3d.cu: three 9-coefficient record groups per node, the row's sum
+    taken as the three iterate planes pass; every level via HZ_G3_MIN_NODES=0,
+    forced work splits via HZ_G3_CTAS) against the element kernels (HZ_G3=0),
+    bitwise, through whole V / W / K cycles."""
+    extra = {} if ctas == "0" else {"HZ_G3_CTAS": ctas}
+    with tempfile.TemporaryDirectory() as d:
+        new = _run(os.path.join(d, "a.npz"), "1", n, nl, "c64", stencil, kind, HZ_G3_MIN_NODES="0", **extra)
+        old = _run(os.path.join(d, "b.npz"), "1", n, nl, "c64", stencil, kind, HZ_G3="0")
+    assert np.all(np.isfinite(new["cycle"]))
+    assert np.array_equal(new["cycle"], old["cycle"]), rel_err(new["cycle"], old["cycle"])
+
+
 def test_27_point_streaming_apply_matches_specification():
     """k = 8 takes the streaming kernel: against the numpy / scipy statement of
     the operator (tests/hzt_util.csr27), complex128."""
