@@ -256,8 +256,8 @@ __device__ __forceinline__ void cp_async_elem(V* smem, const V* gmem) {
 // (double-buffered) and read conflict-free by all 8 warps; lane partial sums
 // meet in an xor butterfly, so no split-K partials and no second launch.
 // Deterministic: fixed per-lane order, fixed butterfly.
-template <class T, int RW, int KG, int LC, int PF>
-__global__ void __launch_bounds__(256)
+template <class T, int RW, int KG, int LC, int PF, int NW>
+__global__ void __launch_bounds__(32 * NW)
 bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx_t<T>* __restrict__ r,
                cplx_t<T>* out, const cplx_t<T>* c_in, T sign) {
   using V = cplx_t<T>;
@@ -267,7 +267,7 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
   constexpr int RS = KG + 1;
   __shared__ __align__(16) V rs[2][LC * RS];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int i0 = int(blockIdx.x) * (8 * RW);
+  const int i0 = int(blockIdx.x) * (NW * RW);
   const int q0 = blockIdx.y * KG;
   const int nch = (m + LC - 1) / LC;
   // rows past the end are clamped (computed, not stored): no predicates in the loop
@@ -275,7 +275,7 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
   bool live[RW];
 #pragma unroll
   for (int t = 0; t < RW; ++t) {
-    const int row = i0 + w + 8 * t;
+    const int row = i0 + w + NW * t;
     live[t] = row < m;
     prow[t] = P + int64_t(min(row, m - 1)) * ld + lane;
   }
@@ -283,7 +283,7 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
   auto stage = [&](int c, V* dst) {
     const int l0 = c * LC;
 #pragma unroll
-    for (int e = tid; e < LC * KG; e += 256) {
+    for (int e = tid; e < LC * KG; e += 32 * NW) {
       const int l = e / KG, q = e % KG;
       if (l0 + l < m)
         cp_async_elem(dst + l * RS + q, rq + (l0 + l) * k + q);
@@ -359,7 +359,7 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
     for (int q = 0; q < KG; ++q) {
       if (lane != q) continue;
       V v = acc[t][q];
-      const int o = (i0 + w + 8 * t) * k + q0 + q;
+      const int o = (i0 + w + NW * t) * k + q0 + q;
       if (c_in) {
         const V cv = c_in[o];
         v = mk(cv.x + sign * v.x, cv.y + sign * v.y);
@@ -373,19 +373,35 @@ template <class T, int RW, int KG>
 void bt_rows_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
                 const cplx_t<T>* c_in, T sign, cudaStream_t s) {
   constexpr int LC = sizeof(T) == 8 ? 128 : 256;  // r chunk: 32 KB of static shared memory, double-buffered
-  // chunks of P in registers (PF - 1 in flight): two-row warps prefetch two
-  // chunks ahead (config 4: 9.31 vs 9.47 ms per cycle), one-row warps one
-  // (config 3: 1.86 vs 1.91); HZ_BT_PF=0 / 1 forces shallow / deep
+  // chunks of P in registers (PF - 1 in flight). One chunk ahead is the default: two or three ahead
+  // (HZ_BT_PF=1) measured within noise on configs 3 and 4 in interleaved repetitions (8.90 vs 8.98 ms per
+  // cycle on config 4, profiles/r02_bt_cycle_ab.txt) and its 165 registers keep the two chains of the
+  // two-sided sweep from sharing the SMs
   static const int pf_env = [] {
     const char* e = std::getenv("HZ_BT_PF");
-    return e ? std::atoi(e) : -1;
+    return e ? std::atoi(e) : 0;
   }();
-  const bool deep = pf_env >= 0 ? pf_env == 1 : RW == 2;
+  const bool deep = pf_env == 1;
+  // warps per CTA: 8; 4-warp CTAs (HZ_BT_NW=4: three per SM even with the deep prefetch, but each CTA stages
+  // the whole chunk of r) measured equal or slower (8.98 vs 8.96, 1.92 vs 1.86 ms per cycle)
+  static const int nw_env = [] {
+    const char* e = std::getenv("HZ_BT_NW");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool four = nw_env == 4;
+  if (four) {
+    const dim3 grid(unsigned((m + 4 * RW - 1) / (4 * RW)), unsigned(k / KG));
+    if (deep)
+      bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3), 4><<<grid, 128, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+    else
+      bt_rows_kernel<T, RW, KG, LC, 2, 4><<<grid, 128, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+    return;
+  }
   const dim3 grid(unsigned((m + 8 * RW - 1) / (8 * RW)), unsigned(k / KG));
   if (deep)
-    bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3)><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+    bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3), 8><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
   else
-    bt_rows_kernel<T, RW, KG, LC, 2><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+    bt_rows_kernel<T, RW, KG, LC, 2, 8><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
 }
 
 template <class T>
