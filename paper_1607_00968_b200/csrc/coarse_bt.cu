@@ -26,6 +26,7 @@
 #include "devbuf.hpp"
 #include "kernels.hpp"
 #include "profile.hpp"
+#include "tma.cuh"
 
 namespace hz {
 
@@ -184,16 +185,47 @@ __global__ void schur_kernel(LevelGeom g, const double2* __restrict__ coef, int 
   S[e] = s;
 }
 
+// Programmatic dependent launch for the plane-step chain (HZ_BT_PDL=1, default off:
+// measured 6 % slower per cycle on config 3, neutral on config 4): a step's
+// kernel is launched while its predecessor still runs, does everything that
+// does not depend on the data (operator loads, the next block's L2 prefetch)
+// and only then waits for the predecessor's results (griddepcontrol.wait: the
+// whole prerequisite grid complete and visible). Every global write comes after
+// the wait, so the scratch blocks are never overwritten under a running reader.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+
+bool bt_pdl() {  // read per launch: the tests switch it within one process
+  const char* e = std::getenv("HZ_BT_PDL");
+  return e && e[0] == '1';
+}
+
+template <class... KA, class... A>
+void launch_chain(void (*kern)(KA...), dim3 grid, dim3 block, cudaStream_t s, A... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = bt_pdl() ? 1 : 0;
+  HZ_CUDA(cudaLaunchKernelEx(&cfg, kern, KA(args)...));
+}
+
 // r = b_j - L_j y_{j-dir} for one plane, all k columns (L = plane j -> j-dir
 // coupling; b may be r itself: the middle plane of the twisted sweep
 // subtracts both neighbours in two passes)
 template <class T>
 __global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, int j, int dir, const cplx_t<T>* b,
-                              const cplx_t<T>* __restrict__ yprev, cplx_t<T>* r, int k) {
+                              const cplx_t<T>* yprev, cplx_t<T>* r, int k) {
   using V = cplx_t<T>;
   const int n0 = int(g.n0), n1 = int(g.n1);
   const int m = n0 * n1;
   const int e = int(blockIdx.x) * 256 + threadIdx.x;
+  pdl_launch_dependents();
   if (e >= m * k) return;
   const int row = e / k;
   const int q = e - row * k;
@@ -207,10 +239,17 @@ __global__ void couple_kernel(LevelGeom g, const cplx_t<T>* __restrict__ coef, i
 #pragma unroll
     for (int dx = -1; dx <= 1; ++dx) {
       const int s9 = (dy + 1) * 3 + dx + 1;
+      av[s9] = __ldg(&coef[int64_t(plane_s(dx, dy, -dir)) * g.nodes + int64_t(j) * m + row]);
+    }
+  pdl_wait();  // yprev (and b, when it is r itself) come from the preceding step
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int s9 = (dy + 1) * 3 + dx + 1;
       const int li = ri + dx, lj = rj + dy;
       ok[s9] = li >= 0 && li < n0 && lj >= 0 && lj < n1;
-      av[s9] = __ldg(&coef[int64_t(plane_s(dx, dy, -dir)) * g.nodes + int64_t(j) * m + row]);
-      yv[s9] = __ldg(&yprev[ok[s9] ? (li + n0 * lj) * k + q : e]);
+      yv[s9] = yprev[ok[s9] ? (li + n0 * lj) * k + q : e];
     }
   V s = b[e];
 #pragma unroll
@@ -259,9 +298,18 @@ __device__ __forceinline__ void cp_async_elem(V* smem, const V* gmem) {
 template <class T, int RW, int KG, int LC, int PF, int NW>
 __global__ void __launch_bounds__(32 * NW)
 bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx_t<T>* __restrict__ r,
-               cplx_t<T>* out, const cplx_t<T>* c_in, T sign) {
+               cplx_t<T>* out, const cplx_t<T>* c_in, T sign, const cplx_t<T>* __restrict__ Pnext) {
   using V = cplx_t<T>;
   constexpr int U = LC / 32;
+  // The factor blocks do not depend on the data: the rows this CTA will own
+  // in the chain's next plane step are brought into L2 now (one bulk prefetch
+  // per row), while this latency-bound step leaves the HBM mostly idle.
+  if (Pnext != nullptr && blockIdx.y == 0 && threadIdx.x < NW * RW) {
+    const int row = int(blockIdx.x) * (NW * RW) + int(threadIdx.x);
+    if (row < m)
+      tma::prefetch_l2(Pnext + int64_t(row) * ld, uint32_t((size_t(m) * sizeof(V) + 15) / 16 * 16));
+  }
+  pdl_launch_dependents();
   // chunk of r in its natural [l][q] order, rows padded to KG + 1 values: the
   // staging writes and the per-lane reads (lane = l) are both conflict free
   constexpr int RS = KG + 1;
@@ -313,11 +361,12 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
   // the row's chunks of P are loaded PF - 1 chunks ahead of the one being
   // multiplied (registers, rotated by unrolling)
   V pq[PF][RW][U];
-  stage(0, rs[0]);
-  tiled::cp_async_commit();
 #pragma unroll
   for (int f = 0; f < PF - 1; ++f)
     if (f < nch) load_p(f, pq[f]);
+  pdl_wait();  // r and c_in come from the preceding step; P does not
+  stage(0, rs[0]);
+  tiled::cp_async_commit();
   for (int c0 = 0; c0 < nch; c0 += PF) {
 #pragma unroll
     for (int f = 0; f < PF; ++f) {
@@ -371,7 +420,7 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
 
 template <class T, int RW, int KG>
 void bt_rows_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
-                const cplx_t<T>* c_in, T sign, cudaStream_t s) {
+                const cplx_t<T>* c_in, T sign, const cplx_t<T>* Pnext, cudaStream_t s) {
   constexpr int LC = sizeof(T) == 8 ? 128 : 256;  // r chunk: 32 KB of static shared memory, double-buffered
   // chunks of P in registers (PF - 1 in flight). One chunk ahead is the default: two or three ahead
   // (HZ_BT_PF=1) measured within noise on configs 3 and 4 in interleaved repetitions (8.90 vs 8.98 ms per
@@ -392,21 +441,21 @@ void bt_rows_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T
   if (four) {
     const dim3 grid(unsigned((m + 4 * RW - 1) / (4 * RW)), unsigned(k / KG));
     if (deep)
-      bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3), 4><<<grid, 128, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+      launch_chain(bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3), 4>, grid, dim3(128), s, int(m), k, P, int(ld), r, out, c_in, sign, Pnext);
     else
-      bt_rows_kernel<T, RW, KG, LC, 2, 4><<<grid, 128, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+      launch_chain(bt_rows_kernel<T, RW, KG, LC, 2, 4>, grid, dim3(128), s, int(m), k, P, int(ld), r, out, c_in, sign, Pnext);
     return;
   }
   const dim3 grid(unsigned((m + 8 * RW - 1) / (8 * RW)), unsigned(k / KG));
   if (deep)
-    bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3), 8><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+    launch_chain(bt_rows_kernel<T, RW, KG, LC, (RW == 1 ? 4 : 3), 8>, grid, dim3(256), s, int(m), k, P, int(ld), r, out, c_in, sign, Pnext);
   else
-    bt_rows_kernel<T, RW, KG, LC, 2, 8><<<grid, 256, 0, s>>>(int(m), k, P, int(ld), r, out, c_in, sign);
+    launch_chain(bt_rows_kernel<T, RW, KG, LC, 2, 8>, grid, dim3(256), s, int(m), k, P, int(ld), r, out, c_in, sign, Pnext);
 }
 
 template <class T>
 void bt_rows(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
-             const cplx_t<T>* c_in, T sign, cudaStream_t s) {
+             const cplx_t<T>* c_in, T sign, const cplx_t<T>* Pnext, cudaStream_t s) {
   // two rows per warp above one CTA per SM (HZ_BT_RW=1 / 2 forces)
   static const int rw_env = [] {
     const char* e = std::getenv("HZ_BT_RW");
@@ -416,9 +465,9 @@ void bt_rows(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* 
   auto go = [&](auto kg) {
     constexpr int KG = decltype(kg)::value;
     if (two)
-      bt_rows_go<T, 2, KG>(m, k, P, ld, r, out, c_in, sign, s);
+      bt_rows_go<T, 2, KG>(m, k, P, ld, r, out, c_in, sign, Pnext, s);
     else
-      bt_rows_go<T, 1, KG>(m, k, P, ld, r, out, c_in, sign, s);
+      bt_rows_go<T, 1, KG>(m, k, P, ld, r, out, c_in, sign, Pnext, s);
   };
   if (k % 8 == 0)
     go(std::integral_constant<int, 8>());
@@ -436,9 +485,9 @@ void bt_rows(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* 
 // FP32-issue/HBM balance (profiles/r02_bt_rows_ab.txt)
 template <class T>
 void bt_step(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
-             const cplx_t<T>* c_in, T sign, cplx_t<T>* part, cudaStream_t s) {
+             const cplx_t<T>* c_in, T sign, cplx_t<T>* part, const cplx_t<T>* Pnext, cudaStream_t s) {
   if (bt_rowmajor(m))
-    bt_rows<T>(m, k, P, ld, r, out, c_in, sign, s);
+    bt_rows<T>(m, k, P, ld, r, out, c_in, sign, Pnext, s);
   else
     launch_coarse_gemm<T>(m, k, P, ld, r, out, c_in, sign, part, s);
 }
@@ -628,6 +677,13 @@ void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, co
   ProfScope prof(sizeof(T) == 8 ? "coarse_bt_c128" : "coarse_bt_c64",
                  (2.0 * np - 1.0) * double(m) * m * sizeof(V), s, 8.0 * (2.0 * np - 1.0) * double(m) * m * k);
   const bool two = mid < np - 1;  // a bottom-up chain exists
+  // HZ_BT_L2PF (default 0): each row-owner plane step prefetches the chain's next factor block into L2.
+  // Measured neutral on config 3 and 4 % slower on config 4 (profiles/r02_bt_pdl_ab.txt): the steps are not
+  // bound by the latency of the factor loads
+  const char* pfe = std::getenv("HZ_BT_L2PF");
+  const int pf = pfe ? std::atoi(pfe) : 0;
+  // 1: the chain's next block; 2: the step's own block (useful when the step is launched early, HZ_BT_PDL)
+  auto nx = [&](const V* next, const V* self) -> const V* { return pf == 1 ? next : pf == 2 ? self : nullptr; };
   cudaStream_t s2 = two ? aux.s2 : s;
   V* r2 = r + pk;
   V* part2 = part + int64_t(std::max(coarse_split(m, k), 1)) * pk;
@@ -646,38 +702,47 @@ void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, co
   for (int j = 0; j < mid; ++j) {
     const V* rhs = b + j * pk;
     if (j > 0) {
-      couple_kernel<T><<<gk, 256, 0, s>>>(g, coef, j, 1, rhs, x + (j - 1) * pk, r, k);
+      launch_chain(couple_kernel<T>, dim3(gk), dim3(256), s, g, coef, j, 1, rhs, x + (j - 1) * pk, r, k);
       rhs = r;
     }
-    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, rhs, x + j * pk, nullptr, T(1), part, s);
+    // next on this chain: the next plane's E (the middle plane's after the last one)
+    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, rhs, x + j * pk, nullptr, T(1), part,
+               nx(ET + int64_t(j + 1) * m * ld, ET + int64_t(j) * m * ld), s);
   }
   for (int j = np - 1; j > mid; --j) {
     const V* rhs = b + j * pk;
     if (j < np - 1) {
-      couple_kernel<T><<<gk, 256, 0, s2>>>(g, coef, j, -1, rhs, x + (j + 1) * pk, r2, k);
+      launch_chain(couple_kernel<T>, dim3(gk), dim3(256), s2, g, coef, j, -1, rhs, x + (j + 1) * pk, r2, k);
       rhs = r2;
     }
-    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, rhs, x + j * pk, nullptr, T(1), part2, s2);
+    // next on this chain: E of plane j - 1, then the first block of its back substitution
+    bt_step<T>(m, k, ET + int64_t(j) * m * ld, ld, rhs, x + j * pk, nullptr, T(1), part2,
+               nx(j - 1 > mid ? ET + int64_t(j - 1) * m * ld : FT + int64_t(mid + 1) * m * ld,
+                  ET + int64_t(j) * m * ld),
+               s2);
   }
   join();
   {  // middle plane: both neighbours' contributions
     const V* rhs = b + mid * pk;
     if (mid > 0) {
-      couple_kernel<T><<<gk, 256, 0, s>>>(g, coef, mid, 1, rhs, x + (mid - 1) * pk, r, k);
+      launch_chain(couple_kernel<T>, dim3(gk), dim3(256), s, g, coef, mid, 1, rhs, x + (mid - 1) * pk, r, k);
       rhs = r;
     }
     if (mid < np - 1) {
-      couple_kernel<T><<<gk, 256, 0, s>>>(g, coef, mid, -1, rhs, x + (mid + 1) * pk, r, k);
+      launch_chain(couple_kernel<T>, dim3(gk), dim3(256), s, g, coef, mid, -1, rhs, x + (mid + 1) * pk, r, k);
       rhs = r;
     }
-    bt_step<T>(m, k, ET + int64_t(mid) * m * ld, ld, rhs, x + mid * pk, nullptr, T(1), part, s);
+    bt_step<T>(m, k, ET + int64_t(mid) * m * ld, ld, rhs, x + mid * pk, nullptr, T(1), part,
+               nx(mid > 0 ? FT + int64_t(mid - 1) * m * ld : nullptr, ET + int64_t(mid) * m * ld), s);
   }
   // back substitution outward: x_j = y_j - F_j x_{j +- 1}
   fork();
   for (int j = mid - 1; j >= 0; --j)
-    bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j + 1) * pk, x + j * pk, x + j * pk, T(-1), part, s);
+    bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j + 1) * pk, x + j * pk, x + j * pk, T(-1), part,
+               nx(j > 0 ? FT + int64_t(j - 1) * m * ld : nullptr, FT + int64_t(j) * m * ld), s);
   for (int j = mid + 1; j < np; ++j)
-    bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j - 1) * pk, x + j * pk, x + j * pk, T(-1), part2, s2);
+    bt_step<T>(m, k, FT + int64_t(j) * m * ld, ld, x + (j - 1) * pk, x + j * pk, x + j * pk, T(-1), part2,
+               nx(j + 1 < np ? FT + int64_t(j + 1) * m * ld : nullptr, FT + int64_t(j) * m * ld), s2);
   join();
   HZ_LAUNCH_CHECK();
 }

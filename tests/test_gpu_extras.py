@@ -216,6 +216,44 @@ def test_block_tridiagonal_coarse_solve_matches_reference(ref, n, nl, inverse, r
     assert rel_err(S.cycle(b), H.cycle(b, kind="V")) <= 1e-11
 
 
+@pytest.mark.parametrize("n,nl", [((33, 33, 17), 2), ((17, 33, 25), 2)])
+def test_block_tridiagonal_prefetch_and_dependent_launch_bitwise(n, nl, monkeypatch):
+    """The plane-step chain with the next factor block prefetched into L2
+    (HZ_BT_L2PF = 1 next block, 2 own block) and with programmatic dependent
+    launches (HZ_BT_PDL = 1: a step starts while its predecessor runs and waits
+    for it only before touching the data) gives the bits of the plain chain,
+    through direct launches and through the graph-replayed c64 cycle."""
+    import torch
+    monkeypatch.setenv("HZ_COARSE", "bt")
+    cfg = configs.small_problem(3, n, seed=3)
+    P = hz.HelmholtzProblem.from_config(cfg)
+    outs = {}
+    for pf, pdl in (("0", "0"), ("1", "0"), ("1", "1"), ("2", "1"), ("0", "1")):
+        monkeypatch.setenv("HZ_BT_L2PF", pf)
+        monkeypatch.setenv("HZ_BT_PDL", pdl)
+        S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
+                                                           cycle=hz.CycleSpec("V"), precond_precision="c64",
+                                                           fgmres_restart=5, tol=1e-6, max_cycles=30))
+        R = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
+                                                           cycle=hz.CycleSpec("V")))
+        b = configs.random_block(cfg.num_nodes, 8, seed=5)
+        res = [R.cycle(b)]
+        for _ in range(3):
+            res.append(R.cycle(b))  # repeated launches of the chain
+        try:
+            X, rep = S.solve_block(b)  # graph-replayed c64 cycles
+        except hz.ConvergenceError:
+            X = None
+        outs[(pf, pdl)] = (res, X)
+    base = outs[("0", "0")]
+    for key, (res, X) in outs.items():
+        for a, c in zip(res, base[0]):
+            assert np.array_equal(a, c), key
+        assert (X is None) == (base[1] is None)
+        if X is not None:
+            assert np.array_equal(X, base[1]), key
+
+
 def test_config3_three_levels_block_tridiagonal(ref):
     """Config-3 recipe at 65x65x33 with the converging 3-level hierarchy: the
     coarsest level (17x17x9) is solved by the plane block-tridiagonal solver."""
