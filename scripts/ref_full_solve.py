@@ -57,10 +57,24 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--block", type=int, default=0)
-    ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "cfg2_bench_block0.npz"))
+    ap.add_argument("--config", type=int, default=2, help="2: the bench workload; 3: BASELINE config 3 at full size "
+                    "(129x129x65, the converging 3-level variant of scripts/run_configs.py, 8-column blocks)")
+    ap.add_argument("--out", default=None)
     args = ap.parse_args()
+    if args.out is None:
+        name = f"cfg2_bench_block{args.block}.npz" if args.config == 2 else f"cfg{args.config}_full_block{args.block}.npz"
+        args.out = os.path.join(ROOT, "tests", "golden", name)
 
-    cfg = bench.build_workload(0, 1, bench.WORKLOAD["k"])
+    if args.config == 2:
+        cfg = bench.build_workload(0, 1, bench.WORKLOAD["k"])
+        settings = dict(bench.WORKLOAD, block=args.block)
+    else:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import run_configs
+        cfg = run_configs.make(args.config)
+        settings = dict(config=args.config, n=list(map(int, cfg.n)), nlevels=cfg.nlevels, shift=cfg.shift,
+                        restart=cfg.restart, cycle=cfg.cycle, pre=cfg.pre, post=cfg.post, wj=cfg.jacobi_weight,
+                        tol=cfg.tol, block=args.block, krylov_block=cfg.krylov_block)
     b = cfg.krylov_block
     cols = slice(args.block * b, (args.block + 1) * b)
     B = cfg.rhs_block(cols)
@@ -80,7 +94,7 @@ def main():
         converged=np.asarray(rep.converged), history=np.asarray(rep.history), nodes=nodes, x_sample=X[nodes],
         x_norm=np.linalg.norm(X, axis=0), source_nodes=np.asarray(cfg.source_nodes[cols]),
         setup_s=setup_s, solve_s=solve_s, threads=args.threads, cpu=cpu_model(),
-        settings=str(dict(bench.WORKLOAD, block=args.block)))
+        settings=str(settings))
     print(f"reference block {args.block}: cycles {rep.cycles}, col_cycles {list(rep.col_cycles)}, "
           f"max rel residual {np.max(rep.rel_residual):.3e}, converged {rep.all_converged()}, "
           f"setup {setup_s:.1f} s, solve {solve_s:.1f} s ({solve_s / max(rep.cycles, 1):.3f} s/cycle) "
