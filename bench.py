@@ -55,18 +55,24 @@ WORKLOADS = {
                  max_cycles=2000, precond="c64", krylov_block=8, stencil=7),
     # BASELINE config 4's per-GPU shard (--workload cfg4): 3D 257x257x129 with
     # the compact 27-point fine operator, 8 of the 64 surface sources per GPU,
-    # c128 FGMRES(10) + c64 V(2,2), 3 levels (4 and 5 levels stall below
-    # 1e-2 in 500 cycles with either stencil: profiles/r02_cfg4_levels.txt)
-    "cfg4": dict(cfg=4, k=8, nlevels=3, shift=0.5, jacobi_weight=0.8, cycle="V", restart=10, tol=1e-6,
+    # c128 FGMRES(5) + c64 W(2,2), 3 levels (4 and 5 levels stall below
+    # 1e-2 in 500 cycles with either stencil: profiles/r02_cfg4_levels.txt);
+    # W-cycle, shift 0.3, w_J 0.9 from profiles/r02_sweep_cfg4.txt (110 cycles;
+    # V(2,2) at shift 0.5 / w_J 0.8 with FGMRES(10): 179-201 cycles)
+    "cfg4": dict(cfg=4, k=8, nlevels=3, shift=0.3, jacobi_weight=0.9, cycle="W", restart=5, tol=1e-6,
                  max_cycles=600, precond="c64", krylov_block=0, stencil=27),
     # BASELINE config 3 (--workload cfg3): 3D 129x129x65, 7-point operator, the
     # 16 surface sources as 2 concurrent blocks of 8, c128 FGMRES(5) + c64
-    # V(2,2), 3 levels (the literal 4 levels stall): the paper's own
-    # grid (BASELINE.md Table 1). Its reference numbers come from the committed
-    # full reference solves (tests/golden/cfg3_full_block*.npz): the
+    # W(2,2), 3 levels (the literal 4 levels stall): the paper's own
+    # grid (BASELINE.md Table 1). W-cycle, shift 0.25, w_J 0.9 from the sweeps of
+    # profiles/r02_sweep_cfg3.txt (80 cycles, 80.3 RHS/s; V at the same shift
+    # 130 cycles, 65.8; V at shift 0.5 / w_J 0.8 155 cycles, 54.8; the
+    # reference's own defaults are the W-cycle and shift 0.2). Its reference
+    # numbers come from the committed full reference solves at these settings
+    # (tests/golden/cfg3_bench_block*.npz, scripts/ref_full_solve.py --bench): the
     # reference's banded-LU setup of the 33x33x17 coarsest grid alone takes
     # minutes on host cores, too long for a bench step.
-    "cfg3": dict(cfg=3, k=16, nlevels=3, shift=0.5, jacobi_weight=0.8, cycle="V", restart=5, tol=1e-6,
+    "cfg3": dict(cfg=3, k=16, nlevels=3, shift=0.25, jacobi_weight=0.9, cycle="W", restart=5, tol=1e-6,
                  max_cycles=600, precond="c64", krylov_block=8, stencil=7),
 }
 WORKLOAD = WORKLOADS["cfg2"]
@@ -212,7 +218,7 @@ def ref_cycles_measured():
     ({block: cycles}, cpu model of the run)."""
     import numpy as np
     out, cpu = {}, None
-    stem = "cfg3_full_block" if WORKLOAD["cfg"] == 3 else "cfg2_bench_block"
+    stem = "cfg3_bench_block" if WORKLOAD["cfg"] == 3 else "cfg2_bench_block"
     for b in range(8):
         f = os.path.join(ROOT, "tests", "golden", f"{stem}{b}.npz")
         if os.path.exists(f):
@@ -316,7 +322,7 @@ def fixture_baseline():
     b = cfg.krylov_block if 0 < cfg.krylov_block < cfg.k else cfg.k
     secs, cyc, cols, cpu, thr = 0.0, [], 0, None, None
     for blk in range(-(-cfg.k // b)):
-        f = os.path.join(ROOT, "tests", "golden", f"cfg3_full_block{blk}.npz")
+        f = os.path.join(ROOT, "tests", "golden", f"cfg3_bench_block{blk}.npz")
         if not os.path.exists(f):
             continue
         g = np.load(f)
@@ -329,8 +335,8 @@ def fixture_baseline():
     return cols / secs, thr, (f"full reference solves (block_fgmres to 1e-6, c128 preconditioner, 3 levels with the "
                               f"banded LU of the 33x33x17 coarsest grid; setup excluded) of {cols} of the workload's "
                               f"{cfg.k} sources in {b}-column blocks: {', '.join(map(str, cyc))} cycles, {secs:.0f} s "
-                              f"on {thr} threads of {cpu}, measured when tests/golden/cfg3_full_block*.npz were "
-                              f"generated (scripts/ref_full_solve.py --config 3), not re-run here: the reference's "
+                              f"on {thr} threads of {cpu}, measured when tests/golden/cfg3_bench_block*.npz were "
+                              f"generated (scripts/ref_full_solve.py --config 3 --bench), not re-run here: the reference's "
                               f"setup alone takes minutes")
 
 

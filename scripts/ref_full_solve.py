@@ -57,48 +57,58 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--blocks", default=None, help="comma-separated blocks solved in one run (one setup)")
     ap.add_argument("--config", type=int, default=2, help="2: the bench workload; 3: BASELINE config 3 at full size "
                     "(129x129x65, the converging 3-level variant of scripts/run_configs.py, 8-column blocks)")
+    ap.add_argument("--bench", action="store_true", help="config 3 with bench.py --workload cfg3's solver settings "
+                    "(-> cfg3_bench_block<b>.npz) instead of scripts/run_configs.py's recipe")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
-    if args.out is None:
-        name = f"cfg2_bench_block{args.block}.npz" if args.config == 2 else f"cfg{args.config}_full_block{args.block}.npz"
-        args.out = os.path.join(ROOT, "tests", "golden", name)
+    blocks = [int(x) for x in args.blocks.split(",")] if args.blocks else [args.block]
 
     if args.config == 2:
         cfg = bench.build_workload(0, 1, bench.WORKLOAD["k"])
-        settings = dict(bench.WORKLOAD, block=args.block)
+        settings = dict(bench.WORKLOAD)
+        stem = "cfg2_bench_block"
+    elif args.bench:
+        bench.WORKLOAD = bench.WORKLOADS[f"cfg{args.config}"]
+        cfg = bench.build_workload(0, 1, bench.WORKLOAD["k"])
+        settings = dict(bench.WORKLOAD)
+        stem = f"cfg{args.config}_bench_block"
     else:
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         import run_configs
         cfg = run_configs.make(args.config)
         settings = dict(config=args.config, n=list(map(int, cfg.n)), nlevels=cfg.nlevels, shift=cfg.shift,
                         restart=cfg.restart, cycle=cfg.cycle, pre=cfg.pre, post=cfg.post, wj=cfg.jacobi_weight,
-                        tol=cfg.tol, block=args.block, krylov_block=cfg.krylov_block)
+                        tol=cfg.tol, krylov_block=cfg.krylov_block)
+        stem = f"cfg{args.config}_full_block"
     b = cfg.krylov_block
-    cols = slice(args.block * b, (args.block + 1) * b)
-    B = cfg.rhs_block(cols)
     ref.set_num_threads(args.threads)
     t0 = time.perf_counter()
     R = ref.RefProblem.from_config(cfg)
     H = ref.RefHierarchy(R, cfg.nlevels, cfg.shift)
     setup_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    X, rep = ref.krylov_solve(R, H, B, method="fgmres", kind=cfg.cycle, pre=cfg.pre, post=cfg.post,
-                              wj=cfg.jacobi_weight, restart=cfg.restart, tol=cfg.tol,
-                              max_cycles=cfg.max_cycles)
-    solve_s = time.perf_counter() - t0
     nodes = sample_nodes(cfg)
-    np.savez_compressed(
-        args.out, cycles=rep.cycles, col_cycles=np.asarray(rep.col_cycles), rel_residual=np.asarray(rep.rel_residual),
-        converged=np.asarray(rep.converged), history=np.asarray(rep.history), nodes=nodes, x_sample=X[nodes],
-        x_norm=np.linalg.norm(X, axis=0), source_nodes=np.asarray(cfg.source_nodes[cols]),
-        setup_s=setup_s, solve_s=solve_s, threads=args.threads, cpu=cpu_model(),
-        settings=str(settings))
-    print(f"reference block {args.block}: cycles {rep.cycles}, col_cycles {list(rep.col_cycles)}, "
-          f"max rel residual {np.max(rep.rel_residual):.3e}, converged {rep.all_converged()}, "
-          f"setup {setup_s:.1f} s, solve {solve_s:.1f} s ({solve_s / max(rep.cycles, 1):.3f} s/cycle) "
-          f"on {args.threads} threads ({cpu_model()}) -> {args.out}")
+    for block in blocks:
+        out = args.out if (args.out and len(blocks) == 1) else os.path.join(ROOT, "tests", "golden", f"{stem}{block}.npz")
+        cols = slice(block * b, (block + 1) * b)
+        B = cfg.rhs_block(cols)
+        t0 = time.perf_counter()
+        X, rep = ref.krylov_solve(R, H, B, method="fgmres", kind=cfg.cycle, pre=cfg.pre, post=cfg.post,
+                                  wj=cfg.jacobi_weight, restart=cfg.restart, tol=cfg.tol,
+                                  max_cycles=cfg.max_cycles)
+        solve_s = time.perf_counter() - t0
+        np.savez_compressed(
+            out, cycles=rep.cycles, col_cycles=np.asarray(rep.col_cycles), rel_residual=np.asarray(rep.rel_residual),
+            converged=np.asarray(rep.converged), history=np.asarray(rep.history), nodes=nodes, x_sample=X[nodes],
+            x_norm=np.linalg.norm(X, axis=0), source_nodes=np.asarray(cfg.source_nodes[cols]),
+            setup_s=setup_s, solve_s=solve_s, threads=args.threads, cpu=cpu_model(),
+            settings=str(dict(settings, block=block)))
+        print(f"reference block {block}: cycles {rep.cycles}, col_cycles {list(map(int, rep.col_cycles))}, "
+              f"max rel residual {np.max(rep.rel_residual):.3e}, converged {rep.all_converged()}, "
+              f"setup {setup_s:.1f} s, solve {solve_s:.1f} s ({solve_s / max(rep.cycles, 1):.3f} s/cycle) "
+              f"on {args.threads} threads ({cpu_model()}) -> {out}", flush=True)
 
 
 if __name__ == "__main__":

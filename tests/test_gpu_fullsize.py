@@ -121,23 +121,36 @@ def _golden(name):
     return os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)
 
 
-@pytest.mark.parametrize("block,precond", [(0, "c64"), (0, "c128"), (1, "c64")])
-def test_config3_full_size_block_matches_reference_full_solve(block, precond):
+@pytest.mark.parametrize("stem,block,precond", [("cfg3_full_block", 0, "c64"), ("cfg3_full_block", 0, "c128"),
+                                                ("cfg3_full_block", 1, "c64"), ("cfg3_bench_block", 0, "c64"),
+                                                ("cfg3_bench_block", 1, "c64")])
+def test_config3_full_size_block_matches_reference_full_solve(stem, block, precond):
     """BASELINE config 3 at full size (129x129x65, 16 surface sources, the
-    converging 3-level variant: FGMRES(5) + V(2,2), shift 0.5, 8-column blocks)
-    against the REFERENCE's own block_fgmres run to 1e-6 on the same block
-    (scripts/ref_full_solve.py --config 3 -> tests/golden/cfg3_full_block*.npz;
-    complex128 preconditioner, banded LU of the 33x33x17 coarsest grid):
+    converging 3-level variant: FGMRES(5) + V(2,2), 8-column blocks) against
+    the REFERENCE's own block_fgmres run to 1e-6 on the same block (complex128
+    preconditioner, banded LU of the 33x33x17 coarsest grid), with the recipe
+    of scripts/run_configs.py (shift 0.5, w_J 0.8: cfg3_full_block*.npz,
+    scripts/ref_full_solve.py --config 3) and with the settings of
+    bench.py --workload cfg3 (cfg3_bench_block*.npz, --config 3 --bench):
     solution on the receiver plane's first row and a strided node sample within
     1e-5 per column, whole-field norms within 1e-5, cycles within 5 %."""
     import os, sys
-    path = _golden(f"cfg3_full_block{block}.npz")
+    path = _golden(f"{stem}{block}.npz")
     if not os.path.exists(path):
         pytest.skip("reference fixture not generated")
     g = np.load(path)
-    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
-    from run_configs import make
-    cfg = make(3)
+    if stem == "cfg3_bench_block":
+        import bench
+        saved = bench.WORKLOAD
+        bench.WORKLOAD = bench.WORKLOADS["cfg3"]
+        try:
+            cfg = bench.build_workload(0, 1, 16)
+        finally:
+            bench.WORKLOAD = saved
+    else:
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+        from run_configs import make
+        cfg = make(3)
     b = cfg.krylov_block
     cfg.precond_precision, cfg.krylov_block = precond, 0
     S = hz.HelmholtzSolver(hz.HelmholtzProblem.from_config(cfg), hz.HelmholtzSolveOptions.from_config(cfg))
