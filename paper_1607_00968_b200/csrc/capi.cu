@@ -33,6 +33,7 @@ void count_launch() {
 }
 void add_launches(int64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 void set_capturing(bool on) { g_capturing = on; }
+bool is_capturing() { return g_capturing; }
 
 // ---- per-kernel event profiler (profile.hpp)
 namespace {

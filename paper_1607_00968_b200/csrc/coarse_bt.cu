@@ -18,6 +18,7 @@
 // each S_j is inverted by Gauss-Jordan with partial pivoting. Agreement with
 // the reference's banded LU is to cond(A_c) * eps (tested).
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -353,11 +354,15 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
         for (int u = 0; u < U; ++u) pv[t][u] = l0 + lane + 32 * u < m ? __ldg(prow[t] + l0 + 32 * u) : czero<V>();
     }
   };
-  V acc[RW][KG];
+  // Two real-scaled accumulators per output, sum Re(P) r and sum Im(P) r, combined as A + i B after the loop:
+  // both updates are scalar x pair FMAs (FFMA2 with a broadcast operand), independent of each other. The
+  // complex-FMA form needed an (Im P, Im P) register pair per product, which the compiler rebuilt with two
+  // MOVs for every four FFMA2 (ncu: 21 % of the kernel's instructions), and chained its two FMAs.
+  V accA[RW][KG], accB[RW][KG];
 #pragma unroll
   for (int t = 0; t < RW; ++t)
 #pragma unroll
-    for (int q = 0; q < KG; ++q) acc[t][q] = czero<V>();
+    for (int q = 0; q < KG; ++q) accA[t][q] = accB[t][q] = czero<V>();
   // the row's chunks of P are loaded PF - 1 chunks ahead of the one being
   // multiplied (registers, rotated by unrolling)
   V pq[PF][RW][U];
@@ -384,7 +389,10 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
           for (int q = 0; q < KG; ++q) {
             const V rv = b[32 * u * RS + q];
 #pragma unroll
-            for (int t = 0; t < RW; ++t) acc[t][q] = cfma(pq[f][t][u], rv, acc[t][q]);
+            for (int t = 0; t < RW; ++t) {
+              accA[t][q] = crfma(pq[f][t][u].x, rv, accA[t][q]);
+              accB[t][q] = crfma(pq[f][t][u].y, rv, accB[t][q]);
+            }
           }
         }
         __syncthreads();
@@ -392,6 +400,11 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
     }
   }
   tiled::cp_async_wait<0>();
+  V acc[RW][KG];
+#pragma unroll
+  for (int t = 0; t < RW; ++t)
+#pragma unroll
+    for (int q = 0; q < KG; ++q) acc[t][q] = mk(accA[t][q].x - accB[t][q].y, accA[t][q].y + accB[t][q].x);
 #pragma unroll
   for (int t = 0; t < RW; ++t)
 #pragma unroll
@@ -674,8 +687,7 @@ void bt_solve(const LevelGeom& g, const cplx_t<T>* coef, const cplx_t<T>* ET, co
   const int64_t ld = inv_ld(m);
   const int64_t pk = m * k;
   const int gk = grid_for(pk, 256);
-  ProfScope prof(sizeof(T) == 8 ? "coarse_bt_c128" : "coarse_bt_c64",
-                 (2.0 * np - 1.0) * double(m) * m * sizeof(V), s, 8.0 * (2.0 * np - 1.0) * double(m) * m * k);
+  // (profiled by the caller, Hierarchy::coarse_solve: one scope around the direct chain or its graph)
   const bool two = mid < np - 1;  // a bottom-up chain exists
   // HZ_BT_L2PF (default 0): each row-owner plane step prefetches the chain's next factor block into L2.
   // Measured neutral on config 3 and 4 % slower on config 4 (profiles/r02_bt_pdl_ab.txt): the steps are not

@@ -46,6 +46,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 void count_launch();
 void add_launches(int64_t n);
 void set_capturing(bool on);  // this thread is capturing a CUDA graph
+bool is_capturing();
 #define HZ_CUDA(x) ::hz::cuda_check((x), #x, __FILE__, __LINE__)
 #define HZ_LAUNCH_CHECK()                                                              \
   do {                                                                                 \

@@ -640,9 +640,74 @@ void Hierarchy<T>::ensure_ws(int k) {
   ws_k_ = k;
 }
 
+// HZ_BT_GRAPH (default 1): outside a captured cycle the plane solver's chain
+// runs from its own CUDA graph (first use direct, captured on the second);
+// the same kernels in the same order, so the results are bitwise those of
+// the direct launches.
 template <class T>
 void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
   ensure_ws(k);
+  if (!bt_) {
+    launch_coarse_solve<T>(coarse_n(), k, ainvT_.get(), b, x, cpart_.get(), s);
+    return;
+  }
+  const auto& Lc = levels_.back();
+  const LevelGeom gT = bt_permuted_geom(LevelGeom(Lc.dims[0], Lc.dims[1], Lc.dims[2], k), bt_perm_);
+  const double m = double(gT.n0) * gT.n1, np = double(gT.n2);
+  ProfScope prof(sizeof(T) == 8 ? "coarse_bt_c128" : "coarse_bt_c64", (2.0 * np - 1.0) * m * m * sizeof(V), s,
+                 8.0 * (2.0 * np - 1.0) * m * m * k);
+  const char* ge = std::getenv("HZ_BT_GRAPH");
+  if (sl_ || is_capturing() || (ge && ge[0] == '0')) {
+    coarse_solve_bt(k, b, x, s);
+    return;
+  }
+  if (bt_graphs_.size() > 32) {  // caller-owned blocks at ever new addresses
+    for (auto& kv : bt_graphs_)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+    bt_graphs_.clear();
+  }
+  const auto key = std::make_tuple(static_cast<const void*>(b), static_cast<const void*>(x), k);
+  auto it = bt_graphs_.find(key);
+  if (it == bt_graphs_.end()) {  // first use: direct (function attributes, lazy state)
+    coarse_solve_bt(k, b, x, s);
+    bt_graphs_.emplace(key, GraphRec{});
+    return;
+  }
+  GraphRec& g = it->second;
+  if (!g.exec) {
+    cudaGraph_t graph = nullptr;
+    HZ_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    set_capturing(true);
+    try {
+      coarse_solve_bt(k, b, x, s);
+    } catch (...) {
+      set_capturing(false);
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    set_capturing(false);
+    HZ_CUDA(cudaStreamEndCapture(s, &graph));
+    size_t nn = 0;
+    HZ_CUDA(cudaGraphGetNodes(graph, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    HZ_CUDA(cudaGraphGetNodes(graph, nodes.data(), &nn));
+    g.kernels = 0;
+    for (auto nd : nodes) {
+      cudaGraphNodeType ty;
+      HZ_CUDA(cudaGraphNodeGetType(nd, &ty));
+      if (ty == cudaGraphNodeTypeKernel) ++g.kernels;
+    }
+    const cudaError_t st = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    HZ_CUDA(st);
+  }
+  HZ_CUDA(cudaGraphLaunch(g.exec, s));
+  add_launches(g.kernels);
+}
+
+template <class T>
+void Hierarchy<T>::coarse_solve_bt(int k, const V* b, V* x, cudaStream_t s) {
   if (bt_) {
     const auto& Lc = levels_.back();
     const LevelGeom gc(Lc.dims[0], Lc.dims[1], Lc.dims[2], k);
@@ -823,6 +888,9 @@ void Hierarchy<T>::clear_graphs() {
   for (auto& kv : graphs_)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   graphs_.clear();
+  for (auto& kv : bt_graphs_)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  bt_graphs_.clear();
 }
 
 template <class T>

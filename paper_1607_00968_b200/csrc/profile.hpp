@@ -12,6 +12,7 @@
 namespace hz {
 
 bool profiling_enabled();
+bool is_capturing();  // common.cuh: this thread is capturing a CUDA graph (no event records then)
 void profile_record(const char* name, double bytes, double flops, cudaEvent_t a, cudaEvent_t b,
                     cudaStream_t s = nullptr);
 cudaEvent_t profile_event();
@@ -22,7 +23,7 @@ class ProfScope {
  public:
   ProfScope(const char* name, double bytes, cudaStream_t s, double flops = 0.0)
       : name_(name), bytes_(bytes), flops_(flops), s_(s) {
-    if (profiling_enabled()) {
+    if (profiling_enabled() && !is_capturing()) {
       a_ = profile_event();
       b_ = profile_event();
       cudaEventRecord(a_, s_);

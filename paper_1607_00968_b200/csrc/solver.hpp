@@ -201,6 +201,11 @@ class Hierarchy {
   };
   std::map<GraphKey, GraphRec> graphs_;
   void clear_graphs();
+  // the plane-solver chain of a coarsest-level solve (≈ 130-260 dependent
+  // launches) as its own graph per (b, x, k), replayed wherever the cycle
+  // itself is not graph-replayed (complex128 cycles, profiled runs)
+  std::map<std::tuple<const void*, const void*, int>, GraphRec> bt_graphs_;
+  void coarse_solve_bt(int k, const V* b, V* x, cudaStream_t s);
   // high-priority stream of the coarse part of the cycle (coarse_visit)
   cudaStream_t hp_ = nullptr;
   cudaEvent_t hp_fork_ = nullptr, hp_join_ = nullptr;

@@ -228,9 +228,11 @@ def test_block_tridiagonal_prefetch_and_dependent_launch_bitwise(n, nl, monkeypa
     cfg = configs.small_problem(3, n, seed=3)
     P = hz.HelmholtzProblem.from_config(cfg)
     outs = {}
-    for pf, pdl in (("0", "0"), ("1", "0"), ("1", "1"), ("2", "1"), ("0", "1")):
+    for pf, pdl, graph in (("0", "0", "0"), ("0", "0", "1"), ("1", "0", "1"), ("1", "1", "1"), ("2", "1", "0"),
+                           ("0", "1", "1")):
         monkeypatch.setenv("HZ_BT_L2PF", pf)
         monkeypatch.setenv("HZ_BT_PDL", pdl)
+        monkeypatch.setenv("HZ_BT_GRAPH", graph)  # the chain replayed from its own CUDA graph (default) or launched directly
         S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
                                                            cycle=hz.CycleSpec("V"), precond_precision="c64",
                                                            fgmres_restart=5, tol=1e-6, max_cycles=30))
@@ -244,8 +246,8 @@ def test_block_tridiagonal_prefetch_and_dependent_launch_bitwise(n, nl, monkeypa
             X, rep = S.solve_block(b)  # graph-replayed c64 cycles
         except hz.ConvergenceError:
             X = None
-        outs[(pf, pdl)] = (res, X)
-    base = outs[("0", "0")]
+        outs[(pf, pdl, graph)] = (res, X)
+    base = outs[("0", "0", "0")]
     for key, (res, X) in outs.items():
         for a, c in zip(res, base[0]):
             assert np.array_equal(a, c), key
