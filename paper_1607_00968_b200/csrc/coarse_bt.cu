@@ -202,11 +202,11 @@ bool bt_pdl() {  // read per launch: the tests switch it within one process
 }
 
 template <class... KA, class... A>
-void launch_chain(void (*kern)(KA...), dim3 grid, dim3 block, cudaStream_t s, A... args) {
+void launch_chain_smem(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -214,6 +214,10 @@ void launch_chain(void (*kern)(KA...), dim3 grid, dim3 block, cudaStream_t s, A.
   cfg.attrs = at;
   cfg.numAttrs = bt_pdl() ? 1 : 0;
   HZ_CUDA(cudaLaunchKernelEx(&cfg, kern, KA(args)...));
+}
+template <class... KA, class... A>
+void launch_chain(void (*kern)(KA...), dim3 grid, dim3 block, cudaStream_t s, A... args) {
+  launch_chain_smem(kern, grid, block, 0, s, args...);
 }
 
 // r = b_j - L_j y_{j-dir} for one plane, all k columns (L = plane j -> j-dir
@@ -431,6 +435,164 @@ bt_rows_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx
   }
 }
 
+// The plane step with all of r resident in shared memory (HZ_BT_RES): the
+// row-owner kernel re-stages r chunk by chunk with two CTA barriers per
+// chunk, and its warps spend most of their time between those barriers and
+// the staging latency (ncu: issue 34 %, no dominant stall). Here a CTA of NW
+// warps owns NW * RW rows, copies r once ([l][KG + 1] padded rows, conflict
+// free for lane = l reads), and its warps then stream their rows of P with
+// no barrier at all, the next chunk's loads always in flight. 16 warps x 2
+// rows make 68 CTAs of 154 KB for a 2,145-node plane: one CTA per SM, the
+// two chains of the two-sided sweep side by side on 136 SMs. Same per-lane
+// and butterfly order as the row-owner kernel: bitwise the same results.
+template <class T, int RW, int KG, int LC, int NW>
+__global__ void __launch_bounds__(32 * NW, 1)
+bt_rows_res_kernel(int m, int k, const cplx_t<T>* __restrict__ P, int ld, const cplx_t<T>* __restrict__ r,
+                   cplx_t<T>* out, const cplx_t<T>* c_in, T sign) {
+  using V = cplx_t<T>;
+  constexpr int U = LC / 32, RS = KG + 1;
+  extern __shared__ __align__(16) unsigned char bt_smem[];
+  V* rs = reinterpret_cast<V*>(bt_smem);
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int i0 = int(blockIdx.x) * (NW * RW);
+  const int q0 = blockIdx.y * KG;
+  const int nch = (m + LC - 1) / LC;
+  const V* prow[RW];
+  bool live[RW];
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    const int row = i0 + w + NW * t;
+    live[t] = row < m;
+    prow[t] = P + int64_t(min(row, m - 1)) * ld + lane;
+  }
+  auto load_p = [&](int c, V (&pv)[RW][U]) {
+    const int l0 = c * LC;
+    if (l0 + LC <= m) {
+#pragma unroll
+      for (int t = 0; t < RW; ++t)
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[t][u] = __ldg(prow[t] + l0 + 32 * u);
+    } else {
+#pragma unroll
+      for (int t = 0; t < RW; ++t)
+#pragma unroll
+        for (int u = 0; u < U; ++u) pv[t][u] = l0 + lane + 32 * u < m ? __ldg(prow[t] + l0 + 32 * u) : czero<V>();
+    }
+  };
+  V pq[2][RW][U];
+  load_p(0, pq[0]);  // P does not depend on the preceding step
+  pdl_launch_dependents();
+  pdl_wait();
+  {  // r -> shared memory, rows past m zero
+    const V* rq = r + q0;
+    const int tot = nch * LC * KG;
+    for (int e = tid; e < tot; e += 32 * NW) {
+      const int l = e / KG, q = e % KG;
+      if (l < m)
+        cp_async_elem(rs + l * RS + q, rq + l * k + q);
+      else
+        rs[l * RS + q] = czero<V>();
+    }
+    tiled::cp_async_commit();
+    tiled::cp_async_wait<0>();
+  }
+  __syncthreads();
+  V accA[RW][KG], accB[RW][KG];
+#pragma unroll
+  for (int t = 0; t < RW; ++t)
+#pragma unroll
+    for (int q = 0; q < KG; ++q) accA[t][q] = accB[t][q] = czero<V>();
+  for (int c0 = 0; c0 < nch; c0 += 2) {
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int c = c0 + f;
+      if (c < nch) {
+        if (c + 1 < nch) load_p(c + 1, pq[f ^ 1]);
+        const V* b = rs + (c * LC + lane) * RS;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int q = 0; q < KG; ++q) {
+            const V rv = b[32 * u * RS + q];
+#pragma unroll
+            for (int t = 0; t < RW; ++t) {
+              accA[t][q] = crfma(pq[f][t][u].x, rv, accA[t][q]);
+              accB[t][q] = crfma(pq[f][t][u].y, rv, accB[t][q]);
+            }
+          }
+        }
+      }
+    }
+  }
+  V acc[RW][KG];
+#pragma unroll
+  for (int t = 0; t < RW; ++t)
+#pragma unroll
+    for (int q = 0; q < KG; ++q) acc[t][q] = mk(accA[t][q].x - accB[t][q].y, accA[t][q].y + accB[t][q].x);
+#pragma unroll
+  for (int t = 0; t < RW; ++t)
+#pragma unroll
+    for (int q = 0; q < KG; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[t][q].x += __shfl_xor_sync(0xffffffffu, acc[t][q].x, o);
+        acc[t][q].y += __shfl_xor_sync(0xffffffffu, acc[t][q].y, o);
+      }
+#pragma unroll
+  for (int t = 0; t < RW; ++t) {
+    if (!live[t]) continue;
+#pragma unroll
+    for (int q = 0; q < KG; ++q) {
+      if (lane != q) continue;
+      V v = acc[t][q];
+      const int o = (i0 + w + NW * t) * k + q0 + q;
+      if (c_in) {
+        const V cv = c_in[o];
+        v = mk(cv.x + sign * v.x, cv.y + sign * v.y);
+      }
+      out[o] = v;
+    }
+  }
+}
+
+// HZ_BT_RES = "NW[:RW[:LC]]" (warps per CTA, rows per warp, columns per chunk) selects the resident-r kernel
+// where r fits in shared memory; 0: off
+template <class T>
+bool bt_rows_res_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
+                    const cplx_t<T>* c_in, T sign, cudaStream_t s) {
+  using V = cplx_t<T>;
+  int nw = 16, rw = sizeof(T) == 8 ? 1 : 2, lc = 128;
+  const char* e = std::getenv("HZ_BT_RES");
+  if (e) std::sscanf(e, "%d:%d:%d", &nw, &rw, &lc);
+  if (nw <= 0 || k % 8 != 0) return false;
+  const int64_t nch = (m + lc - 1) / lc;
+  const size_t smem = size_t(nch) * lc * 9 * sizeof(V);
+  if (smem > 200 * 1024) return false;
+  auto launch = [&](auto kern, int nw_, int rw_) {
+    allow_dyn_smem(reinterpret_cast<const void*>(kern), int(smem));
+    const dim3 grid(unsigned((m + nw_ * rw_ - 1) / (nw_ * rw_)), unsigned(k / 8));
+    launch_chain_smem(kern, grid, dim3(32 * nw_), smem, s, int(m), k, P, int(ld), r, out, c_in, sign);
+  };
+#define HZ_BT_RES_CASE(NW_, RW_, LC_)                          \
+  if (nw == NW_ && rw == RW_ && lc == LC_) {                   \
+    launch(bt_rows_res_kernel<T, RW_, 8, LC_, NW_>, NW_, RW_); \
+    return true;                                               \
+  }
+  HZ_BT_RES_CASE(16, 2, 128)
+  HZ_BT_RES_CASE(16, 1, 128)
+  HZ_BT_RES_CASE(8, 2, 128)
+  if constexpr (sizeof(T) == 4) {
+    HZ_BT_RES_CASE(16, 2, 256)
+    HZ_BT_RES_CASE(16, 1, 256)
+    HZ_BT_RES_CASE(8, 2, 256)
+    HZ_BT_RES_CASE(8, 4, 128)
+    HZ_BT_RES_CASE(24, 1, 256)
+    HZ_BT_RES_CASE(32, 1, 128)
+  }
+#undef HZ_BT_RES_CASE
+  return false;
+}
+
 template <class T, int RW, int KG>
 void bt_rows_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
                 const cplx_t<T>* c_in, T sign, const cplx_t<T>* Pnext, cudaStream_t s) {
@@ -475,6 +637,7 @@ void bt_rows(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* 
     return e ? std::atoi(e) : 0;
   }();
   const bool two = rw_env ? rw_env == 2 : m > int64_t(kNumSMs) * 8;
+  if (bt_rows_res_go<T>(m, k, P, ld, r, out, c_in, sign, s)) return;
   auto go = [&](auto kg) {
     constexpr int KG = decltype(kg)::value;
     if (two)
