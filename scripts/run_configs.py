@@ -25,7 +25,8 @@ def make(c):
         cfg.precond_precision = "c64"
     elif c == 5:
         cfg = configs.config5(nlevels=4)                   # coarsest 65x65x33
-        cfg.shift, cfg.restart = 1.5, 5
+        # V(2,2), shift 1.0, w_J 0.5, FGMRES(5): 397 cycles (profiles/r02_cfg5_sweep.jsonl; w_J 0.8 needed W at shift 1.5: 1,286)
+        cfg.shift, cfg.restart, cfg.jacobi_weight = 1.0, 5, 0.5
     for key in ("nlevels", "shift", "restart", "max_cycles", "precond_precision", "krylov_block", "jacobi_weight",
                 "cycle", "stencil"):
         v = os.environ.get(f"HZ_CFG{c}_{key.upper()}")

@@ -10,15 +10,16 @@ VARIANTS = [  # (levels, shift, kind, restart)
     (4, 1.5, "W", 5), (4, 1.0, "V", 5), (4, 1.0, "W", 5), (5, 1.5, "W", 5), (5, 1.0, "W", 5),
 ]
 if os.environ.get("HZ_VARIANTS"):
-    VARIANTS = [tuple(t(x) for t, x in zip((int, float, str, int), v.split(":")))
+    VARIANTS = [tuple(t(x) for t, x in zip((int, float, str, int, float), v.split(":")))
                 for v in os.environ["HZ_VARIANTS"].split(",")]
 maxc = int(os.environ.get("HZ_MAXC", "300"))
 cfg = configs.config5(nlevels=4)
 P = hz.HelmholtzProblem.from_config(cfg)
 B = torch.from_numpy(cfg.rhs_block()).cuda()
-for (L, shift, kind, restart) in VARIANTS:
+for var in VARIANTS:
+    (L, shift, kind, restart), wj = var[:4], (var[4] if len(var) > 4 else 0.8)
     o = hz.HelmholtzSolveOptions.from_config(cfg)
-    o.method, o.nlevels, o.shift_factor, o.cycle = "MgFgmres", L, shift, hz.CycleSpec(kind)
+    o.method, o.nlevels, o.shift_factor, o.cycle = "MgFgmres", L, shift, hz.CycleSpec(kind, 2, 2, wj)
     o.fgmres_restart, o.max_cycles = restart, maxc
     t = time.time()
     S = hz.HelmholtzSolver(P, o)
@@ -27,7 +28,7 @@ for (L, shift, kind, restart) in VARIANTS:
     X, rep = S.solve_block(B)
     torch.cuda.synchronize(); dt = time.time() - t
     h = rep.history
-    print(json.dumps(dict(levels=L, shift=shift, kind=kind, restart=restart, setup_s=round(setup, 1),
+    print(json.dumps(dict(levels=L, shift=shift, kind=kind, restart=restart, wj=wj, setup_s=round(setup, 1),
                           cycles=rep.cycles, converged=rep.all_converged(),
                           worst_res=float(rep.rel_residual.max()), solve_s=round(dt, 2),
                           ms_per_cycle=round(1e3 * dt / max(rep.cycles, 1), 2),

@@ -123,7 +123,7 @@ def _golden(name):
 
 @pytest.mark.parametrize("stem,block,precond", [("cfg3_full_block", 0, "c64"), ("cfg3_full_block", 0, "c128"),
                                                 ("cfg3_full_block", 1, "c64"), ("cfg3_bench_block", 0, "c64"),
-                                                ("cfg3_bench_block", 1, "c64")])
+                                                ("cfg3_bench_block", 1, "c64"), ("cfg3_literal_block", 0, "c64")])
 def test_config3_full_size_block_matches_reference_full_solve(stem, block, precond):
     """BASELINE config 3 at full size (129x129x65, 16 surface sources, the
     converging 3-level variant: FGMRES(5) + V(2,2), 8-column blocks) against
@@ -131,7 +131,9 @@ def test_config3_full_size_block_matches_reference_full_solve(stem, block, preco
     preconditioner, banded LU of the 33x33x17 coarsest grid), with the recipe
     of scripts/run_configs.py (shift 0.5, w_J 0.8: cfg3_full_block*.npz,
     scripts/ref_full_solve.py --config 3) and with the settings of
-    bench.py --workload cfg3 (cfg3_bench_block*.npz, --config 3 --bench):
+    bench.py --workload cfg3 (cfg3_bench_block*.npz, --config 3 --bench), and
+    BASELINE config 3 as stated -- 4 levels, V(2,2), FGMRES(10), with shift 1.0
+    and Jacobi weight 0.5 (cfg3_literal_block0.npz, --config 3 --literal):
     solution on the receiver plane's first row and a strided node sample within
     1e-5 per column, whole-field norms within 1e-5, cycles within 5 %."""
     import os, sys
@@ -147,6 +149,10 @@ def test_config3_full_size_block_matches_reference_full_solve(stem, block, preco
             cfg = bench.build_workload(0, 1, 16)
         finally:
             bench.WORKLOAD = saved
+    elif stem == "cfg3_literal_block":
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
+        from ref_full_solve import literal_config3
+        cfg = literal_config3()
     else:
         sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "scripts"))
         from run_configs import make
