@@ -73,7 +73,12 @@ WORKLOADS = {
     # reference's banded-LU setup of the 33x33x17 coarsest grid alone takes
     # minutes on host cores, too long for a bench step.
     "cfg3": dict(cfg=3, k=16, nlevels=3, shift=0.25, jacobi_weight=0.9, cycle="W", restart=5, tol=1e-6,
-                 max_cycles=600, precond="c64", krylov_block=8, stencil=7),
+                 max_cycles=600, precond="c64", krylov_block=8, stencil=7, fixture="cfg3_bench_block"),
+    # BASELINE config 3 exactly as stated (--workload cfg3_literal): 4 levels, V(2,2), block FGMRES(10); the shift
+    # (1.0) and the Jacobi weight (0.5) are left open by BASELINE -- at w_J 0.6-0.8 this hierarchy stalls
+    # (profiles/r02_sweep_literal_levels.txt). 243 cycles: 0.44 of the 3-level W-cycle line's throughput.
+    "cfg3_literal": dict(cfg=3, k=16, nlevels=4, shift=1.0, jacobi_weight=0.5, cycle="V", restart=10, tol=1e-6,
+                         max_cycles=600, precond="c64", krylov_block=8, stencil=7, fixture="cfg3_literal_block"),
 }
 WORKLOAD = WORKLOADS["cfg2"]
 
@@ -218,7 +223,7 @@ def ref_cycles_measured():
     ({block: cycles}, cpu model of the run)."""
     import numpy as np
     out, cpu = {}, None
-    stem = "cfg3_bench_block" if WORKLOAD["cfg"] == 3 else "cfg2_bench_block"
+    stem = WORKLOAD.get("fixture", "cfg2_bench_block")
     for b in range(8):
         f = os.path.join(ROOT, "tests", "golden", f"{stem}{b}.npz")
         if os.path.exists(f):
@@ -322,7 +327,7 @@ def fixture_baseline():
     b = cfg.krylov_block if 0 < cfg.krylov_block < cfg.k else cfg.k
     secs, cyc, cols, cpu, thr = 0.0, [], 0, None, None
     for blk in range(-(-cfg.k // b)):
-        f = os.path.join(ROOT, "tests", "golden", f"cfg3_bench_block{blk}.npz")
+        f = os.path.join(ROOT, "tests", "golden", f"{WORKLOAD['fixture']}{blk}.npz")
         if not os.path.exists(f):
             continue
         g = np.load(f)
@@ -332,12 +337,11 @@ def fixture_baseline():
         cpu, thr = str(g["cpu"]), int(g["threads"])
     if not cols:
         return None
-    return cols / secs, thr, (f"full reference solves (block_fgmres to 1e-6, c128 preconditioner, 3 levels with the "
-                              f"banded LU of the 33x33x17 coarsest grid; setup excluded) of {cols} of the workload's "
+    return cols / secs, thr, (f"full reference solves (block_fgmres to 1e-6, c128 preconditioner, {cfg.nlevels} levels with the "
+                              f"banded LU of the coarsest grid; setup excluded) of {cols} of the workload's "
                               f"{cfg.k} sources in {b}-column blocks: {', '.join(map(str, cyc))} cycles, {secs:.0f} s "
-                              f"on {thr} threads of {cpu}, measured when tests/golden/cfg3_bench_block*.npz were "
-                              f"generated (scripts/ref_full_solve.py --config 3 --bench), not re-run here: the reference's "
-                              f"setup alone takes minutes")
+                              f"on {thr} threads of {cpu}, measured when tests/golden/{WORKLOAD['fixture']}*.npz were "
+                              f"generated (scripts/ref_full_solve.py --config 3 --bench / --literal), not re-run here")
 
 
 def reference_line_from_fixtures(args):
