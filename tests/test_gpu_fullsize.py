@@ -124,7 +124,7 @@ def _golden(name):
 @pytest.mark.parametrize("stem,block,precond", [("cfg3_full_block", 0, "c64"), ("cfg3_full_block", 0, "c128"),
                                                 ("cfg3_full_block", 1, "c64"), ("cfg3_bench_block", 0, "c64"),
                                                 ("cfg3_bench_block", 1, "c64"), ("cfg3_literal_block", 0, "c128"),
-                                                ("cfg3_literal_block", 0, "c64")])
+                                                ("cfg3_literal_block", 0, "c64"), ("cfg3_literal_block", 1, "c128")])
 def test_config3_full_size_block_matches_reference_full_solve(stem, block, precond):
     """BASELINE config 3 at full size (129x129x65, 16 surface sources, the
     converging 3-level variant: FGMRES(5) + V(2,2), 8-column blocks) against
