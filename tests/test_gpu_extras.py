@@ -228,28 +228,35 @@ def test_block_tridiagonal_prefetch_and_dependent_launch_bitwise(n, nl, monkeypa
     cfg = configs.small_problem(3, n, seed=3)
     P = hz.HelmholtzProblem.from_config(cfg)
     outs = {}
-    for pf, pdl, graph in (("0", "0", "0"), ("0", "0", "1"), ("1", "0", "1"), ("1", "1", "1"), ("2", "1", "0"),
-                           ("0", "1", "1")):
+    for pf, pdl, graph, res in (("0", "0", "0", None), ("0", "0", "1", None), ("1", "0", "1", None), ("1", "1", "1", None),
+                                ("2", "1", "0", None), ("0", "1", "1", None), ("0", "0", "1", "0"), ("1", "1", "0", "0"),
+                                ("0", "0", "1", "8:2:128")):
         monkeypatch.setenv("HZ_BT_L2PF", pf)
         monkeypatch.setenv("HZ_BT_PDL", pdl)
         monkeypatch.setenv("HZ_BT_GRAPH", graph)  # the chain replayed from its own CUDA graph (default) or launched directly
+        # plane-step kernel: r resident in shared memory (default), its 8-warp shape, or the row-owner kernel ("0"):
+        # the same per-lane and butterfly order, hence the same bits
+        if res is None:
+            monkeypatch.delenv("HZ_BT_RES", raising=False)
+        else:
+            monkeypatch.setenv("HZ_BT_RES", res)
         S = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
                                                            cycle=hz.CycleSpec("V"), precond_precision="c64",
                                                            fgmres_restart=5, tol=1e-6, max_cycles=30))
         R = hz.HelmholtzSolver(P, hz.HelmholtzSolveOptions(method="MgFgmres", nlevels=nl, shift_factor=0.5,
                                                            cycle=hz.CycleSpec("V")))
         b = configs.random_block(cfg.num_nodes, 8, seed=5)
-        res = [R.cycle(b)]
+        cyc = [R.cycle(b)]
         for _ in range(3):
-            res.append(R.cycle(b))  # repeated launches of the chain
+            cyc.append(R.cycle(b))  # repeated launches of the chain
         try:
             X, rep = S.solve_block(b)  # graph-replayed c64 cycles
         except hz.ConvergenceError:
             X = None
-        outs[(pf, pdl, graph)] = (res, X)
-    base = outs[("0", "0", "0")]
-    for key, (res, X) in outs.items():
-        for a, c in zip(res, base[0]):
+        outs[(pf, pdl, graph, res)] = (cyc, X)
+    base = outs[("0", "0", "0", None)]
+    for key, (cyc, X) in outs.items():
+        for a, c in zip(cyc, base[0]):
             assert np.array_equal(a, c), key
         assert (X is None) == (base[1] is None)
         if X is not None:
