@@ -560,9 +560,9 @@ def run_ours(args):
     roofline = roof(dom)
     roofline["share"] = table[dom]["share"]
     if dom.startswith("coarse_bt"):
-        roofline["note"] = ("the event profile times the two-sided plane-solver chain (~130 dependent launches) on its own, outside "
-                            "the graph-replayed cycle; inside it the chain is bandwidth bound (config 4: 0.92 ms per solve for "
-                            "4.7 GB of factors = 5.1 TB/s, timing-only cut in profiles/r02_bt_res_ab.txt, DESIGN.md section 3)")
+        roofline["note"] = ("the event profile times the two-sided plane-solver chain (~130 dependent launches) on its own; inside "
+                            "the graph-replayed W-cycle a solve takes 1.83 ms on config 4 (4.7 GB of factors, 2.6 TB/s; timing-only "
+                            "cut in profiles/r02_bt_res_ab.txt, DESIGN.md section 3)")
     stencil = [n_ for n_ in kern if n_.startswith(("jacobi", "residual", "apply", "restrict", "prolong", "fused"))]
     roof_st = None
     if stencil:
