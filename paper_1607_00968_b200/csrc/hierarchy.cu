@@ -657,7 +657,10 @@ void Hierarchy<T>::coarse_solve(int k, const V* b, V* x, cudaStream_t s) {
   ProfScope prof(sizeof(T) == 8 ? "coarse_bt_c128" : "coarse_bt_c64", (2.0 * np - 1.0) * m * m * sizeof(V), s,
                  8.0 * (2.0 * np - 1.0) * m * m * k);
   const char* ge = std::getenv("HZ_BT_GRAPH");
-  if (sl_ || is_capturing() || (ge && ge[0] == '0')) {
+  // a stream some caller is capturing takes the launches directly (they join the caller's graph)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  HZ_CUDA(cudaStreamIsCapturing(s, &cap));
+  if (sl_ || is_capturing() || cap != cudaStreamCaptureStatusNone || (ge && ge[0] == '0')) {
     coarse_solve_bt(k, b, x, s);
     return;
   }
