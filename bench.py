@@ -61,6 +61,10 @@ WORKLOADS = {
     # V(2,2) at shift 0.5 / w_J 0.8 with FGMRES(10): 179-201 cycles)
     "cfg4": dict(cfg=4, k=8, nlevels=3, shift=0.3, jacobi_weight=0.9, cycle="W", restart=5, tol=1e-6,
                  max_cycles=600, precond="c64", krylov_block=0, stencil=27),
+    # config 4's shard with the level count SURVEY §8d assigns it (--workload cfg4_literal): 5 levels, V(2,2); shift
+    # 1.0 and Jacobi weight 0.5 (at 0.6-0.8 this hierarchy stalls): 400 cycles, 0.41 of the 3-level W-cycle line
+    "cfg4_literal": dict(cfg=4, k=8, nlevels=5, shift=1.0, jacobi_weight=0.5, cycle="V", restart=5, tol=1e-6,
+                         max_cycles=900, precond="c64", krylov_block=0, stencil=27),
     # BASELINE config 3 (--workload cfg3): 3D 129x129x65, 7-point operator, the
     # 16 surface sources as 2 concurrent blocks of 8, c128 FGMRES(5) + c64
     # W(2,2), 3 levels (the literal 4 levels stall): the paper's own
