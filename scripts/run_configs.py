@@ -24,9 +24,10 @@ def make(c):
         cfg.source_nodes = cfg.source_nodes[:8]            # k = 8 per GPU (64 RHS sharded 8 per GPU)
         cfg.precond_precision = "c64"
     elif c == 5:
-        cfg = configs.config5(nlevels=4)                   # coarsest 65x65x33
-        # V(2,2), shift 1.0, w_J 0.5, FGMRES(5): 397 cycles (profiles/r02_cfg5_sweep.jsonl; w_J 0.8 needed W at shift 1.5: 1,286)
-        cfg.shift, cfg.restart, cfg.jacobi_weight = 1.0, 5, 0.5
+        cfg = configs.config5(nlevels=6)                   # the literal 6 levels, coarsest 17x17x9
+        # V(2,2), shift 1.2, w_J 0.5, FGMRES(5): 433 cycles, 20.3 s (profiles/r02_cfg5_sweep.jsonl; 4 levels / shift 1.0:
+        # 397 cycles, 20.1 s; w_J 0.8 needed 4 levels + W at shift 1.5: 1,286 cycles, 84.8 s)
+        cfg.shift, cfg.restart, cfg.jacobi_weight = 1.2, 5, 0.5
     for key in ("nlevels", "shift", "restart", "max_cycles", "precond_precision", "krylov_block", "jacobi_weight",
                 "cycle", "stencil"):
         v = os.environ.get(f"HZ_CFG{c}_{key.upper()}")
