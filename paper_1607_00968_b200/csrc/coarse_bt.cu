@@ -561,7 +561,7 @@ template <class T>
 bool bt_rows_res_go(int64_t m, int k, const cplx_t<T>* P, int64_t ld, const cplx_t<T>* r, cplx_t<T>* out,
                     const cplx_t<T>* c_in, T sign, cudaStream_t s) {
   using V = cplx_t<T>;
-  int nw = 16, rw = sizeof(T) == 8 ? 1 : 2, lc = 128;
+  int nw = sizeof(T) == 8 ? 8 : 16, rw = 2, lc = 128;  // c128: 8 warps (config 3, c128 W-cycle: 3.95 vs 4.06 ms with 16 x 1, 4.42 row-owner)
   const char* e = std::getenv("HZ_BT_RES");
   if (e) std::sscanf(e, "%d:%d:%d", &nw, &rw, &lc);
   if (nw <= 0 || k % 8 != 0) return false;
